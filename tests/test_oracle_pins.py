@@ -1,0 +1,348 @@
+"""Pins for the CPU oracle (``-m "not gpu"``): each oracle function is tied to something
+other than itself -- the SPEC/hand worked examples under tests/golden/, closed forms,
+brute force on tiny inputs, and exact-arithmetic identities the paper fixes.
+
+A plausible mistake (dropped term, wrong sign, wrong index, transposed operand,
+unstable sort, wrong zero convention) fails at least one of these.
+"""
+import itertools
+import math
+
+import numpy as np
+import pytest
+
+import oracle as O
+import synth
+from conftest import golden
+
+SPEC = golden("spec_examples.json")
+HAND = golden("hand_mlp.json")
+PACK = golden("gptq_packing.json")
+
+
+# ----------------------------------------------------------------------------- worked examples
+def test_eq1_spec_examples():
+    for ex in SPEC["eq1"]:
+        out = O.eq1_g_idx_naive(ex["K"], ex["G"])
+        if "out" in ex:
+            assert out.tolist() == ex["out"], ex["cite"]
+        else:
+            assert int(out[-1]) == ex["last"], ex["cite"]
+
+
+def test_eq3_spec_examples():
+    for ex in SPEC["eq3"]:
+        assert O.eq3_g_idx_actorder(ex["phi"], ex["G"]).tolist() == ex["out"], ex["cite"]
+
+
+def test_alg1_spec_examples():
+    for ex in SPEC["alg1"]:
+        P, g_opt = O.alg1_reorder(ex["g"])
+        assert P.tolist() == ex["P"], ex["cite"]
+        assert g_opt.tolist() == ex["g_opt"], ex["cite"]
+
+
+def test_invert_spec_examples():
+    for ex in SPEC["invert"]:
+        assert O.invert_permutation(ex["P"]).tolist() == ex["Q"], ex["cite"]
+    rng = np.random.default_rng(3)
+    P = rng.permutation(50)
+    assert O.invert_permutation(O.invert_permutation(P)).tolist() == P.tolist()
+
+
+def test_metadata_loads_spec_examples():
+    for ex in SPEC["metadata_loads"]:
+        if "g" in ex:
+            assert O.metadata_loads(ex["g"]) == ex["loads"], ex["cite"]
+        else:
+            K, G = ex["K"], ex["G"]
+            assert O.metadata_loads(np.arange(K) // G) == ex["ordered_loads"], ex["cite"]
+
+
+def test_all_reduce_spec_example():
+    ex = SPEC["all_reduce_sum"][0]
+    parts = [np.array([[float(v)]]) for v in ex["parts"]]
+    assert O.tp_dequant._all_reduce_sum(parts)[0, 0] == ex["out"]
+
+
+# ----------------------------------------------------------------------------- Alg. 1
+def _bruteforce_stable_argsort(g):
+    """O(K^2) rank construction: rank[j] = #{i : (g[i], i) < (g[j], j)}; P[rank[j]] = j."""
+    K = len(g)
+    P = [None] * K
+    for j in range(K):
+        r = 0
+        for i in range(K):
+            if g[i] < g[j] or (g[i] == g[j] and i < j):
+                r += 1
+        P[r] = j
+    return P
+
+
+def test_alg1_vs_bruteforce_1000_arrays():
+    """SPEC.md:L460 acceptance: Alg. 1 vs an independent brute-force stable sort, K <= 512."""
+    rng = np.random.default_rng(1234)
+    for t in range(1000):
+        K = int(rng.integers(1, 65)) if t < 950 else int(rng.integers(65, 513))
+        G = int(rng.integers(1, K + 1))
+        phi = rng.permutation(K)
+        g = (phi // G).tolist() if t % 2 == 0 else rng.integers(0, max(1, K // G + 1), size=K).tolist()
+        P, g_opt = O.alg1_reorder(g)
+        assert P.tolist() == _bruteforce_stable_argsort(g)
+        assert g_opt.tolist() == sorted(g)
+
+
+@pytest.mark.parametrize("K,G", [(256, 32), (8192, 128), (1000, 128), (5, 2), (7, 3), (28672, 128)])
+def test_alg1_closed_form(K, G):
+    """g_idx_optimized[i] = floor(i/G): Eq. 3 is a permutation of Eq. 1's multiset
+    (SPEC.md:L103), so sorting it gives Eq. 1 back ("consecutive")."""
+    phi = np.random.default_rng(K + G).permutation(K)
+    g = O.eq3_g_idx_actorder(phi, G)
+    P, g_opt = O.alg1_reorder(g)
+    assert g_opt.tolist() == [i // G for i in range(K)]
+    assert sorted(P.tolist()) == list(range(K))
+    # within a group the original indices stay ascending (stability, reading c6)
+    for gg in range(-(-K // G)):
+        members = P[g_opt == gg]
+        assert np.all(np.diff(members) > 0)
+
+
+def test_alg1_stable_differs_from_argsort_phi():
+    """Reading c6: argsort(phi) also orders the groups but is a different P."""
+    K, G = 64, 8
+    phi = np.random.default_rng(0).permutation(K)
+    g = O.eq3_g_idx_actorder(phi, G)
+    P, _ = O.alg1_reorder(g)
+    assert P.tolist() != np.argsort(phi).tolist()
+    assert (g[np.argsort(phi)] == np.arange(K) // G).all()
+
+
+def test_multiset_law_and_load_floor():
+    """SPEC.md:L103/L105 and acceptance L459: ordered = ceil(K/G) loads; random phi
+    with K >= 64, G <= K/8 needs >= 2x that, over 20 seeds."""
+    for seed in range(20):
+        rng = np.random.default_rng(seed)
+        K = int(rng.integers(64, 2048))
+        G = int(rng.integers(1, K // 8 + 1))
+        phi = rng.permutation(K)
+        g = O.eq3_g_idx_actorder(phi, G)
+        assert sorted(g.tolist()) == O.eq1_g_idx_naive(K, G).tolist()
+        ng = -(-K // G)
+        _, g_opt = O.alg1_reorder(g)
+        assert O.metadata_loads(g_opt) == ng
+        assert O.metadata_loads(g) >= 2 * ng
+    # Llama-70B K1 (SURVEY.md §8(c) locality pin: unordered 8058 vs ordered 64 at seed 0)
+    g = O.eq3_g_idx_actorder(np.random.default_rng(0).permutation(8192), 128)
+    assert O.metadata_loads(O.alg1_reorder(g)[1]) == 64
+    assert O.metadata_loads(g) > 8000
+
+
+def test_synth_gidx_is_eq3():
+    p = synth.make_problem(256, 512, 256, 32, 1, seed=5)
+    assert p.w1.g_idx.tolist() == O.eq3_g_idx_actorder(p.w1.phi, 32).tolist()
+    assert p.w2.g_idx.tolist() == O.eq3_g_idx_actorder(p.w2.phi, 32).tolist()
+
+
+# ----------------------------------------------------------------------------- packing / dequant
+def test_unpack_golden_words():
+    c = PACK["qweight_column"]
+    q = O.unpack_qweight(np.array([[c["word"]]], dtype=np.uint32), 8)
+    assert q[:, 0].tolist() == c["q_rows"]
+    c = PACK["qweight_column2"]
+    q = O.unpack_qweight(np.array([[c["word"]]], dtype=np.uint32), 8)
+    assert q[:, 0].tolist() == c["q_rows"]
+    c = PACK["qzeros_row"]
+    z = O.unpack_qzeros(np.array([[c["word"]]], dtype=np.uint32), 8)
+    assert z[0].tolist() == c["z_cols"]
+
+
+def test_unpack_roundtrip_synth_packer():
+    p = synth.make_problem(64, 128, 48, 16, 2, seed=9)
+    assert (O.unpack_qweight(p.w1.qweight, 64) == p.w1.q).all()
+    assert (O.unpack_qzeros(p.w1.qzeros, 128) == p.w1.z).all()
+
+
+def _hand_layer(d):
+    g = O.eq3_g_idx_actorder(d["phi"], d["G"])
+    return O.OLayer(q=np.array(d["q"], dtype=np.int64), s=np.array(d["s"], dtype=np.float64),
+                    z=np.array(d["z"], dtype=np.int64), g=g, G=d["G"])
+
+
+def test_dequant_hand_example():
+    L1, L2 = _hand_layer(HAND["layer1"]), _hand_layer(HAND["layer2"])
+    assert L1.g.tolist() == HAND["g1"] and L2.g.tolist() == HAND["g2"]
+    assert O.dequantize(L1).tolist() == HAND["W1"]
+    assert O.dequantize(L2).tolist() == HAND["W2"]
+
+
+def test_dequant_vs_scalar_loop():
+    """Vectorised fancy-indexed dequant vs a scalar loop of the definition."""
+    rng = np.random.default_rng(7)
+    K, N, G = 24, 5, 8
+    g = O.eq3_g_idx_actorder(rng.permutation(K), G)
+    q = rng.integers(0, 16, (K, N))
+    z = rng.integers(0, 16, (K // G, N))
+    s = rng.uniform(0.1, 2, (K // G, N))
+    W = O.dequantize(O.OLayer(q=q, s=s, z=z, g=g, G=G))
+    for k in range(K):
+        for n in range(N):
+            assert W[k, n] == s[g[k]][n] * (float(q[k][n]) - float(z[g[k]][n]))
+
+
+def test_dequant_G_equals_K_per_column():
+    """G = K: one group, g == 0 and P = identity for any phi; dequant reduces to the
+    per-column s[0,n]*(q-z[0,n]) (north_star pin)."""
+    rng = np.random.default_rng(11)
+    K, N = 32, 16
+    phi = rng.permutation(K)
+    g = O.eq3_g_idx_actorder(phi, K)
+    assert (g == 0).all()
+    P, _ = O.alg1_reorder(g)
+    assert P.tolist() == list(range(K))
+    q = rng.integers(0, 16, (K, N))
+    z = rng.integers(0, 16, (1, N))
+    s = rng.uniform(0.1, 2, (1, N))
+    W = O.dequantize(O.OLayer(q=q, s=s, z=z, g=g, G=K))
+    for n in range(N):
+        col = [s[0][n] * (q[k][n] - z[0][n]) for k in range(K)]
+        assert W[:, n].tolist() == col
+
+
+# ----------------------------------------------------------------------------- MLP / Alg. 2 / Alg. 3
+def test_hand_mlp_dense_and_tp():
+    L1, L2 = _hand_layer(HAND["layer1"]), _hand_layer(HAND["layer2"])
+    X = np.array(HAND["X"])
+    Y1, Y2 = O.dense_mlp(X, O.dequantize(L1), O.dequantize(L2))
+    assert Y1.tolist() == HAND["Y1"] and Y2.tolist() == HAND["Y2"]
+    for tp in (1, 2):
+        a3 = O.alg3_tp_aware(X, L1, L2, tp)
+        a2 = O.alg2_naive(X, L1, L2, tp)
+        assert a3["Y2"].tolist() == HAND["Y2"]
+        assert a2["Y2"].tolist() == HAND["Y2"]
+        assert a3["P1"].tolist() == HAND["P1"] and a3["P2"].tolist() == HAND["P2"]
+    a3 = O.alg3_tp_aware(X, L1, L2, 2)
+    assert [y.tolist() for y in a3["Y1_local"]] == HAND["tp2_tp_aware_Y1_local"]
+    assert [y.tolist() for y in a3["Y2_local"]] == HAND["tp2_tp_aware_Y2_local"]
+    a2 = O.alg2_naive(X, L1, L2, 2)
+    assert [y.tolist() for y in a2["Y1_local"]] == HAND["tp2_naive_Y1_local"]
+    assert [y.tolist() for y in a2["Y1_chunk"]] == HAND["tp2_naive_Y1_chunk"]
+
+
+def _olayers(p):
+    return (O.layer_from_checkpoint(p.w1.qweight, p.w1.scales_bits, p.w1.qzeros, p.w1.g_idx,
+                                    p.K1, p.N1, p.G),
+            O.layer_from_checkpoint(p.w2.qweight, p.w2.scales_bits, p.w2.qzeros, p.w2.g_idx,
+                                    p.N1, p.N2, p.G))
+
+
+def _bruteforce_mlp(X, L1, L2):
+    """Triple loops of the definition in pure Python (tiny sizes only)."""
+    M, K1 = X.shape
+    N1, N2 = L1.N, L2.N
+    W1 = [[L1.s[L1.g[k]][n] * (int(L1.q[k][n]) - int(L1.z[L1.g[k]][n])) for n in range(N1)] for k in range(K1)]
+    W2 = [[L2.s[L2.g[k]][n] * (int(L2.q[k][n]) - int(L2.z[L2.g[k]][n])) for n in range(N2)] for k in range(N1)]
+    Y1 = [[sum(float(X[m][k]) * W1[k][n] for k in range(K1)) for n in range(N1)] for m in range(M)]
+    Y2 = [[sum(Y1[m][k] * W2[k][n] for k in range(N1)) for n in range(N2)] for m in range(M)]
+    return np.array(Y1), np.array(Y2)
+
+
+def test_integer_regime_bit_exact_all_tp():
+    """Integer-exact regime (X in -2..2, q,z in 0..15, s = 2^-e): every product/partial sum
+    is an exact dyadic rational in fp64, so naive (Alg. 2) = TP-aware (Alg. 3) = dense
+    (unordered act_order dequant) = brute force, BIT-EXACTLY, at tp = 1/2/4/8
+    (SPEC.md:L330 equivalence theorem; north_star 'reordered equals unreordered,
+    TP=k equals TP=1').  Non-square K1 != N1 != N2 catches transposed operands."""
+    p = synth.make_problem(64, 128, 48, 16, 3, seed=4, integer_regime=True)
+    L1, L2 = _olayers(p)
+    X = p.X.astype(np.float64)
+    Y1d, Y2d = O.dense_mlp(X, O.dequantize(L1), O.dequantize(L2))
+    Y1b, Y2b = _bruteforce_mlp(X, L1, L2)
+    assert (Y1d == Y1b).all() and (Y2d == Y2b).all()
+    for tp in (1, 2, 4, 8):
+        a2 = O.alg2_naive(X, L1, L2, tp)
+        a3 = O.alg3_tp_aware(X, L1, L2, tp)
+        assert (a2["Y2"] == Y2d).all(), tp
+        assert (a3["Y2"] == Y2d).all(), tp
+        n = p.N1 // tp
+        # Alg. 3 rank r's Y1 is Y1 restricted to the P2 columns of its shard
+        for r in range(tp):
+            assert (a3["Y1_local"][r] == Y1d[:, a3["P2"][r * n:(r + 1) * n]]).all()
+            assert (a2["Y1_local"][r] == Y1d[:, r * n:(r + 1) * n]).all()
+            assert (a2["Y1_chunk"][r] == a3["Y1_local"][r]).all()
+
+
+def test_float_regime_tp_invariance():
+    p = synth.make_problem(128, 256, 96, 32, 5, seed=2)
+    L1, L2 = _olayers(p)
+    X = p.X.astype(np.float64)
+    _, Y2d = O.dense_mlp(X, O.dequantize(L1), O.dequantize(L2))
+    for tp in (1, 2, 4, 8):
+        for f in (O.alg2_naive, O.alg3_tp_aware):
+            Y2 = f(X, L1, L2, tp)["Y2"]
+            assert np.max(np.abs(Y2 - Y2d)) <= 1e-12 * np.max(np.abs(Y2d))
+
+
+def test_tp_aware_w1_is_column_permuted_naive():
+    """dequant(W1[P1,P2]) = permute_cols(dequant(W1[P1]), P2)."""
+    p = synth.make_problem(64, 128, 48, 16, 1, seed=6)
+    L1, L2 = _olayers(p)
+    P1, _ = O.alg1_reorder(L1.g)
+    P2, _ = O.alg1_reorder(L2.g)
+    Wn = O.dequantize(O.permute_rows(L1, P1))
+    Wa = O.dequantize(O.permute_cols(O.permute_rows(L1, P1), P2))
+    assert (Wa == Wn[:, P2]).all()
+    # and reordering rows is exact: W[P1] dequantized with the ordered g equals rows of W
+    assert (Wn == O.dequantize(L1)[P1]).all()
+
+
+def test_identity_phi_variants_identical():
+    """identity phi => P1 = P2 = identity and both variants hold the same bytes."""
+    p = synth.make_problem(64, 128, 64, 16, 1, seed=8, identity_phi=True)
+    L1, L2 = _olayers(p)
+    for tp in (1, 2, 4):
+        for r in range(tp):
+            a = O.canonical_shard(L1, L2, tp, r, "tp_aware")
+            b = O.canonical_shard(L1, L2, tp, r, "naive")
+            assert a["P1"].tolist() == list(range(64)) and a["P2"].tolist() == list(range(128))
+            for key in ("w1_q", "w1_s", "w1_z", "w2_q"):
+                assert (a[key] == b[key]).all()
+
+
+def test_shard_maps_cover_and_groups():
+    p = synth.make_problem(64, 256, 64, 16, 1, seed=10)
+    L1, L2 = _olayers(p)
+    P2, g2_opt = O.alg1_reorder(L2.g)
+    for tp in (1, 2, 4, 8):
+        n = 256 // tp
+        cols = np.concatenate([O.shard_maps(P2, 256, tp, r, "tp_aware", 16)["w1_cols"] for r in range(tp)])
+        assert cols.tolist() == P2.tolist()
+        for r in range(tp):
+            mp = O.shard_maps(P2, 256, tp, r, "tp_aware", 16)
+            # W2 shard owns whole ordered groups [r n/G, (r+1) n/G)
+            gs = g2_opt[r * n:(r + 1) * n]
+            assert gs.min() == mp["w2_group_lo"] and gs.max() == mp["w2_group_hi"] - 1
+            src = mp["gather_src"]
+            assert (src[:, 0] * n + src[:, 1] == P2[r * n:(r + 1) * n]).all()
+
+
+def test_naive_gather_map_matches_alg2():
+    p = synth.make_problem(64, 128, 48, 16, 2, seed=12)
+    L1, L2 = _olayers(p)
+    X = p.X.astype(np.float64)
+    for tp in (2, 4):
+        a2 = O.alg2_naive(X, L1, L2, tp)
+        buf = np.stack(a2["Y1_local"])  # [tp][M][n]  (NCCL AllGather layout, reading c17)
+        for r in range(tp):
+            src = O.shard_maps(a2["P2"], 128, tp, r, "naive", 16)["gather_src"]
+            y1in = buf[src[:, 0], :, src[:, 1]].T
+            assert (y1in == a2["Y1_chunk"][r]).all()
+
+
+def test_check_rows_close():
+    ref = np.array([[1.0, -2.0, 0.0], [0.0, 0.0, 0.0]])
+    ok, w = O.check_rows_close(ref + [[0.019, 0, 0], [0, 0, 0]], ref)
+    assert ok and abs(w - 0.0095) < 1e-12
+    ok, _ = O.check_rows_close(ref + [[0.021, 0, 0], [0, 0, 0]], ref)
+    assert not ok
+    ok, _ = O.check_rows_close(ref + [[0, 0, 0], [0, 1e-30, 0]], ref)
+    assert not ok
