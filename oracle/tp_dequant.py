@@ -23,6 +23,7 @@ __all__ = [
     "unpack_qweight", "unpack_qzeros", "fp16_bits_to_f64", "OLayer", "layer_from_checkpoint",
     "dequantize", "metadata_loads", "dense_mlp", "permute_rows", "permute_cols",
     "alg2_naive", "alg3_tp_aware", "shard_maps", "canonical_shard", "check_rows_close",
+    "dense_mlp_columns",
 ]
 
 
@@ -150,6 +151,22 @@ def dense_mlp(X, W1, W2):
     Y1 = X @ W1
     Y2 = Y1 @ W2
     return Y1, Y2
+
+
+def dense_mlp_columns(X, L1: OLayer, L2: OLayer, cols2=None, chunk: int = 2048):
+    """The same definition as ``dense_mlp(X, dequantize(L1), dequantize(L2))`` evaluated one
+    block of output columns at a time so full-size shapes fit in host memory: column j of
+    Y1 is X . W1[:, j] (column blocks of W1 dequantized independently), and only the
+    requested columns ``cols2`` of Y2 = Y1 . W2[:, cols2] are produced (sampled outputs).
+    Returns (Y1 [M][N1], Y2 [M][len(cols2)])."""
+    X = np.asarray(X, dtype=np.float64)
+    Y1 = np.empty((X.shape[0], L1.N))
+    for lo in range(0, L1.N, chunk):
+        hi = min(L1.N, lo + chunk)
+        Y1[:, lo:hi] = X @ dequantize(_col_block(L1, lo, hi))
+    cols2 = np.arange(L2.N) if cols2 is None else np.asarray(cols2, dtype=np.int64)
+    L2c = OLayer(q=L2.q[:, cols2], s=L2.s[:, cols2], z=L2.z[:, cols2], g=L2.g, G=L2.G)
+    return Y1, Y1 @ dequantize(L2c)
 
 
 # ----------------------------------------------------------------------------- M[P1, P2]

@@ -1,0 +1,582 @@
+// Host half of libtpq: the C-ABI of include/tpq.h.
+//   * gptq_reorder      -- Alg. 1 as a stable counting sort.
+//   * tp_shard_mlp      -- offline TP-aware transform (Alg. 3 Require L137),
+//                          Megatron column/row split, repack into the device
+//                          fragment-native layout (csrc/internal.h), H2D upload, stream-K plan.
+//   * tp_mlp_forward*   -- enqueue the per-rank kernels (tpq_kernels.cu) and the NCCL
+//                          collectives (AllReduce PAPER.md:L142; AllGather L117 for Alg. 2).
+#include "tpq.h"
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "internal.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define TPQ_CUDA(call)                                                                  \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess) return fail(TPQ_ECUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+  } while (0)
+
+#define TPQ_NCCL(call)                                                                   \
+  do {                                                                                   \
+    ncclResult_t r_ = (call);                                                            \
+    if (r_ != ncclSuccess) return fail(TPQ_ENCCL, "%s: %s", #call, ncclGetErrorString(r_)); \
+  } while (0)
+
+template <class F>
+void parallel_for(int64_t n, F f) {
+  unsigned nt = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  if (n < 4096 || nt == 1) {
+    for (int64_t i = 0; i < n; ++i) f(i);
+    return;
+  }
+  std::vector<std::thread> th;
+  for (unsigned t = 0; t < nt; ++t)
+    th.emplace_back([=, &f] {
+      for (int64_t i = (int64_t)t * n / nt; i < (int64_t)(t + 1) * n / nt; ++i) f(i);
+    });
+  for (auto& x : th) x.join();
+}
+
+// Canonical (unpacked, reordered) shard of one layer: q[K][N] codes, s[ng][N] fp16 bits,
+// z[ng][N] codes.
+struct Canon {
+  int64_t K = 0, N = 0;
+  int G = 0;
+  std::vector<uint8_t> q, z;
+  std::vector<uint16_t> s;
+};
+
+// Pack a canonical shard into the device layout of internal.h.
+std::vector<uint8_t> pack_layer(const Canon& c) {
+  const int G = c.G, S = G / 16, CW = S >= 4 ? 4 : S;
+  const int64_t NB = c.N / tpq::kBlockCols, NG = c.K / G, UB = tpq::unit_bytes(G);
+  std::vector<uint8_t> out((size_t)(NB * NG * UB), 0);
+  parallel_for(NB * NG, [&](int64_t u) {
+    const int64_t b = u / NG, g = u % NG;
+    uint8_t* rec = out.data() + u * UB;
+    uint32_t* words = reinterpret_cast<uint32_t*>(rec);
+    auto Q = [&](int64_t k, int64_t n) -> uint32_t { return c.q[(size_t)(k * c.N + n)]; };
+    for (int t = 0; t < 4; ++t)
+      for (int lane = 0; lane < 32; ++lane)
+        for (int s = 0; s < S; ++s) {
+          const int64_t r0 = b * 64 + 16 * t + lane / 4, r1 = r0 + 8;
+          const int64_t k0 = g * G + 16 * s + 2 * (lane % 4);
+          const uint32_t w = Q(k0, r0) | Q(k0, r1) << 4 | Q(k0 + 8, r0) << 8 | Q(k0 + 8, r1) << 12 |
+                             Q(k0 + 1, r0) << 16 | Q(k0 + 1, r1) << 20 | Q(k0 + 9, r0) << 24 |
+                             Q(k0 + 9, r1) << 28;
+          const int cidx = s / CW;
+          words[((cidx * 4 + t) * 32 + lane) * CW + (s % CW)] = w;
+        }
+    uint8_t* meta = rec + 32LL * G;
+    for (int rr = 0; rr < 8; ++rr)
+      for (int t = 0; t < 4; ++t) {
+        const int64_t r0 = b * 64 + 16 * t + rr, r1 = r0 + 8;
+        const uint16_t s0 = c.s[(size_t)(g * c.N + r0)], s1 = c.s[(size_t)(g * c.N + r1)];
+        memcpy(meta + (rr * 4 + t) * 4, &s0, 2);
+        memcpy(meta + (rr * 4 + t) * 4 + 2, &s1, 2);
+        meta[128 + rr * 4 + t] = (uint8_t)(c.z[(size_t)(g * c.N + r0)] | (c.z[(size_t)(g * c.N + r1)] << 4));
+      }
+  });
+  return out;
+}
+
+// Inverse of pack_layer (test export).
+void unpack_layer(const std::vector<uint8_t>& pk, int64_t K, int64_t N, int G, uint8_t* q, uint16_t* s,
+                  uint8_t* z) {
+  const int S = G / 16, CW = S >= 4 ? 4 : S;
+  const int64_t NB = N / tpq::kBlockCols, NG = K / G, UB = tpq::unit_bytes(G);
+  parallel_for(NB * NG, [&](int64_t u) {
+    const int64_t b = u / NG, g = u % NG;
+    const uint8_t* rec = pk.data() + u * UB;
+    const uint32_t* words = reinterpret_cast<const uint32_t*>(rec);
+    for (int t = 0; t < 4; ++t)
+      for (int lane = 0; lane < 32; ++lane)
+        for (int st = 0; st < S; ++st) {
+          const uint32_t w = words[((st / CW * 4 + t) * 32 + lane) * CW + (st % CW)];
+          const int64_t r0 = b * 64 + 16 * t + lane / 4, r1 = r0 + 8;
+          const int64_t k0 = g * G + 16 * st + 2 * (lane % 4);
+          const int64_t ks[8] = {k0, k0, k0 + 8, k0 + 8, k0 + 1, k0 + 1, k0 + 9, k0 + 9};
+          const int64_t ns[8] = {r0, r1, r0, r1, r0, r1, r0, r1};
+          for (int i = 0; i < 8; ++i) q[ks[i] * N + ns[i]] = (w >> (4 * i)) & 0xF;
+        }
+    const uint8_t* meta = rec + 32LL * G;
+    for (int rr = 0; rr < 8; ++rr)
+      for (int t = 0; t < 4; ++t) {
+        const int64_t r0 = b * 64 + 16 * t + rr, r1 = r0 + 8;
+        memcpy(&s[g * N + r0], meta + (rr * 4 + t) * 4, 2);
+        memcpy(&s[g * N + r1], meta + (rr * 4 + t) * 4 + 2, 2);
+        z[g * N + r0] = meta[128 + rr * 4 + t] & 0xF;
+        z[g * N + r1] = meta[128 + rr * 4 + t] >> 4;
+      }
+  });
+}
+
+inline uint32_t nib(uint32_t w, int i) { return (w >> (4 * i)) & 0xFu; }
+
+}  // namespace
+
+struct tpq_mlp {
+  int64_t K1 = 0, N1 = 0, N2 = 0, n = 0, M_max = 0;
+  int G1 = 0, G2 = 0, tp = 1, rank = 0, variant = 1, device = -1;
+  std::vector<int32_t> P1, P2, w1_cols, w2_rows, gather_cols;
+  int32_t w2_group_lo = 0, w2_group_hi = 0;
+  std::vector<uint8_t> pk1, pk2;  // packed host copies
+  tpq::LayerDev L1, L2;
+  // device buffers
+  void* d_w1 = nullptr;
+  void* d_w2 = nullptr;
+  int32_t* d_P1 = nullptr;
+  int32_t* d_gcols = nullptr;  // naive: P2[r n .. (r+1) n)
+  void* d_xf1 = nullptr;       // frag X[:, P1], 16 rows
+  void* d_xf2 = nullptr;       // frag Y1, 16 rows
+  void* d_y1 = nullptr;        // row-major Y1 scratch [16][n] (naive send slot lives in d_buf)
+  void* d_buf = nullptr;       // AllGather buffer [tp][16][n]
+  void* d_xin = nullptr;       // host-forward staging [M_max][K1]
+  void* d_yout = nullptr;      // host-forward staging [M_max][N2]
+  float* d_ws = nullptr;
+  int* d_cnt = nullptr;
+  ncclComm_t comm = nullptr;
+};
+
+namespace {
+
+int validate_layer(const gptq_layer* w, const char* name) {
+  if (!w) return fail(TPQ_EINVAL, "%s is NULL", name);
+  if (!w->qweight || !w->scales || !w->qzeros || !w->g_idx)
+    return fail(TPQ_EINVAL, "%s: NULL array", name);
+  if (w->bits != 4) return fail(TPQ_EUNSUPPORTED, "%s: bits=%d (only 4 supported)", name, w->bits);
+  if (w->K < 8 || w->N < 8 || w->K % 8 || w->N % 8)
+    return fail(TPQ_EINVAL, "%s: K=%lld N=%lld must be positive multiples of 8 (GPTQ packing)", name,
+                (long long)w->K, (long long)w->N);
+  if (w->G < 1) return fail(TPQ_EINVAL, "%s: G=%d", name, w->G);
+  return TPQ_OK;
+}
+
+int validate_perm(const int32_t* P, const gptq_layer* w, const char* name) {
+  if (!P) return fail(TPQ_EINVAL, "%s is NULL", name);
+  std::vector<uint8_t> seen((size_t)w->K, 0);
+  for (int64_t i = 0; i < w->K; ++i) {
+    const int32_t p = P[i];
+    if (p < 0 || p >= w->K || seen[p]) return fail(TPQ_EINVAL, "%s is not a permutation (index %lld)", name, (long long)i);
+    seen[p] = 1;
+    if (w->g_idx[p] != (int32_t)(i / w->G))
+      return fail(TPQ_EINVAL,
+                  "%s does not order g_idx: g_idx[P[%lld]] = %d != floor(i/G) = %lld (use gptq_reorder, Alg. 1)",
+                  name, (long long)i, w->g_idx[p], (long long)(i / w->G));
+  }
+  return TPQ_OK;
+}
+
+void free_dev(tpq_mlp* h) {
+  if (h->device < 0) return;
+  cudaSetDevice(h->device);
+  void* ptrs[] = {h->d_w1, h->d_w2, h->d_P1, h->d_gcols, h->d_xf1, h->d_xf2, h->d_y1,
+                  h->d_buf, h->d_xin, h->d_yout, h->d_ws, h->d_cnt};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+}
+
+int dev_alloc(void** p, size_t bytes) {
+  cudaError_t e = cudaMalloc(p, bytes ? bytes : 16);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(e == cudaErrorMemoryAllocation ? TPQ_ENOMEM : TPQ_ECUDA, "cudaMalloc(%zu): %s", bytes,
+                cudaGetErrorString(e));
+  }
+  return TPQ_OK;
+}
+
+void plan_layer(tpq::LayerDev& L, int64_t K, int64_t N, int G, int device) {
+  L.K = K;
+  L.N = N;
+  L.G = G;
+  L.NB = (int)(N / tpq::kBlockCols);
+  L.NG = (int)(K / G);
+  L.U = (int64_t)L.NB * L.NG;
+  int sms = 148;
+  if (device >= 0) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  for (int MT = 1; MT <= tpq::kMaxMT; ++MT) {
+    int bps = device >= 0 ? tpq::gemv_blocks_per_sm(G, MT) : 1;
+    if (bps < 1) bps = 1;
+    int64_t grid = (int64_t)sms * bps;
+    const int64_t cap = std::max<int64_t>(1, L.U / 8);  // >= 8 units (one per warp) per CTA
+    grid = std::min(grid, cap);
+    L.grid[MT] = (int)grid;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* tpq_last_error(void) { return g_err.c_str(); }
+int tpq_version(void) { return (1 << 16) | 0; }
+
+int gptq_reorder(const int32_t* g_idx, int64_t K, int32_t G, int32_t* perm_out, int32_t* g_idx_sorted_out) {
+  try {
+    if (!g_idx || !perm_out) return fail(TPQ_EINVAL, "gptq_reorder: NULL pointer");
+    if (K < 1 || G < 1) return fail(TPQ_EINVAL, "gptq_reorder: K=%lld G=%d must be >= 1", (long long)K, G);
+    if (K > INT32_MAX) return fail(TPQ_EINVAL, "gptq_reorder: K too large");
+    const int64_t ng = (K + G - 1) / G;
+    std::vector<int64_t> cnt((size_t)ng + 1, 0);
+    for (int64_t i = 0; i < K; ++i) {
+      const int32_t g = g_idx[i];
+      if (g < 0 || g >= ng)
+        return fail(TPQ_EINVAL, "gptq_reorder: g_idx[%lld]=%d outside [0,%lld)", (long long)i, g, (long long)ng);
+      cnt[(size_t)g + 1]++;
+    }
+    for (int64_t g = 0; g < ng; ++g) {
+      const int64_t want = std::min<int64_t>(G, K - g * G);
+      if (cnt[(size_t)g + 1] != want)
+        return fail(TPQ_EINVAL, "gptq_reorder: group %lld has %lld rows, Eq. 3 requires %lld", (long long)g,
+                    (long long)cnt[(size_t)g + 1], (long long)want);
+    }
+    for (int64_t g = 0; g < ng; ++g) cnt[(size_t)g + 1] += cnt[(size_t)g];
+    // stable counting sort: visiting i in ascending order keeps ties in original order (c6)
+    for (int64_t i = 0; i < K; ++i) perm_out[cnt[(size_t)g_idx[i]]++] = (int32_t)i;
+    if (g_idx_sorted_out)
+      for (int64_t i = 0; i < K; ++i) g_idx_sorted_out[i] = g_idx[perm_out[i]];
+    return TPQ_OK;
+  } catch (const std::bad_alloc&) {
+    return fail(TPQ_ENOMEM, "gptq_reorder: out of host memory");
+  } catch (...) {
+    return fail(TPQ_EINVAL, "gptq_reorder: unexpected exception");
+  }
+}
+
+int tp_shard_mlp(const gptq_layer* w1, const gptq_layer* w2, const int32_t* P1, const int32_t* P2, int tp, int rank,
+                 int variant, int64_t M_max, int device, tpq_mlp** out) {
+  if (!out) return fail(TPQ_EINVAL, "tp_shard_mlp: out is NULL");
+  *out = nullptr;
+  int rc;
+  if ((rc = validate_layer(w1, "w1"))) return rc;
+  if ((rc = validate_layer(w2, "w2"))) return rc;
+  if (w1->N != w2->K)
+    return fail(TPQ_EINVAL, "w1->N=%lld != w2->K=%lld", (long long)w1->N, (long long)w2->K);
+  if (tp != 1 && tp != 2 && tp != 4 && tp != 8) return fail(TPQ_EINVAL, "tp=%d not in {1,2,4,8}", tp);
+  if (rank < 0 || rank >= tp) return fail(TPQ_EINVAL, "rank=%d not in [0,%d)", rank, tp);
+  if (variant != TPQ_NAIVE && variant != TPQ_TP_AWARE) return fail(TPQ_EINVAL, "variant=%d", variant);
+  if (M_max < 1 || M_max > 512) return fail(TPQ_EINVAL, "M_max=%lld not in [1,512]", (long long)M_max);
+  if (device < -1) return fail(TPQ_EINVAL, "device=%d", device);
+  const int64_t K1 = w1->K, N1 = w1->N, N2 = w2->N;
+  if (N1 % tp) return fail(TPQ_EINVAL, "N1=%lld not divisible by tp=%d (CHUNK)", (long long)N1, tp);
+  const int64_t n = N1 / tp;
+  for (int G : {w1->G, w2->G})
+    if (G != 32 && G != 64 && G != 128) return fail(TPQ_EUNSUPPORTED, "G=%d not in {32,64,128}", G);
+  if (K1 % w1->G) return fail(TPQ_EUNSUPPORTED, "K1=%lld not a multiple of G1=%d (ragged group, c13)", (long long)K1, w1->G);
+  if (n % tpq::kBlockCols || N2 % tpq::kBlockCols)
+    return fail(TPQ_EINVAL, "n=N1/tp=%lld and N2=%lld must be multiples of 64", (long long)n, (long long)N2);
+  if (n % w2->G) return fail(TPQ_EINVAL, "n=%lld not a multiple of G2=%d: W2 shard would split a group (c12)", (long long)n, w2->G);
+  if ((rc = validate_perm(P1, w1, "P1"))) return rc;
+  if ((rc = validate_perm(P2, w2, "P2"))) return rc;
+
+  tpq_mlp* h = nullptr;
+  try {
+    h = new tpq_mlp();
+    h->K1 = K1; h->N1 = N1; h->N2 = N2; h->n = n; h->M_max = M_max;
+    h->G1 = w1->G; h->G2 = w2->G; h->tp = tp; h->rank = rank; h->variant = variant; h->device = device;
+    h->P1.assign(P1, P1 + K1);
+    h->P2.assign(P2, P2 + N1);
+    h->w1_cols.resize(n);
+    h->w2_rows.resize(n);
+    for (int64_t j = 0; j < n; ++j) {
+      h->w1_cols[j] = variant == TPQ_TP_AWARE ? P2[rank * n + j] : (int32_t)(rank * n + j);  // W1[P1,P2] vs W1[P1]
+      h->w2_rows[j] = P2[rank * n + j];                                                         // W2[P2] row block r
+    }
+    h->gather_cols.assign(P2 + rank * n, P2 + (rank + 1) * n);
+    h->w2_group_lo = (int32_t)(rank * n / w2->G);
+    h->w2_group_hi = (int32_t)((rank + 1) * n / w2->G);
+
+    // ---- canonical shards ----
+    Canon c1, c2;
+    c1.K = K1; c1.N = n; c1.G = w1->G;
+    c1.q.resize((size_t)(K1 * n));
+    parallel_for(K1, [&](int64_t k) {  // row k of W1[P1] = original row P1[k]
+      const int32_t src = P1[k];
+      const uint32_t* row = w1->qweight + (size_t)(src / 8) * N1;
+      for (int64_t j = 0; j < n; ++j) c1.q[(size_t)(k * n + j)] = (uint8_t)nib(row[h->w1_cols[j]], src % 8);
+    });
+    const int64_t ng1 = K1 / w1->G;
+    c1.s.resize((size_t)(ng1 * n));
+    c1.z.resize((size_t)(ng1 * n));
+    for (int64_t g = 0; g < ng1; ++g)
+      for (int64_t j = 0; j < n; ++j) {
+        const int32_t col = h->w1_cols[j];
+        c1.s[(size_t)(g * n + j)] = w1->scales[(size_t)(g * N1 + col)];
+        c1.z[(size_t)(g * n + j)] = (uint8_t)nib(w1->qzeros[(size_t)(g * (N1 / 8) + col / 8)], col % 8);
+      }
+    c2.K = n; c2.N = N2; c2.G = w2->G;
+    c2.q.resize((size_t)(n * N2));
+    parallel_for(n, [&](int64_t i) {  // local row i of W2[P2] block r = original row P2[r n + i]
+      const int32_t src = h->w2_rows[i];
+      const uint32_t* row = w2->qweight + (size_t)(src / 8) * N2;
+      for (int64_t j = 0; j < N2; ++j) c2.q[(size_t)(i * N2 + j)] = (uint8_t)nib(row[j], src % 8);
+    });
+    const int64_t ng2 = n / w2->G;
+    c2.s.resize((size_t)(ng2 * N2));
+    c2.z.resize((size_t)(ng2 * N2));
+    for (int64_t lg = 0; lg < ng2; ++lg) {
+      const int64_t g = h->w2_group_lo + lg;
+      for (int64_t j = 0; j < N2; ++j) {
+        c2.s[(size_t)(lg * N2 + j)] = w2->scales[(size_t)(g * N2 + j)];
+        c2.z[(size_t)(lg * N2 + j)] = (uint8_t)nib(w2->qzeros[(size_t)(g * (N2 / 8) + j / 8)], j % 8);
+      }
+    }
+    h->pk1 = pack_layer(c1);
+    h->pk2 = pack_layer(c2);
+    plan_layer(h->L1, K1, n, w1->G, device);
+    plan_layer(h->L2, n, N2, w2->G, device);
+
+    if (device >= 0) {
+      TPQ_CUDA(cudaSetDevice(device));
+      auto A = [&](void** p, size_t b) { return dev_alloc(p, b); };
+      const size_t ws_floats = (size_t)std::max(std::max(h->L1.grid[1], h->L1.grid[2]),
+                                                std::max(h->L2.grid[1], h->L2.grid[2])) * 2 * 16 * 64;
+      if ((rc = A(&h->d_w1, h->pk1.size())) || (rc = A(&h->d_w2, h->pk2.size())) ||
+          (rc = A((void**)&h->d_P1, K1 * 4)) || (rc = A((void**)&h->d_gcols, n * 4)) ||
+          (rc = A(&h->d_xf1, 16 * K1 * 2)) || (rc = A(&h->d_xf2, 16 * n * 2)) ||
+          (rc = A(&h->d_y1, 16 * n * 2)) || (rc = A(&h->d_buf, (size_t)tp * 16 * n * 2)) ||
+          (rc = A(&h->d_xin, (size_t)M_max * K1 * 2)) || (rc = A(&h->d_yout, (size_t)M_max * N2 * 2)) ||
+          (rc = A((void**)&h->d_ws, ws_floats * 2 * 4)) ||
+          (rc = A((void**)&h->d_cnt, (size_t)(h->L1.NB + h->L2.NB) * 4))) {
+        free_dev(h);
+        delete h;
+        return rc;
+      }
+      TPQ_CUDA(cudaMemcpy(h->d_w1, h->pk1.data(), h->pk1.size(), cudaMemcpyHostToDevice));
+      TPQ_CUDA(cudaMemcpy(h->d_w2, h->pk2.data(), h->pk2.size(), cudaMemcpyHostToDevice));
+      TPQ_CUDA(cudaMemcpy(h->d_P1, P1, K1 * 4, cudaMemcpyHostToDevice));
+      TPQ_CUDA(cudaMemcpy(h->d_gcols, h->gather_cols.data(), n * 4, cudaMemcpyHostToDevice));
+      TPQ_CUDA(cudaMemset(h->d_cnt, 0, (size_t)(h->L1.NB + h->L2.NB) * 4));
+      TPQ_CUDA(cudaMemset(h->d_xf1, 0, 16 * K1 * 2));
+      TPQ_CUDA(cudaMemset(h->d_xf2, 0, 16 * n * 2));
+      h->L1.packed = (const uint8_t*)h->d_w1;
+      h->L2.packed = (const uint8_t*)h->d_w2;
+      h->L1.ws = h->d_ws;
+      h->L2.ws = h->d_ws + ws_floats;  // separate partial slots per layer
+      h->L1.cnt = h->d_cnt;
+      h->L2.cnt = h->d_cnt + h->L1.NB;
+      TPQ_CUDA(cudaDeviceSynchronize());
+    }
+    *out = h;
+    return TPQ_OK;
+  } catch (const std::bad_alloc&) {
+    if (h) { free_dev(h); delete h; }
+    return fail(TPQ_ENOMEM, "tp_shard_mlp: out of host memory");
+  } catch (...) {
+    if (h) { free_dev(h); delete h; }
+    return fail(TPQ_EINVAL, "tp_shard_mlp: unexpected exception");
+  }
+}
+
+int tpq_mlp_destroy(tpq_mlp* h) {
+  if (!h) return TPQ_OK;
+  if (h->comm) ncclCommDestroy(h->comm);
+  free_dev(h);
+  delete h;
+  return TPQ_OK;
+}
+
+int tpq_comm_unique_id(uint8_t out[128]) {
+  if (!out) return fail(TPQ_EINVAL, "NULL");
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  ncclUniqueId id;
+  TPQ_NCCL(ncclGetUniqueId(&id));
+  memcpy(out, &id, 128);
+  return TPQ_OK;
+}
+
+int tpq_comm_init(tpq_mlp* h, const uint8_t id[128], int tp, int rank) {
+  if (!h || !id) return fail(TPQ_EINVAL, "NULL");
+  if (h->device < 0) return fail(TPQ_ESTATE, "host-only handle has no device");
+  if (tp != h->tp || rank != h->rank) return fail(TPQ_EINVAL, "tp/rank (%d,%d) != handle's (%d,%d)", tp, rank, h->tp, h->rank);
+  if (h->comm) return fail(TPQ_ESTATE, "comm already initialised");
+  TPQ_CUDA(cudaSetDevice(h->device));
+  ncclUniqueId uid;
+  memcpy(&uid, id, 128);
+  TPQ_NCCL(ncclCommInitRank(&h->comm, tp, uid, rank));
+  return TPQ_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+int check_fwd(tpq_mlp* h, const void* X, int64_t M, const void* Y) {
+  if (!h || !X || !Y) return fail(TPQ_EINVAL, "NULL argument");
+  if (h->device < 0) return fail(TPQ_ESTATE, "host-only handle (device=-1) cannot run the forward");
+  if (M < 1 || M > h->M_max) return fail(TPQ_EINVAL, "M=%lld not in [1, M_max=%lld]", (long long)M, (long long)h->M_max);
+  return TPQ_OK;
+}
+
+// Gather + layer 1 + (naive: AllGather + P2 gather) + layer 2 for one chunk of <= 16 rows.
+// Writes the rank-local partial Y2 (row-major [mc][N2] at Y).  `collective` enables the naive
+// AllGather (tp > 1); otherwise the naive path must be at tp == 1.
+int chunk_forward(tpq_mlp* h, const uint16_t* X, int mc, void* Y, cudaStream_t st, bool collective) {
+  TPQ_CUDA(tpq::launch_to_frag(X, h->K1, h->d_P1, tpq::GATHER_COLS, 0, mc, h->K1, h->d_xf1, st));  // X[:, P1]
+  if (h->variant == TPQ_TP_AWARE) {
+    // Alg. 3 L1: Y1_local lands directly in the layout layer 2 consumes (already in P2 order)
+    TPQ_CUDA(tpq::launch_gemv(h->L1, h->d_xf1, mc, h->d_xf2, tpq::OUT_FRAG, 0, st));
+  } else {
+    // Alg. 2 L1 into this rank's slot of the AllGather buffer [tp][mc][n]
+    uint8_t* slot = (uint8_t*)h->d_buf + (size_t)h->rank * mc * h->n * 2;
+    TPQ_CUDA(tpq::launch_gemv(h->L1, h->d_xf1, mc, slot, tpq::OUT_ROWMAJOR, h->n, st));
+    if (h->tp > 1) {
+      if (!collective) return fail(TPQ_ESTATE, "naive variant with tp > 1 needs the AllGather (use tp_mlp_forward)");
+      TPQ_NCCL(ncclAllGather(slot, h->d_buf, (size_t)mc * h->n, ncclFloat16, h->comm, st));  // Alg. 2 L2
+    }
+    // Alg. 2 L3-4: Y1_global[:, P2] then CHUNK(rank), fused into one gather to the frag layout
+    TPQ_CUDA(tpq::launch_to_frag(h->d_buf, 0, h->d_gcols, tpq::GATHER_ALLGATHER, h->n, mc, h->n, h->d_xf2, st));
+  }
+  TPQ_CUDA(tpq::launch_gemv(h->L2, h->d_xf2, mc, Y, tpq::OUT_ROWMAJOR, h->N2, st));  // L2 GEMM
+  return TPQ_OK;
+}
+
+int forward_impl(tpq_mlp* h, const void* X, int64_t M, void* Y, cudaStream_t st, bool collective) {
+  if (collective && h->tp > 1 && !h->comm) return fail(TPQ_ESTATE, "tp=%d requires tpq_comm_init", h->tp);
+  TPQ_CUDA(cudaSetDevice(h->device));
+  for (int64_t m0 = 0; m0 < M; m0 += 16) {
+    const int mc = (int)std::min<int64_t>(16, M - m0);
+    int rc = chunk_forward(h, (const uint16_t*)X + m0 * h->K1, mc, (uint8_t*)Y + (size_t)m0 * h->N2 * 2, st,
+                           collective);
+    if (rc) return rc;
+  }
+  if (collective && h->tp > 1)  // Alg. 2 L6 / Alg. 3 L3
+    TPQ_NCCL(ncclAllReduce(Y, Y, (size_t)M * h->N2, ncclFloat16, ncclSum, h->comm, st));
+  return TPQ_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int tp_mlp_forward(tpq_mlp* h, const void* X, int64_t M, void* Y, void* stream) {
+  int rc = check_fwd(h, X, M, Y);
+  if (rc) return rc;
+  return forward_impl(h, X, M, Y, (cudaStream_t)stream, true);
+}
+
+int tp_mlp_forward_local(tpq_mlp* h, const void* X, int64_t M, void* Y2_local, void* stream) {
+  int rc = check_fwd(h, X, M, Y2_local);
+  if (rc) return rc;
+  return forward_impl(h, X, M, Y2_local, (cudaStream_t)stream, false);
+}
+
+int tp_mlp_forward_host(tpq_mlp* h, const uint16_t* X_host, int64_t M, uint16_t* Y_host, void* stream) {
+  int rc = check_fwd(h, X_host, M, Y_host);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  TPQ_CUDA(cudaSetDevice(h->device));
+  TPQ_CUDA(cudaMemcpyAsync(h->d_xin, X_host, (size_t)M * h->K1 * 2, cudaMemcpyHostToDevice, st));
+  if ((rc = forward_impl(h, h->d_xin, M, h->d_yout, st, true))) return rc;
+  TPQ_CUDA(cudaMemcpyAsync(Y_host, h->d_yout, (size_t)M * h->N2 * 2, cudaMemcpyDeviceToHost, st));
+  TPQ_CUDA(cudaStreamSynchronize(st));
+  return TPQ_OK;
+}
+
+int tpq_layer1(tpq_mlp* h, const void* X, int64_t M, void* Y1_local, void* stream) {
+  int rc = check_fwd(h, X, M, Y1_local);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  TPQ_CUDA(cudaSetDevice(h->device));
+  for (int64_t m0 = 0; m0 < M; m0 += 16) {
+    const int mc = (int)std::min<int64_t>(16, M - m0);
+    TPQ_CUDA(tpq::launch_to_frag((const uint16_t*)X + m0 * h->K1, h->K1, h->d_P1, tpq::GATHER_COLS, 0, mc, h->K1,
+                                 h->d_xf1, st));
+    TPQ_CUDA(tpq::launch_gemv(h->L1, h->d_xf1, mc, (uint8_t*)Y1_local + (size_t)m0 * h->n * 2, tpq::OUT_ROWMAJOR,
+                              h->n, st));
+  }
+  return TPQ_OK;
+}
+
+int tpq_naive_gather(tpq_mlp* h, const void* buf, int64_t M, void* Y1in, void* stream) {
+  int rc = check_fwd(h, buf, M, Y1in);
+  if (rc) return rc;
+  if (h->variant != TPQ_NAIVE) return fail(TPQ_EINVAL, "tpq_naive_gather needs a TPQ_NAIVE handle");
+  TPQ_CUDA(cudaSetDevice(h->device));
+  TPQ_CUDA(tpq::launch_gather_rowmajor(buf, 0, h->d_gcols, tpq::GATHER_ALLGATHER, h->n, (int)M, h->n, Y1in,
+                                       (cudaStream_t)stream));
+  return TPQ_OK;
+}
+
+int tpq_layer2(tpq_mlp* h, const void* Y1in, int64_t M, void* Y2_local, void* stream) {
+  int rc = check_fwd(h, Y1in, M, Y2_local);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  TPQ_CUDA(cudaSetDevice(h->device));
+  for (int64_t m0 = 0; m0 < M; m0 += 16) {
+    const int mc = (int)std::min<int64_t>(16, M - m0);
+    TPQ_CUDA(tpq::launch_to_frag((const uint16_t*)Y1in + m0 * h->n, h->n, nullptr, tpq::GATHER_COLS, 0, mc, h->n,
+                                 h->d_xf2, st));
+    TPQ_CUDA(tpq::launch_gemv(h->L2, h->d_xf2, mc, (uint8_t*)Y2_local + (size_t)m0 * h->N2 * 2, tpq::OUT_ROWMAJOR,
+                              h->N2, st));
+  }
+  return TPQ_OK;
+}
+
+int tpq_sum_partials(const void* const* parts, int nparts, int64_t count, void* out, void* stream) {
+  if (!parts || !out || nparts < 1 || nparts > 8 || count < 0) return fail(TPQ_EINVAL, "bad arguments");
+  for (int i = 0; i < nparts; ++i)
+    if (!parts[i]) return fail(TPQ_EINVAL, "parts[%d] is NULL", i);
+  if (count == 0) return TPQ_OK;
+  TPQ_CUDA(tpq::launch_sum_partials(parts, nparts, count, out, (cudaStream_t)stream));
+  return TPQ_OK;
+}
+
+int tpq_mlp_info(const tpq_mlp* h, tpq_mlp_info_t* o) {
+  if (!h || !o) return fail(TPQ_EINVAL, "NULL");
+  o->K1 = h->K1; o->N1 = h->N1; o->N2 = h->N2; o->n = h->n; o->M_max = h->M_max;
+  o->G1 = h->G1; o->G2 = h->G2; o->tp = h->tp; o->rank = h->rank; o->variant = h->variant; o->device = h->device;
+  o->w1_bytes = (int64_t)h->pk1.size();
+  o->w2_bytes = (int64_t)h->pk2.size();
+  o->units1 = h->L1.U;
+  o->units2 = h->L2.U;
+  o->grid1 = h->L1.grid[1];
+  o->grid2 = h->L2.grid[1];
+  o->has_comm = h->comm != nullptr;
+  return TPQ_OK;
+}
+
+int tpq_mlp_index_maps(const tpq_mlp* h, int32_t* w1_cols, int32_t* w2_rows, int32_t* lo, int32_t* hi) {
+  if (!h) return fail(TPQ_EINVAL, "NULL handle");
+  if (w1_cols) memcpy(w1_cols, h->w1_cols.data(), h->n * 4);
+  if (w2_rows) memcpy(w2_rows, h->w2_rows.data(), h->n * 4);
+  if (lo) *lo = h->w2_group_lo;
+  if (hi) *hi = h->w2_group_hi;
+  return TPQ_OK;
+}
+
+int tpq_mlp_export_canonical(const tpq_mlp* h, int layer, uint8_t* q, uint16_t* s, uint8_t* z) {
+  if (!h || !q || !s || !z) return fail(TPQ_EINVAL, "NULL");
+  if (layer == 1) unpack_layer(h->pk1, h->K1, h->n, h->G1, q, s, z);
+  else if (layer == 2) unpack_layer(h->pk2, h->n, h->N2, h->G2, q, s, z);
+  else return fail(TPQ_EINVAL, "layer=%d", layer);
+  return TPQ_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,234 @@
+"""GPU parity: the CUDA path (through the C-ABI) vs the fp64 oracle on the same seeded inputs.
+
+Tolerance (reading c14, north_star): per output row m, max_n |err| <= 1e-2 * max_n |Y_oracle|.
+Index plumbing is checked bit-exactly with one-hot probes in the integer regime.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - GPU box only
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2402_04925_b200 as tpq  # noqa: E402
+
+DEV = torch.device("cuda:0")
+TOL = 1e-2
+
+
+def _prep(p):
+    P1, _ = tpq.gptq_reorder(p.w1.g_idx, p.w1.G)
+    P2, _ = tpq.gptq_reorder(p.w2.g_idx, p.w2.G)
+    return P1, P2
+
+
+def _olayers(p):
+    return (O.layer_from_checkpoint(p.w1.qweight, p.w1.scales_bits, p.w1.qzeros, p.w1.g_idx, p.K1, p.N1, p.w1.G),
+            O.layer_from_checkpoint(p.w2.qweight, p.w2.scales_bits, p.w2.qzeros, p.w2.g_idx, p.N1, p.N2, p.w2.G))
+
+
+def _dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+def _empty(*shape):
+    return torch.full(shape, float("nan"), dtype=torch.float16, device=DEV)
+
+
+def _np(t):
+    torch.cuda.synchronize()
+    return t.float().cpu().numpy().astype(np.float64)
+
+
+def _assert_close(y, ref, what):
+    ok, worst = O.check_rows_close(y, ref, TOL)
+    assert ok, f"{what}: worst row error ratio {worst:.3e} > {TOL}"
+    return worst
+
+
+@pytest.mark.parametrize("M", [1, 3, 8, 9, 16])
+def test_tiny_tp_aware_vs_oracle(M):
+    p = synth.make_named("tiny", M, seed=0)
+    P1, P2 = _prep(p)
+    L1, L2 = _olayers(p)
+    ref = O.alg3_tp_aware(p.X, L1, L2, 1)
+    h = tpq.TpMlp(p.w1, p.w2, P1, P2, M_max=16)
+    X = _dev(p.X)
+    Y = _empty(M, p.N2)
+    h.forward(X, M, Y)
+    _assert_close(_np(Y), ref["Y2"], "Y2")
+    Y1 = _empty(M, p.N1)
+    h.layer1(X, M, Y1)
+    _assert_close(_np(Y1), ref["Y1_local"][0], "Y1")
+    h.close()
+
+
+@pytest.mark.parametrize("G", [32, 64, 128])
+@pytest.mark.parametrize("M", [1, 5, 16])
+def test_group_sizes_ragged_tail(G, M):
+    """Several 64-col blocks x groups, N not a multiple of the CTA count (ragged stream-K)."""
+    p = synth.make_problem(1024, 1472, 640, G, M, seed=G + M)
+    P1, P2 = _prep(p)
+    L1, L2 = _olayers(p)
+    Y1r, Y2r = O.dense_mlp(p.X, O.dequantize(L1), O.dequantize(L2))
+    h = tpq.TpMlp(p.w1, p.w2, P1, P2, M_max=16)
+    X = _dev(p.X)
+    Y = _empty(M, p.N2)
+    h.forward(X, M, Y)
+    _assert_close(_np(Y), Y2r, "Y2")
+    h.close()
+
+
+def test_onehot_probes_exact_plumbing():
+    """Integer regime + X = e_k: Y1_local[m, j] = W1[k, w1_cols[j]] exactly representable in
+    fp16, so the device result must equal the oracle bit-for-bit: exposes P1 (row gather),
+    P2 (column permutation) and the packed layout."""
+    p = synth.make_problem(512, 1024, 256, 32, 16, seed=21, integer_regime=True)
+    ks = np.random.default_rng(5).choice(512, size=16, replace=False)
+    X = synth.onehot_x(16, 512, ks)
+    P1, P2 = _prep(p)
+    L1, L2 = _olayers(p)
+    W1 = O.dequantize(L1)
+    for tp in (1, 2, 4):
+        for rank in range(tp):
+            h = tpq.TpMlp(p.w1, p.w2, P1, P2, tp=tp, rank=rank, M_max=16)
+            cols, _, _, _ = h.index_maps()
+            Y1 = _empty(16, 1024 // tp)
+            h.layer1(_dev(X), 16, Y1)
+            assert (_np(Y1) == W1[ks][:, cols]).all()
+            h.close()
+
+
+@pytest.mark.parametrize("tp", [2, 4, 8])
+def test_tp_shards_on_one_gpu_tp_aware(tp):
+    """Every rank's shard on cuda:0; partials summed in rank order (tpq_sum_partials): equals
+    the oracle's Alg. 3 (and its per-rank Y1_local)."""
+    M = 4
+    p = synth.make_problem(512, 2048, 512, 128, M, seed=tp)
+    P1, P2 = _prep(p)
+    L1, L2 = _olayers(p)
+    ref = O.alg3_tp_aware(p.X, L1, L2, tp)
+    X = _dev(p.X)
+    parts = []
+    for r in range(tp):
+        h = tpq.TpMlp(p.w1, p.w2, P1, P2, tp=tp, rank=r, M_max=16)
+        y2 = _empty(M, p.N2)
+        h.forward_local(X, M, y2)
+        y1 = _empty(M, p.N1 // tp)
+        h.layer1(X, M, y1)
+        _assert_close(_np(y1), ref["Y1_local"][r], f"Y1 rank {r}")
+        _assert_close(_np(y2), ref["Y2_local"][r], f"Y2_local rank {r}")
+        parts.append(y2)
+        h.close()
+    Y = _empty(M, p.N2)
+    tpq.sum_partials(parts, Y)
+    _assert_close(_np(Y), ref["Y2"], "Y2")
+
+
+@pytest.mark.parametrize("tp", [1, 2, 4])
+def test_naive_variant_staged(tp):
+    """Alg. 2 step by step: layer1 per rank -> AllGather buffer [tp][M][n] -> P2 gather +
+    CHUNK -> layer2 -> rank-order sum; and the fused forward at tp = 1."""
+    M = 3
+    p = synth.make_problem(512, 2048, 512, 128, M, seed=40 + tp)
+    P1, P2 = _prep(p)
+    L1, L2 = _olayers(p)
+    ref = O.alg2_naive(p.X, L1, L2, tp)
+    n = p.N1 // tp
+    X = _dev(p.X)
+    hs = [tpq.TpMlp(p.w1, p.w2, P1, P2, tp=tp, rank=r, variant=tpq.TPQ_NAIVE, M_max=16) for r in range(tp)]
+    buf = torch.empty(tp, M, n, dtype=torch.float16, device=DEV)
+    for r, h in enumerate(hs):
+        h.layer1(X, M, buf[r])
+        _assert_close(_np(buf[r]), ref["Y1_local"][r], f"Y1_local {r}")
+    parts = []
+    for r, h in enumerate(hs):
+        y1in = _empty(M, n)
+        h.naive_gather(buf, M, y1in)
+        # the gather is pure data movement: bit-exact vs indexing the device buffer
+        src = O.shard_maps(ref["P2"], p.N1, tp, r, "naive", 128)["gather_src"]
+        b = buf.cpu().numpy()
+        assert (y1in.cpu().numpy() == b[src[:, 0], :, src[:, 1]].T).all()
+        y2 = _empty(M, p.N2)
+        h.layer2(y1in, M, y2)
+        parts.append(y2)
+    Y = _empty(M, p.N2)
+    tpq.sum_partials(parts, Y)
+    _assert_close(_np(Y), ref["Y2"], "Y2 naive")
+    if tp == 1:
+        Yf = _empty(M, p.N2)
+        hs[0].forward(X, M, Yf)
+        _assert_close(_np(Yf), ref["Y2"], "Y2 naive fused")
+    for h in hs:
+        h.close()
+
+
+def test_deterministic_and_graph_capturable():
+    M = 16
+    p = synth.make_problem(2048, 4096, 2048, 128, M, seed=77)
+    P1, P2 = _prep(p)
+    h = tpq.TpMlp(p.w1, p.w2, P1, P2, M_max=16)
+    X = _dev(p.X)
+    Ya, Yb = _empty(M, p.N2), _empty(M, p.N2)
+    h.forward(X, M, Ya)
+    for _ in range(3):
+        h.forward(X, M, Yb)
+        torch.cuda.synchronize()
+        assert torch.equal(Ya, Yb)
+    s = torch.cuda.Stream()
+    Yg = _empty(M, p.N2)
+    with torch.cuda.stream(s):
+        h.forward(X, M, Yg, stream=s)  # warm
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            h.forward(X, M, Yg, stream=s)
+    Yg.fill_(0)
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(Ya, Yg)
+    h.close()
+
+
+def test_m_above_16_chunks_and_host_e2e():
+    M = 37
+    p = synth.make_problem(1024, 2048, 1024, 128, M, seed=3)
+    P1, P2 = _prep(p)
+    L1, L2 = _olayers(p)
+    _, Y2r = O.dense_mlp(p.X, O.dequantize(L1), O.dequantize(L2))
+    h = tpq.TpMlp(p.w1, p.w2, P1, P2, M_max=64)
+    Yh = np.zeros((M, p.N2), np.float16)
+    h.forward_host(p.X, Yh, stream=torch.cuda.current_stream().cuda_stream)
+    _assert_close(Yh.astype(np.float64), Y2r, "Y2 host e2e")
+    Y = _empty(M, p.N2)
+    h.forward(_dev(p.X), M, Y)
+    assert (Y.cpu().numpy() == Yh).all()
+    with pytest.raises(tpq.TPQError):
+        h.forward(_dev(p.X), 65, Y)
+    h.close()
+
+
+@pytest.mark.parametrize("shape,M", [("llama70b", 1), ("llama70b", 16), ("granite20b", 4)])
+def test_full_size_sampled(shape, M):
+    """BASELINE.json configs at full size in the launch configuration bench.py times:
+    all of Y1 and 512 sampled columns of Y2 against the oracle."""
+    p = synth.make_named(shape, M, seed=0)
+    P1, P2 = _prep(p)
+    L1, L2 = _olayers(p)
+    cols = np.sort(np.random.default_rng(0).choice(p.N2, 512, replace=False))
+    h = tpq.TpMlp(p.w1, p.w2, P1, P2, M_max=16)
+    X = _dev(p.X)
+    Y = _empty(M, p.N2)
+    h.forward(X, M, Y)
+    Y1 = _empty(M, p.N1)
+    h.layer1(X, M, Y1)
+    P1o, _ = O.alg1_reorder(L1.g)
+    P2o, _ = O.alg1_reorder(L2.g)
+    Y1r, Y2r = O.dense_mlp_columns(p.X, L1, L2, cols2=cols)
+    _assert_close(_np(Y1), Y1r[:, P2o], "Y1 (P2 order)")
+    _assert_close(_np(Y)[:, cols], Y2r, "Y2 sampled")
+    h.close()

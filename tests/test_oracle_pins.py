@@ -346,3 +346,17 @@ def test_check_rows_close():
     assert not ok
     ok, _ = O.check_rows_close(ref + [[0, 0, 0], [0, 1e-30, 0]], ref)
     assert not ok
+
+
+def test_dense_mlp_columns_equals_dense():
+    """The column-blocked evaluation used at full size is the same definition: bit-equal to
+    dense_mlp on the integer regime (and on sampled columns)."""
+    p = synth.make_problem(64, 128, 48, 16, 3, seed=13, integer_regime=True)
+    L1, L2 = _olayers(p)
+    X = p.X.astype(np.float64)
+    Y1, Y2 = O.dense_mlp(X, O.dequantize(L1), O.dequantize(L2))
+    Y1c, Y2c = O.dense_mlp_columns(X, L1, L2, chunk=24)
+    assert (Y1c == Y1).all() and (Y2c == Y2).all()
+    cols = np.array([47, 0, 5])
+    _, Y2s = O.dense_mlp_columns(X, L1, L2, cols2=cols, chunk=7)
+    assert (Y2s == Y2[:, cols]).all()
