@@ -108,13 +108,19 @@ int tp_shard_mlp(const gptq_layer* w1, const gptq_layer* w2, const int32_t* P1,
 int tpq_mlp_destroy(tpq_mlp* h); /* NULL is a no-op; frees device memory and the NCCL comm */
 
 /* ---------------------------------------------------------------------------------------
- * NCCL bootstrap for tp > 1 (the collectives of PAPER.md:L117 AllGather / L121, L142
- * AllReduce run over NVLink/NVSwitch).  Rank 0 calls tpq_comm_unique_id, the caller ships
+ * NCCL communicator for tp > 1 (the collectives of PAPER.md:L117 AllGather / L121, L142
+ * AllReduce run over NVLink 5 / NVSwitch).  Rank 0 calls tpq_comm_unique_id, the caller ships
  * the 128 bytes to every rank (e.g. a torch.distributed broadcast), then every rank calls
- * tpq_comm_init (collective, blocking).  The comm is owned by the handle.
+ * tpq_comm_create (collective, blocking) for its device.  One communicator serves any number
+ * of MLP handles (a model's layers): tpq_mlp_set_comm attaches it WITHOUT taking ownership;
+ * the comm must outlive every forward enqueued with it and be destroyed by its creator.
+ * Errors: TPQ_EINVAL (NULL, tp/rank mismatch with the handle), TPQ_ENCCL, TPQ_ECUDA.
  * ------------------------------------------------------------------------------------- */
+typedef struct tpq_comm tpq_comm;
 int tpq_comm_unique_id(uint8_t out[128]);
-int tpq_comm_init(tpq_mlp* h, const uint8_t id[128], int tp, int rank);
+int tpq_comm_create(const uint8_t id[128], int tp, int rank, int device, tpq_comm** out);
+int tpq_comm_destroy(tpq_comm* c); /* NULL is a no-op */
+int tpq_mlp_set_comm(tpq_mlp* h, tpq_comm* c); /* c may be NULL to detach */
 
 /* ---------------------------------------------------------------------------------------
  * tp_mlp_forward -- the hot path, one rank.  TPQ_TP_AWARE = Alg. 3:
@@ -161,6 +167,13 @@ int tpq_layer2(tpq_mlp* h, const void* Y1in, int64_t M, void* Y2_local, void* st
  * `parts` is a HOST array of nparts dev pointers. */
 int tpq_sum_partials(const void* const* parts, int nparts, int64_t count, void* out,
                      void* stream);
+
+/* Optional timing hook (benchmarking): `events` is a HOST array of 6 cudaEvent_t (as void*)
+ * created on the handle's device, or NULL to disable.  While set, each forward records on its
+ * stream: [0] before the X[:,P1] gather, [1] before the layer-1 GEMV, [2] after it, [3] before
+ * the layer-2 GEMV (after the naive AllGather + P2 gather; == [2] for TP-aware), [4] after the
+ * layer-2 GEMV, [5] after the AllReduce.  The array is copied; events stay caller-owned. */
+int tpq_mlp_set_timing(tpq_mlp* h, void* const* events);
 
 /* ------------------------------- introspection / test-only exports ------------------- */
 typedef struct tpq_mlp_info_t {

@@ -21,9 +21,10 @@ _CODES = {1: "EINVAL", 2: "EUNSUPPORTED", 3: "ECUDA", 4: "ENCCL", 5: "ENOMEM", 6
 # Every symbol include/tpq.h declares (tests check the .so exports all of them).
 EXPORTS = [
     "tpq_last_error", "tpq_version", "gptq_reorder", "tp_shard_mlp", "tpq_mlp_destroy",
-    "tpq_comm_unique_id", "tpq_comm_init", "tp_mlp_forward", "tp_mlp_forward_host",
+    "tpq_comm_unique_id", "tpq_comm_create", "tpq_comm_destroy", "tpq_mlp_set_comm",
+    "tp_mlp_forward", "tp_mlp_forward_host",
     "tp_mlp_forward_local", "tpq_layer1", "tpq_naive_gather", "tpq_layer2", "tpq_sum_partials",
-    "tpq_mlp_info", "tpq_mlp_index_maps", "tpq_mlp_export_canonical",
+    "tpq_mlp_info", "tpq_mlp_index_maps", "tpq_mlp_export_canonical", "tpq_mlp_set_timing",
 ]
 
 
@@ -67,7 +68,9 @@ def lib() -> C.CDLL:
                              C.c_int, i64, C.c_int, C.POINTER(vp)],
             "tpq_mlp_destroy": [vp],
             "tpq_comm_unique_id": [vp],
-            "tpq_comm_init": [vp, vp, C.c_int, C.c_int],
+            "tpq_comm_create": [vp, C.c_int, C.c_int, C.c_int, C.POINTER(vp)],
+            "tpq_comm_destroy": [vp],
+            "tpq_mlp_set_comm": [vp, vp],
             "tp_mlp_forward": [vp, vp, i64, vp, vp],
             "tp_mlp_forward_host": [vp, vp, i64, vp, vp],
             "tp_mlp_forward_local": [vp, vp, i64, vp, vp],
@@ -78,6 +81,7 @@ def lib() -> C.CDLL:
             "tpq_mlp_info": [vp, C.POINTER(MlpInfo)],
             "tpq_mlp_index_maps": [vp, vp, vp, C.POINTER(i32), C.POINTER(i32)],
             "tpq_mlp_export_canonical": [vp, C.c_int, vp, vp, vp],
+            "tpq_mlp_set_timing": [vp, vp],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -148,6 +152,27 @@ def _layer_struct(layer) -> tuple[GptqLayer, list]:
     return s, keep
 
 
+class Comm:
+    """NCCL communicator (tpq_comm_create); every rank constructs it with the same uid."""
+
+    def __init__(self, uid: bytes, tp: int, rank: int, device: int):
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        c = C.c_void_p()
+        _check(lib().tpq_comm_create(C.cast(buf, C.c_void_p), tp, rank, device, C.byref(c)))
+        self._c = c
+
+    def close(self):
+        if getattr(self, "_c", None):
+            _check(lib().tpq_comm_destroy(self._c))
+            self._c = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 class TpMlp:
     """One rank's shard (tp_shard_mlp handle)."""
 
@@ -176,9 +201,10 @@ class TpMlp:
             pass
 
     # --- collectives
-    def comm_init(self, uid: bytes, tp: int, rank: int):
-        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
-        _check(lib().tpq_comm_init(self._h, C.cast(buf, C.c_void_p), tp, rank))
+    def set_comm(self, comm: "Comm | None"):
+        """Attach (not own) a communicator; keep `comm` alive while forwards are in flight."""
+        self._comm = comm
+        _check(lib().tpq_mlp_set_comm(self._h, comm._c if comm is not None else None))
 
     # --- forward (device pointers / torch tensors)
     def forward(self, X, M: int, Y, stream=None):
@@ -200,6 +226,14 @@ class TpMlp:
 
     def layer2(self, Y1in, M: int, Y2, stream=None):
         _check(lib().tpq_layer2(self._h, _ptr(Y1in), M, _ptr(Y2), _stream(stream)))
+
+    def set_timing(self, events):
+        """events: 6 torch.cuda.Event (or None to disable); see tpq_mlp_set_timing."""
+        if events is None:
+            _check(lib().tpq_mlp_set_timing(self._h, None))
+            return
+        arr = (C.c_void_p * 6)(*[e.cuda_event for e in events])
+        _check(lib().tpq_mlp_set_timing(self._h, C.cast(arr, C.c_void_p)))
 
     # --- test exports
     def index_maps(self):

@@ -140,6 +140,11 @@ inline uint32_t nib(uint32_t w, int i) { return (w >> (4 * i)) & 0xFu; }
 
 }  // namespace
 
+struct tpq_comm {
+  ncclComm_t comm;
+  int tp, rank, device;
+};
+
 struct tpq_mlp {
   int64_t K1 = 0, N1 = 0, N2 = 0, n = 0, M_max = 0;
   int G1 = 0, G2 = 0, tp = 1, rank = 0, variant = 1, device = -1;
@@ -161,6 +166,8 @@ struct tpq_mlp {
   float* d_ws = nullptr;
   int* d_cnt = nullptr;
   ncclComm_t comm = nullptr;
+  cudaEvent_t ev[6] = {};
+  bool timing = false;
 };
 
 namespace {
@@ -396,8 +403,7 @@ int tp_shard_mlp(const gptq_layer* w1, const gptq_layer* w2, const int32_t* P1, 
 
 int tpq_mlp_destroy(tpq_mlp* h) {
   if (!h) return TPQ_OK;
-  if (h->comm) ncclCommDestroy(h->comm);
-  free_dev(h);
+  free_dev(h);  // the attached comm is not owned
   delete h;
   return TPQ_OK;
 }
@@ -411,15 +417,44 @@ int tpq_comm_unique_id(uint8_t out[128]) {
   return TPQ_OK;
 }
 
-int tpq_comm_init(tpq_mlp* h, const uint8_t id[128], int tp, int rank) {
-  if (!h || !id) return fail(TPQ_EINVAL, "NULL");
-  if (h->device < 0) return fail(TPQ_ESTATE, "host-only handle has no device");
-  if (tp != h->tp || rank != h->rank) return fail(TPQ_EINVAL, "tp/rank (%d,%d) != handle's (%d,%d)", tp, rank, h->tp, h->rank);
-  if (h->comm) return fail(TPQ_ESTATE, "comm already initialised");
-  TPQ_CUDA(cudaSetDevice(h->device));
+int tpq_comm_create(const uint8_t id[128], int tp, int rank, int device, tpq_comm** out) {
+  if (!id || !out) return fail(TPQ_EINVAL, "NULL");
+  *out = nullptr;
+  if (tp < 1 || rank < 0 || rank >= tp) return fail(TPQ_EINVAL, "tp=%d rank=%d", tp, rank);
+  if (device < 0) return fail(TPQ_EINVAL, "device=%d", device);
+  TPQ_CUDA(cudaSetDevice(device));
   ncclUniqueId uid;
   memcpy(&uid, id, 128);
-  TPQ_NCCL(ncclCommInitRank(&h->comm, tp, uid, rank));
+  ncclComm_t c = nullptr;
+  TPQ_NCCL(ncclCommInitRank(&c, tp, uid, rank));
+  tpq_comm* tc = new (std::nothrow) tpq_comm{c, tp, rank, device};
+  if (!tc) {
+    ncclCommDestroy(c);
+    return fail(TPQ_ENOMEM, "tpq_comm_create");
+  }
+  *out = tc;
+  return TPQ_OK;
+}
+
+int tpq_comm_destroy(tpq_comm* c) {
+  if (!c) return TPQ_OK;
+  ncclResult_t r = ncclCommDestroy(c->comm);
+  delete c;
+  if (r != ncclSuccess) return fail(TPQ_ENCCL, "ncclCommDestroy: %s", ncclGetErrorString(r));
+  return TPQ_OK;
+}
+
+int tpq_mlp_set_comm(tpq_mlp* h, tpq_comm* c) {
+  if (!h) return fail(TPQ_EINVAL, "NULL handle");
+  if (!c) {
+    h->comm = nullptr;
+    return TPQ_OK;
+  }
+  if (h->device < 0) return fail(TPQ_ESTATE, "host-only handle has no device");
+  if (c->tp != h->tp || c->rank != h->rank || c->device != h->device)
+    return fail(TPQ_EINVAL, "comm (tp=%d rank=%d dev=%d) does not match handle (tp=%d rank=%d dev=%d)", c->tp, c->rank,
+                c->device, h->tp, h->rank, h->device);
+  h->comm = c->comm;
   return TPQ_OK;
 }
 
@@ -437,15 +472,21 @@ int check_fwd(tpq_mlp* h, const void* X, int64_t M, const void* Y) {
 // Gather + layer 1 + (naive: AllGather + P2 gather) + layer 2 for one chunk of <= 16 rows.
 // Writes the rank-local partial Y2 (row-major [mc][N2] at Y).  `collective` enables the naive
 // AllGather (tp > 1); otherwise the naive path must be at tp == 1.
+#define TPQ_MARK(i) \
+  if (h->timing) TPQ_CUDA(cudaEventRecord(h->ev[i], st))
+
 int chunk_forward(tpq_mlp* h, const uint16_t* X, int mc, void* Y, cudaStream_t st, bool collective) {
   TPQ_CUDA(tpq::launch_to_frag(X, h->K1, h->d_P1, tpq::GATHER_COLS, 0, mc, h->K1, h->d_xf1, st));  // X[:, P1]
+  TPQ_MARK(1);
   if (h->variant == TPQ_TP_AWARE) {
     // Alg. 3 L1: Y1_local lands directly in the layout layer 2 consumes (already in P2 order)
     TPQ_CUDA(tpq::launch_gemv(h->L1, h->d_xf1, mc, h->d_xf2, tpq::OUT_FRAG, 0, st));
+    TPQ_MARK(2);
   } else {
     // Alg. 2 L1 into this rank's slot of the AllGather buffer [tp][mc][n]
     uint8_t* slot = (uint8_t*)h->d_buf + (size_t)h->rank * mc * h->n * 2;
     TPQ_CUDA(tpq::launch_gemv(h->L1, h->d_xf1, mc, slot, tpq::OUT_ROWMAJOR, h->n, st));
+    TPQ_MARK(2);
     if (h->tp > 1) {
       if (!collective) return fail(TPQ_ESTATE, "naive variant with tp > 1 needs the AllGather (use tp_mlp_forward)");
       TPQ_NCCL(ncclAllGather(slot, h->d_buf, (size_t)mc * h->n, ncclFloat16, h->comm, st));  // Alg. 2 L2
@@ -453,13 +494,16 @@ int chunk_forward(tpq_mlp* h, const uint16_t* X, int mc, void* Y, cudaStream_t s
     // Alg. 2 L3-4: Y1_global[:, P2] then CHUNK(rank), fused into one gather to the frag layout
     TPQ_CUDA(tpq::launch_to_frag(h->d_buf, 0, h->d_gcols, tpq::GATHER_ALLGATHER, h->n, mc, h->n, h->d_xf2, st));
   }
+  TPQ_MARK(3);
   TPQ_CUDA(tpq::launch_gemv(h->L2, h->d_xf2, mc, Y, tpq::OUT_ROWMAJOR, h->N2, st));  // L2 GEMM
+  TPQ_MARK(4);
   return TPQ_OK;
 }
 
 int forward_impl(tpq_mlp* h, const void* X, int64_t M, void* Y, cudaStream_t st, bool collective) {
-  if (collective && h->tp > 1 && !h->comm) return fail(TPQ_ESTATE, "tp=%d requires tpq_comm_init", h->tp);
+  if (collective && h->tp > 1 && !h->comm) return fail(TPQ_ESTATE, "tp=%d requires tpq_mlp_set_comm", h->tp);
   TPQ_CUDA(cudaSetDevice(h->device));
+  TPQ_MARK(0);
   for (int64_t m0 = 0; m0 < M; m0 += 16) {
     const int mc = (int)std::min<int64_t>(16, M - m0);
     int rc = chunk_forward(h, (const uint16_t*)X + m0 * h->K1, mc, (uint8_t*)Y + (size_t)m0 * h->N2 * 2, st,
@@ -468,6 +512,7 @@ int forward_impl(tpq_mlp* h, const void* X, int64_t M, void* Y, cudaStream_t st,
   }
   if (collective && h->tp > 1)  // Alg. 2 L6 / Alg. 3 L3
     TPQ_NCCL(ncclAllReduce(Y, Y, (size_t)M * h->N2, ncclFloat16, ncclSum, h->comm, st));
+  TPQ_MARK(5);
   return TPQ_OK;
 }
 
@@ -545,6 +590,20 @@ int tpq_sum_partials(const void* const* parts, int nparts, int64_t count, void* 
     if (!parts[i]) return fail(TPQ_EINVAL, "parts[%d] is NULL", i);
   if (count == 0) return TPQ_OK;
   TPQ_CUDA(tpq::launch_sum_partials(parts, nparts, count, out, (cudaStream_t)stream));
+  return TPQ_OK;
+}
+
+int tpq_mlp_set_timing(tpq_mlp* h, void* const* events) {
+  if (!h) return fail(TPQ_EINVAL, "NULL handle");
+  if (!events) {
+    h->timing = false;
+    return TPQ_OK;
+  }
+  for (int i = 0; i < 6; ++i) {
+    if (!events[i]) return fail(TPQ_EINVAL, "events[%d] is NULL", i);
+    h->ev[i] = (cudaEvent_t)events[i];
+  }
+  h->timing = true;
   return TPQ_OK;
 }
 

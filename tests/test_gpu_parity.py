@@ -72,7 +72,7 @@ def test_tiny_tp_aware_vs_oracle(M):
 @pytest.mark.parametrize("M", [1, 5, 16])
 def test_group_sizes_ragged_tail(G, M):
     """Several 64-col blocks x groups, N not a multiple of the CTA count (ragged stream-K)."""
-    p = synth.make_problem(1024, 1472, 640, G, M, seed=G + M)
+    p = synth.make_problem(1024, 1408, 640, G, M, seed=G + M)
     P1, P2 = _prep(p)
     L1, L2 = _olayers(p)
     Y1r, Y2r = O.dense_mlp(p.X, O.dequantize(L1), O.dequantize(L2))
