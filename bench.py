@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--sweep", action="store_true", help="also time M=1,4 (extra 'sweep' key)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="launch every step eagerly (no CUDA graph)")
     ap.add_argument("--sim-tp", type=int, default=0,
                     help="single GPU: time one rank's shard of a TP=k MLP (no collective)")
     return ap.parse_args()
@@ -158,7 +159,7 @@ def run_reference(a):
     tp = a.gpus
     K1, N1, N2, G = synth.SHAPES[a.shape]
     p = synth.make_named(a.shape, a.m, a.seed)
-    den = 8 if a.shape != "tiny" else 1
+    den = 4 if a.shape != "tiny" else 1
     for _ in range(min(a.warmup, 1)):
         oracle_sample_time(p, den)
     ts = [oracle_sample_time(p, den) for _ in range(max(1, min(a.steps, 3)))]
@@ -233,10 +234,30 @@ def main():
             fwd(hs[i % R])
     sync_all()
 
-    # ---------------- timed region: K steps, per-kernel events via the library timing hook
-    K = a.steps
-    n_ev = min(K, 512)  # event sets for the last n_ev steps (per-kernel averages)
+    # ---------------- timed region: K steps, per-kernel events via the library timing hook.
+    # Default: the steps are replayed from a CUDA graph of `per_graph` consecutive forwards
+    # (rotating the weight replicas) so host launch overhead is not measured; --no-graph
+    # launches every forward eagerly through the C-ABI.
+    per_graph = R * max(1, 16 // R)
+    n_ev = per_graph if not a.no_graph else min(a.steps, 512)
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(n_ev)]
+    for es_ in evs:  # torch creates the cudaEvent_t lazily, on first record
+        for e in es_:
+            e.record(stream)
+    sync_all()
+    graph = None
+    if not a.no_graph:
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=stream):
+            for i in range(per_graph):
+                h = hs[i % R]
+                h.set_timing(evs[i])
+                fwd(h)
+                h.set_timing(None)
+        for _ in range(max(3, a.warmup // per_graph)):
+            graph.replay()
+        sync_all()
+    K = -(-a.steps // per_graph) * per_graph if graph is not None else a.steps
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     clocks = ClockSampler(local)
     clocks.start()
@@ -244,14 +265,18 @@ def main():
     sync_all()
     with torch.cuda.stream(stream):
         start.record(stream)
-        for i in range(K):
-            h = hs[i % R]
-            j = i - (K - n_ev)
-            if j >= 0:
-                h.set_timing(evs[j])
-            fwd(h)
-            if j >= 0:
-                h.set_timing(None)
+        if graph is not None:
+            for _ in range(K // per_graph):
+                graph.replay()
+        else:
+            for i in range(K):
+                h = hs[i % R]
+                j = i - (K - n_ev)
+                if j >= 0:
+                    h.set_timing(evs[j])
+                fwd(h)
+                if j >= 0:
+                    h.set_timing(None)
         end.record(stream)
     sync_all()
     clk = clocks.stop()
@@ -299,6 +324,7 @@ def main():
                         + (" (one rank's shard, no collective)" if sim_tp else ""),
             "M": M, "tp": shard_tp, "variant": a.variant, "int4_weights": True,
             "cold_l2": f"{R} rotating weight replicas x {step_bytes / 1e6:.1f} MB >= 3 x L2 ({l2_cache / 1e6:.0f} MB)",
+            "launch": "eager C-ABI calls" if graph is None else f"CUDA graph of {per_graph} forwards, replayed",
             "parallelism": f"tp{shard_tp}",
         },
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -317,7 +343,7 @@ def main():
     if rank == 0 and a.sweep:
         line["sweep"] = sweep_m(hs, p, R, stream, dev, sim_tp)
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
-        den = 8 if a.shape != "tiny" else 1
+        den = 4 if a.shape != "tiny" else 1
         t = oracle_sample_time(synth.make_named(a.shape, M, a.seed), den)
         line["cpu_baseline"] = {"value": t * 1e6, "unit": "us", "cores": cpu_cores(), "kind": "oracle",
                                 "sample": f"Alg.3 tp=1 fp64 oracle on W1[:, :N1/{den}], W2[:N1/{den}, :] "
