@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -225,6 +226,7 @@ void plan_layer(tpq::LayerDev& L, int64_t K, int64_t N, int G, int device) {
   L.NB = (int)(N / tpq::kBlockCols);
   L.NG = (int)(K / G);
   L.U = (int64_t)L.NB * L.NG;
+  if (const char* d = getenv("TPQ_GEMV_DEBUG")) L.dbg = atoi(d);
   int sms = 148;
   if (device >= 0) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   for (int MT = 1; MT <= tpq::kMaxMT; ++MT) {
@@ -472,8 +474,9 @@ int check_fwd(tpq_mlp* h, const void* X, int64_t M, const void* Y) {
 // Gather + layer 1 + (naive: AllGather + P2 gather) + layer 2 for one chunk of <= 16 rows.
 // Writes the rank-local partial Y2 (row-major [mc][N2] at Y).  `collective` enables the naive
 // AllGather (tp > 1); otherwise the naive path must be at tp == 1.
+// External event record: under stream capture this becomes a timed event node of the graph.
 #define TPQ_MARK(i) \
-  if (h->timing) TPQ_CUDA(cudaEventRecord(h->ev[i], st))
+  if (h->timing) TPQ_CUDA(cudaEventRecordWithFlags(h->ev[i], st, cudaEventRecordExternal))
 
 int chunk_forward(tpq_mlp* h, const uint16_t* X, int mc, void* Y, cudaStream_t st, bool collective) {
   TPQ_CUDA(tpq::launch_to_frag(X, h->K1, h->d_P1, tpq::GATHER_COLS, 0, mc, h->K1, h->d_xf1, st));  // X[:, P1]

@@ -87,10 +87,13 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;"); }
 
 // ------------------------------------------------------------------ GEMV
-template <int S>
+// OCC = resident CTAs per SM (register budget 255 / OCC=1, 128 / OCC=2); NS = TMA ring stages
+// per warp, sized so OCC x 8 warps x NS units are in flight per SM.
+template <int S, int MT>
 struct Cfg {
   static constexpr int UNIT = 32 * 16 * S + kMetaBytes;        // bytes per (block, group) record
-  static constexpr int NS = S == 8 ? 4 : (S == 4 ? 6 : 8);      // ring stages per warp
+  static constexpr int OCC = MT == 1 ? 2 : 1;
+  static constexpr int NS = (OCC == 2 ? 2 : 4) * (S == 8 ? 1 : (S == 4 ? 2 : 3)) / (S == 2 ? 1 : 1);
   static constexpr int CW = S >= 4 ? 4 : S;                     // u32 words per lane per chunk
   static constexpr int NC = S / CW;                             // chunks per tile
   static constexpr int RING = 8 * NS * UNIT;                    // ring bytes per CTA (8 warps)
@@ -99,7 +102,7 @@ struct Cfg {
 template <int MT>
 __host__ __device__ constexpr int red_bytes() { return 8 * MT * 8 * kBlockCols * 4; }
 template <int S, int MT>
-constexpr size_t gemv_smem() { return (size_t)Cfg<S>::RING + red_bytes<MT>() + 8 * Cfg<S>::NS * 8; }
+constexpr size_t gemv_smem() { return (size_t)Cfg<S, MT>::RING + red_bytes<MT>() + 8 * Cfg<S, MT>::NS * 8; }
 
 template <int S, int MT>
 struct Frag {
@@ -110,7 +113,7 @@ struct Frag {
 
 template <int S, int MT>
 __device__ __forceinline__ void read_unit(Frag<S, MT>& f, const uint8_t* unit, int lane) {
-  using C = Cfg<S>;
+  using C = Cfg<S, MT>;
 #pragma unroll
   for (int c = 0; c < C::NC; ++c)
 #pragma unroll
@@ -227,6 +230,7 @@ struct GemvArgs {
   int64_t out_ld;
   float* ws;
   int* cnt;
+  int dbg;  // profiling aid (TPQ_GEMV_DEBUG): 1 = skip compute, 2 = skip HBM (compute on stale smem)
 };
 
 __device__ __forceinline__ int64_t cta_start(int64_t c, int64_t U, int grid) { return c * U / grid; }
@@ -291,8 +295,8 @@ struct WarpSeq {
 };
 
 template <int S, int MT>
-__global__ void __launch_bounds__(kThreads, 1) k_gemv(const GemvArgs a) {
-  using C = Cfg<S>;
+__global__ void __launch_bounds__(kThreads, Cfg<S, MT>::OCC) k_gemv(const GemvArgs a) {
+  using C = Cfg<S, MT>;
   constexpr int E = MT * 8 * kBlockCols;  // outputs per block (padded rows)
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* ring = smem;                                              // [8 warps][NS][UNIT]
@@ -350,14 +354,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemv(const GemvArgs a) {
 #pragma unroll
         for (int i = 0; i < 4; ++i) acc[t][mt][i] = 0.f;
 
-#pragma unroll 1
-    for (int g = gb + warp; g < ge; g += 8) {
+    // consume one unit: wait for its TMA stage, pull the fragments to registers, refill the
+    // stage with the unit NS ahead, prefetch the next unit's X into `xn`, then compute.
+    auto step = [&](const uint32_t(&xc)[MT][S][2], uint32_t(&xn)[MT][S][2]) {
       const int slot = idx % C::NS;
-      mbar_wait(my_bars + slot, (uint32_t)((idx / C::NS) & 1));
+      if (a.dbg != 2) mbar_wait(my_bars + slot, (uint32_t)((idx / C::NS) & 1));
       Frag<S, MT> f;
       read_unit<S, MT>(f, my_ring + slot * C::UNIT, lane);
       __syncwarp();
-      if (lane == 0 && prod.valid) {  // refill the slot just drained with the unit NS ahead
+      if (lane == 0 && prod.valid && a.dbg != 2) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_arrive_expect_tx(my_bars + slot, C::UNIT);
         bulk_g2s(my_ring + slot * C::UNIT, a.packed + ((size_t)prod.b * a.NG + prod.g) * C::UNIT, C::UNIT,
@@ -366,16 +371,30 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemv(const GemvArgs a) {
       if (prod.valid) prod.next();
       ++idx;
       cons.next();
-      uint32_t xn[MT][S][2];
       if (cons.valid) load_x<S, MT>(xn, a.xf, kchunks, cons.g, lane, a.M);
-      compute_unit<S, MT>(f, x, acc);
+      if (a.dbg != 1) {
+        compute_unit<S, MT>(f, xc, acc);
+      } else {
+        acc[0][0][0] += __uint_as_float(f.w[0][0] ^ f.w[3][S - 1] ^ f.zz);
+      }
+    };
+    uint32_t x2[MT][S][2];
+#pragma unroll 1
+    for (int g = gb + warp; g < ge; g += 16) {  // two units per trip: x -> x2 -> x, no copies
+      step(x, x2);
+      if (g + 8 >= ge) {
+        if (cons.valid) {
 #pragma unroll
-      for (int mt = 0; mt < MT; ++mt)
+          for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-        for (int s = 0; s < S; ++s) {
-          x[mt][s][0] = xn[mt][s][0];
-          x[mt][s][1] = xn[mt][s][1];
+            for (int s = 0; s < S; ++s) {
+              x[mt][s][0] = x2[mt][s][0];
+              x[mt][s][1] = x2[mt][s][1];
+            }
         }
+        break;
+      }
+      step(x2, x);
     }
 
     // ---- CTA reduction over the 8 warps (fixed order) ----
@@ -570,6 +589,7 @@ cudaError_t launch_gemv(const LayerDev& L, const void* xf, int M, void* out, int
   a.out_ld = out_ld;
   a.ws = L.ws;
   a.cnt = L.cnt;
+  a.dbg = L.dbg;
   const int S = L.G / 16;
 #define TPQ_GEMV(SV, MTV) \
   if (S == SV && MT == MTV) return launch_gemv_t<SV, MTV>(a, st);
