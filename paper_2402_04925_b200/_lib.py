@@ -12,7 +12,8 @@ import os
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libtpq.so")
+# TPQ_LIB_PATH may point at the profiling build (libtpq_prof.so) for wait-cycle accounting.
+LIB_PATH = os.environ.get("TPQ_LIB_PATH") or os.path.join(_PKG, "libtpq.so")
 
 TPQ_OK, TPQ_EINVAL, TPQ_EUNSUPPORTED, TPQ_ECUDA, TPQ_ENCCL, TPQ_ENOMEM, TPQ_ESTATE = range(7)
 TPQ_NAIVE, TPQ_TP_AWARE = 0, 1

@@ -37,8 +37,10 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, prof: bool = False) -> str:
+    """prof=True builds libtpq_prof.so with -DTPQ_PROF (wait-cycle accounting, profiling only)."""
+    lib = LIB.replace("libtpq.so", "libtpq_prof.so") if prof else LIB
+    if not force and not prof and not _stale():
         return LIB
     nr = nccl_root()
     cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC,-O3",
@@ -47,15 +49,16 @@ def build(force: bool = False, verbose: bool = False) -> str:
            *[os.path.join(CSRC, s) for s in SOURCES],
            "-L", os.path.join(nr, "lib"), "-l:libnccl.so.2",
            f"-Xlinker=-rpath,{os.path.join(nr, 'lib')}",
-           "-o", LIB + ".tmp"]
+           *(["-DTPQ_PROF"] if prof else []),
+           "-o", lib + ".tmp"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + " ".join(cmd) + "\n" + r.stdout + r.stderr)
     if verbose:
         sys.stderr.write(r.stdout + r.stderr)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(lib + ".tmp", lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, prof="--prof" in sys.argv))

@@ -73,35 +73,30 @@ struct Canon {
 };
 
 // Pack a canonical shard into the device layout of internal.h.
+// Nibble slot (0..7) of k0 + i inside a code word (internal.h): k0,k0+1 -> n0,n4; k0+2,k0+3 -> n1,n5;
+// k0+4,k0+5 -> n2,n6; k0+6,k0+7 -> n3,n7.
+constexpr int kNibbleOfK[8] = {0, 4, 1, 5, 2, 6, 3, 7};
+
 std::vector<uint8_t> pack_layer(const Canon& c) {
-  const int G = c.G, S = G / 16, CW = S >= 4 ? 4 : S;
-  const int64_t NB = c.N / tpq::kBlockCols, NG = c.K / G, UB = tpq::unit_bytes(G);
-  std::vector<uint8_t> out((size_t)(NB * NG * UB), 0);
-  parallel_for(NB * NG, [&](int64_t u) {
-    const int64_t b = u / NG, g = u % NG;
+  const int G = c.G, NCH = G / 32;
+  const int64_t NT = c.N / tpq::kTileCols, NG = c.K / G, UB = tpq::unit_bytes(G);
+  std::vector<uint8_t> out((size_t)(NT * NG * UB), 0);
+  parallel_for(NT * NG, [&](int64_t u) {
+    const int64_t t = u / NG, g = u % NG;
     uint8_t* rec = out.data() + u * UB;
     uint32_t* words = reinterpret_cast<uint32_t*>(rec);
-    auto Q = [&](int64_t k, int64_t n) -> uint32_t { return c.q[(size_t)(k * c.N + n)]; };
-    for (int t = 0; t < 4; ++t)
-      for (int lane = 0; lane < 32; ++lane)
-        for (int s = 0; s < S; ++s) {
-          const int64_t r0 = b * 64 + 16 * t + lane / 4, r1 = r0 + 8;
-          const int64_t k0 = g * G + 16 * s + 2 * (lane % 4);
-          const uint32_t w = Q(k0, r0) | Q(k0, r1) << 4 | Q(k0 + 8, r0) << 8 | Q(k0 + 8, r1) << 12 |
-                             Q(k0 + 1, r0) << 16 | Q(k0 + 1, r1) << 20 | Q(k0 + 9, r0) << 24 |
-                             Q(k0 + 9, r1) << 28;
-          const int cidx = s / CW;
-          words[((cidx * 4 + t) * 32 + lane) * CW + (s % CW)] = w;
+    for (int j = 0; j < tpq::kTileCols; ++j) {
+      const int64_t n = t * tpq::kTileCols + j;
+      for (int ch = 0; ch < NCH; ++ch)
+        for (int w = 0; w < 4; ++w) {
+          const int64_t k0 = g * G + 32 * ch + 8 * w;
+          uint32_t word = 0;
+          for (int i = 0; i < 8; ++i) word |= (uint32_t)c.q[(size_t)((k0 + i) * c.N + n)] << (4 * kNibbleOfK[i]);
+          words[(ch * tpq::kTileCols + j) * 4 + w] = word;
         }
-    uint8_t* meta = rec + 32LL * G;
-    for (int rr = 0; rr < 8; ++rr)
-      for (int t = 0; t < 4; ++t) {
-        const int64_t r0 = b * 64 + 16 * t + rr, r1 = r0 + 8;
-        const uint16_t s0 = c.s[(size_t)(g * c.N + r0)], s1 = c.s[(size_t)(g * c.N + r1)];
-        memcpy(meta + (rr * 4 + t) * 4, &s0, 2);
-        memcpy(meta + (rr * 4 + t) * 4 + 2, &s1, 2);
-        meta[128 + rr * 4 + t] = (uint8_t)(c.z[(size_t)(g * c.N + r0)] | (c.z[(size_t)(g * c.N + r1)] << 4));
-      }
+      memcpy(rec + 64LL * G + 2 * j, &c.s[(size_t)(g * c.N + n)], 2);
+      rec[64LL * G + 256 + j / 2] |= (uint8_t)(c.z[(size_t)(g * c.N + n)] << (4 * (j & 1)));
+    }
   });
   return out;
 }
@@ -109,31 +104,23 @@ std::vector<uint8_t> pack_layer(const Canon& c) {
 // Inverse of pack_layer (test export).
 void unpack_layer(const std::vector<uint8_t>& pk, int64_t K, int64_t N, int G, uint8_t* q, uint16_t* s,
                   uint8_t* z) {
-  const int S = G / 16, CW = S >= 4 ? 4 : S;
-  const int64_t NB = N / tpq::kBlockCols, NG = K / G, UB = tpq::unit_bytes(G);
-  parallel_for(NB * NG, [&](int64_t u) {
-    const int64_t b = u / NG, g = u % NG;
+  const int NCH = G / 32;
+  const int64_t NT = N / tpq::kTileCols, NG = K / G, UB = tpq::unit_bytes(G);
+  parallel_for(NT * NG, [&](int64_t u) {
+    const int64_t t = u / NG, g = u % NG;
     const uint8_t* rec = pk.data() + u * UB;
     const uint32_t* words = reinterpret_cast<const uint32_t*>(rec);
-    for (int t = 0; t < 4; ++t)
-      for (int lane = 0; lane < 32; ++lane)
-        for (int st = 0; st < S; ++st) {
-          const uint32_t w = words[((st / CW * 4 + t) * 32 + lane) * CW + (st % CW)];
-          const int64_t r0 = b * 64 + 16 * t + lane / 4, r1 = r0 + 8;
-          const int64_t k0 = g * G + 16 * st + 2 * (lane % 4);
-          const int64_t ks[8] = {k0, k0, k0 + 8, k0 + 8, k0 + 1, k0 + 1, k0 + 9, k0 + 9};
-          const int64_t ns[8] = {r0, r1, r0, r1, r0, r1, r0, r1};
-          for (int i = 0; i < 8; ++i) q[ks[i] * N + ns[i]] = (w >> (4 * i)) & 0xF;
+    for (int j = 0; j < tpq::kTileCols; ++j) {
+      const int64_t n = t * tpq::kTileCols + j;
+      for (int ch = 0; ch < NCH; ++ch)
+        for (int w = 0; w < 4; ++w) {
+          const uint32_t word = words[(ch * tpq::kTileCols + j) * 4 + w];
+          const int64_t k0 = g * G + 32 * ch + 8 * w;
+          for (int i = 0; i < 8; ++i) q[(k0 + i) * N + n] = (word >> (4 * kNibbleOfK[i])) & 0xF;
         }
-    const uint8_t* meta = rec + 32LL * G;
-    for (int rr = 0; rr < 8; ++rr)
-      for (int t = 0; t < 4; ++t) {
-        const int64_t r0 = b * 64 + 16 * t + rr, r1 = r0 + 8;
-        memcpy(&s[g * N + r0], meta + (rr * 4 + t) * 4, 2);
-        memcpy(&s[g * N + r1], meta + (rr * 4 + t) * 4 + 2, 2);
-        z[g * N + r0] = meta[128 + rr * 4 + t] & 0xF;
-        z[g * N + r1] = meta[128 + rr * 4 + t] >> 4;
-      }
+      memcpy(&s[g * N + n], rec + 64LL * G + 2 * j, 2);
+      z[g * N + n] = (rec[64LL * G + 256 + j / 2] >> (4 * (j & 1))) & 0xF;
+    }
   });
 }
 
@@ -158,9 +145,8 @@ struct tpq_mlp {
   void* d_w2 = nullptr;
   int32_t* d_P1 = nullptr;
   int32_t* d_gcols = nullptr;  // naive: P2[r n .. (r+1) n)
-  void* d_xf1 = nullptr;       // frag X[:, P1], 16 rows
-  void* d_xf2 = nullptr;       // frag Y1, 16 rows
-  void* d_y1 = nullptr;        // row-major Y1 scratch [16][n] (naive send slot lives in d_buf)
+  void* d_xf1 = nullptr;       // layer-1 B operand: X[:, P1] (xext layout, internal.h)
+  void* d_xf2 = nullptr;       // layer-2 B operand: Y1_local (xext layout)
   void* d_buf = nullptr;       // AllGather buffer [tp][16][n]
   void* d_xin = nullptr;       // host-forward staging [M_max][K1]
   void* d_yout = nullptr;      // host-forward staging [M_max][N2]
@@ -203,8 +189,7 @@ int validate_perm(const int32_t* P, const gptq_layer* w, const char* name) {
 void free_dev(tpq_mlp* h) {
   if (h->device < 0) return;
   cudaSetDevice(h->device);
-  void* ptrs[] = {h->d_w1, h->d_w2, h->d_P1, h->d_gcols, h->d_xf1, h->d_xf2, h->d_y1,
-                  h->d_buf, h->d_xin, h->d_yout, h->d_ws, h->d_cnt};
+  void* ptrs[] = {h->d_w1, h->d_w2, h->d_P1, h->d_gcols, h->d_xf1, h->d_xf2, h->d_buf, h->d_xin, h->d_yout, h->d_ws, h->d_cnt};
   for (void* p : ptrs)
     if (p) cudaFree(p);
 }
@@ -219,24 +204,25 @@ int dev_alloc(void** p, size_t bytes) {
   return TPQ_OK;
 }
 
+// Stream-K plan: a persistent grid of SMs x resident CTAs, each CTA a contiguous range of
+// (tile, group) units; at least 4 units per CTA so the TMA ring has work to overlap.
 void plan_layer(tpq::LayerDev& L, int64_t K, int64_t N, int G, int device) {
   L.K = K;
   L.N = N;
   L.G = G;
-  L.NB = (int)(N / tpq::kBlockCols);
+  L.NT = (int)(N / tpq::kTileCols);
   L.NG = (int)(K / G);
-  L.U = (int64_t)L.NB * L.NG;
-  if (const char* d = getenv("TPQ_GEMV_DEBUG")) L.dbg = atoi(d);
+  L.U = (int64_t)L.NT * L.NG;
   int sms = 148;
   if (device >= 0) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-  for (int MT = 1; MT <= tpq::kMaxMT; ++MT) {
-    int bps = device >= 0 ? tpq::gemv_blocks_per_sm(G, MT) : 1;
-    if (bps < 1) bps = 1;
-    int64_t grid = (int64_t)sms * bps;
-    const int64_t cap = std::max<int64_t>(1, L.U / 8);  // >= 8 units (one per warp) per CTA
-    grid = std::min(grid, cap);
-    L.grid[MT] = (int)grid;
-  }
+  int bps = device >= 0 ? tpq::gemv_blocks_per_sm(G) : 2;
+  if (bps < 1) bps = 1;
+  if (const char* e = getenv("TPQ_CTAS_PER_SM")) bps = std::max(1, std::min(bps, atoi(e)));  // tuning aid
+  const int64_t cap = std::max<int64_t>(1, L.U / 4);
+  L.grid = (int)std::min<int64_t>((int64_t)sms * bps, cap);
+  if (getenv("TPQ_VERBOSE"))
+    fprintf(stderr, "[tpq] layer K=%lld N=%lld G=%d: %d SMs x %d CTAs/SM -> grid %d over %lld units\n", (long long)K,
+            (long long)N, G, sms, bps, L.grid, (long long)L.U);
 }
 
 }  // namespace
@@ -298,8 +284,9 @@ int tp_shard_mlp(const gptq_layer* w1, const gptq_layer* w2, const int32_t* P1, 
   for (int G : {w1->G, w2->G})
     if (G != 32 && G != 64 && G != 128) return fail(TPQ_EUNSUPPORTED, "G=%d not in {32,64,128}", G);
   if (K1 % w1->G) return fail(TPQ_EUNSUPPORTED, "K1=%lld not a multiple of G1=%d (ragged group, c13)", (long long)K1, w1->G);
-  if (n % tpq::kBlockCols || N2 % tpq::kBlockCols)
-    return fail(TPQ_EINVAL, "n=N1/tp=%lld and N2=%lld must be multiples of 64", (long long)n, (long long)N2);
+  if (n % tpq::kTileCols || N2 % tpq::kTileCols)
+    return fail(TPQ_EINVAL, "n=N1/tp=%lld and N2=%lld must be multiples of 128 (device tiles)", (long long)n,
+                (long long)N2);
   if (n % w2->G) return fail(TPQ_EINVAL, "n=%lld not a multiple of G2=%d: W2 shard would split a group (c12)", (long long)n, w2->G);
   if ((rc = validate_perm(P1, w1, "P1"))) return rc;
   if ((rc = validate_perm(P2, w2, "P2"))) return rc;
@@ -362,35 +349,41 @@ int tp_shard_mlp(const gptq_layer* w1, const gptq_layer* w2, const int32_t* P1, 
     plan_layer(h->L2, n, N2, w2->G, device);
 
     if (device >= 0) {
-      TPQ_CUDA(cudaSetDevice(device));
-      auto A = [&](void** p, size_t b) { return dev_alloc(p, b); };
-      const size_t ws_floats = (size_t)std::max(std::max(h->L1.grid[1], h->L1.grid[2]),
-                                                std::max(h->L2.grid[1], h->L2.grid[2])) * 2 * 16 * 64;
-      if ((rc = A(&h->d_w1, h->pk1.size())) || (rc = A(&h->d_w2, h->pk2.size())) ||
-          (rc = A((void**)&h->d_P1, K1 * 4)) || (rc = A((void**)&h->d_gcols, n * 4)) ||
-          (rc = A(&h->d_xf1, 16 * K1 * 2)) || (rc = A(&h->d_xf2, 16 * n * 2)) ||
-          (rc = A(&h->d_y1, 16 * n * 2)) || (rc = A(&h->d_buf, (size_t)tp * 16 * n * 2)) ||
-          (rc = A(&h->d_xin, (size_t)M_max * K1 * 2)) || (rc = A(&h->d_yout, (size_t)M_max * N2 * 2)) ||
-          (rc = A((void**)&h->d_ws, ws_floats * 2 * 4)) ||
-          (rc = A((void**)&h->d_cnt, (size_t)(h->L1.NB + h->L2.NB) * 4))) {
+      auto upload = [&]() -> int {
+        TPQ_CUDA(cudaSetDevice(device));
+        int r;
+        auto A = [&](void** p, size_t b) { return dev_alloc(p, b); };
+        const size_t ws1 = (size_t)h->L1.grid * 2 * tpq::kNPad * tpq::kTileCols;
+        const size_t ws2 = (size_t)h->L2.grid * 2 * tpq::kNPad * tpq::kTileCols;
+        const size_t xb1 = (size_t)tpq::xext_bytes(K1, w1->G), xb2 = (size_t)tpq::xext_bytes(n, w2->G);
+        const size_t ncnt = (size_t)(h->L1.NT + h->L2.NT);
+        if ((r = A(&h->d_w1, h->pk1.size())) || (r = A(&h->d_w2, h->pk2.size())) ||
+            (r = A((void**)&h->d_P1, K1 * 4)) || (r = A((void**)&h->d_gcols, n * 4)) || (r = A(&h->d_xf1, xb1)) ||
+            (r = A(&h->d_xf2, xb2)) || (r = A(&h->d_buf, (size_t)tp * tpq::kMaxM * n * 2)) ||
+            (r = A(&h->d_xin, (size_t)M_max * K1 * 2)) || (r = A(&h->d_yout, (size_t)M_max * N2 * 2)) ||
+            (r = A((void**)&h->d_ws, (ws1 + ws2) * 4)) || (r = A((void**)&h->d_cnt, ncnt * 4)))
+          return r;
+        TPQ_CUDA(cudaMemcpy(h->d_w1, h->pk1.data(), h->pk1.size(), cudaMemcpyHostToDevice));
+        TPQ_CUDA(cudaMemcpy(h->d_w2, h->pk2.data(), h->pk2.size(), cudaMemcpyHostToDevice));
+        TPQ_CUDA(cudaMemcpy(h->d_P1, P1, K1 * 4, cudaMemcpyHostToDevice));
+        TPQ_CUDA(cudaMemcpy(h->d_gcols, h->gather_cols.data(), n * 4, cudaMemcpyHostToDevice));
+        TPQ_CUDA(cudaMemset(h->d_cnt, 0, ncnt * 4));
+        TPQ_CUDA(cudaMemset(h->d_xf1, 0, xb1));  // padding rows / unused correction slots stay 0
+        TPQ_CUDA(cudaMemset(h->d_xf2, 0, xb2));
+        h->L1.packed = (const uint8_t*)h->d_w1;
+        h->L2.packed = (const uint8_t*)h->d_w2;
+        h->L1.ws = h->d_ws;
+        h->L2.ws = h->d_ws + ws1;  // separate partial slots per layer
+        h->L1.cnt = h->d_cnt;
+        h->L2.cnt = h->d_cnt + h->L1.NT;
+        TPQ_CUDA(cudaDeviceSynchronize());
+        return TPQ_OK;
+      };
+      if ((rc = upload())) {
         free_dev(h);
         delete h;
         return rc;
       }
-      TPQ_CUDA(cudaMemcpy(h->d_w1, h->pk1.data(), h->pk1.size(), cudaMemcpyHostToDevice));
-      TPQ_CUDA(cudaMemcpy(h->d_w2, h->pk2.data(), h->pk2.size(), cudaMemcpyHostToDevice));
-      TPQ_CUDA(cudaMemcpy(h->d_P1, P1, K1 * 4, cudaMemcpyHostToDevice));
-      TPQ_CUDA(cudaMemcpy(h->d_gcols, h->gather_cols.data(), n * 4, cudaMemcpyHostToDevice));
-      TPQ_CUDA(cudaMemset(h->d_cnt, 0, (size_t)(h->L1.NB + h->L2.NB) * 4));
-      TPQ_CUDA(cudaMemset(h->d_xf1, 0, 16 * K1 * 2));
-      TPQ_CUDA(cudaMemset(h->d_xf2, 0, 16 * n * 2));
-      h->L1.packed = (const uint8_t*)h->d_w1;
-      h->L2.packed = (const uint8_t*)h->d_w2;
-      h->L1.ws = h->d_ws;
-      h->L2.ws = h->d_ws + ws_floats;  // separate partial slots per layer
-      h->L1.cnt = h->d_cnt;
-      h->L2.cnt = h->d_cnt + h->L1.NB;
-      TPQ_CUDA(cudaDeviceSynchronize());
     }
     *out = h;
     return TPQ_OK;
@@ -479,26 +472,26 @@ int check_fwd(tpq_mlp* h, const void* X, int64_t M, const void* Y) {
   if (h->timing) TPQ_CUDA(cudaEventRecordWithFlags(h->ev[i], st, cudaEventRecordExternal))
 
 int chunk_forward(tpq_mlp* h, const uint16_t* X, int mc, void* Y, cudaStream_t st, bool collective) {
-  TPQ_CUDA(tpq::launch_to_frag(X, h->K1, h->d_P1, tpq::GATHER_COLS, 0, mc, h->K1, h->d_xf1, st));  // X[:, P1]
+  TPQ_CUDA(tpq::launch_to_xext(X, h->K1, h->d_P1, tpq::GATHER_COLS, 0, mc, h->K1, h->G1, h->d_xf1, st));  // X[:,P1]
   TPQ_MARK(1);
   if (h->variant == TPQ_TP_AWARE) {
-    // Alg. 3 L1: Y1_local lands directly in the layout layer 2 consumes (already in P2 order)
-    TPQ_CUDA(tpq::launch_gemv(h->L1, h->d_xf1, mc, h->d_xf2, tpq::OUT_FRAG, 0, st));
+    // Alg. 3 L1: Y1_local lands directly in the operand layout layer 2 consumes (already in P2 order)
+    TPQ_CUDA(tpq::launch_gemv(h->L1, h->d_xf1, mc, h->d_xf2, tpq::OUT_XEXT, 0, h->G2, st));
     TPQ_MARK(2);
   } else {
     // Alg. 2 L1 into this rank's slot of the AllGather buffer [tp][mc][n]
     uint8_t* slot = (uint8_t*)h->d_buf + (size_t)h->rank * mc * h->n * 2;
-    TPQ_CUDA(tpq::launch_gemv(h->L1, h->d_xf1, mc, slot, tpq::OUT_ROWMAJOR, h->n, st));
+    TPQ_CUDA(tpq::launch_gemv(h->L1, h->d_xf1, mc, slot, tpq::OUT_ROWMAJOR, h->n, 0, st));
     TPQ_MARK(2);
     if (h->tp > 1) {
       if (!collective) return fail(TPQ_ESTATE, "naive variant with tp > 1 needs the AllGather (use tp_mlp_forward)");
       TPQ_NCCL(ncclAllGather(slot, h->d_buf, (size_t)mc * h->n, ncclFloat16, h->comm, st));  // Alg. 2 L2
     }
-    // Alg. 2 L3-4: Y1_global[:, P2] then CHUNK(rank), fused into one gather to the frag layout
-    TPQ_CUDA(tpq::launch_to_frag(h->d_buf, 0, h->d_gcols, tpq::GATHER_ALLGATHER, h->n, mc, h->n, h->d_xf2, st));
+    // Alg. 2 L3-4: Y1_global[:, P2] then CHUNK(rank), fused into one gather to the operand layout
+    TPQ_CUDA(tpq::launch_to_xext(h->d_buf, 0, h->d_gcols, tpq::GATHER_ALLGATHER, h->n, mc, h->n, h->G2, h->d_xf2, st));
   }
   TPQ_MARK(3);
-  TPQ_CUDA(tpq::launch_gemv(h->L2, h->d_xf2, mc, Y, tpq::OUT_ROWMAJOR, h->N2, st));  // L2 GEMM
+  TPQ_CUDA(tpq::launch_gemv(h->L2, h->d_xf2, mc, Y, tpq::OUT_ROWMAJOR, h->N2, 0, st));  // L2 GEMM
   TPQ_MARK(4);
   return TPQ_OK;
 }
@@ -554,10 +547,10 @@ int tpq_layer1(tpq_mlp* h, const void* X, int64_t M, void* Y1_local, void* strea
   TPQ_CUDA(cudaSetDevice(h->device));
   for (int64_t m0 = 0; m0 < M; m0 += 16) {
     const int mc = (int)std::min<int64_t>(16, M - m0);
-    TPQ_CUDA(tpq::launch_to_frag((const uint16_t*)X + m0 * h->K1, h->K1, h->d_P1, tpq::GATHER_COLS, 0, mc, h->K1,
-                                 h->d_xf1, st));
+    TPQ_CUDA(tpq::launch_to_xext((const uint16_t*)X + m0 * h->K1, h->K1, h->d_P1, tpq::GATHER_COLS, 0, mc, h->K1,
+                                 h->G1, h->d_xf1, st));
     TPQ_CUDA(tpq::launch_gemv(h->L1, h->d_xf1, mc, (uint8_t*)Y1_local + (size_t)m0 * h->n * 2, tpq::OUT_ROWMAJOR,
-                              h->n, st));
+                              h->n, 0, st));
   }
   return TPQ_OK;
 }
@@ -579,10 +572,10 @@ int tpq_layer2(tpq_mlp* h, const void* Y1in, int64_t M, void* Y2_local, void* st
   TPQ_CUDA(cudaSetDevice(h->device));
   for (int64_t m0 = 0; m0 < M; m0 += 16) {
     const int mc = (int)std::min<int64_t>(16, M - m0);
-    TPQ_CUDA(tpq::launch_to_frag((const uint16_t*)Y1in + m0 * h->n, h->n, nullptr, tpq::GATHER_COLS, 0, mc, h->n,
-                                 h->d_xf2, st));
+    TPQ_CUDA(tpq::launch_to_xext((const uint16_t*)Y1in + m0 * h->n, h->n, nullptr, tpq::GATHER_COLS, 0, mc, h->n,
+                                 h->G2, h->d_xf2, st));
     TPQ_CUDA(tpq::launch_gemv(h->L2, h->d_xf2, mc, (uint8_t*)Y2_local + (size_t)m0 * h->N2 * 2, tpq::OUT_ROWMAJOR,
-                              h->N2, st));
+                              h->N2, 0, st));
   }
   return TPQ_OK;
 }
@@ -595,6 +588,12 @@ int tpq_sum_partials(const void* const* parts, int nparts, int64_t count, void* 
   TPQ_CUDA(tpq::launch_sum_partials(parts, nparts, count, out, (cudaStream_t)stream));
   return TPQ_OK;
 }
+
+#ifdef TPQ_PROF
+// Profiling build only (libtpq_prof.so): accumulated wait cycles per role, then reset.
+int tpq_debug_prof(unsigned long long* out) { return tpq::prof_read(out) ? TPQ_ECUDA : TPQ_OK; }
+int tpq_debug_trace(long long* out) { return tpq::trace_read(out) ? TPQ_ECUDA : TPQ_OK; }
+#endif
 
 int tpq_mlp_set_timing(tpq_mlp* h, void* const* events) {
   if (!h) return fail(TPQ_EINVAL, "NULL handle");
@@ -618,8 +617,8 @@ int tpq_mlp_info(const tpq_mlp* h, tpq_mlp_info_t* o) {
   o->w2_bytes = (int64_t)h->pk2.size();
   o->units1 = h->L1.U;
   o->units2 = h->L2.U;
-  o->grid1 = h->L1.grid[1];
-  o->grid2 = h->L2.grid[1];
+  o->grid1 = h->L1.grid;
+  o->grid2 = h->L2.grid;
   o->has_comm = h->comm != nullptr;
   return TPQ_OK;
 }

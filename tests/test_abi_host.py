@@ -80,7 +80,8 @@ def _olayers(p):
 @pytest.mark.parametrize("variant", ["tp_aware", "naive"])
 @pytest.mark.parametrize("tp", [1, 2, 4, 8])
 def test_shard_maps_and_packed_layout_match_oracle(tp, variant):
-    p = synth.make_named("tiny", 1, seed=3)
+    # tiny config widened to N1=1024 so every tp gives whole 128-column device tiles
+    p = synth.make_problem(256, 1024, 256, 32, 1, seed=3)
     P1, P2 = _prep(p)
     L1, L2 = _olayers(p)
     v = tpq.TPQ_TP_AWARE if variant == "tp_aware" else tpq.TPQ_NAIVE
@@ -101,7 +102,7 @@ def test_shard_maps_and_packed_layout_match_oracle(tp, variant):
         assert (ref["w1_g"] == np.arange(p.K1) // p.G).all()
         assert (ref["w2_g"] == np.arange(p.N1 // tp) // p.G).all()
         i = h.info
-        assert i.w1_bytes == (p.N1 // tp // 64) * (p.K1 // p.G) * (32 * p.G + 160)
+        assert i.w1_bytes == (p.N1 // tp // 128) * (p.K1 // p.G) * (64 * p.G + 320)
         h.close()
 
 
