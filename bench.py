@@ -234,30 +234,45 @@ def main():
             fwd(hs[i % R])
     sync_all()
 
-    # ---------------- timed region: K steps, per-kernel events via the library timing hook.
-    # Default: the steps are replayed from a CUDA graph of `per_graph` consecutive forwards
-    # (rotating the weight replicas) so host launch overhead is not measured; --no-graph
-    # launches every forward eagerly through the C-ABI.
+    # ---------------- timed region: exactly K steps.
+    # Default: the steps are replayed from CUDA graphs of consecutive forwards (rotating the
+    # weight replicas) so host launch overhead is not measured: a graph of `per_graph` forwards
+    # replayed K // per_graph times plus a graph of the K % per_graph remaining forwards.  No
+    # timing events sit inside these graphs (an event node between kernels would break the
+    # programmatic-dependent-launch overlap); the per-kernel breakdown comes from a separate
+    # graph with the library's event hook, replayed after the timed region.
+    # --no-graph launches every forward eagerly through the C-ABI.
+    K = a.steps
     per_graph = R * max(1, 16 // R)
-    n_ev = per_graph if not a.no_graph else min(a.steps, 512)
+    rem = K % per_graph
+
+    def capture(n, timed_evs=None):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            for i in range(n):
+                h = hs[i % R]
+                if timed_evs is not None:
+                    h.set_timing(timed_evs[i])
+                fwd(h)
+                if timed_evs is not None:
+                    h.set_timing(None)
+        return g
+
+    n_ev = per_graph
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(n_ev)]
     for es_ in evs:  # torch creates the cudaEvent_t lazily, on first record
         for e in es_:
             e.record(stream)
     sync_all()
-    graph = None
+    graph = graph_rem = None
     if not a.no_graph:
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph, stream=stream):
-            for i in range(per_graph):
-                h = hs[i % R]
-                h.set_timing(evs[i])
-                fwd(h)
-                h.set_timing(None)
+        graph = capture(per_graph)
+        graph_rem = capture(rem) if rem else None
         for _ in range(max(3, a.warmup // per_graph)):
             graph.replay()
+        if graph_rem is not None:
+            graph_rem.replay()
         sync_all()
-    K = -(-a.steps // per_graph) * per_graph if graph is not None else a.steps
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     clocks = ClockSampler(local)
     clocks.start()
@@ -268,15 +283,11 @@ def main():
         if graph is not None:
             for _ in range(K // per_graph):
                 graph.replay()
+            if graph_rem is not None:
+                graph_rem.replay()
         else:
             for i in range(K):
-                h = hs[i % R]
-                j = i - (K - n_ev)
-                if j >= 0:
-                    h.set_timing(evs[j])
-                fwd(h)
-                if j >= 0:
-                    h.set_timing(None)
+                fwd(hs[i % R])
         end.record(stream)
     sync_all()
     clk = clocks.stop()
@@ -286,6 +297,20 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     ms_per_step = total_ms / K
+
+    # ---------------- per-kernel breakdown (events around each launch; not the headline)
+    with torch.cuda.stream(stream):
+        if graph is not None:
+            gev = capture(per_graph, evs)
+            for _ in range(3):
+                gev.replay()
+        else:
+            for i in range(n_ev):
+                h = hs[i % R]
+                h.set_timing(evs[i])
+                fwd(h)
+                h.set_timing(None)
+    sync_all()
     t_l1 = statistics.mean(e[1].elapsed_time(e[2]) for e in evs) * 1e3  # us
     t_l2 = statistics.mean(e[3].elapsed_time(e[4]) for e in evs) * 1e3
     t_gather = statistics.mean(e[0].elapsed_time(e[1]) for e in evs) * 1e3
@@ -324,7 +349,8 @@ def main():
                         + (" (one rank's shard, no collective)" if sim_tp else ""),
             "M": M, "tp": shard_tp, "variant": a.variant, "int4_weights": True,
             "cold_l2": f"{R} rotating weight replicas x {step_bytes / 1e6:.1f} MB >= 3 x L2 ({l2_cache / 1e6:.0f} MB)",
-            "launch": "eager C-ABI calls" if graph is None else f"CUDA graph of {per_graph} forwards, replayed",
+            "launch": "eager C-ABI calls" if graph is None else
+                      f"CUDA graphs: {per_graph} forwards x {K // per_graph} replays + {rem}",
             "parallelism": f"tp{shard_tp}",
         },
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

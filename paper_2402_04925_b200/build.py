@@ -37,10 +37,11 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False, prof: bool = False) -> str:
-    """prof=True builds libtpq_prof.so with -DTPQ_PROF (wait-cycle accounting, profiling only)."""
-    lib = LIB.replace("libtpq.so", "libtpq_prof.so") if prof else LIB
-    if not force and not prof and not _stale():
+def build(force: bool = False, verbose: bool = False, prof: bool = False, defines=(), name=None) -> str:
+    """prof=True builds libtpq_prof.so with -DTPQ_PROF (per-CTA timeline, profiling only);
+    `defines` + `name` build experiment variants (e.g. ablations) next to the product library."""
+    lib = os.path.join(PKG, name) if name else (LIB.replace("libtpq.so", "libtpq_prof.so") if prof else LIB)
+    if not force and not prof and not name and not _stale():
         return LIB
     nr = nccl_root()
     cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC,-O3",
@@ -49,7 +50,7 @@ def build(force: bool = False, verbose: bool = False, prof: bool = False) -> str
            *[os.path.join(CSRC, s) for s in SOURCES],
            "-L", os.path.join(nr, "lib"), "-l:libnccl.so.2",
            f"-Xlinker=-rpath,{os.path.join(nr, 'lib')}",
-           *(["-DTPQ_PROF"] if prof else []),
+           *(["-DTPQ_PROF"] if prof else []), *[f"-D{d}" for d in defines],
            "-o", lib + ".tmp"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:

@@ -78,24 +78,28 @@ struct Canon {
 constexpr int kNibbleOfK[8] = {0, 4, 1, 5, 2, 6, 3, 7};
 
 std::vector<uint8_t> pack_layer(const Canon& c) {
-  const int G = c.G, NCH = G / 32;
-  const int64_t NT = c.N / tpq::kTileCols, NG = c.K / G, UB = tpq::unit_bytes(G);
-  std::vector<uint8_t> out((size_t)(NT * NG * UB), 0);
-  parallel_for(NT * NG, [&](int64_t u) {
-    const int64_t t = u / NG, g = u % NG;
+  const int G = c.G, KG = tpq::kUnitK / G;
+  const int64_t NT = c.N / tpq::kTileCols, NKB = c.K / tpq::kUnitK, UB = tpq::unit_bytes(G);
+  constexpr int64_t kCodes = tpq::kUnitK * tpq::kTileCols / 2;
+  std::vector<uint8_t> out((size_t)(NT * NKB * UB), 0);
+  parallel_for(NT * NKB, [&](int64_t u) {
+    const int64_t t = u / NKB, kb = u % NKB;
     uint8_t* rec = out.data() + u * UB;
     uint32_t* words = reinterpret_cast<uint32_t*>(rec);
     for (int j = 0; j < tpq::kTileCols; ++j) {
       const int64_t n = t * tpq::kTileCols + j;
-      for (int ch = 0; ch < NCH; ++ch)
+      for (int ch = 0; ch < tpq::kUnitK / 32; ++ch)
         for (int w = 0; w < 4; ++w) {
-          const int64_t k0 = g * G + 32 * ch + 8 * w;
+          const int64_t k0 = kb * tpq::kUnitK + 32 * ch + 8 * w;
           uint32_t word = 0;
           for (int i = 0; i < 8; ++i) word |= (uint32_t)c.q[(size_t)((k0 + i) * c.N + n)] << (4 * kNibbleOfK[i]);
           words[(ch * tpq::kTileCols + j) * 4 + w] = word;
         }
-      memcpy(rec + 64LL * G + 2 * j, &c.s[(size_t)(g * c.N + n)], 2);
-      rec[64LL * G + 256 + j / 2] |= (uint8_t)(c.z[(size_t)(g * c.N + n)] << (4 * (j & 1)));
+      for (int gi = 0; gi < KG; ++gi) {
+        const int64_t g = kb * KG + gi;
+        memcpy(rec + kCodes + 256 * gi + 2 * j, &c.s[(size_t)(g * c.N + n)], 2);
+        rec[kCodes + 256 * KG + 64 * gi + j / 2] |= (uint8_t)(c.z[(size_t)(g * c.N + n)] << (4 * (j & 1)));
+      }
     }
   });
   return out;
@@ -104,22 +108,26 @@ std::vector<uint8_t> pack_layer(const Canon& c) {
 // Inverse of pack_layer (test export).
 void unpack_layer(const std::vector<uint8_t>& pk, int64_t K, int64_t N, int G, uint8_t* q, uint16_t* s,
                   uint8_t* z) {
-  const int NCH = G / 32;
-  const int64_t NT = N / tpq::kTileCols, NG = K / G, UB = tpq::unit_bytes(G);
-  parallel_for(NT * NG, [&](int64_t u) {
-    const int64_t t = u / NG, g = u % NG;
+  const int KG = tpq::kUnitK / G;
+  const int64_t NT = N / tpq::kTileCols, NKB = K / tpq::kUnitK, UB = tpq::unit_bytes(G);
+  constexpr int64_t kCodes = tpq::kUnitK * tpq::kTileCols / 2;
+  parallel_for(NT * NKB, [&](int64_t u) {
+    const int64_t t = u / NKB, kb = u % NKB;
     const uint8_t* rec = pk.data() + u * UB;
     const uint32_t* words = reinterpret_cast<const uint32_t*>(rec);
     for (int j = 0; j < tpq::kTileCols; ++j) {
       const int64_t n = t * tpq::kTileCols + j;
-      for (int ch = 0; ch < NCH; ++ch)
+      for (int ch = 0; ch < tpq::kUnitK / 32; ++ch)
         for (int w = 0; w < 4; ++w) {
           const uint32_t word = words[(ch * tpq::kTileCols + j) * 4 + w];
-          const int64_t k0 = g * G + 32 * ch + 8 * w;
+          const int64_t k0 = kb * tpq::kUnitK + 32 * ch + 8 * w;
           for (int i = 0; i < 8; ++i) q[(k0 + i) * N + n] = (word >> (4 * kNibbleOfK[i])) & 0xF;
         }
-      memcpy(&s[g * N + n], rec + 64LL * G + 2 * j, 2);
-      z[g * N + n] = (rec[64LL * G + 256 + j / 2] >> (4 * (j & 1))) & 0xF;
+      for (int gi = 0; gi < KG; ++gi) {
+        const int64_t g = kb * KG + gi;
+        memcpy(&s[g * N + n], rec + kCodes + 256 * gi + 2 * j, 2);
+        z[g * N + n] = (rec[kCodes + 256 * KG + 64 * gi + j / 2] >> (4 * (j & 1))) & 0xF;
+      }
     }
   });
 }
@@ -145,13 +153,14 @@ struct tpq_mlp {
   void* d_w2 = nullptr;
   int32_t* d_P1 = nullptr;
   int32_t* d_gcols = nullptr;  // naive: P2[r n .. (r+1) n)
-  void* d_xf1 = nullptr;       // layer-1 B operand: X[:, P1] (xext layout, internal.h)
-  void* d_xf2 = nullptr;       // layer-2 B operand: Y1_local (xext layout)
+  void* d_x1 = nullptr;        // layer-1 input X[:, P1], row-major [16][K1]
+  void* d_y1 = nullptr;        // layer-1 output = layer-2 input, row-major [16][n]
   void* d_buf = nullptr;       // AllGather buffer [tp][16][n]
   void* d_xin = nullptr;       // host-forward staging [M_max][K1]
   void* d_yout = nullptr;      // host-forward staging [M_max][N2]
   float* d_ws = nullptr;
   int* d_cnt = nullptr;
+  CUtensorMap xmap1 = {}, xmap2 = {};  // TMA views of d_x1 / d_y1 (GEMV activation operand)
   ncclComm_t comm = nullptr;
   cudaEvent_t ev[6] = {};
   bool timing = false;
@@ -189,7 +198,7 @@ int validate_perm(const int32_t* P, const gptq_layer* w, const char* name) {
 void free_dev(tpq_mlp* h) {
   if (h->device < 0) return;
   cudaSetDevice(h->device);
-  void* ptrs[] = {h->d_w1, h->d_w2, h->d_P1, h->d_gcols, h->d_xf1, h->d_xf2, h->d_buf, h->d_xin, h->d_yout, h->d_ws, h->d_cnt};
+  void* ptrs[] = {h->d_w1, h->d_w2, h->d_P1, h->d_gcols, h->d_x1, h->d_y1, h->d_buf, h->d_xin, h->d_yout, h->d_ws, h->d_cnt};
   for (void* p : ptrs)
     if (p) cudaFree(p);
 }
@@ -204,25 +213,26 @@ int dev_alloc(void** p, size_t bytes) {
   return TPQ_OK;
 }
 
-// Stream-K plan: a persistent grid of SMs x resident CTAs, each CTA a contiguous range of
-// (tile, group) units; at least 4 units per CTA so the TMA ring has work to overlap.
+// Stream-K plan: a persistent grid of one CTA per SM, each CTA a contiguous range of
+// (tile, k-block) units; at least 4 units per CTA so the TMA ring has work to overlap.
 void plan_layer(tpq::LayerDev& L, int64_t K, int64_t N, int G, int device) {
   L.K = K;
   L.N = N;
   L.G = G;
   L.NT = (int)(N / tpq::kTileCols);
-  L.NG = (int)(K / G);
-  L.U = (int64_t)L.NT * L.NG;
+  L.NKB = (int)(K / tpq::kUnitK);
+  L.U = (int64_t)L.NT * L.NKB;
   int sms = 148;
-  if (device >= 0) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-  int bps = device >= 0 ? tpq::gemv_blocks_per_sm(G) : 2;
-  if (bps < 1) bps = 1;
-  if (const char* e = getenv("TPQ_CTAS_PER_SM")) bps = std::max(1, std::min(bps, atoi(e)));  // tuning aid
+  if (device >= 0) {
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    tpq::gemv_prepare(G);
+  }
+  if (const char* e = getenv("TPQ_GRID")) sms = std::max(1, std::min(sms, atoi(e)));  // tuning aid
   const int64_t cap = std::max<int64_t>(1, L.U / 4);
-  L.grid = (int)std::min<int64_t>((int64_t)sms * bps, cap);
+  L.grid = (int)std::min<int64_t>((int64_t)sms, cap);
   if (getenv("TPQ_VERBOSE"))
-    fprintf(stderr, "[tpq] layer K=%lld N=%lld G=%d: %d SMs x %d CTAs/SM -> grid %d over %lld units\n", (long long)K,
-            (long long)N, G, sms, bps, L.grid, (long long)L.U);
+    fprintf(stderr, "[tpq] layer K=%lld N=%lld G=%d: grid %d over %lld units\n", (long long)K, (long long)N, G,
+            L.grid, (long long)L.U);
 }
 
 }  // namespace
@@ -284,6 +294,8 @@ int tp_shard_mlp(const gptq_layer* w1, const gptq_layer* w2, const int32_t* P1, 
   for (int G : {w1->G, w2->G})
     if (G != 32 && G != 64 && G != 128) return fail(TPQ_EUNSUPPORTED, "G=%d not in {32,64,128}", G);
   if (K1 % w1->G) return fail(TPQ_EUNSUPPORTED, "K1=%lld not a multiple of G1=%d (ragged group, c13)", (long long)K1, w1->G);
+  if (K1 % tpq::kUnitK)
+    return fail(TPQ_EUNSUPPORTED, "K1=%lld not a multiple of 128 (device k-blocks)", (long long)K1);
   if (n % tpq::kTileCols || N2 % tpq::kTileCols)
     return fail(TPQ_EINVAL, "n=N1/tp=%lld and N2=%lld must be multiples of 128 (device tiles)", (long long)n,
                 (long long)N2);
@@ -355,11 +367,10 @@ int tp_shard_mlp(const gptq_layer* w1, const gptq_layer* w2, const int32_t* P1, 
         auto A = [&](void** p, size_t b) { return dev_alloc(p, b); };
         const size_t ws1 = (size_t)h->L1.grid * 2 * tpq::kNPad * tpq::kTileCols;
         const size_t ws2 = (size_t)h->L2.grid * 2 * tpq::kNPad * tpq::kTileCols;
-        const size_t xb1 = (size_t)tpq::xext_bytes(K1, w1->G), xb2 = (size_t)tpq::xext_bytes(n, w2->G);
         const size_t ncnt = (size_t)(h->L1.NT + h->L2.NT);
         if ((r = A(&h->d_w1, h->pk1.size())) || (r = A(&h->d_w2, h->pk2.size())) ||
-            (r = A((void**)&h->d_P1, K1 * 4)) || (r = A((void**)&h->d_gcols, n * 4)) || (r = A(&h->d_xf1, xb1)) ||
-            (r = A(&h->d_xf2, xb2)) || (r = A(&h->d_buf, (size_t)tp * tpq::kMaxM * n * 2)) ||
+            (r = A((void**)&h->d_P1, K1 * 4)) || (r = A((void**)&h->d_gcols, n * 4)) || (r = A(&h->d_x1, (size_t)tpq::kMaxM * K1 * 2)) ||
+            (r = A(&h->d_y1, (size_t)tpq::kMaxM * n * 2)) || (r = A(&h->d_buf, (size_t)tp * tpq::kMaxM * n * 2)) ||
             (r = A(&h->d_xin, (size_t)M_max * K1 * 2)) || (r = A(&h->d_yout, (size_t)M_max * N2 * 2)) ||
             (r = A((void**)&h->d_ws, (ws1 + ws2) * 4)) || (r = A((void**)&h->d_cnt, ncnt * 4)))
           return r;
@@ -368,8 +379,8 @@ int tp_shard_mlp(const gptq_layer* w1, const gptq_layer* w2, const int32_t* P1, 
         TPQ_CUDA(cudaMemcpy(h->d_P1, P1, K1 * 4, cudaMemcpyHostToDevice));
         TPQ_CUDA(cudaMemcpy(h->d_gcols, h->gather_cols.data(), n * 4, cudaMemcpyHostToDevice));
         TPQ_CUDA(cudaMemset(h->d_cnt, 0, ncnt * 4));
-        TPQ_CUDA(cudaMemset(h->d_xf1, 0, xb1));  // padding rows / unused correction slots stay 0
-        TPQ_CUDA(cudaMemset(h->d_xf2, 0, xb2));
+        if (!tpq::make_xmap(&h->xmap1, h->d_x1, K1) || !tpq::make_xmap(&h->xmap2, h->d_y1, n))
+          return fail(TPQ_ECUDA, "cuTensorMapEncodeTiled failed for the activation buffers");
         h->L1.packed = (const uint8_t*)h->d_w1;
         h->L2.packed = (const uint8_t*)h->d_w2;
         h->L1.ws = h->d_ws;
@@ -469,29 +480,39 @@ int check_fwd(tpq_mlp* h, const void* X, int64_t M, const void* Y) {
 // AllGather (tp > 1); otherwise the naive path must be at tp == 1.
 // External event record: under stream capture this becomes a timed event node of the graph.
 #define TPQ_MARK(i) \
-  if (h->timing) TPQ_CUDA(cudaEventRecordWithFlags(h->ev[i], st, cudaEventRecordExternal))
+  if (h->timing) TPQ_CUDA(mark_event(h->ev[i], st))
+
+// Under stream capture an external record becomes a timed event node of the graph; outside a
+// capture a plain record is the only legal form.
+static cudaError_t mark_event(cudaEvent_t e, cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaError_t err = cudaStreamIsCapturing(st, &cs);
+  if (err != cudaSuccess) return err;
+  return cs == cudaStreamCaptureStatusActive ? cudaEventRecordWithFlags(e, st, cudaEventRecordExternal)
+                                             : cudaEventRecord(e, st);
+}
 
 int chunk_forward(tpq_mlp* h, const uint16_t* X, int mc, void* Y, cudaStream_t st, bool collective) {
-  TPQ_CUDA(tpq::launch_to_xext(X, h->K1, h->d_P1, tpq::GATHER_COLS, 0, mc, h->K1, h->G1, h->d_xf1, st));  // X[:,P1]
+  TPQ_CUDA(tpq::launch_gather_rowmajor(X, h->K1, h->d_P1, tpq::GATHER_COLS, 0, mc, h->K1, h->d_x1, st));  // X[:,P1]
   TPQ_MARK(1);
   if (h->variant == TPQ_TP_AWARE) {
-    // Alg. 3 L1: Y1_local lands directly in the operand layout layer 2 consumes (already in P2 order)
-    TPQ_CUDA(tpq::launch_gemv(h->L1, h->d_xf1, mc, h->d_xf2, tpq::OUT_XEXT, 0, h->G2, st));
+    // Alg. 3 L1: Y1_local is already in the row order of this rank's W2[P2] block (no exchange)
+    TPQ_CUDA(tpq::launch_gemv(h->L1, h->xmap1, mc, h->d_y1, h->n, st));
     TPQ_MARK(2);
   } else {
     // Alg. 2 L1 into this rank's slot of the AllGather buffer [tp][mc][n]
     uint8_t* slot = (uint8_t*)h->d_buf + (size_t)h->rank * mc * h->n * 2;
-    TPQ_CUDA(tpq::launch_gemv(h->L1, h->d_xf1, mc, slot, tpq::OUT_ROWMAJOR, h->n, 0, st));
+    TPQ_CUDA(tpq::launch_gemv(h->L1, h->xmap1, mc, slot, h->n, st));
     TPQ_MARK(2);
     if (h->tp > 1) {
       if (!collective) return fail(TPQ_ESTATE, "naive variant with tp > 1 needs the AllGather (use tp_mlp_forward)");
       TPQ_NCCL(ncclAllGather(slot, h->d_buf, (size_t)mc * h->n, ncclFloat16, h->comm, st));  // Alg. 2 L2
     }
-    // Alg. 2 L3-4: Y1_global[:, P2] then CHUNK(rank), fused into one gather to the operand layout
-    TPQ_CUDA(tpq::launch_to_xext(h->d_buf, 0, h->d_gcols, tpq::GATHER_ALLGATHER, h->n, mc, h->n, h->G2, h->d_xf2, st));
+    // Alg. 2 L3-4: Y1_global[:, P2] then CHUNK(rank), fused into one gather
+    TPQ_CUDA(tpq::launch_gather_rowmajor(h->d_buf, 0, h->d_gcols, tpq::GATHER_ALLGATHER, h->n, mc, h->n, h->d_y1, st));
   }
   TPQ_MARK(3);
-  TPQ_CUDA(tpq::launch_gemv(h->L2, h->d_xf2, mc, Y, tpq::OUT_ROWMAJOR, h->N2, 0, st));  // L2 GEMM
+  TPQ_CUDA(tpq::launch_gemv(h->L2, h->xmap2, mc, Y, h->N2, st));  // L2 GEMM
   TPQ_MARK(4);
   return TPQ_OK;
 }
@@ -547,10 +568,9 @@ int tpq_layer1(tpq_mlp* h, const void* X, int64_t M, void* Y1_local, void* strea
   TPQ_CUDA(cudaSetDevice(h->device));
   for (int64_t m0 = 0; m0 < M; m0 += 16) {
     const int mc = (int)std::min<int64_t>(16, M - m0);
-    TPQ_CUDA(tpq::launch_to_xext((const uint16_t*)X + m0 * h->K1, h->K1, h->d_P1, tpq::GATHER_COLS, 0, mc, h->K1,
-                                 h->G1, h->d_xf1, st));
-    TPQ_CUDA(tpq::launch_gemv(h->L1, h->d_xf1, mc, (uint8_t*)Y1_local + (size_t)m0 * h->n * 2, tpq::OUT_ROWMAJOR,
-                              h->n, 0, st));
+    TPQ_CUDA(tpq::launch_gather_rowmajor((const uint16_t*)X + m0 * h->K1, h->K1, h->d_P1, tpq::GATHER_COLS, 0, mc,
+                                         h->K1, h->d_x1, st));
+    TPQ_CUDA(tpq::launch_gemv(h->L1, h->xmap1, mc, (uint8_t*)Y1_local + (size_t)m0 * h->n * 2, h->n, st));
   }
   return TPQ_OK;
 }
@@ -572,10 +592,10 @@ int tpq_layer2(tpq_mlp* h, const void* Y1in, int64_t M, void* Y2_local, void* st
   TPQ_CUDA(cudaSetDevice(h->device));
   for (int64_t m0 = 0; m0 < M; m0 += 16) {
     const int mc = (int)std::min<int64_t>(16, M - m0);
-    TPQ_CUDA(tpq::launch_to_xext((const uint16_t*)Y1in + m0 * h->n, h->n, nullptr, tpq::GATHER_COLS, 0, mc, h->n,
-                                 h->G2, h->d_xf2, st));
-    TPQ_CUDA(tpq::launch_gemv(h->L2, h->d_xf2, mc, (uint8_t*)Y2_local + (size_t)m0 * h->N2 * 2, tpq::OUT_ROWMAJOR,
-                              h->N2, 0, st));
+    // the GEMV reads its activations through the TMA view of d_y1
+    TPQ_CUDA(tpq::launch_gather_rowmajor((const uint16_t*)Y1in + m0 * h->n, h->n, nullptr, tpq::GATHER_COLS, 0, mc,
+                                         h->n, h->d_y1, st));
+    TPQ_CUDA(tpq::launch_gemv(h->L2, h->xmap2, mc, (uint8_t*)Y2_local + (size_t)m0 * h->N2 * 2, h->N2, st));
   }
   return TPQ_OK;
 }
@@ -590,7 +610,8 @@ int tpq_sum_partials(const void* const* parts, int nparts, int64_t count, void* 
 }
 
 #ifdef TPQ_PROF
-// Profiling build only (libtpq_prof.so): accumulated wait cycles per role, then reset.
+// Profiling build only (libtpq_prof.so): per-CTA GEMV timeline of the last launches.
+int tpq_debug_cta(unsigned long long* out) { return tpq::cta_read(out) ? TPQ_ECUDA : TPQ_OK; }
 int tpq_debug_prof(unsigned long long* out) { return tpq::prof_read(out) ? TPQ_ECUDA : TPQ_OK; }
 int tpq_debug_trace(long long* out) { return tpq::trace_read(out) ? TPQ_ECUDA : TPQ_OK; }
 #endif

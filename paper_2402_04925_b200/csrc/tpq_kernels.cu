@@ -1,23 +1,24 @@
 // sm_100a kernels of the TP-aware GPTQ MLP hot path (arxiv 2402.04925).
 //
-//  k_tcgemv<G>     one dequant-GEMM layer for M <= 16:  Y = X . deq(W),  deq = s * (q - z)
+//  k_dqgemv<G>     one dequant-GEMM layer for M <= 16:  Y = X . deq(W),  deq = s (q - z)
 //                  (PAPER.md:L19 per-group scales/zeros; after Alg. 1 every group is G
-//                  consecutive rows, so the fp32 scale is applied once per group).
-//                  Blackwell-native: per CTA, one warp streams (128-column tile x group) weight
-//                  records and the matching activation block into a shared-memory ring with TMA
-//                  bulk copies (mbarrier complete_tx, L2 evict-first for the weights); four
-//                  warps turn int4 codes into f16 MMA operands with LOP3 magic numbers straight
-//                  into TENSOR MEMORY (tcgen05.st, A operand); one thread issues tcgen05.mma
-//                  kind::f16 (M=128 columns, N=16 batch rows, A from TMEM, B = activations from
-//                  smem, D fp32 in TMEM); the same four warps read D back per group (tcgen05.ld)
-//                  and apply the fp32 scale.  The zero point and the magic-number offsets are
-//                  folded into one extra K=16 MMA per group (correction block, internal.h).
-//                  Persistent stream-K over units with a deterministic last-arriver fix-up;
-//                  programmatic dependent launch (weight prefetch overlaps the previous kernel).
-//  k_to_xext       X[:, P1] gather (Alg. 3 L1) or the naive AllGather
-//                  re-permute + CHUNK (Alg. 2 L3-4) into the B-operand layout.
-//  k_gather_rm     the same gathers to row-major (staged API).
+//                  consecutive rows, so a 128-row k-block carries 128/G groups'
+//                  metadata next to its codes).  Blackwell-native: per SM one persistent CTA;
+//                  one warp streams (128-column tile x 128-row k-block) weight records into a
+//                  shared-memory ring with TMA bulk copies (mbarrier complete_tx, L2 evict-first);
+//                  16 warps turn int4 codes into s (q - z) f16 with LOP3 magic numbers straight
+//                  into TENSOR MEMORY (tcgen05.st, the MMA A operand); one warp stages the M real
+//                  activation slice (tensor TMA); one thread issues tcgen05.mma kind::f16 (M=128
+//                  columns, N=16 batch rows, A from TMEM, B = activations from smem), the
+//                  accumulator of a tile segment stays in TMEM; four warps read it back once per
+//                  segment.  Persistent stream-K over units with a deterministic last-arriver
+//                  fix-up; programmatic dependent launch (weight prefetch overlaps the previous
+//                  kernel).
+//  k_gather_rm     X[:, P1] gather (Alg. 3 L1) or the naive AllGather re-permute
+//                  + CHUNK (Alg. 2 L3-4), row-major.
 //  k_sum_partials  rank-order sum (single-GPU shard simulation only).
+#include <cuda.h>  // CUtensorMap; the map is encoded on the host through the runtime's driver entry point
+#include <cudaTypedefs.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -58,62 +59,45 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-// Wait used by the producer / MMA warps: poll with a short sleep between probes so a waiting
-// helper warp does not steal issue slots from the dequant warps on its scheduler.
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
-  uint32_t done;
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
-      : "=r"(done)
-      : "r"(smem_u32(bar)), "r"(parity)
-      : "memory");
-  while (!done) {
-    __nanosleep(32);
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-  }
-}
-// Optional wait-time accounting (build with -DTPQ_PROF; profiling aid, not in the product build).
+// Per-CTA timeline (build with -DTPQ_PROF; profiling aid, not in the product build): entry,
+// work start, end (globaltimer ns) and SM id per CTA, per layer (N > K selects the slot).
 #ifdef TPQ_PROF
-__device__ unsigned long long g_tpq_prof[16];
-#define TPQ_PROF_DECL long long _pt[16] = {0}; const long long _t_start = clock64();
-#define TPQ_WAIT(bar, par, k)              \
-  do {                                     \
-    const long long _t0 = clock64();       \
-    mbar_wait(bar, par);                   \
-    _pt[k] += clock64() - _t0;             \
+__device__ unsigned long long g_tpq_cta[2][1024][4];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define TPQ_CTA(e, v) \
+  if (blockIdx.x < 1024) g_tpq_cta[a.NT * kTileCols > a.NKB * kUnitK][blockIdx.x][e] = (v);
+// per-unit event timeline of CTA 0 of the layer-2 launch: [warp][unit < 64][event]
+__device__ long long g_tpq_trace[24][64][4];
+#define TPQ_EV(e, i) \
+  if (blockIdx.x == 0 && a.NT * kTileCols < a.NKB * kUnitK && lane == 0 && (i) < 64) g_tpq_trace[warp][i][e] = clock64();
+// wait-cycle accounting per role (slot k), flushed by lane 0 of every warp at the end
+__device__ unsigned long long g_tpq_prof[32];
+#define TPQ_PDECL long long _pt[4] = {0, 0, 0, 0}; const long long _t_start = clock64();
+#define TPQ_W(bar, par, k)               \
+  do {                                   \
+    const long long _t0 = clock64();     \
+    mbar_wait(bar, par);                 \
+    _pt[k] += clock64() - _t0;           \
   } while (0)
-#define TPQ_WAITS(bar, par, k)             \
-  do {                                     \
-    const long long _t0 = clock64();       \
-    mbar_wait_sleep(bar, par);             \
-    _pt[k] += clock64() - _t0;             \
-  } while (0)
-__device__ long long g_tpq_trace[16][32][8];
-#define TPQ_EV(e, i)                                                                      \
-  if (blockIdx.x == 0 && (threadIdx.x & 31) == 0 && (i) < 32) g_tpq_trace[threadIdx.x >> 5][i][e] = clock64();
-#define TPQ_TIC(k) const long long _tic##k = clock64();
-#define TPQ_TOC(k, slot) _pt[slot] += clock64() - _tic##k;
-#define TPQ_PROF_FLUSH(ktot)                                                  \
-  do {                                                                        \
-    _pt[ktot] += clock64() - _t_start;                                        \
-    if ((threadIdx.x & 31) == 0)                                              \
-      for (int _k = 0; _k < 16; ++_k)                                         \
-        if (_pt[_k]) atomicAdd(&g_tpq_prof[_k], (unsigned long long)_pt[_k]); \
-  } while (0)
+#define TPQ_T0(k) const long long _tt##k = clock64();
+#define TPQ_T1(k, slot) _pt[slot] += clock64() - _tt##k;
+#define TPQ_PFLUSH(base)                                                                \
+  if (lane == 0) {                                                                      \
+    atomicAdd(&g_tpq_prof[(base) + 4], (unsigned long long)(clock64() - _t_start));     \
+    for (int _k = 0; _k < 4; ++_k) atomicAdd(&g_tpq_prof[(base) + _k], (unsigned long long)_pt[_k]); \
+  }
 #else
-#define TPQ_PROF_DECL
-#define TPQ_WAIT(bar, par, k) mbar_wait(bar, par)
-#define TPQ_WAITS(bar, par, k) mbar_wait_sleep(bar, par)
-#define TPQ_TIC(k)
-#define TPQ_TOC(k, slot)
+#define TPQ_CTA(e, v)
 #define TPQ_EV(e, i)
-#define TPQ_PROF_FLUSH(ktot) \
-  do {                       \
-  } while (0)
+#define TPQ_PDECL
+#define TPQ_W(bar, par, k) mbar_wait(bar, par)
+#define TPQ_T0(k)
+#define TPQ_T1(k, slot)
+#define TPQ_PFLUSH(base)
 #endif
 // 1-D TMA bulk copy global -> shared, completion counted on `bar` in bytes.
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
@@ -124,14 +108,17 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
 }
+// 2-D tensor TMA global -> shared (tensor map in kernel parameter space), completion on `bar`.
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+      "[%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-  return p;
-}
-__device__ __forceinline__ uint64_t policy_evict_last() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
@@ -143,39 +130,12 @@ __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.syn
 // tcgen05.st 32x32b: each thread of the warp writes N consecutive 32-bit TMEM columns of its lane.
 #define TPQ_R4(b) "r"(r[b]), "r"(r[b + 1]), "r"(r[b + 2]), "r"(r[b + 3])
 #define TPQ_R16(b) TPQ_R4(b), TPQ_R4(b + 4), TPQ_R4(b + 8), TPQ_R4(b + 12)
-__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
-          taddr),
-      TPQ_R16(0)
-      : "memory");
-}
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* r) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
       "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
       TPQ_R16(0), TPQ_R16(16)
       : "memory");
-}
-__device__ __forceinline__ void tmem_st64(uint32_t taddr, const uint32_t* r) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x64.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
-      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32,"
-      "%33,%34,%35,%36,%37,%38,%39,%40,%41,%42,%43,%44,%45,%46,%47,%48,"
-      "%49,%50,%51,%52,%53,%54,%55,%56,%57,%58,%59,%60,%61,%62,%63,%64};" ::"r"(taddr),
-      TPQ_R16(0), TPQ_R16(16), TPQ_R16(32), TPQ_R16(48)
-      : "memory");
-}
-__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t* r) {
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), TPQ_R4(0),
-               TPQ_R4(4)
-               : "memory");
-}
-__device__ __forceinline__ void tmem_st4(uint32_t taddr, const uint32_t* r) {
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr), TPQ_R4(0) : "memory");
-}
-__device__ __forceinline__ void tmem_st1(uint32_t taddr, uint32_t v) {
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(taddr), "r"(v) : "memory");
 }
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* v) {
   asm volatile(
@@ -193,19 +153,10 @@ __device__ __forceinline__ bool elect_one() {
   asm volatile("{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}" : "=r"(e));
   return e != 0;
 }
-// D[tmem] (+)= A[tmem] . B[smem]   (tcgen05.mma kind::f16, cta_group::1).  Called by a whole warp
-// with warp-uniform operands; one elected lane issues (keeps the operands in uniform registers:
-// ~11 cycles per N=16 MMA instead of ~80 when issued from a divergent single-lane branch,
+// D[tmem] (+)= A[tmem] . B[smem]  (tcgen05.mma kind::f16, cta_group::1), issued by one lane that
+// the caller elects once for a whole group of MMAs; the operands are computed warp-uniformly
+// beforehand so they stay in uniform registers (~11 cycles per N=16 MMA back to back,
 // tools/probe_tmem_lat.cu).
-__device__ __forceinline__ void umma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
-                                        uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-// Single-lane forms (caller elects the lane once for a whole group of MMAs).
 __device__ __forceinline__ void umma_ts1(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
                                          uint32_t accumulate) {
   asm volatile(
@@ -218,175 +169,146 @@ __device__ __forceinline__ void umma_commit1(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
 }
-__device__ __forceinline__ void umma_commit(uint64_t* bar) {
-  asm volatile(
-      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
-      : "memory");
-}
-// K-major, SWIZZLE_NONE smem descriptor: 8x16B core matrices, LBO = 128 B between the two k-halves
-// of a k16 block, SBO = byte distance between the two 8-row groups, version 1 (sm_100).  Verified
-// by tools/probe_tcgen05.cu.
-__device__ __forceinline__ uint64_t bdesc(uint32_t saddr, uint32_t sbo) {
-  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)(128 >> 4) << 16) | ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) |
-         (1ull << 46);
-}
-// Offset (in halves) of element (m, kk) of group g in the activation operand (internal.h).
-__device__ __forceinline__ int64_t xoff(int64_t g, int m, int kk, int G) {
-  return (g * kNPad + m) * (G + 16) + kk;
+// K-major SWIZZLE_128B smem descriptor (sm_100 version 1, layout type 2 in bits 61-63): rows of
+// 128 B (64 f16 of K) in 8-row, 1024-byte swizzle atoms (16-byte chunk c of row r stored at chunk
+// c ^ (r % 8)), SBO = 1024 B between 8-row groups, LBO unused (1).  The k16 block j of a row starts
+// 32 j bytes into it: the start address advances by 32 B, the hardware applies the XOR.
+__device__ __forceinline__ uint64_t bdesc_sw128(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | (1ull << 16) | ((uint64_t)(1024 >> 4) << 32) | (1ull << 46) |
+         (2ull << 61);
 }
 // instruction descriptor: D f32, A/B f16, both K-major, N = 16, M = 128
 constexpr uint32_t kIdesc = (1u << 4) | ((uint32_t)(kNPad >> 3) << 17) | ((uint32_t)(kTileCols >> 4) << 24);
 
 // ------------------------------------------------------------------ GEMV configuration
-// Warp roles (480 threads, two CTAs per SM):
-//   warps 0-7   dequant: warp w converts the codes of TMEM lane quarter w%4 (weight columns
-//               32(w%4)..+31) for k-half w/4 of the unit into the A operand in TMEM (tcgen05.st).
-//   warps 8-11  epilogue: lane quarter w-8; tcgen05.ld of D per unit, fp32 scale, tile output.
-//   warp 12     TMA producer: weight records (ring full/empty).
-//   warp 13     MMA issuer: (G/16 + 1) tcgen05.mma per unit and the commits.
-//   warp 14     activation stager: the M real rows of each unit's activation block (xfull/xempty).
-// Only barrier waits connect the roles, so each warp's per-unit latency overlaps the others'.
-constexpr int kGemvThreads = 480;
+// Unit = (128-column tile t, 128-row k-block kb): one weight record (internal.h), 8 MMAs of
+// K = 16.  A CTA owns a contiguous range of units (stream-K); the units of one tile inside that
+// range form a "segment" whose fp32 result the epilogue accumulates in registers.
+//
+// Arithmetic: the A operand is the exact f16 integer (q - z) (LOP3 magic number 1024 + q, resp.
+// 1024 + 16 q, minus one HSUB2 / HFMA2 -- exact, |q - z| <= 15); the MMA accumulates
+// sum_k (q - z) x in fp32 per group (one TMEM accumulator per group of the unit); the epilogue
+// applies the group's scale in fp32.  Per code word (8 weights): 5 ALU-pipe + 4 FMA-pipe ops.
+//
+// Hand-offs go per PAIR of consecutive units (p = i / 2): an mbarrier wait costs ~90-180 cycles
+// even when the phase has already completed (B300_MICROARCH.md "mbarrier"; measured here with
+// tools/prof_waits.py), comparable to the ~375 cycles per unit the SM has at HBM speed, so every
+// role waits once per pair.  Weight stages stay per unit.
+//
+// Warp roles (768 threads, one CTA per SM):
+//   warps 0-15  dequant, two sets of 8: set w/8 takes the pairs p with p % 2 == set.  Warp w of a
+//               set converts lane quarter w%4 (columns 32(w%4)..+31) of k-half (w/4)%2 of both
+//               units into the pair's TMEM A buffer (tcgen05.st 32x32b.x32) and hands the group
+//               scales to the epilogue.
+//   warps 16-19 epilogue: per pair, tcgen05.ld of the group accumulators (lane quarter w-16),
+//               x scale into registers; at a segment end the tile output or the stream-K partial
+//               + deterministic fix-up.
+//   warp 20     TMA producer: weight records into the NS-stage ring (L2 evict-first).
+//   warp 21     activation stager: per unit two 2-D tensor TMAs (16 rows x 64 k each, 128-byte
+//               rows, 128B swizzle) landing directly in the K-major SW128 operand layout.
+//   warps 22-23 MMA issuers, warp 22 + p%2 takes pair p: 16 x tcgen05.mma kind::f16 (M=128, N=16,
+//               K=16, A from TMEM) + one commit, which frees the pair's A buffer and activation
+//               slot and hands its accumulators to the epilogue.
+constexpr int kSetWarps = 8, kEpiWarp0 = 16, kProdWarp = 20, kStageWarp = 21, kMmaWarp = 22;
+constexpr int kGemvThreads = 24 * 32;
+
 template <int G>
 struct TC {
-  static constexpr int KB = G / 16 + 1;                        // k16 blocks per group incl. correction
-  static constexpr int UB = 64 * G + 320;                      // weight record bytes
-  static constexpr int UBP = (UB + 127) / 128 * 128;
-  static constexpr int XG = KB * kNPad * 32;                   // activation block bytes per group
-  static constexpr int NS = G == 128 ? 6 : (G == 64 ? 10 : 16);  // weight ring stages
-  static constexpr int NX = NS;                                  // activation ring stages
-  static constexpr int STAGE = UBP;
-  static constexpr int XRING = NS * STAGE;                       // byte offset of the activation ring
-  // TMEM A / D buffers: 3 A buffers break the dequant -> MMA -> a_empty -> dequant loop; the
-  // epilogue warps keep up with 2 D buffers.  3*72 + 2*16 = 248 <= 256 columns: two CTAs per SM.
-  static constexpr int NA = 3, ND = 2;
-  static constexpr int SR = 8;                                 // scale ring (> NA + ND units deep)
-  static constexpr int ACOLS = G / 2 + 8;                      // f16x2 columns (+ correction block)
-  static constexpr int DCOLS = kNPad;
-  static constexpr int USED = ND * DCOLS + NA * ACOLS;
-  static constexpr int TCOLS = USED <= 32 ? 32 : USED <= 64 ? 64 : USED <= 128 ? 128 : USED <= 256 ? 256 : 512;
-  static constexpr int WPW = G / 16;                           // u32 code words per column per k-half
-  static constexpr int SCRATCH = kTileCols * 33 * 4;           // epilogue reduction scratch
-  static constexpr int SCALES = XRING + NX * XG + SCRATCH;     // byte offset of the scale ring
-  static constexpr int BARS = SCALES + SR * kTileCols * 4;     // byte offset of the mbarriers
-  static constexpr int SMEM = BARS + 8 * (2 * NS + 2 * NX + 2 * NA + 2 * ND + SR);
+  static constexpr int KG = kUnitK / G;                      // groups per unit
+  static constexpr int GPH = G >= kUnitK / 2 ? 1 : (kUnitK / 2) / G;  // groups per k-half
+  static constexpr int UB = (int)unit_bytes_c(G);            // weight record bytes
+  static constexpr int STAGE = (UB + 127) / 128 * 128;
+  static constexpr int NS = G == 32 ? 18 : 20;               // weight ring stages (units, ~170 KB in flight)
+  static constexpr int XU = kNPad * kUnitK * 2;              // activation bytes per unit (16 rows x 128 k)
+  static constexpr int NX = 4;                               // activation pair slots
+  // unit slice = two TMA boxes (64 k, 16 rows) of 2 KB: k-half kq at kq * 2048, row m at m * 128
+  // (8-row swizzle atoms of 1024 B), 16-byte chunk swizzled by m % 8
+  static constexpr int DU = KG * kNPad;                      // accumulator columns per unit
+  static constexpr int AU = kUnitK / 2;                      // f16x2 A columns per unit
+  // Ring depths are even: pair p and pair p - depth then belong to the same dequant set and the same
+  // MMA warp, which consumed the older phase before waiting on the newer one.  With an odd depth
+  // the MMA warp of pair p can wait on a barrier whose previous phase (the other set's pair) has
+  // not completed yet, and the phase-parity test passes two phases early.
+  static constexpr int NA = 2;                               // TMEM A pair buffers (one per dequant set)
+  static constexpr int ND = G == 32 ? 2 : 4;                 // TMEM accumulator pair sets
+  static constexpr int TCOLS = 512;
+  static_assert(ND * 2 * DU + NA * 2 * AU <= TCOLS, "TMEM budget");
+  // pair-done ring.  Phase-parity waits need the awaited completion to be the latest one of its
+  // barrier.  Stager (pair p-NX) and epilogue (pair p) are safe for RD >= NX, ND.  The dequant set
+  // waits for pair p-NA while the other set's pairs may complete out of order (two MMA warps):
+  // RD - NA even makes the next pair on that barrier, p - NA + RD > p, one of this set's own
+  // pairs, which cannot complete before this set has written it.
+  static constexpr int RD = NA + 2;
+  static_assert(RD >= NX && RD >= ND && (RD - NA) % 2 == 0, "done ring aliasing");
+  static_assert(NA % 2 == 0 && NX % 2 == 0 && ND % 2 == 0, "odd ring depth");
+  static constexpr int SRP = 8;                              // scale ring in pairs (> NA + ND)
+  static_assert(SRP > NA + ND, "scale ring too shallow");
+  static constexpr int XRING = 0;                            // 1024-aligned (swizzle atoms)
+  static constexpr int WRING = NX * 2 * XU;                  // weight stages
+  static constexpr int SRING = WRING + NS * STAGE;           // fp16 scales [2 SRP units][KG][128]
+  static constexpr int BARS = SRING + 2 * SRP * KG * kTileCols * 2;
+  static constexpr int SMEM = BARS + 8 * (2 * NS + NX + NA + ND + RD + SRP);
 };
 
 struct GemvArgs {
   const uint8_t* packed;
-  const uint8_t* xext;
   int M;
-  int64_t K, N;
-  int NT, NG;
-  int64_t U;
+  int NT, NKB;      // tiles, k-blocks per tile
+  int64_t U;        // NT * NKB units
   int grid;
-  void* out;
-  int out_mode;
+  __half* out;      // [M][out_ld] row-major
   int64_t out_ld;
-  int next_G;
   float* ws;
   int* cnt;
 };
 
 __device__ __forceinline__ int64_t cta_start(int64_t c, int64_t U, int grid) { return c * U / grid; }
-// CTA whose range contains unit u:  largest c with floor(c U / grid) <= u.
+// CTA owning unit u under cta_start (inverse of the floor partition).
 __device__ __forceinline__ int cta_of_unit(int64_t u, int64_t U, int grid) {
   return (int)(((u + 1) * grid + U - 1) / U) - 1;
 }
 
-__device__ __forceinline__ uint32_t split_hi_lo(float v) {
-  const __half hi = __float2half_rn(v);
-  const __half lo = __float2half_rn(v - __half2float(hi));
-  return (uint32_t)__half_as_ushort(hi) | ((uint32_t)__half_as_ushort(lo) << 16);
-}
-
-// Write one finished 128-column tile (thread t owns column n = tile*128 + t, rows 0..15).
-// Called by the 128 epilogue threads together (uses named barrier 1 and `scratch`); t = column.
-__device__ void write_tile(const GemvArgs& a, int tile, int t, const float (&acc)[kNPad], float* scratch) {
-  const int64_t n = (int64_t)tile * kTileCols + t;
-  if (a.out_mode == OUT_ROWMAJOR) {
-    __half* out = reinterpret_cast<__half*>(a.out);
-#pragma unroll
-    for (int m = 0; m < kNPad; ++m)
-      if (m < a.M) out[(int64_t)m * a.out_ld + n] = __float2half_rn(acc[m]);
-    return;
-  }
-  // OUT_XEXT: B operand of the next layer (k' = n, group size G2), plus its correction block.
-  const int G2 = a.next_G;
-  const int64_t g2 = n / G2;
-  const int kk = (int)(n % G2);
-  const bool lo = (kk & 3) < 2;
-  __half* xo = reinterpret_cast<__half*>(a.out);
-#pragma unroll
-  for (int m = 0; m < kNPad; ++m) {
-    const __half h = __float2half_rn(m < a.M ? acc[m] : 0.f);
-    const __half b = lo ? h : __hmul(h, __float2half(0.0625f));
-    if (m < a.M) xo[xoff(g2, m, kk, G2)] = b;
-    const float bf = __half2float(b);
-    scratch[t * 33 + m] = bf;                        // S_B contribution
-    scratch[t * 33 + 16 + m] = lo ? bf : 16.f * bf;  // S_x contribution
-  }
-  named_bar(1, kTileCols);
-  const int per = kTileCols / G2;  // groups in this tile
-  if (t < per * 32) {
-    const int gi = t >> 5, q = t & 31;
-    const int m = q & 15;
-    if (m < a.M) {
-      float s = 0.f;
-      for (int i = 0; i < G2; ++i) s += scratch[(gi * G2 + i) * 33 + q];
-      const int64_t gg = ((int64_t)tile * kTileCols) / G2 + gi;
-      __half* corr = reinterpret_cast<__half*>(a.out) + xoff(gg, m, G2 + (q < 16 ? 0 : 2), G2);
-      *reinterpret_cast<uint32_t*>(corr) = split_hi_lo(s);
-    }
-  }
-  named_bar(1, kTileCols);
-}
+__device__ __forceinline__ uint32_t h2u(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
+__device__ __forceinline__ __half2 u2h(uint32_t u) { return *reinterpret_cast<__half2*>(&u); }
 
 template <int G>
-__global__ void __launch_bounds__(kGemvThreads, 2) k_tcgemv(const GemvArgs a) {
+__global__ void __launch_bounds__(kGemvThreads, 1) k_dqgemv(const GemvArgs a, const __grid_constant__ CUtensorMap xmap) {
   using C = TC<G>;
   extern __shared__ __align__(1024) uint8_t smem[];
-  float* scratch = reinterpret_cast<float*>(smem + C::XRING + C::NX * C::XG);
-  float* sring = reinterpret_cast<float*>(smem + C::SCALES);  // [SR][128] fp32 scales
+  __half* sring = reinterpret_cast<__half*>(smem + C::SRING);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BARS);
-  uint64_t* full = bars;                 // weight ring: TMA landed
-  uint64_t* empty = full + C::NS;        // weight ring: the 8 dequant warps hold their codes
-  uint64_t* xfull = empty + C::NS;       // activation ring: TMA landed
-  uint64_t* xempty = xfull + C::NX;      // activation ring: MMA commit
-  uint64_t* a_full = xempty + C::NX;     // TMEM A buffer: 8 dequant warps stored their part
-  uint64_t* a_empty = a_full + C::NA;    // TMEM A buffer: MMA commit
-  uint64_t* d_full = a_empty + C::NA;    // TMEM D buffer: MMA commit
-  uint64_t* d_empty = d_full + C::ND;    // TMEM D buffer: 4 epilogue warps read it
-  uint64_t* s_full = d_empty + C::ND;    // scale ring: 4 dequant warps (k-half 0) wrote it
+  uint64_t* full = bars;               // [NS] weight record landed (TMA transaction bytes)
+  uint64_t* empty = full + C::NS;      // [NS] the 8 dequant warps of the unit's set hold their codes
+  uint64_t* xfull = empty + C::NS;     // [NX] the pair's activation slices landed (TMA bytes)
+  uint64_t* a_full = xfull + C::NX;    // [NA] the pair's A operands stored (8 dequant warps)
+  uint64_t* d_empty = a_full + C::NA;  // [ND] epilogue read the pair's accumulators (4 warps)
+  uint64_t* done = d_empty + C::ND;    // [RD] pair p's MMAs completed (one tcgen05.commit): frees its
+                                       //      A buffer and activation slot, hands its accumulators over
+  uint64_t* s_full = done + C::RD;     // [SRP] the pair's scales written (8 dequant warps)
   __shared__ uint32_t s_tmem;
   __shared__ int s_last;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t u0 = cta_start(blockIdx.x, a.U, a.grid);
-  const int64_t u1 = cta_start(blockIdx.x + 1, a.U, a.grid);
-  const int nu = (int)(u1 - u0);
+  const int nu = (int)(cta_start(blockIdx.x + 1, a.U, a.grid) - u0);
+  const int np = (nu + 1) / 2;  // pairs (the last one may hold a single unit)
 
-  if (tid == 0) {
+  if (threadIdx.x == 0) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    TPQ_CTA(0, gtime())
+    TPQ_CTA(3, smid)
     for (int s = 0; s < C::NS; ++s) {
       mbar_init(full + s, 1);
-      mbar_init(empty + s, 8);
+      mbar_init(empty + s, kSetWarps);
     }
-    for (int s = 0; s < C::NX; ++s) {
-      mbar_init(xfull + s, 32);  // 32 stager lanes (cp.async.mbarrier.arrive.noinc)
-      mbar_init(xempty + s, 1);
-    }
-    for (int b = 0; b < C::NA; ++b) {
-      mbar_init(a_full + b, 8);
-      mbar_init(a_empty + b, 1);
-    }
-    for (int d = 0; d < C::ND; ++d) {
-      mbar_init(d_full + d, 1);
-      mbar_init(d_empty + d, 4);
-    }
-    for (int r = 0; r < C::SR; ++r) mbar_init(s_full + r, 4);
+    for (int s = 0; s < C::NX; ++s) mbar_init(xfull + s, 1);
+    for (int b = 0; b < C::NA; ++b) mbar_init(a_full + b, kSetWarps);
+    for (int d = 0; d < C::ND; ++d) mbar_init(d_empty + d, 4);
+    for (int r = 0; r < C::RD; ++r) mbar_init(done + r, 1);
+    for (int r = 0; r < C::SRP; ++r) mbar_init(s_full + r, kSetWarps);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 13) {
+  if (warp == kMmaWarp) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)),
                  "n"(C::TCOLS)
                  : "memory");
@@ -396,254 +318,263 @@ __global__ void __launch_bounds__(kGemvThreads, 2) k_tcgemv(const GemvArgs a) {
   __syncthreads();
   tc_fence_after();
   pdl_launch_dependents();
-  // warp-uniform TMEM base (shfl keeps it in the uniform datapath for the MMA operands)
-  const uint32_t tmem = __shfl_sync(0xffffffffu, s_tmem, 0);
-  const uint32_t d_col0 = 0, a_col0 = C::ND * C::DCOLS;
+  const uint32_t tmem = __shfl_sync(0xffffffffu, s_tmem, 0);  // warp-uniform TMEM base
+  // TMEM columns: accumulator pair set d at d * 2DU (unit h of the pair at + h DU, group g at + g 16);
+  // A pair buffer b at kA0 + b * 2AU (unit h at + h AU)
+  constexpr uint32_t kA0 = C::ND * 2 * C::DU;
 
-  if (warp == 12) {
+  if (warp < 2 * kSetWarps) {
+    // ===================== dequant: int4 -> exact f16 (q - z) -> TMEM A =====================
+    const int set = warp / kSetWarps, qw = warp & 3, kh = (warp >> 2) & 1;
+    const int col = qw * 32 + lane;  // weight column of the tile = TMEM lane
+    const uint32_t lane_base = (uint32_t)(qw * 32) << 16;
+    const __half2 k16 = __float2half2_rn(0.0625f);
+    TPQ_PDECL
+    for (int p = set; p < np; p += 2) {
+      const int b = p % C::NA;
+#pragma unroll 1
+      for (int h = 0; h < 2; ++h) {
+        const int i = 2 * p + h;
+        if (i >= nu) break;
+        const int s = i % C::NS;
+        TPQ_W(full + s, (uint32_t)((i / C::NS) & 1), 0);
+        TPQ_EV(0, i)
+        const uint8_t* st = smem + C::WRING + s * C::STAGE;
+        // code words k = 64 kh + 8w .. +7 (w < 8): chunks 2kh, 2kh+1 of this column (16 B each)
+        const uint4 c0 = *reinterpret_cast<const uint4*>(st + ((kh * 2 + 0) * kTileCols + col) * 16);
+        const uint4 c1 = *reinterpret_cast<const uint4*>(st + ((kh * 2 + 1) * kTileCols + col) * 16);
+        const uint32_t wv[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+        __half2 zl[C::GPH], zh[C::GPH];
+        __half* sr = sring + (i % (2 * C::SRP)) * (C::KG * kTileCols);
+#pragma unroll
+        for (int j = 0; j < C::GPH; ++j) {
+          const int gi = (kh * (kUnitK / 2)) / G + j;  // group of the unit
+          const uint8_t* meta = st + kUnitK * kTileCols / 2;
+          const int z = (meta[C::KG * 256 + gi * 64 + (col >> 1)] >> (4 * (col & 1))) & 0xF;
+          zl[j] = __float2half2_rn((float)(1024 + z));  // lo slots hold 1024 + q
+          zh[j] = __float2half2_rn((float)(-64 - z));   // hi slots hold 1024 + 16 q: /16 - 64 - z
+          if (G < kUnitK || kh == 0) sr[gi * kTileCols + col] = *reinterpret_cast<const __half*>(meta + gi * 256 + 2 * col);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + s);
+        uint32_t r[32];
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+          const int j = C::GPH == 1 ? 0 : (w * 8) / G;
+          const uint32_t x = wv[w], x8 = x >> 8;
+          // nibble order of a word (internal.h): (k0,k0+1) lo, (k0+2,k0+3) hi of x; the same of x >> 8
+          r[4 * w + 0] = h2u(__hsub2(u2h(lop3_and_or(x, 0x000F000Fu, 0x64006400u)), zl[j]));
+          r[4 * w + 1] = h2u(__hfma2(u2h(lop3_and_or(x, 0x00F000F0u, 0x64006400u)), k16, zh[j]));
+          r[4 * w + 2] = h2u(__hsub2(u2h(lop3_and_or(x8, 0x000F000Fu, 0x64006400u)), zl[j]));
+          r[4 * w + 3] = h2u(__hfma2(u2h(lop3_and_or(x8, 0x00F000F0u, 0x64006400u)), k16, zh[j]));
+        }
+        TPQ_EV(1, i)
+        if (h == 0) {
+          if (p >= C::NA) TPQ_W(done + (p - C::NA) % C::RD, (uint32_t)(((p - C::NA) / C::RD) & 1), 1);  // A free
+          tc_fence_after();
+        }
+        TPQ_EV(2, i)
+        tmem_st32(tmem + lane_base + kA0 + b * 2 * C::AU + h * C::AU + kh * 32, r);  // column c <-> k = 2c, 2c+1
+      }
+      TPQ_T0(st)
+      tmem_wait_st();
+      TPQ_T1(st, 2)
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(s_full + p % C::SRP);
+        mbar_arrive(a_full + b);
+      }
+      TPQ_EV(3, 2 * p)
+    }
+    TPQ_PFLUSH(0)
+  } else if (warp < kProdWarp) {
+    // ===================== epilogue: accumulators x scale -> output / partials ==============
+    const int qw = warp - kEpiWarp0, col = qw * 32 + lane;
+    const uint32_t lane_base = (uint32_t)(qw * 32) << 16;
+    pdl_wait();  // the output may still be read by the previous kernel in the stream
+    float acc[kNPad];
+#pragma unroll
+    for (int m = 0; m < kNPad; ++m) acc[m] = 0.f;
+    TPQ_PDECL
+    int64_t seg_start = u0;
+    int kb = (int)(u0 % a.NKB), tile = (int)(u0 / a.NKB);
+    for (int p = 0; p < np; ++p) {
+      const int d = p % C::ND;
+      TPQ_W(done + p % C::RD, (uint32_t)((p / C::RD) & 1), 0);
+      TPQ_EV(0, 2 * p)
+      tc_fence_after();
+      TPQ_W(s_full + p % C::SRP, (uint32_t)((p / C::SRP) & 1), 1);
+      TPQ_EV(1, 2 * p)
+#pragma unroll 1
+      for (int h = 0; h < 2; ++h) {
+        const int i = 2 * p + h;
+        if (i >= nu) break;
+        const __half* sr = sring + (i % (2 * C::SRP)) * (C::KG * kTileCols);
+#pragma unroll
+        for (int g = 0; g < C::KG; ++g) {  // one group accumulator at a time (register budget)
+          uint32_t v[kNPad];
+          tmem_ld16(tmem + lane_base + d * 2 * C::DU + h * C::DU + g * kNPad, v);
+          const float sc = __half2float(sr[g * kTileCols + col]);
+          tmem_wait_ld();
+#pragma unroll
+          for (int m = 0; m < kNPad; ++m) acc[m] = fmaf(sc, __uint_as_float(v[m]), acc[m]);
+        }
+        const int64_t u = u0 + i;
+        if (kb == a.NKB - 1 || i == nu - 1) {  // segment end
+          const int64_t n = (int64_t)tile * kTileCols + col;
+          const bool full_tile = seg_start == (int64_t)tile * a.NKB && kb == a.NKB - 1;
+          if (full_tile) {
+#pragma unroll
+            for (int m = 0; m < kNPad; ++m)
+              if (m < a.M) a.out[m * a.out_ld + n] = __float2half_rn(acc[m]);
+          } else {
+            // stream-K: this CTA holds part of the tile.  Partial -> own workspace slot (slot 0 = the
+            // CTA's first segment, 1 = its last); the last of the tile's CTAs to arrive sums all
+            // partials in CTA order (deterministic) and writes the tile.
+            const int slot = (seg_start == u0) ? 0 : 1;
+            float* mine = a.ws + ((size_t)blockIdx.x * 2 + slot) * (kNPad * kTileCols);
+#pragma unroll
+            for (int m = 0; m < kNPad; ++m)
+              if (m < a.M) __stcg(mine + m * kTileCols + col, acc[m]);
+            __threadfence();
+            named_bar(1, kTileCols);
+            const int c_first = cta_of_unit((int64_t)tile * a.NKB, a.U, a.grid);
+            const int c_last = cta_of_unit((int64_t)(tile + 1) * a.NKB - 1, a.U, a.grid);
+            if (col == 0) s_last = (atomicAdd(a.cnt + tile, 1) == c_last - c_first);
+            named_bar(1, kTileCols);
+            if (s_last) {
+              __threadfence();
+              float r[kNPad];
+#pragma unroll
+              for (int m = 0; m < kNPad; ++m) r[m] = 0.f;
+              for (int c = c_first; c <= c_last; ++c) {
+                const int cslot = (cta_start(c, a.U, a.grid) / a.NKB == tile) ? 0 : 1;
+                const float* src = a.ws + ((size_t)c * 2 + cslot) * (kNPad * kTileCols);
+#pragma unroll
+                for (int m = 0; m < kNPad; ++m)
+                  if (m < a.M) r[m] += __ldcg(src + m * kTileCols + col);
+              }
+#pragma unroll
+              for (int m = 0; m < kNPad; ++m)
+                if (m < a.M) a.out[m * a.out_ld + n] = __float2half_rn(r[m]);
+              if (col == 0) a.cnt[tile] = 0;  // self-reset for the next launch / graph replay
+            }
+          }
+#pragma unroll
+          for (int m = 0; m < kNPad; ++m) acc[m] = 0.f;
+          seg_start = u + 1;
+        }
+        if (++kb == a.NKB) {
+          kb = 0;
+          ++tile;
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(d_empty + d);
+      TPQ_EV(2, 2 * p)
+    }
+    TPQ_PFLUSH(5)
+  } else if (warp == kProdWarp) {
     // ===================== TMA producer (warp-uniform loop, one elected lane issues) ===========
-    // Weight records do not depend on the previous kernel: the first NS are requested before
-    // griddepcontrol.wait (programmatic dependent launch overlaps them with the previous kernel).
-    TPQ_PROF_DECL
+    // Weight records do not depend on the previous kernel: the first NS are requested before any
+    // griddepcontrol.wait, so they overlap the tail of the previous kernel (PDL).
     const uint64_t pw = policy_evict_first();
+    TPQ_PDECL
     const int pre = nu < C::NS ? nu : C::NS;
     for (int i = 0; i < pre; ++i) {
       if (elect_one()) {
         mbar_arrive_expect_tx(full + i, C::UB);
-        bulk_g2s(smem + i * C::STAGE, a.packed + (u0 + i) * C::UB, C::UB, full + i, pw);
+        bulk_g2s(smem + C::WRING + i * C::STAGE, a.packed + (u0 + i) * C::UB, C::UB, full + i, pw);
       }
       __syncwarp();
     }
     for (int i = 0, s = 0, ph = 0; i + C::NS < nu; ++i) {  // refill as the dequant warps release
-      TPQ_WAIT(empty + s, (uint32_t)ph, 1);
+      TPQ_W(empty + s, (uint32_t)ph, 0);
+      TPQ_EV(0, i + C::NS)
       if (elect_one()) {
         mbar_arrive_expect_tx(full + s, C::UB);
-        bulk_g2s(smem + s * C::STAGE, a.packed + (u0 + i + C::NS) * C::UB, C::UB, full + s, pw);
+        bulk_g2s(smem + C::WRING + s * C::STAGE, a.packed + (u0 + i + C::NS) * C::UB, C::UB, full + s, pw);
       }
       __syncwarp();
-      TPQ_EV(0, i + C::NS)
-      if (++s == C::NS) { s = 0; ph ^= 1; }
-    }
-    TPQ_PROF_FLUSH(8);
-  } else if (warp == 14) {
-    // ===================== activation stager (cp.async, asynchronous) =====================
-    // Unit (tile, g) needs group g's activation block in the tcgen05 canonical B layout.  Only the
-    // M real rows are copied (16-byte cp.async per row chunk, straight from L2); completion is
-    // signalled on xfull by cp.async.mbarrier.arrive, so the warp runs NX units ahead without
-    // waiting for data.  Rows >= M of a stage are never consumed (their D rows are discarded).
-    TPQ_PROF_DECL
-    constexpr int RW = G + 16, CPR = RW / 8;  // halves / 16-byte chunks per row record
-    const uint32_t xring = smem_u32(smem + C::XRING);
-    pdl_wait();  // activations come from the previous kernel in the stream
-    int g = (int)(u0 % a.NG);
-    for (int i = 0, x = 0, phx = 0; i < nu; ++i, g = (g + 1 == a.NG) ? 0 : g + 1) {
-      if (i >= C::NX) TPQ_WAIT(xempty + x, (uint32_t)(phx ^ 1), 0);
-      const __half* src = reinterpret_cast<const __half*>(a.xext) + (int64_t)g * kNPad * RW;
-      const uint32_t dst = xring + x * C::XG;
-      for (int t = lane; t < a.M * CPR; t += 32) {
-        const int m = t / CPR, c = t - m * CPR;
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
-                         dst + (uint32_t)(((m >> 3) * RW * 8 + c * 64 + (m & 7) * 8) * 2)),
-                     "l"(src + m * RW + c * 8)
-                     : "memory");
+      if (++s == C::NS) {
+        s = 0;
+        ph ^= 1;
       }
-      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(xfull + x)) : "memory");
-      TPQ_EV(1, i)
-      if (++x == C::NX) { x = 0; phx ^= 1; }
     }
-    asm volatile("cp.async.wait_all;" ::: "memory");
-    TPQ_PROF_FLUSH(15);
-  } else if (warp == 13) {
-    // ===================== MMA issuer (warp-uniform operands, one elected lane issues) =========
-    TPQ_PROF_DECL
+    TPQ_PFLUSH(10)
+  } else if (warp == kStageWarp) {
+    // ===================== activation stager (tensor TMA) =====================
+    // Slot rows >= M hold stale data; a row of B only feeds the same row of D (discarded).
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&xmap)) : "memory");
+    pdl_wait();  // the activations come from the previous kernel in the stream
+    if (lane == 0) { TPQ_CTA(1, gtime()) }
+    int kb = (int)(u0 % a.NKB);
+    TPQ_PDECL
+    for (int p = 0; p < np; ++p) {
+      const int x = p % C::NX, nh = (2 * p + 1 < nu) ? 2 : 1;
+      if (p >= C::NX) TPQ_W(done + (p - C::NX) % C::RD, (uint32_t)(((p - C::NX) / C::RD) & 1), 0);  // slot free
+      TPQ_EV(0, 2 * p)
+      if (elect_one()) {
+        mbar_arrive_expect_tx(xfull + x, nh * C::XU);
+        for (int h = 0; h < nh; ++h) {
+          const int kbh = (kb + h) % a.NKB;
+          uint8_t* dst = smem + C::XRING + (2 * x + h) * C::XU;
+          tma_load_2d(dst, &xmap, kbh * kUnitK, 0, xfull + x);
+          tma_load_2d(dst + C::XU / 2, &xmap, kbh * kUnitK + kUnitK / 2, 0, xfull + x);
+        }
+      }
+      __syncwarp();
+      kb = (kb + nh) % a.NKB;
+    }
+    TPQ_PFLUSH(15)
+  } else {
+    // ===================== MMA issuers (warp-uniform operands, one elected lane issues) ========
     const uint32_t xring = smem_u32(smem + C::XRING);
-    int x = 0, b = 0, d = 0;
-    uint32_t px = 0, pb = 0, pd = 0;  // phase bits of the ring positions
-    for (int i = 0; i < nu; ++i) {
-      TPQ_WAIT(xfull + x, px, 2);
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // cp.async data -> tensor core
-      TPQ_WAIT(a_full + b, pb, 3);
-      TPQ_EV(0, i)
-      TPQ_WAIT(d_empty + d, pd ^ 1, 4);
-      TPQ_EV(1, i)
+    TPQ_PDECL
+    for (int p = warp - kMmaWarp; p < np; p += 2) {
+      const int d = p % C::ND, b = p % C::NA, x = p % C::NX;
+      const bool two = 2 * p + 1 < nu;
+      TPQ_W(d_empty + d, (uint32_t)(((p / C::ND) & 1) ^ 1), 0);
+      TPQ_EV(0, 2 * p)
+      TPQ_W(a_full + b, (uint32_t)((p / C::NA) & 1), 1);
+      TPQ_EV(1, 2 * p)
+      TPQ_W(xfull + x, (uint32_t)((p / C::NX) & 1), 2);
+      TPQ_EV(2, 2 * p)
       tc_fence_after();
-      const uint64_t bd0 = bdesc(xring + x * C::XG, (G + 16) * 16);
-      uint32_t aop[C::KB];
-      uint64_t bop[C::KB];
-      const uint32_t dt = tmem + d_col0 + d * C::DCOLS, at = tmem + a_col0 + b * C::ACOLS;
+      const uint64_t bd0 = bdesc_sw128(xring + 2 * x * C::XU);
+      const uint32_t dt = tmem + d * 2 * C::DU, at = tmem + kA0 + b * 2 * C::AU;
+      constexpr int J = kUnitK / 16;  // MMAs per unit
+      uint32_t aop[2 * J], dop[2 * J];
+      uint64_t bop[2 * J];
 #pragma unroll
-      for (int j = 0; j < C::KB; ++j) {  // operands first (independent conversions), then back-to-back issue
-        aop[j] = at + j * 8;
-        bop[j] = bd0 + (uint64_t)(j * (256 / 16));
+      for (int j = 0; j < 2 * J; ++j) {  // operands first, then back-to-back issue
+        const int h = j / J, jj = j % J;
+        aop[j] = at + h * C::AU + jj * 8;
+        bop[j] = bd0 + (uint64_t)((h * C::XU + (jj / 4) * (C::XU / 2) + (jj % 4) * 32) >> 4);
+        dop[j] = dt + h * C::DU + (jj / (G / 16)) * kNPad;                // group of the k16 block
       }
+      TPQ_T0(is)
       if (elect_one()) {
 #pragma unroll
-        for (int j = 0; j < C::KB; ++j) umma_ts1(dt, aop[j], bop[j], kIdesc, j > 0);
-        umma_commit1(d_full + d);
-        umma_commit1(a_empty + b);
-        umma_commit1(xempty + x);
-      }
-      __syncwarp();
-      TPQ_EV(2, i)
-      if (++x == C::NX) { x = 0; px ^= 1; }
-      if (++b == C::NA) { b = 0; pb ^= 1; }
-      if (++d == C::ND) { d = 0; pd ^= 1; }
-    }
-    TPQ_PROF_FLUSH(9);
-  } else if (warp < 8) {
-    // ===================== warps 0-7: dequant (regs -> TMEM A) =====================
-    TPQ_PROF_DECL
-    const int qw = warp & 3, kh = warp >> 2;         // lane quarter, k-half
-    const int col = qw * 32 + lane;                  // weight column of the tile = TMEM lane
-    const uint32_t lane_base = (uint32_t)(qw * 32) << 16;
-    if (kh == 1) {  // constant part of the correction block of both A buffers: (-1024,-1024), ., 0 x 6
-      for (int b = 0; b < C::NA; ++b) {
-        const uint32_t cz[4] = {0xE400E400u, 0u, 0u, 0u};
-        const uint32_t z4[4] = {0u, 0u, 0u, 0u};
-        tmem_st4(tmem + lane_base + a_col0 + b * C::ACOLS + G / 2, cz);
-        tmem_st4(tmem + lane_base + a_col0 + b * C::ACOLS + G / 2 + 4, z4);
-      }
-      tmem_wait_st();
-    }
-    for (int i = 0; i < nu; ++i) {
-      const int s = i % C::NS, b = i % C::NA;
-      TPQ_WAIT(full + s, (uint32_t)((i / C::NS) & 1), 5);
-      TPQ_EV(0, i)
-      const uint8_t* st = smem + s * C::STAGE;
-      uint32_t wv[C::WPW];  // this warp's code words: k = kh*G/2 + 8w .. +7, w < WPW
+        for (int j = 0; j < J; ++j) umma_ts1(dop[j], aop[j], bop[j], kIdesc, (j % (G / 16)) ? 1u : 0u);
+        if (two) {
 #pragma unroll
-      for (int w = 0; w < C::WPW; w += (C::WPW >= 4 ? 4 : C::WPW)) {
-        const int gw = kh * C::WPW + w;  // word index within the column
-        const uint8_t* p = st + ((gw >> 2) * kTileCols + col) * 16 + (gw & 3) * 4;
-        if constexpr (C::WPW >= 4) {
-          const uint4 v = *reinterpret_cast<const uint4*>(p);
-          wv[w] = v.x;
-          wv[w + 1] = v.y;
-          wv[w + 2] = v.z;
-          wv[w + 3] = v.w;
-        } else {
-          const uint2 v = *reinterpret_cast<const uint2*>(p);
-          wv[w] = v.x;
-          wv[w + 1] = v.y;
+          for (int j = J; j < 2 * J; ++j) umma_ts1(dop[j], aop[j], bop[j], kIdesc, (j % (G / 16)) ? 1u : 0u);
         }
-      }
-      uint32_t zz = 0;
-      if (kh == 0) {  // hand this unit's fp32 column scale to the epilogue warps
-        sring[(i % C::SR) * kTileCols + col] = __half2float(*reinterpret_cast<const __half*>(st + 64 * G + 2 * col));
-      } else {
-        const uint32_t z = (st[64 * G + 256 + (col >> 1)] >> (4 * (col & 1))) & 0xFu;
-        zz = (uint32_t)__half_as_ushort(__float2half(-(float)z)) * 0x10001u;
+        umma_commit1(done + p % C::RD);
       }
       __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(empty + s);
-        if (kh == 0) mbar_arrive(s_full + i % C::SR);
-      }
-      TPQ_TIC(a)
-      uint32_t r[4 * C::WPW];
-#pragma unroll
-      for (int w = 0; w < C::WPW; ++w) {
-        const uint32_t x = wv[w], x8 = x >> 8;
-        r[4 * w + 0] = lop3_and_or(x, 0x000F000Fu, 0x64006400u);   // k0,k0+1   : 1024 + q
-        r[4 * w + 1] = lop3_and_or(x, 0x00F000F0u, 0x64006400u);   // k0+2,k0+3 : 1024 + 16 q
-        r[4 * w + 2] = lop3_and_or(x8, 0x000F000Fu, 0x64006400u);  // k0+4,k0+5
-        r[4 * w + 3] = lop3_and_or(x8, 0x00F000F0u, 0x64006400u);  // k0+6,k0+7
-      }
-      TPQ_TOC(a, 11)
-      TPQ_EV(1, i)
-      TPQ_TIC(c)
-      TPQ_WAIT(a_empty + b, (uint32_t)(((i / C::NA) & 1) ^ 1), 6);  // MMA of unit i-NA done
-      tc_fence_after();
-      const uint32_t ab = tmem + lane_base + a_col0 + b * C::ACOLS;
-      if constexpr (C::WPW == 8) {
-        tmem_st32(ab + kh * 32, r);
-      } else if constexpr (C::WPW == 4) {
-        tmem_st16(ab + kh * 16, r);
-      } else {
-        tmem_st8(ab + kh * 8, r);
-      }
-      if (kh == 1) tmem_st1(ab + G / 2 + 1, zz);
-      tmem_wait_st();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(a_full + b);
-      TPQ_EV(2, i)
-      TPQ_TOC(c, 13)
+      TPQ_T1(is, 3)
+      TPQ_EV(3, 2 * p)
     }
-    TPQ_PROF_FLUSH(10);
-  } else {
-    // ===================== warps 8-11: epilogue =====================
-    TPQ_PROF_DECL
-    const int qw = warp - 8, col = qw * 32 + lane;
-    const uint32_t lane_base = (uint32_t)(qw * 32) << 16;
-    pdl_wait();  // outputs may still be read by the previous kernel in the stream
-    float acc[kNPad];
-#pragma unroll
-    for (int m = 0; m < kNPad; ++m) acc[m] = 0.f;
-    int64_t seg_start = u0;  // first unit of the current tile segment
-    int g = (int)(u0 % a.NG), tile = (int)(u0 / a.NG);
-    for (int k = 0; k < nu; ++k) {
-      const int d = k % C::ND;
-      TPQ_WAIT(d_full + d, (uint32_t)((k / C::ND) & 1), 7);
-      tc_fence_after();
-      uint32_t v[16];
-      tmem_ld16(tmem + lane_base + d_col0 + d * C::DCOLS, v);
-      TPQ_WAIT(s_full + k % C::SR, (uint32_t)((k / C::SR) & 1), 12);
-      const float s = sring[(k % C::SR) * kTileCols + col];
-      tmem_wait_ld();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(d_empty + d);
-      TPQ_EV(0, k)
-#pragma unroll
-      for (int m = 0; m < kNPad; ++m) acc[m] = fmaf(s, __uint_as_float(v[m]), acc[m]);
-      const int64_t u = u0 + k;
-      if (g == a.NG - 1 || k == nu - 1) {
-        const bool full_tile = (seg_start == (int64_t)tile * a.NG) && (g == a.NG - 1);
-        if (full_tile) {
-          write_tile(a, tile, col, acc, scratch);
-        } else {
-          const int slot = (seg_start == u0) ? 0 : 1;
-          float* mine = a.ws + ((size_t)blockIdx.x * 2 + slot) * (kNPad * kTileCols);
-#pragma unroll
-          for (int m = 0; m < kNPad; ++m)
-            if (m < a.M) __stcg(mine + m * kTileCols + col, acc[m]);
-          __threadfence();
-          named_bar(1, kTileCols);
-          const int c_first = cta_of_unit((int64_t)tile * a.NG, a.U, a.grid);
-          const int c_last = cta_of_unit((int64_t)tile * a.NG + a.NG - 1, a.U, a.grid);
-          if (col == 0) s_last = (atomicAdd(a.cnt + tile, 1) == c_last - c_first);
-          named_bar(1, kTileCols);
-          if (s_last) {
-            __threadfence();
-            float r[kNPad];
-#pragma unroll
-            for (int m = 0; m < kNPad; ++m) r[m] = 0.f;
-            for (int c = c_first; c <= c_last; ++c) {
-              const int cslot = (cta_start(c, a.U, a.grid) / a.NG == tile) ? 0 : 1;
-              const float* src = a.ws + ((size_t)c * 2 + cslot) * (kNPad * kTileCols);
-#pragma unroll
-              for (int m = 0; m < kNPad; ++m)
-                if (m < a.M) r[m] += __ldcg(src + m * kTileCols + col);
-            }
-            write_tile(a, tile, col, r, scratch);
-            if (col == 0) a.cnt[tile] = 0;  // self-reset for the next launch / graph replay
-          }
-        }
-#pragma unroll
-        for (int m = 0; m < kNPad; ++m) acc[m] = 0.f;
-        seg_start = u + 1;
-      }
-      if (++g == a.NG) {
-        g = 0;
-        ++tile;
-      }
-    }
-    TPQ_PROF_FLUSH(14);
+    TPQ_PFLUSH(20)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 13) {
+  if (threadIdx.x == 0) { TPQ_CTA(2, gtime()) }
+  if (warp == kMmaWarp) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::TCOLS) : "memory");
   }
@@ -665,25 +596,19 @@ cudaError_t launch_pdl(Kern k, dim3 grid, dim3 block, size_t smem, cudaStream_t 
 }
 
 template <int G>
-int blocks_per_sm_t() {
+bool prepare_t() {
   constexpr int smem = TC<G>::SMEM;
   static_assert(smem <= 227 * 1024, "GEMV smem over the per-CTA limit");
-  if (cudaFuncSetAttribute(k_tcgemv<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return 0;
-  if (cudaFuncSetAttribute(k_tcgemv<G>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                           (int)cudaSharedmemCarveoutMaxShared) != cudaSuccess)
-    return 0;
-  int nb = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_tcgemv<G>, kGemvThreads, smem) != cudaSuccess) return 0;
-  const int by_tmem = 512 / TC<G>::TCOLS;
+  static_assert(2 * smem > 228 * 1024, "GEMV must be one CTA per SM (TMEM 512 columns)");
+  if (cudaFuncSetAttribute(k_dqgemv<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+    return false;
   if (getenv("TPQ_VERBOSE")) {
     cudaFuncAttributes fa;
-    cudaFuncGetAttributes(&fa, k_tcgemv<G>);
-    fprintf(stderr, "[tpq] k_tcgemv<%d>: regs %d, smem dyn %d static %zu, occupancy %d, tmem cap %d\n", G, fa.numRegs,
-            smem, fa.sharedSizeBytes, nb, by_tmem);
+    cudaFuncGetAttributes(&fa, k_dqgemv<G>);
+    fprintf(stderr, "[tpq] k_dqgemv<%d>: regs %d, smem dyn %d static %zu\n", G, fa.numRegs, smem,
+            fa.sharedSizeBytes);
   }
-  // The occupancy API under-reports here (1) while ncu's block limits (registers 2, smem 2)
-  // admit two CTAs; TMEM (512 columns per SM) is the binding constraint.
-  return nb < 1 ? 0 : by_tmem;
+  return true;
 }
 
 // ------------------------------------------------------------------ gathers
@@ -692,47 +617,6 @@ __device__ __forceinline__ int64_t gather_src(int m, int64_t k, int64_t ld, cons
   if (mode == GATHER_COLS) return (int64_t)m * ld + (idx ? (int64_t)idx[k] : k);
   const int64_t c = idx[k];
   return (c / nn) * (int64_t)M * nn + (int64_t)m * nn + (c % nn);
-}
-
-// One CTA per group: thread (m, c8) builds 8 consecutive k of row m (16 B of the B operand) and
-// the group's correction block from fixed-order sums.
-__global__ void k_to_xext(const __half* __restrict__ src, int64_t ld, const int32_t* __restrict__ idx, int mode,
-                          int64_t nn, int M, int64_t K, int G, uint8_t* __restrict__ dst) {
-  pdl_launch_dependents();
-  pdl_wait();  // src is produced by, and dst still read by, earlier kernels in the stream
-  extern __shared__ float red[];  // [16 m][G/8][2]
-  const int g = blockIdx.x;
-  const int cpr = G / 8;  // 8-k chunks per row
-  const int m = threadIdx.x / cpr, c8 = threadIdx.x % cpr;
-  __half* xo = reinterpret_cast<__half*>(dst);
-  float sb = 0.f, sx = 0.f;
-  uint32_t pk[4] = {0, 0, 0, 0};
-  if (m < M) {
-#pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const int64_t k = (int64_t)g * G + c8 * 8 + e;
-      const __half h = src[gather_src(m, k, ld, idx, mode, nn, M)];
-      const bool lo = (e & 3) < 2;
-      const __half b = lo ? h : __hmul(h, __float2half(0.0625f));
-      const float bf = __half2float(b);
-      sb += bf;
-      sx += lo ? bf : 16.f * bf;
-      pk[e >> 1] |= (uint32_t)__half_as_ushort(b) << (16 * (e & 1));
-    }
-  }
-  if (m < M) *reinterpret_cast<uint4*>(xo + xoff(g, m, c8 * 8, G)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-  red[(m * cpr + c8) * 2 + 0] = sb;
-  red[(m * cpr + c8) * 2 + 1] = sx;
-  __syncthreads();
-  if (c8 == 0 && m < M) {
-    float tb = 0.f, tx = 0.f;
-    for (int i = 0; i < cpr; ++i) {
-      tb += red[(m * cpr + i) * 2 + 0];
-      tx += red[(m * cpr + i) * 2 + 1];
-    }
-    *reinterpret_cast<uint4*>(xo + xoff(g, m, G, G)) = make_uint4(split_hi_lo(tb), split_hi_lo(tx), 0u, 0u);
-    *reinterpret_cast<uint4*>(xo + xoff(g, m, G + 8, G)) = make_uint4(0u, 0u, 0u, 0u);
-  }
 }
 
 __global__ void k_gather_rm(const __half* __restrict__ src, int64_t ld, const int32_t* __restrict__ idx, int mode,
@@ -772,53 +656,61 @@ int grid_for(int64_t work, int per_block) {
 
 // ------------------------------------------------------------------ launchers
 #ifdef TPQ_PROF
-int trace_read(long long* out) {
-  return cudaMemcpyFromSymbol(out, g_tpq_trace, sizeof(long long) * 16 * 32 * 8) != cudaSuccess;
+int cta_read(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, g_tpq_cta, sizeof(unsigned long long) * 2 * 1024 * 4) != cudaSuccess;
 }
-int prof_read(unsigned long long* out) {
-  if (cudaMemcpyFromSymbol(out, g_tpq_prof, sizeof(unsigned long long) * 16) != cudaSuccess) return 1;
-  unsigned long long z[16] = {0};
+int trace_read(long long* out) {
+  return cudaMemcpyFromSymbol(out, g_tpq_trace, sizeof(long long) * 24 * 64 * 4) != cudaSuccess;
+}
+int prof_read(unsigned long long* out) {  // read and reset
+  if (cudaMemcpyFromSymbol(out, g_tpq_prof, sizeof(unsigned long long) * 32) != cudaSuccess) return 1;
+  unsigned long long z[32] = {0};
   return cudaMemcpyToSymbol(g_tpq_prof, z, sizeof(z)) != cudaSuccess;
 }
 #endif
-int gemv_blocks_per_sm(int G) {
-  if (G == 128) return blocks_per_sm_t<128>();
-  if (G == 64) return blocks_per_sm_t<64>();
-  if (G == 32) return blocks_per_sm_t<32>();
-  return 0;
+bool make_xmap(CUtensorMap* map, const void* base, int64_t K) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void**>(&encode), cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !encode)
+      return false;
+  }
+  const cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)kNPad};
+  const cuuint64_t strides[1] = {(cuuint64_t)K * 2};  // bytes between rows
+  const cuuint32_t box[2] = {(cuuint32_t)(kUnitK / 2), (cuuint32_t)kNPad};
+  const cuuint32_t es[2] = {1, 1};
+  return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-cudaError_t launch_gemv(const LayerDev& L, const void* xext, int M, void* out, int out_mode, int64_t out_ld,
-                        int next_G, cudaStream_t st) {
+bool gemv_prepare(int G) {
+  if (G == 128) return prepare_t<128>();
+  if (G == 64) return prepare_t<64>();
+  if (G == 32) return prepare_t<32>();
+  return false;
+}
+
+cudaError_t launch_gemv(const LayerDev& L, const CUtensorMap& xmap, int M, void* out, int64_t out_ld,
+                        cudaStream_t st) {
   if (M < 1 || M > kMaxM) return cudaErrorInvalidValue;
   GemvArgs a;
   a.packed = L.packed;
-  a.xext = reinterpret_cast<const uint8_t*>(xext);
   a.M = M;
-  a.K = L.K;
-  a.N = L.N;
   a.NT = L.NT;
-  a.NG = L.NG;
+  a.NKB = L.NKB;
   a.U = L.U;
   a.grid = L.grid;
-  a.out = out;
-  a.out_mode = out_mode;
+  a.out = reinterpret_cast<__half*>(out);
   a.out_ld = out_ld;
-  a.next_G = next_G;
   a.ws = L.ws;
   a.cnt = L.cnt;
-  if (L.G == 128) return launch_pdl(k_tcgemv<128>, dim3(a.grid), dim3(kGemvThreads), TC<128>::SMEM, st, a);
-  if (L.G == 64) return launch_pdl(k_tcgemv<64>, dim3(a.grid), dim3(kGemvThreads), TC<64>::SMEM, st, a);
-  if (L.G == 32) return launch_pdl(k_tcgemv<32>, dim3(a.grid), dim3(kGemvThreads), TC<32>::SMEM, st, a);
+  if (L.G == 128) return launch_pdl(k_dqgemv<128>, dim3(a.grid), dim3(kGemvThreads), TC<128>::SMEM, st, a, xmap);
+  if (L.G == 64) return launch_pdl(k_dqgemv<64>, dim3(a.grid), dim3(kGemvThreads), TC<64>::SMEM, st, a, xmap);
+  if (L.G == 32) return launch_pdl(k_dqgemv<32>, dim3(a.grid), dim3(kGemvThreads), TC<32>::SMEM, st, a, xmap);
   return cudaErrorInvalidValue;
-}
-
-cudaError_t launch_to_xext(const void* src, int64_t ld, const int32_t* idx, int mode, int64_t nn, int M, int64_t K,
-                           int G, void* dst, cudaStream_t st) {
-  if (M < 1 || M > kMaxM || K % G) return cudaErrorInvalidValue;
-  const int threads = kNPad * (G / 8);
-  return launch_pdl(k_to_xext, dim3((unsigned)(K / G)), dim3(threads), (size_t)threads * 2 * sizeof(float), st,
-                    reinterpret_cast<const __half*>(src), ld, idx, mode, nn, M, K, G, reinterpret_cast<uint8_t*>(dst));
 }
 
 cudaError_t launch_gather_rowmajor(const void* src, int64_t ld, const int32_t* idx, int mode, int64_t nn, int M,

@@ -1,4 +1,4 @@
-"""Wait-cycle accounting per warp role (needs the profiling build):
+"""Wait-cycle accounting per warp role (profiling build):
     python -m paper_2402_04925_b200.build --prof
     TPQ_LIB_PATH=paper_2402_04925_b200/libtpq_prof.so python tools/prof_waits.py --m 1"""
 import argparse
@@ -16,17 +16,16 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--shape", default="llama70b")
 ap.add_argument("--m", type=int, default=1)
 ap.add_argument("--iters", type=int, default=20)
-ap.add_argument("--sim-tp", type=int, default=1)
 a = ap.parse_args()
 p = synth.make_named(a.shape, 16, 0)
 P1, _ = tpq.gptq_reorder(p.w1.g_idx, p.G)
 P2, _ = tpq.gptq_reorder(p.w2.g_idx, p.G)
-h = tpq.TpMlp(p.w1, p.w2, P1, P2, tp=a.sim_tp, M_max=16)
+h = tpq.TpMlp(p.w1, p.w2, P1, P2, tp=1, M_max=16)
 X = torch.from_numpy(p.X).cuda()
 Y = torch.empty(16, p.N2, dtype=torch.float16, device="cuda")
 L = tpq.lib()
 L.tpq_debug_prof.argtypes = [C.c_void_p]
-buf = (C.c_ulonglong * 16)()
+buf = (C.c_ulonglong * 32)()
 h.forward_local(X, a.m, Y)
 torch.cuda.synchronize()
 L.tpq_debug_prof(C.cast(buf, C.c_void_p))  # reset
@@ -35,22 +34,26 @@ for _ in range(a.iters):
 torch.cuda.synchronize()
 L.tpq_debug_prof(C.cast(buf, C.c_void_p))
 v = list(buf)
-names = {0: "prod:xempty", 1: "prod:empty", 8: "prod:TOTAL", 2: "mma:xfull", 3: "mma:a_full", 4: "mma:d_empty",
-         9: "mma:TOTAL", 5: "deq:full", 6: "deq:a_empty", 7: "deq:d_full", 10: "deq:TOTAL"}
-names.update({11: "deq:alu", 12: "epi:s_full", 13: "deq:st(incl a_empty)", 14: "epi:TOTAL"})
-for role, tot, keys in (("producer", 8, [0, 1]), ("mma", 9, [2, 3, 4]), ("dequant", 10, [5, 6, 11, 13]), ("epilogue", 14, [7, 12])):
-    T = v[tot] or 1
-    print(f"{role:9s} total {T:14d} cyc-warps  " + "  ".join(f"{names[k]} {100 * v[k] / T:5.1f}%" for k in keys))
+roles = [("dequant", 0, ["full", "A free", "st+wait", "-"]), ("epilogue", 5, ["done", "s_full", "-", "-"]),
+         ("producer", 10, ["empty", "-", "-", "-"]), ("stager", 15, ["slot free", "-", "-", "-"]),
+         ("mma", 20, ["d_empty", "a_full", "xfull", "issue"])]
+for name, base, keys in roles:
+    T = v[base + 4] or 1
+    print(f"{name:9s} total {T:14d}  " + "  ".join(f"{k} {100 * v[base + i] / T:5.1f}%" for i, k in enumerate(keys) if k != "-"))
 
-# event timeline of CTA 0 (first units), cycles relative to the first event
-L.tpq_debug_trace.argtypes = [C.c_void_p]
-tr = (C.c_longlong * (16 * 32 * 8))()
-L.tpq_debug_trace(C.cast(tr, C.c_void_p))
+# per-unit timeline of CTA 0 (layer-2 launch of the last forward), cycles relative to unit 16's MMA a_full
 import numpy as np  # noqa: E402
-t = np.array(tr, dtype=np.int64).reshape(16, 32, 8)
-t0 = t[t > 0].min()
-rel = np.where(t > 0, t - t0, -1)
-print("unit | W_issue X_issue | deq0: full_ok alu_done a_full_arr | mma13: a_full_ok d_empty_ok issued | epi8: d_ok")
-for i in range(32):
-    print(f"{i:4d} | {rel[12, i, 0]:7d} {rel[12, i, 1]:7d} | " + " ".join(f"{rel[0, i, e]:7d}" for e in range(3)) +
-          " | " + " ".join(f"{rel[13, i, e]:7d}" for e in range(3)) + f" | {rel[8, i, 0]:7d}")
+L.tpq_debug_trace.argtypes = [C.c_void_p]
+tr = (C.c_longlong * (24 * 64 * 4))()
+L.tpq_debug_trace(C.cast(tr, C.c_void_p))
+t = np.array(tr, dtype=np.int64).reshape(24, 64, 4)
+t0 = t[22, 16, 1] or t[22, 16, 0] or 1
+def f(w, i, e):
+    return f"{t[w, i, e] - t0:7d}" if t[w, i, e] else "      -"
+print("pair | prod W(2p) | stage | deq(set p%2 w0, unit 2p): full computed Afree | arrive | mma: d_empty a_full xfull issued | epi: done s_full d_empty_arr")
+for pp in range(5, 22):
+    i = 2 * pp
+    dw = 0 if pp % 2 == 0 else 8
+    mw = 22 + pp % 2
+    print(f"{pp:4d} | {f(20, i, 0)} | {f(21, i, 0)} | {f(dw, i, 0)} {f(dw, i, 1)} {f(dw, i, 2)} | {f(dw, i, 3)} | "
+          f"{f(mw, i, 0)} {f(mw, i, 1)} {f(mw, i, 2)} {f(mw, i, 3)} | {f(16, i, 0)} {f(16, i, 1)} {f(16, i, 2)}")
