@@ -75,6 +75,19 @@ def algorithmic_bytes(K1, N1, N2, G, M, tp):
     return l1, l2, step
 
 
+def ncu_traffic(a, tp):
+    """DRAM bytes (read + write) per GEMV launch from the committed `ncu --set full` capture of the
+    default workload (profiles/roofline_traffic.json); None for other workloads."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "roofline_traffic.json")) as f:
+            d = json.load(f)
+    except Exception:
+        return None
+    if a.shape != "llama70b" or a.m != 16 or tp != 1 or a.variant != "tp_aware":
+        return None
+    return d.get("traffic_bytes_per_launch")
+
+
 class ClockSampler:
     """nvidia-smi sampling of SM clocks + throttle reasons during the timed region."""
 
@@ -354,9 +367,9 @@ def main():
             "parallelism": f"tp{shard_tp}",
         },
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
-                     "kernel": "k_gemv (layer-1 + layer-2 launches)",
-                     "bytes_per_step": l1_bytes + l2_bytes},
+                     "frac": achieved / peak, "traffic": ncu_traffic(a, shard_tp), "peak_kind": peak_kind,
+                     "kernel": "k_dqgemv (layer-1 + layer-2 launches)",
+                     "algorithmic_bytes_per_launch": (l1_bytes + l2_bytes) / 2},
         "breakdown_us": {"gather": t_gather, "gemv_l1": t_l1, "between": t_mid, "gemv_l2": t_l2,
                          "allreduce": t_coll},
         "step_roofline": {"bytes": step_bytes, "GBps": step_bytes / (ms_per_step * 1e-3) / 1e9,

@@ -95,10 +95,11 @@ typedef struct tpq_mlp tpq_mlp; /* opaque: one rank's shard of the two-layer MLP
  *             (packing + index maps + export only; no CUDA call is made; forward = ESTATE).
  *   out       receives the handle (NULL on failure).
  * Requirements (TPQ_EINVAL): bits == 4; K1 % 8 == 0, N1 % 8 == 0, N2 % 8 == 0 (GPTQ packing);
- *   N1 % tp == 0; n % 64 == 0 and N2 % 64 == 0 (64-column device blocks); n % G2 == 0 so each
- *   W2 shard owns whole groups (reading c12); K1 % G1 == 0 (else TPQ_EUNSUPPORTED, c13);
- *   G1, G2 in {32, 64, 128} (else TPQ_EUNSUPPORTED).
- * The library owns the device shard (packed int4 + metadata in its private fragment-native
+ *   N1 % tp == 0; n % 128 == 0 and N2 % 128 == 0 (128-column device tiles); n % G2 == 0 so each
+ *   W2 shard owns whole groups (reading c12); K1 % G1 == 0 and K1 % 128 == 0 (else
+ *   TPQ_EUNSUPPORTED, c13; 128-row device k-blocks); G1, G2 in {32, 64, 128} (else
+ *   TPQ_EUNSUPPORTED).
+ * The library owns the device shard (packed int4 + metadata in its private tile x k-block
  * layout), P1 and the workspace for M_max.  Not thread-safe per
  * handle; distinct handles are independent.
  * ------------------------------------------------------------------------------------- */
@@ -180,7 +181,7 @@ typedef struct tpq_mlp_info_t {
   int64_t K1, N1, N2, n, M_max;
   int32_t G1, G2, tp, rank, variant, device;
   int64_t w1_bytes, w2_bytes;       /* packed device bytes of each layer shard (int4 + meta) */
-  int64_t units1, units2;           /* (64-column block x group) work units per layer */
+  int64_t units1, units2;           /* (128-column tile x 128-row k-block) units per layer */
   int32_t grid1, grid2;             /* CTAs launched per layer (stream-K split)          */
   int32_t has_comm;
 } tpq_mlp_info_t;
