@@ -108,12 +108,12 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
 }
-// 2-D tensor TMA global -> shared (tensor map in kernel parameter space), completion on `bar`.
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+// 3-D tensor TMA global -> shared (tensor map in kernel parameter space), completion on `bar`.
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
   asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
-      "[%4];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
       : "memory");
 }
 __device__ __forceinline__ uint64_t policy_evict_first() {
@@ -204,7 +204,7 @@ constexpr uint32_t kIdesc = (1u << 4) | ((uint32_t)(kNPad >> 3) << 17) | ((uint3
 //               x scale into registers; at a segment end the tile output or the stream-K partial
 //               + deterministic fix-up.
 //   warp 20     TMA producer: weight records into the NS-stage ring (L2 evict-first).
-//   warp 21     activation stager: per unit two 2-D tensor TMAs (16 rows x 64 k each, 128-byte
+//   warp 21     activation stager: per unit one 3-D tensor TMA (2 x 64 k x 16 rows, 128-byte
 //               rows, 128B swizzle) landing directly in the K-major SW128 operand layout.
 //   warps 22-23 MMA issuers, warp 22 + p%2 takes pair p: 16 x tcgen05.mma kind::f16 (M=128, N=16,
 //               K=16, A from TMEM) + one commit, which frees the pair's A buffer and activation
@@ -218,9 +218,15 @@ struct TC {
   static constexpr int GPH = G >= kUnitK / 2 ? 1 : (kUnitK / 2) / G;  // groups per k-half
   static constexpr int UB = (int)unit_bytes_c(G);            // weight record bytes
   static constexpr int STAGE = (UB + 127) / 128 * 128;
-  static constexpr int NS = G == 32 ? 18 : 20;               // weight ring stages (units, ~170 KB in flight)
+#ifndef TPQ_NS
+#define TPQ_NS 20
+#endif
+#ifndef TPQ_NX
+#define TPQ_NX 4
+#endif
+  static constexpr int NS = G == 32 && TPQ_NS > 18 ? 18 : TPQ_NS;  // weight ring stages (units)
   static constexpr int XU = kNPad * kUnitK * 2;              // activation bytes per unit (16 rows x 128 k)
-  static constexpr int NX = 4;                               // activation pair slots
+  static constexpr int NX = TPQ_NX;                          // activation pair slots
   // unit slice = two TMA boxes (64 k, 16 rows) of 2 KB: k-half kq at kq * 2048, row m at m * 128
   // (8-row swizzle atoms of 1024 B), 16-byte chunk swizzled by m % 8
   static constexpr int DU = KG * kNPad;                      // accumulator columns per unit
@@ -238,7 +244,7 @@ struct TC {
   // waits for pair p-NA while the other set's pairs may complete out of order (two MMA warps):
   // RD - NA even makes the next pair on that barrier, p - NA + RD > p, one of this set's own
   // pairs, which cannot complete before this set has written it.
-  static constexpr int RD = NA + 2;
+  static constexpr int RD = NX > NA + 2 ? NX : NA + 2;
   static_assert(RD >= NX && RD >= ND && (RD - NA) % 2 == 0, "done ring aliasing");
   static_assert(NA % 2 == 0 && NX % 2 == 0 && ND % 2 == 0, "odd ring depth");
   static constexpr int SRP = 8;                              // scale ring in pairs (> NA + ND)
@@ -406,73 +412,101 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_dqgemv(const GemvArgs a, co
       tc_fence_after();
       TPQ_W(s_full + p % C::SRP, (uint32_t)((p / C::SRP) & 1), 1);
       TPQ_EV(1, 2 * p)
-#pragma unroll 1
-      for (int h = 0; h < 2; ++h) {
-        const int i = 2 * p + h;
-        if (i >= nu) break;
-        const __half* sr = sring + (i % (2 * C::SRP)) * (C::KG * kTileCols);
-#pragma unroll
-        for (int g = 0; g < C::KG; ++g) {  // one group accumulator at a time (register budget)
-          uint32_t v[kNPad];
-          tmem_ld16(tmem + lane_base + d * 2 * C::DU + h * C::DU + g * kNPad, v);
-          const float sc = __half2float(sr[g * kTileCols + col]);
-          tmem_wait_ld();
-#pragma unroll
-          for (int m = 0; m < kNPad; ++m) acc[m] = fmaf(sc, __uint_as_float(v[m]), acc[m]);
-        }
-        const int64_t u = u0 + i;
-        if (kb == a.NKB - 1 || i == nu - 1) {  // segment end
-          const int64_t n = (int64_t)tile * kTileCols + col;
-          const bool full_tile = seg_start == (int64_t)tile * a.NKB && kb == a.NKB - 1;
-          if (full_tile) {
-#pragma unroll
-            for (int m = 0; m < kNPad; ++m)
-              if (m < a.M) a.out[m * a.out_ld + n] = __float2half_rn(acc[m]);
-          } else {
-            // stream-K: this CTA holds part of the tile.  Partial -> own workspace slot (slot 0 = the
-            // CTA's first segment, 1 = its last); the last of the tile's CTAs to arrive sums all
-            // partials in CTA order (deterministic) and writes the tile.
-            const int slot = (seg_start == u0) ? 0 : 1;
-            float* mine = a.ws + ((size_t)blockIdx.x * 2 + slot) * (kNPad * kTileCols);
-#pragma unroll
-            for (int m = 0; m < kNPad; ++m)
-              if (m < a.M) __stcg(mine + m * kTileCols + col, acc[m]);
-            __threadfence();
-            named_bar(1, kTileCols);
-            const int c_first = cta_of_unit((int64_t)tile * a.NKB, a.U, a.grid);
-            const int c_last = cta_of_unit((int64_t)(tile + 1) * a.NKB - 1, a.U, a.grid);
-            if (col == 0) s_last = (atomicAdd(a.cnt + tile, 1) == c_last - c_first);
-            named_bar(1, kTileCols);
-            if (s_last) {
-              __threadfence();
-              float r[kNPad];
-#pragma unroll
-              for (int m = 0; m < kNPad; ++m) r[m] = 0.f;
-              for (int c = c_first; c <= c_last; ++c) {
-                const int cslot = (cta_start(c, a.U, a.grid) / a.NKB == tile) ? 0 : 1;
-                const float* src = a.ws + ((size_t)c * 2 + cslot) * (kNPad * kTileCols);
-#pragma unroll
-                for (int m = 0; m < kNPad; ++m)
-                  if (m < a.M) r[m] += __ldcg(src + m * kTileCols + col);
-              }
+      const int nh = 2 * p + 1 < nu ? 2 : 1;
+      // per unit: add the unit's scaled group sums, then close the tile segment if it ends here
+      auto finish_unit = [&](int i) {
+          const int64_t u = u0 + i;
+          if (kb == a.NKB - 1 || i == nu - 1) {  // segment end
+            const int64_t n = (int64_t)tile * kTileCols + col;
+            const bool full_tile = seg_start == (int64_t)tile * a.NKB && kb == a.NKB - 1;
+            if (full_tile) {
 #pragma unroll
               for (int m = 0; m < kNPad; ++m)
-                if (m < a.M) a.out[m * a.out_ld + n] = __float2half_rn(r[m]);
-              if (col == 0) a.cnt[tile] = 0;  // self-reset for the next launch / graph replay
-            }
-          }
+                if (m < a.M) a.out[m * a.out_ld + n] = __float2half_rn(acc[m]);
+            } else {
+              // stream-K: this CTA holds part of the tile.  Partial -> own workspace slot (slot 0 = the
+              // CTA's first segment, 1 = its last); the last of the tile's CTAs to arrive sums all
+              // partials in CTA order (deterministic) and writes the tile.
+              const int slot = (seg_start == u0) ? 0 : 1;
+              float* mine = a.ws + ((size_t)blockIdx.x * 2 + slot) * (kNPad * kTileCols);
 #pragma unroll
-          for (int m = 0; m < kNPad; ++m) acc[m] = 0.f;
-          seg_start = u + 1;
+              for (int m = 0; m < kNPad; ++m)
+                if (m < a.M) __stcg(mine + m * kTileCols + col, acc[m]);
+              __threadfence();
+              named_bar(1, kTileCols);
+              const int c_first = cta_of_unit((int64_t)tile * a.NKB, a.U, a.grid);
+              const int c_last = cta_of_unit((int64_t)(tile + 1) * a.NKB - 1, a.U, a.grid);
+              if (col == 0) s_last = (atomicAdd(a.cnt + tile, 1) == c_last - c_first);
+              named_bar(1, kTileCols);
+              if (s_last) {
+                __threadfence();
+                float r[kNPad];
+#pragma unroll
+                for (int m = 0; m < kNPad; ++m) r[m] = 0.f;
+                for (int c = c_first; c <= c_last; ++c) {
+                  const int cslot = (cta_start(c, a.U, a.grid) / a.NKB == tile) ? 0 : 1;
+                  const float* src = a.ws + ((size_t)c * 2 + cslot) * (kNPad * kTileCols);
+#pragma unroll
+                  for (int m = 0; m < kNPad; ++m)
+                    if (m < a.M) r[m] += __ldcg(src + m * kTileCols + col);
+                }
+#pragma unroll
+                for (int m = 0; m < kNPad; ++m)
+                  if (m < a.M) a.out[m * a.out_ld + n] = __float2half_rn(r[m]);
+                if (col == 0) a.cnt[tile] = 0;  // self-reset for the next launch / graph replay
+              }
+            }
+#pragma unroll
+            for (int m = 0; m < kNPad; ++m) acc[m] = 0.f;
+            seg_start = u + 1;
+          }
+          if (++kb == a.NKB) {
+            kb = 0;
+            ++tile;
+          }
+      };
+      if constexpr (C::KG == 1) {
+        // both units' accumulators in flight at once, released before the arithmetic
+        uint32_t v0[kNPad], v1[kNPad];
+        const uint32_t dcol = tmem + lane_base + d * 2 * C::DU;
+        tmem_ld16(dcol, v0);
+        if (nh == 2) tmem_ld16(dcol + C::DU, v1);
+        const __half* sr = sring + ((2 * p) % (2 * C::SRP)) * kTileCols;
+        const float sc0 = __half2float(sr[col]), sc1 = __half2float(sr[kTileCols + col]);
+        tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(d_empty + d);
+#pragma unroll
+        for (int m = 0; m < kNPad; ++m) acc[m] = fmaf(sc0, __uint_as_float(v0[m]), acc[m]);
+        finish_unit(2 * p);
+        if (nh == 2) {
+#pragma unroll
+          for (int m = 0; m < kNPad; ++m) acc[m] = fmaf(sc1, __uint_as_float(v1[m]), acc[m]);
+          finish_unit(2 * p + 1);
         }
-        if (++kb == a.NKB) {
-          kb = 0;
-          ++tile;
+      } else {
+#pragma unroll 1
+        for (int h = 0; h < nh; ++h) {
+          const int i = 2 * p + h;
+          const __half* sr = sring + (i % (2 * C::SRP)) * (C::KG * kTileCols);
+#pragma unroll
+          for (int g = 0; g < C::KG; ++g) {  // one group accumulator at a time (register budget)
+            uint32_t v[kNPad];
+            tmem_ld16(tmem + lane_base + d * 2 * C::DU + h * C::DU + g * kNPad, v);
+            const float sc = __half2float(sr[g * kTileCols + col]);
+            tmem_wait_ld();
+#pragma unroll
+            for (int m = 0; m < kNPad; ++m) acc[m] = fmaf(sc, __uint_as_float(v[m]), acc[m]);
+          }
+          if (h == nh - 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(d_empty + d);
+          }
+          finish_unit(i);
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(d_empty + d);
       TPQ_EV(2, 2 * p)
     }
     TPQ_PFLUSH(5)
@@ -514,19 +548,18 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_dqgemv(const GemvArgs a, co
     TPQ_PDECL
     for (int p = 0; p < np; ++p) {
       const int x = p % C::NX, nh = (2 * p + 1 < nu) ? 2 : 1;
+      const int kb1 = kb + 1 == a.NKB ? 0 : kb + 1;
       if (p >= C::NX) TPQ_W(done + (p - C::NX) % C::RD, (uint32_t)(((p - C::NX) / C::RD) & 1), 0);  // slot free
       TPQ_EV(0, 2 * p)
+      TPQ_T0(tm)
       if (elect_one()) {
         mbar_arrive_expect_tx(xfull + x, nh * C::XU);
-        for (int h = 0; h < nh; ++h) {
-          const int kbh = (kb + h) % a.NKB;
-          uint8_t* dst = smem + C::XRING + (2 * x + h) * C::XU;
-          tma_load_2d(dst, &xmap, kbh * kUnitK, 0, xfull + x);
-          tma_load_2d(dst + C::XU / 2, &xmap, kbh * kUnitK + kUnitK / 2, 0, xfull + x);
-        }
+        tma_load_3d(smem + C::XRING + 2 * x * C::XU, &xmap, 0, 0, 2 * kb, xfull + x);
+        if (nh == 2) tma_load_3d(smem + C::XRING + (2 * x + 1) * C::XU, &xmap, 0, 0, 2 * kb1, xfull + x);
       }
       __syncwarp();
-      kb = (kb + nh) % a.NKB;
+      TPQ_T1(tm, 1)
+      kb = nh == 2 ? (kb1 + 1 == a.NKB ? 0 : kb1 + 1) : kb1;
     }
     TPQ_PFLUSH(15)
   } else {
@@ -677,11 +710,12 @@ bool make_xmap(CUtensorMap* map, const void* base, int64_t K) {
         q != cudaDriverEntryPointSuccess || !encode)
       return false;
   }
-  const cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)kNPad};
-  const cuuint64_t strides[1] = {(cuuint64_t)K * 2};  // bytes between rows
-  const cuuint32_t box[2] = {(cuuint32_t)(kUnitK / 2), (cuuint32_t)kNPad};
-  const cuuint32_t es[2] = {1, 1};
-  return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+  // dims (64 k, 16 rows, K/64 k-halves); box (64, 16, 2) = one unit's slice: k-half kq at kq * 2048
+  const cuuint64_t dims[3] = {(cuuint64_t)(kUnitK / 2), (cuuint64_t)kNPad, (cuuint64_t)(K / (kUnitK / 2))};
+  const cuuint64_t strides[2] = {(cuuint64_t)K * 2, (cuuint64_t)kUnitK};  // bytes: row, k-half
+  const cuuint32_t box[3] = {(cuuint32_t)(kUnitK / 2), (cuuint32_t)kNPad, 2};
+  const cuuint32_t es[3] = {1, 1, 1};
+  return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(base), dims, strides, box, es,
                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }

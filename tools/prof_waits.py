@@ -35,7 +35,7 @@ torch.cuda.synchronize()
 L.tpq_debug_prof(C.cast(buf, C.c_void_p))
 v = list(buf)
 roles = [("dequant", 0, ["full", "A free", "st+wait", "-"]), ("epilogue", 5, ["done", "s_full", "-", "-"]),
-         ("producer", 10, ["empty", "-", "-", "-"]), ("stager", 15, ["slot free", "-", "-", "-"]),
+         ("producer", 10, ["empty", "-", "-", "-"]), ("stager", 15, ["slot free", "tma issue", "-", "-"]),
          ("mma", 20, ["d_empty", "a_full", "xfull", "issue"])]
 for name, base, keys in roles:
     T = v[base + 4] or 1
