@@ -247,13 +247,14 @@ struct TC {
   static constexpr int RD = NX > NA + 2 ? NX : NA + 2;
   static_assert(RD >= NX && RD >= ND && (RD - NA) % 2 == 0, "done ring aliasing");
   static_assert(NA % 2 == 0 && NX % 2 == 0 && ND % 2 == 0, "odd ring depth");
-  static constexpr int SRP = 8;                              // scale ring in pairs (> NA + ND)
+  static constexpr int SRP = 8;                              // scale ring in pairs (> NA + ND: a slot is
+                                                             // rewritten only after the epilogue read it)
   static_assert(SRP > NA + ND, "scale ring too shallow");
   static constexpr int XRING = 0;                            // 1024-aligned (swizzle atoms)
   static constexpr int WRING = NX * 2 * XU;                  // weight stages
   static constexpr int SRING = WRING + NS * STAGE;           // fp16 scales [2 SRP units][KG][128]
   static constexpr int BARS = SRING + 2 * SRP * KG * kTileCols * 2;
-  static constexpr int SMEM = BARS + 8 * (2 * NS + NX + NA + ND + RD + SRP);
+  static constexpr int SMEM = BARS + 8 * (2 * NS + NX + NA + ND + RD);
 };
 
 struct GemvArgs {
@@ -290,7 +291,6 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_dqgemv(const GemvArgs a, co
   uint64_t* d_empty = a_full + C::NA;  // [ND] epilogue read the pair's accumulators (4 warps)
   uint64_t* done = d_empty + C::ND;    // [RD] pair p's MMAs completed (one tcgen05.commit): frees its
                                        //      A buffer and activation slot, hands its accumulators over
-  uint64_t* s_full = done + C::RD;     // [SRP] the pair's scales written (8 dequant warps)
   __shared__ uint32_t s_tmem;
   __shared__ int s_last;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -311,7 +311,6 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_dqgemv(const GemvArgs a, co
     for (int b = 0; b < C::NA; ++b) mbar_init(a_full + b, kSetWarps);
     for (int d = 0; d < C::ND; ++d) mbar_init(d_empty + d, 4);
     for (int r = 0; r < C::RD; ++r) mbar_init(done + r, 1);
-    for (int r = 0; r < C::SRP; ++r) mbar_init(s_full + r, kSetWarps);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == kMmaWarp) {
@@ -387,10 +386,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_dqgemv(const GemvArgs a, co
       TPQ_T1(st, 2)
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(s_full + p % C::SRP);
-        mbar_arrive(a_full + b);
-      }
+      if (lane == 0) mbar_arrive(a_full + b);
       TPQ_EV(3, 2 * p)
     }
     TPQ_PFLUSH(0)
@@ -410,7 +406,9 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_dqgemv(const GemvArgs a, co
       TPQ_W(done + p % C::RD, (uint32_t)((p / C::RD) & 1), 0);
       TPQ_EV(0, 2 * p)
       tc_fence_after();
-      TPQ_W(s_full + p % C::SRP, (uint32_t)((p / C::SRP) & 1), 1);
+      // The pair's scales need no wait of their own: the dequant warps wrote them before their
+      // a_full arrive (release), which the MMA warp acquired before the commit that completes
+      // `done` (acquired above), so the writes happen-before this read.
       TPQ_EV(1, 2 * p)
       const int nh = 2 * p + 1 < nu ? 2 : 1;
       // per unit: add the unit's scaled group sums, then close the tile segment if it ends here
