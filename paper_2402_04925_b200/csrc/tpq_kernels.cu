@@ -226,7 +226,7 @@ struct TC {
 #endif
   static constexpr int NS = G == 32 && TPQ_NS > 18 ? 18 : TPQ_NS;  // weight ring stages (units)
   static constexpr int XU = kNPad * kUnitK * 2;              // activation bytes per unit (16 rows x 128 k)
-  static constexpr int NX = TPQ_NX;                          // activation pair slots
+  static constexpr int NX = G == 128 ? TPQ_NX : 4;           // activation pair slots
   // unit slice = two TMA boxes (64 k, 16 rows) of 2 KB: k-half kq at kq * 2048, row m at m * 128
   // (8-row swizzle atoms of 1024 B), 16-byte chunk swizzled by m % 8
   static constexpr int DU = KG * kNPad;                      // accumulator columns per unit
@@ -236,7 +236,10 @@ struct TC {
   // the MMA warp of pair p can wait on a barrier whose previous phase (the other set's pair) has
   // not completed yet, and the phase-parity test passes two phases early.
   static constexpr int NA = 2;                               // TMEM A pair buffers (one per dequant set)
-  static constexpr int ND = G == 32 ? 2 : 4;                 // TMEM accumulator pair sets
+#ifndef TPQ_ND
+#define TPQ_ND 6
+#endif
+  static constexpr int ND = G == 32 ? 2 : (G == 64 && TPQ_ND > 4 ? 4 : TPQ_ND);  // TMEM accumulator pair sets
   static constexpr int TCOLS = 512;
   static_assert(ND * 2 * DU + NA * 2 * AU <= TCOLS, "TMEM budget");
   // pair-done ring.  Phase-parity waits need the awaited completion to be the latest one of its
@@ -244,10 +247,10 @@ struct TC {
   // waits for pair p-NA while the other set's pairs may complete out of order (two MMA warps):
   // RD - NA even makes the next pair on that barrier, p - NA + RD > p, one of this set's own
   // pairs, which cannot complete before this set has written it.
-  static constexpr int RD = NX > NA + 2 ? NX : NA + 2;
+  static constexpr int RD = NX > ND ? (NX > NA + 2 ? NX : NA + 2) : (ND > NA + 2 ? ND : NA + 2);
   static_assert(RD >= NX && RD >= ND && (RD - NA) % 2 == 0, "done ring aliasing");
   static_assert(NA % 2 == 0 && NX % 2 == 0 && ND % 2 == 0, "odd ring depth");
-  static constexpr int SRP = 8;                              // scale ring in pairs (> NA + ND: a slot is
+  static constexpr int SRP = NA + ND + 2;                     // scale ring in pairs (> NA + ND: a slot is
                                                              // rewritten only after the epilogue read it)
   static_assert(SRP > NA + ND, "scale ring too shallow");
   static constexpr int XRING = 0;                            // 1024-aligned (swizzle atoms)
