@@ -37,7 +37,8 @@ struct LayerDev {
   int G = 0, NT = 0, NKB = 0;
   int64_t U = 0;           // NT * NKB units
   int grid = 0;            // persistent CTAs (stream-K), one per SM
-  float* ws = nullptr;     // [grid][2 slots][16][128] fp32 stream-K partials
+  float* ws = nullptr;     // [grid][2 slots][16][128] fp32 stream-K partials (GEMV)
+  float* ws_mm = nullptr;  // [grid][2 slots][256][128] fp32 stream-K partials (A7 GEMM)
   int* cnt = nullptr;      // [NT] arrival counters (self-resetting)
 };
 
@@ -51,10 +52,15 @@ bool gemv_prepare(int G);
 cudaError_t launch_gemv(const LayerDev& L, const CUtensorMap& xmap, int M, void* out, int64_t out_ld,
                         cudaStream_t st);
 
+// A7 (M > 16): out[m][n] = sum_k x[m][k] deq(W)[k][n] for M <= nb rows (nb in {64, 128, 256}), x a
+// [nb][K] fp16 row-major buffer described by xmap (make_xmap with rows = nb), out [M][out_ld].
+cudaError_t launch_gemm(const LayerDev& L, const CUtensorMap& xmap, int nb, int M, void* out, int64_t out_ld,
+                        cudaStream_t st);
+
 // Tensor map of a [16][K] fp16 row-major activation buffer for the GEMV's TMA: box (64 k, 16 rows)
 // with 128-byte swizzle = half a unit's slice in the K-major SW128 operand layout.  Returns false
 // if the driver entry point is unavailable or encoding fails.
-bool make_xmap(CUtensorMap* map, const void* base, int64_t K);
+bool make_xmap(CUtensorMap* map, const void* base, int64_t K, int rows);
 
 // Row-major gather dst[m*K + k] = v(m, k):
 //   GATHER_COLS:      v(m, k) = src[m*ld + (idx ? idx[k] : k)]

@@ -136,6 +136,8 @@ inline uint32_t nib(uint32_t w, int i) { return (w >> (4 * i)) & 0xFu; }
 
 }  // namespace
 
+constexpr int kGemmRows = 256;  // A7: activation rows per GEMM pass
+
 struct tpq_comm {
   ncclComm_t comm;
   int tp, rank, device;
@@ -155,12 +157,14 @@ struct tpq_mlp {
   int32_t* d_gcols = nullptr;  // naive: P2[r n .. (r+1) n)
   void* d_x1 = nullptr;        // layer-1 input X[:, P1], row-major [16][K1]
   void* d_y1 = nullptr;        // layer-1 output = layer-2 input, row-major [16][n]
-  void* d_buf = nullptr;       // AllGather buffer [tp][16][n]
+  void* d_buf = nullptr;       // AllGather buffer [tp][rows][n]
   void* d_xin = nullptr;       // host-forward staging [M_max][K1]
   void* d_yout = nullptr;      // host-forward staging [M_max][N2]
   float* d_ws = nullptr;
   int* d_cnt = nullptr;
-  CUtensorMap xmap1 = {}, xmap2 = {};  // TMA views of d_x1 / d_y1 (GEMV activation operand)
+  CUtensorMap xmap1 = {}, xmap2 = {};  // TMA views of d_x1 / d_y1 (GEMV activation operand, 16 rows)
+  CUtensorMap mm1[3] = {}, mm2[3] = {};  // A7 views of d_x1 / d_y1 with 64 / 128 / 256 rows
+  int rows = 16;                       // activation rows per pass: 16 (GEMV) or 256 (M_max > 16)
   ncclComm_t comm = nullptr;
   cudaEvent_t ev[6] = {};
   bool timing = false;
@@ -367,24 +371,32 @@ int tp_shard_mlp(const gptq_layer* w1, const gptq_layer* w2, const int32_t* P1, 
         auto A = [&](void** p, size_t b) { return dev_alloc(p, b); };
         const size_t ws1 = (size_t)h->L1.grid * 2 * tpq::kNPad * tpq::kTileCols;
         const size_t ws2 = (size_t)h->L2.grid * 2 * tpq::kNPad * tpq::kTileCols;
+        h->rows = M_max > tpq::kMaxM ? kGemmRows : tpq::kMaxM;
+        const size_t wm1 = M_max > tpq::kMaxM ? (size_t)h->L1.grid * 2 * kGemmRows * tpq::kTileCols : 0;
+        const size_t wm2 = M_max > tpq::kMaxM ? (size_t)h->L2.grid * 2 * kGemmRows * tpq::kTileCols : 0;
         const size_t ncnt = (size_t)(h->L1.NT + h->L2.NT);
         if ((r = A(&h->d_w1, h->pk1.size())) || (r = A(&h->d_w2, h->pk2.size())) ||
-            (r = A((void**)&h->d_P1, K1 * 4)) || (r = A((void**)&h->d_gcols, n * 4)) || (r = A(&h->d_x1, (size_t)tpq::kMaxM * K1 * 2)) ||
-            (r = A(&h->d_y1, (size_t)tpq::kMaxM * n * 2)) || (r = A(&h->d_buf, (size_t)tp * tpq::kMaxM * n * 2)) ||
+            (r = A((void**)&h->d_P1, K1 * 4)) || (r = A((void**)&h->d_gcols, n * 4)) || (r = A(&h->d_x1, (size_t)h->rows * K1 * 2)) ||
+            (r = A(&h->d_y1, (size_t)h->rows * n * 2)) || (r = A(&h->d_buf, (size_t)tp * h->rows * n * 2)) ||
             (r = A(&h->d_xin, (size_t)M_max * K1 * 2)) || (r = A(&h->d_yout, (size_t)M_max * N2 * 2)) ||
-            (r = A((void**)&h->d_ws, (ws1 + ws2) * 4)) || (r = A((void**)&h->d_cnt, ncnt * 4)))
+            (r = A((void**)&h->d_ws, (ws1 + ws2 + wm1 + wm2) * 4)) || (r = A((void**)&h->d_cnt, ncnt * 4)))
           return r;
         TPQ_CUDA(cudaMemcpy(h->d_w1, h->pk1.data(), h->pk1.size(), cudaMemcpyHostToDevice));
         TPQ_CUDA(cudaMemcpy(h->d_w2, h->pk2.data(), h->pk2.size(), cudaMemcpyHostToDevice));
         TPQ_CUDA(cudaMemcpy(h->d_P1, P1, K1 * 4, cudaMemcpyHostToDevice));
         TPQ_CUDA(cudaMemcpy(h->d_gcols, h->gather_cols.data(), n * 4, cudaMemcpyHostToDevice));
         TPQ_CUDA(cudaMemset(h->d_cnt, 0, ncnt * 4));
-        if (!tpq::make_xmap(&h->xmap1, h->d_x1, K1) || !tpq::make_xmap(&h->xmap2, h->d_y1, n))
-          return fail(TPQ_ECUDA, "cuTensorMapEncodeTiled failed for the activation buffers");
+        bool mok = tpq::make_xmap(&h->xmap1, h->d_x1, K1, tpq::kNPad) && tpq::make_xmap(&h->xmap2, h->d_y1, n, tpq::kNPad);
+        if (h->rows > tpq::kMaxM)
+          for (int v = 0; v < 3; ++v)
+            mok = mok && tpq::make_xmap(&h->mm1[v], h->d_x1, K1, 64 << v) && tpq::make_xmap(&h->mm2[v], h->d_y1, n, 64 << v);
+        if (!mok) return fail(TPQ_ECUDA, "cuTensorMapEncodeTiled failed for the activation buffers");
         h->L1.packed = (const uint8_t*)h->d_w1;
         h->L2.packed = (const uint8_t*)h->d_w2;
         h->L1.ws = h->d_ws;
         h->L2.ws = h->d_ws + ws1;  // separate partial slots per layer
+        h->L1.ws_mm = wm1 ? h->d_ws + ws1 + ws2 : nullptr;
+        h->L2.ws_mm = wm2 ? h->d_ws + ws1 + ws2 + wm1 : nullptr;
         h->L1.cnt = h->d_cnt;
         h->L2.cnt = h->d_cnt + h->L1.NT;
         TPQ_CUDA(cudaDeviceSynchronize());
@@ -492,17 +504,28 @@ static cudaError_t mark_event(cudaEvent_t e, cudaStream_t st) {
                                              : cudaEventRecord(e, st);
 }
 
+// One dequant-GEMM layer for mc rows: the GEMV (mc <= 16) or the A7 tensor-core GEMM (mc <= 256).
+cudaError_t run_layer(tpq_mlp* h, int layer, int mc, void* out, int64_t out_ld, cudaStream_t st) {
+  const tpq::LayerDev& L = layer == 1 ? h->L1 : h->L2;
+  if (mc <= tpq::kMaxM) return tpq::launch_gemv(L, layer == 1 ? h->xmap1 : h->xmap2, mc, out, out_ld, st);
+  const int v = mc <= 64 ? 0 : mc <= 128 ? 1 : 2;
+  return tpq::launch_gemm(L, layer == 1 ? h->mm1[v] : h->mm2[v], 64 << v, mc, out, out_ld, st);
+}
+
+// Rows per pass of the forward: 16 (GEMV) while M <= 16, else up to 256 (A7).
+int64_t pass_rows(const tpq_mlp* h, int64_t M) { return M <= tpq::kMaxM ? tpq::kMaxM : h->rows; }
+
 int chunk_forward(tpq_mlp* h, const uint16_t* X, int mc, void* Y, cudaStream_t st, bool collective) {
   TPQ_CUDA(tpq::launch_gather_rowmajor(X, h->K1, h->d_P1, tpq::GATHER_COLS, 0, mc, h->K1, h->d_x1, st));  // X[:,P1]
   TPQ_MARK(1);
   if (h->variant == TPQ_TP_AWARE) {
     // Alg. 3 L1: Y1_local is already in the row order of this rank's W2[P2] block (no exchange)
-    TPQ_CUDA(tpq::launch_gemv(h->L1, h->xmap1, mc, h->d_y1, h->n, st));
+    TPQ_CUDA(run_layer(h, 1, mc, h->d_y1, h->n, st));
     TPQ_MARK(2);
   } else {
     // Alg. 2 L1 into this rank's slot of the AllGather buffer [tp][mc][n]
     uint8_t* slot = (uint8_t*)h->d_buf + (size_t)h->rank * mc * h->n * 2;
-    TPQ_CUDA(tpq::launch_gemv(h->L1, h->xmap1, mc, slot, h->n, st));
+    TPQ_CUDA(run_layer(h, 1, mc, slot, h->n, st));
     TPQ_MARK(2);
     if (h->tp > 1) {
       if (!collective) return fail(TPQ_ESTATE, "naive variant with tp > 1 needs the AllGather (use tp_mlp_forward)");
@@ -512,7 +535,7 @@ int chunk_forward(tpq_mlp* h, const uint16_t* X, int mc, void* Y, cudaStream_t s
     TPQ_CUDA(tpq::launch_gather_rowmajor(h->d_buf, 0, h->d_gcols, tpq::GATHER_ALLGATHER, h->n, mc, h->n, h->d_y1, st));
   }
   TPQ_MARK(3);
-  TPQ_CUDA(tpq::launch_gemv(h->L2, h->xmap2, mc, Y, h->N2, st));  // L2 GEMM
+  TPQ_CUDA(run_layer(h, 2, mc, Y, h->N2, st));  // L2 GEMM
   TPQ_MARK(4);
   return TPQ_OK;
 }
@@ -521,8 +544,9 @@ int forward_impl(tpq_mlp* h, const void* X, int64_t M, void* Y, cudaStream_t st,
   if (collective && h->tp > 1 && !h->comm) return fail(TPQ_ESTATE, "tp=%d requires tpq_mlp_set_comm", h->tp);
   TPQ_CUDA(cudaSetDevice(h->device));
   TPQ_MARK(0);
-  for (int64_t m0 = 0; m0 < M; m0 += 16) {
-    const int mc = (int)std::min<int64_t>(16, M - m0);
+  const int64_t R = pass_rows(h, M);
+  for (int64_t m0 = 0; m0 < M; m0 += R) {
+    const int mc = (int)std::min<int64_t>(R, M - m0);
     int rc = chunk_forward(h, (const uint16_t*)X + m0 * h->K1, mc, (uint8_t*)Y + (size_t)m0 * h->N2 * 2, st,
                            collective);
     if (rc) return rc;
@@ -566,11 +590,12 @@ int tpq_layer1(tpq_mlp* h, const void* X, int64_t M, void* Y1_local, void* strea
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
   TPQ_CUDA(cudaSetDevice(h->device));
-  for (int64_t m0 = 0; m0 < M; m0 += 16) {
-    const int mc = (int)std::min<int64_t>(16, M - m0);
+  const int64_t R = pass_rows(h, M);
+  for (int64_t m0 = 0; m0 < M; m0 += R) {
+    const int mc = (int)std::min<int64_t>(R, M - m0);
     TPQ_CUDA(tpq::launch_gather_rowmajor((const uint16_t*)X + m0 * h->K1, h->K1, h->d_P1, tpq::GATHER_COLS, 0, mc,
                                          h->K1, h->d_x1, st));
-    TPQ_CUDA(tpq::launch_gemv(h->L1, h->xmap1, mc, (uint8_t*)Y1_local + (size_t)m0 * h->n * 2, h->n, st));
+    TPQ_CUDA(run_layer(h, 1, mc, (uint8_t*)Y1_local + (size_t)m0 * h->n * 2, h->n, st));
   }
   return TPQ_OK;
 }
@@ -590,12 +615,13 @@ int tpq_layer2(tpq_mlp* h, const void* Y1in, int64_t M, void* Y2_local, void* st
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
   TPQ_CUDA(cudaSetDevice(h->device));
-  for (int64_t m0 = 0; m0 < M; m0 += 16) {
-    const int mc = (int)std::min<int64_t>(16, M - m0);
+  const int64_t R = pass_rows(h, M);
+  for (int64_t m0 = 0; m0 < M; m0 += R) {
+    const int mc = (int)std::min<int64_t>(R, M - m0);
     // the GEMV reads its activations through the TMA view of d_y1
     TPQ_CUDA(tpq::launch_gather_rowmajor((const uint16_t*)Y1in + m0 * h->n, h->n, nullptr, tpq::GATHER_COLS, 0, mc,
                                          h->n, h->d_y1, st));
-    TPQ_CUDA(tpq::launch_gemv(h->L2, h->xmap2, mc, (uint8_t*)Y2_local + (size_t)m0 * h->N2 * 2, h->N2, st));
+    TPQ_CUDA(run_layer(h, 2, mc, (uint8_t*)Y2_local + (size_t)m0 * h->N2 * 2, h->N2, st));
   }
   return TPQ_OK;
 }

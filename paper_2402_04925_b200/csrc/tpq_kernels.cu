@@ -614,6 +614,253 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_dqgemv(const GemvArgs a, co
   }
 }
 
+// ------------------------------------------------------------------ A7: tensor-core path, M > 16
+// k_dqgemm<G, NB>: the same product for NB (64 / 128 / 256) activation rows per launch, where the
+// tensor pipe, not HBM, is the limit.  Same weight records and stream-K split
+// as the GEMV; differences:
+//   * the fp16 scale is folded into the A operand, A = fp16(s (q - z)) (one rounding of the exact
+//     (q - z) times s), so a tile segment accumulates entirely in one TMEM accumulator of NB
+//     columns and the epilogue runs once per segment instead of once per unit;
+//   * N = NB per tcgen05.mma (M = 128, K = 16); the activation slice of a unit is NB rows x 128 k,
+//     one 3-D tensor TMA (box 64 k x NB rows x 2, 128B swizzle);
+//   * hand-offs per unit (a unit carries 8 MMAs of N = NB: the tensor pipe, not the barriers,
+//     paces it).
+// Warps: 0-7 dequant (lane quarter w%4, k-half w/4), 8-11 epilogue, 12 producer, 13 stager,
+// 14 MMA issuer.
+constexpr int kMmWarps = 15;
+template <int G, int NB>
+struct TM {
+  static constexpr int KG = kUnitK / G, GPH = G >= kUnitK / 2 ? 1 : (kUnitK / 2) / G;
+  static constexpr int UB = (int)unit_bytes_c(G), STAGE = (UB + 127) / 128 * 128;
+  static constexpr int XU = NB * kUnitK * 2;  // activation slice bytes per unit
+  static constexpr int NX = 2;                // activation slots
+  static constexpr int NS = NB == 256 ? 8 : 12;
+  static constexpr int NA = 2, AU = kUnitK / 2;  // A buffers (units), columns per unit
+  static constexpr int RD = 2;                   // unit-done ring (>= NA, NX; single in-order issuer)
+  static_assert(NB + NA * AU <= 512, "TMEM budget");
+  static constexpr int XRING = 0, WRING = NX * XU, BARS = WRING + NS * STAGE;
+  static constexpr int SMEM = BARS + 8 * (2 * NS + NX + NA + RD + 2);
+  static constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(NB >> 3) << 17) | ((uint32_t)(kTileCols >> 4) << 24);
+};
+
+struct GemmArgs {
+  const uint8_t* packed;
+  int M;            // rows of this launch (<= NB)
+  int NT, NKB;
+  int64_t U;
+  int grid;
+  __half* out;      // [M][out_ld]
+  int64_t out_ld;
+  float* ws;        // [grid][2][NB][128]
+  int* cnt;
+};
+
+template <int G, int NB>
+__global__ void __launch_bounds__(kMmWarps * 32, 1) k_dqgemm(const GemmArgs a, const __grid_constant__ CUtensorMap xmap) {
+  using C = TM<G, NB>;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BARS);
+  uint64_t* full = bars;              // [NS] weight record landed
+  uint64_t* empty = full + C::NS;     // [NS] dequant warps hold their codes (8)
+  uint64_t* xfull = empty + C::NS;    // [NX] activation slice landed
+  uint64_t* a_full = xfull + C::NX;   // [NA] A operand stored (8)
+  uint64_t* done = a_full + C::NA;    // [RD] unit's MMAs completed (frees A buffer and activation slot)
+  uint64_t* d_full = done + C::RD;    // segment accumulator final
+  uint64_t* d_empty = d_full + 1;     // epilogue read it (4)
+  __shared__ uint32_t s_tmem;
+  __shared__ int s_last;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t u0 = cta_start(blockIdx.x, a.U, a.grid);
+  const int nu = (int)(cta_start(blockIdx.x + 1, a.U, a.grid) - u0);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::NS; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, 8);
+    }
+    for (int s = 0; s < C::NX; ++s) mbar_init(xfull + s, 1);
+    for (int b = 0; b < C::NA; ++b) mbar_init(a_full + b, 8);
+    for (int r = 0; r < C::RD; ++r) mbar_init(done + r, 1);
+    mbar_init(d_full, 1);
+    mbar_init(d_empty, 4);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 14) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&s_tmem)) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  pdl_launch_dependents();
+  const uint32_t tmem = __shfl_sync(0xffffffffu, s_tmem, 0);
+  constexpr uint32_t kA0 = NB;  // TMEM: accumulator columns [0, NB), A buffer b at NB + b * AU
+
+  if (warp < 8) {
+    // ===================== dequant: A = fp16(s (q - z)) -> TMEM =====================
+    const int qw = warp & 3, kh = warp >> 2, col = qw * 32 + lane;
+    const uint32_t lane_base = (uint32_t)(qw * 32) << 16;
+    const __half2 k16 = __float2half2_rn(0.0625f);
+    for (int i = 0; i < nu; ++i) {
+      const int s = i % C::NS, b = i % C::NA;
+      mbar_wait(full + s, (uint32_t)((i / C::NS) & 1));
+      const uint8_t* st = smem + C::WRING + s * C::STAGE;
+      const uint4 c0 = *reinterpret_cast<const uint4*>(st + ((kh * 2 + 0) * kTileCols + col) * 16);
+      const uint4 c1 = *reinterpret_cast<const uint4*>(st + ((kh * 2 + 1) * kTileCols + col) * 16);
+      const uint32_t wv[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+      __half2 zl[C::GPH], zh[C::GPH], sc[C::GPH];
+#pragma unroll
+      for (int j = 0; j < C::GPH; ++j) {
+        const int gi = (kh * (kUnitK / 2)) / G + j;
+        const uint8_t* meta = st + kUnitK * kTileCols / 2;
+        const int z = (meta[C::KG * 256 + gi * 64 + (col >> 1)] >> (4 * (col & 1))) & 0xF;
+        const __half sv = *reinterpret_cast<const __half*>(meta + gi * 256 + 2 * col);
+        zl[j] = __float2half2_rn((float)(1024 + z));
+        zh[j] = __float2half2_rn((float)(-64 - z));
+        sc[j] = __halves2half2(sv, sv);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + s);
+      uint32_t r[32];
+#pragma unroll
+      for (int w = 0; w < 8; ++w) {
+        const int j = C::GPH == 1 ? 0 : (w * 8) / G;
+        const uint32_t x = wv[w], x8 = x >> 8;
+        r[4 * w + 0] = h2u(__hmul2(__hsub2(u2h(lop3_and_or(x, 0x000F000Fu, 0x64006400u)), zl[j]), sc[j]));
+        r[4 * w + 1] = h2u(__hmul2(__hfma2(u2h(lop3_and_or(x, 0x00F000F0u, 0x64006400u)), k16, zh[j]), sc[j]));
+        r[4 * w + 2] = h2u(__hmul2(__hsub2(u2h(lop3_and_or(x8, 0x000F000Fu, 0x64006400u)), zl[j]), sc[j]));
+        r[4 * w + 3] = h2u(__hmul2(__hfma2(u2h(lop3_and_or(x8, 0x00F000F0u, 0x64006400u)), k16, zh[j]), sc[j]));
+      }
+      if (i >= C::NA) mbar_wait(done + (i - C::NA) % C::RD, (uint32_t)(((i - C::NA) / C::RD) & 1));  // A free
+      tc_fence_after();
+      tmem_st32(tmem + lane_base + kA0 + b * C::AU + kh * 32, r);
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(a_full + b);
+    }
+  } else if (warp < 12) {
+    // ===================== epilogue: once per tile segment =====================
+    const int qw = warp - 8, col = qw * 32 + lane;
+    const uint32_t lane_base = (uint32_t)(qw * 32) << 16;
+    pdl_wait();
+    int64_t seg_start = u0;
+    int kb = (int)(u0 % a.NKB), tile = (int)(u0 / a.NKB), seg = 0;
+    for (int i = 0; i < nu; ++i) {
+      if (kb == a.NKB - 1 || i == nu - 1) {  // unit i closes a segment
+        const int64_t n = (int64_t)tile * kTileCols + col;
+        const bool full_tile = seg_start == (int64_t)tile * a.NKB && kb == a.NKB - 1;
+        mbar_wait(d_full, (uint32_t)(seg & 1));
+        tc_fence_after();
+        const int slot = (seg_start == u0) ? 0 : 1;
+        float* mine = a.ws + ((size_t)blockIdx.x * 2 + slot) * ((size_t)NB * kTileCols);
+        for (int m0 = 0; m0 < a.M; m0 += 16) {  // 16 rows per tcgen05.ld
+          uint32_t v[16];
+          tmem_ld16(tmem + lane_base + m0, v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int m = 0; m < 16; ++m) {
+            if (m0 + m >= a.M) break;
+            if (full_tile) a.out[(int64_t)(m0 + m) * a.out_ld + n] = __float2half_rn(__uint_as_float(v[m]));
+            else __stcg(mine + (size_t)(m0 + m) * kTileCols + col, __uint_as_float(v[m]));
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(d_empty);
+        if (!full_tile) {
+          __threadfence();
+          named_bar(1, kTileCols);
+          const int c_first = cta_of_unit((int64_t)tile * a.NKB, a.U, a.grid);
+          const int c_last = cta_of_unit((int64_t)(tile + 1) * a.NKB - 1, a.U, a.grid);
+          if (col == 0) s_last = (atomicAdd(a.cnt + tile, 1) == c_last - c_first);
+          named_bar(1, kTileCols);
+          if (s_last) {
+            __threadfence();
+            for (int m = 0; m < a.M; ++m) {
+              float r = 0.f;
+              for (int c = c_first; c <= c_last; ++c) {
+                const int cslot = (cta_start(c, a.U, a.grid) / a.NKB == tile) ? 0 : 1;
+                r += __ldcg(a.ws + ((size_t)c * 2 + cslot) * ((size_t)NB * kTileCols) + (size_t)m * kTileCols + col);
+              }
+              a.out[(int64_t)m * a.out_ld + n] = __float2half_rn(r);
+            }
+            if (col == 0) a.cnt[tile] = 0;
+          }
+        }
+        ++seg;
+        seg_start = u0 + i + 1;
+      }
+      if (++kb == a.NKB) {
+        kb = 0;
+        ++tile;
+      }
+    }
+  } else if (warp == 12) {
+    // ===================== weight producer =====================
+    const uint64_t pw = policy_evict_first();
+    for (int i = 0; i < nu; ++i) {
+      const int s = i % C::NS;
+      if (i >= C::NS) mbar_wait(empty + s, (uint32_t)(((i / C::NS) & 1) ^ 1));
+      if (elect_one()) {
+        mbar_arrive_expect_tx(full + s, C::UB);
+        bulk_g2s(smem + C::WRING + s * C::STAGE, a.packed + (u0 + i) * C::UB, C::UB, full + s, pw);
+      }
+      __syncwarp();
+    }
+  } else if (warp == 13) {
+    // ===================== activation stager (one 3-D tensor TMA per unit) =====================
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&xmap)) : "memory");
+    pdl_wait();
+    int kb = (int)(u0 % a.NKB);
+    for (int i = 0; i < nu; ++i) {
+      const int x = i % C::NX;
+      if (i >= C::NX) mbar_wait(done + (i - C::NX) % C::RD, (uint32_t)(((i - C::NX) / C::RD) & 1));
+      if (elect_one()) {
+        mbar_arrive_expect_tx(xfull + x, C::XU);
+        tma_load_3d(smem + C::XRING + x * C::XU, &xmap, 0, 0, 2 * kb, xfull + x);
+      }
+      __syncwarp();
+      if (++kb == a.NKB) kb = 0;
+    }
+  } else {
+    // ===================== MMA issuer =====================
+    const uint32_t xring = smem_u32(smem + C::XRING);
+    int kb = (int)(u0 % a.NKB), seg = 0;
+    for (int i = 0; i < nu; ++i) {
+      const bool first = i == 0 || kb == 0, last = i == nu - 1 || kb == a.NKB - 1;
+      const int b = i % C::NA, x = i % C::NX;
+      if (first) mbar_wait(d_empty, (uint32_t)((seg & 1) ^ 1));
+      mbar_wait(a_full + b, (uint32_t)((i / C::NA) & 1));
+      mbar_wait(xfull + x, (uint32_t)((i / C::NX) & 1));
+      tc_fence_after();
+      const uint64_t bd0 = bdesc_sw128(xring + x * C::XU);
+      const uint32_t at = tmem + kA0 + b * C::AU;
+      uint32_t aop[8];
+      uint64_t bop[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        aop[j] = at + j * 8;
+        bop[j] = bd0 + (uint64_t)(((j / 4) * (C::XU / 2) + (j % 4) * 32) >> 4);
+      }
+      if (elect_one()) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) umma_ts1(tmem, aop[j], bop[j], C::IDESC, (first && j == 0) ? 0u : 1u);
+        umma_commit1(done + i % C::RD);
+        if (last) umma_commit1(d_full);
+      }
+      __syncwarp();
+      if (last) ++seg;
+      if (++kb == a.NKB) kb = 0;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 14) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  }
+}
+
 template <class Kern, class... Args>
 cudaError_t launch_pdl(Kern k, dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
   cudaLaunchConfig_t cfg = {};
@@ -702,7 +949,7 @@ int prof_read(unsigned long long* out) {  // read and reset
   return cudaMemcpyToSymbol(g_tpq_prof, z, sizeof(z)) != cudaSuccess;
 }
 #endif
-bool make_xmap(CUtensorMap* map, const void* base, int64_t K) {
+bool make_xmap(CUtensorMap* map, const void* base, int64_t K, int rows) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   if (!encode) {
     cudaDriverEntryPointQueryResult q;
@@ -711,20 +958,32 @@ bool make_xmap(CUtensorMap* map, const void* base, int64_t K) {
         q != cudaDriverEntryPointSuccess || !encode)
       return false;
   }
-  // dims (64 k, 16 rows, K/64 k-halves); box (64, 16, 2) = one unit's slice: k-half kq at kq * 2048
-  const cuuint64_t dims[3] = {(cuuint64_t)(kUnitK / 2), (cuuint64_t)kNPad, (cuuint64_t)(K / (kUnitK / 2))};
+  // dims (64 k, rows, K/64 k-halves); box (64, rows, 2) = one unit's slice: k-half kq at kq * rows * 128
+  const cuuint64_t dims[3] = {(cuuint64_t)(kUnitK / 2), (cuuint64_t)rows, (cuuint64_t)(K / (kUnitK / 2))};
   const cuuint64_t strides[2] = {(cuuint64_t)K * 2, (cuuint64_t)kUnitK};  // bytes: row, k-half
-  const cuuint32_t box[3] = {(cuuint32_t)(kUnitK / 2), (cuuint32_t)kNPad, 2};
+  const cuuint32_t box[3] = {(cuuint32_t)(kUnitK / 2), (cuuint32_t)rows, 2};
   const cuuint32_t es[3] = {1, 1, 1};
   return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(base), dims, strides, box, es,
                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+template <int G, int NB>
+bool prepare_mm_t() {
+  constexpr int smem = TM<G, NB>::SMEM;
+  static_assert(smem <= 227 * 1024, "GEMM smem over the per-CTA limit");
+  static_assert(2 * smem > 228 * 1024, "GEMM must be one CTA per SM (TMEM 512 columns)");
+  return cudaFuncSetAttribute(k_dqgemm<G, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) == cudaSuccess;
+}
+template <int G>
+bool prepare_mm_g() {
+  return prepare_mm_t<G, 64>() && prepare_mm_t<G, 128>() && prepare_mm_t<G, 256>();
+}
+
 bool gemv_prepare(int G) {
-  if (G == 128) return prepare_t<128>();
-  if (G == 64) return prepare_t<64>();
-  if (G == 32) return prepare_t<32>();
+  if (G == 128) return prepare_t<128>() && prepare_mm_g<128>();
+  if (G == 64) return prepare_t<64>() && prepare_mm_g<64>();
+  if (G == 32) return prepare_t<32>() && prepare_mm_g<32>();
   return false;
 }
 
@@ -745,6 +1004,34 @@ cudaError_t launch_gemv(const LayerDev& L, const CUtensorMap& xmap, int M, void*
   if (L.G == 128) return launch_pdl(k_dqgemv<128>, dim3(a.grid), dim3(kGemvThreads), TC<128>::SMEM, st, a, xmap);
   if (L.G == 64) return launch_pdl(k_dqgemv<64>, dim3(a.grid), dim3(kGemvThreads), TC<64>::SMEM, st, a, xmap);
   if (L.G == 32) return launch_pdl(k_dqgemv<32>, dim3(a.grid), dim3(kGemvThreads), TC<32>::SMEM, st, a, xmap);
+  return cudaErrorInvalidValue;
+}
+
+template <int G>
+cudaError_t launch_mm_g(int nb, const GemmArgs& a, const CUtensorMap& map, cudaStream_t st) {
+  if (nb == 64) return launch_pdl(k_dqgemm<G, 64>, dim3(a.grid), dim3(kMmWarps * 32), TM<G, 64>::SMEM, st, a, map);
+  if (nb == 128) return launch_pdl(k_dqgemm<G, 128>, dim3(a.grid), dim3(kMmWarps * 32), TM<G, 128>::SMEM, st, a, map);
+  if (nb == 256) return launch_pdl(k_dqgemm<G, 256>, dim3(a.grid), dim3(kMmWarps * 32), TM<G, 256>::SMEM, st, a, map);
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_gemm(const LayerDev& L, const CUtensorMap& xmap, int nb, int M, void* out, int64_t out_ld,
+                        cudaStream_t st) {
+  if (M < 1 || M > nb) return cudaErrorInvalidValue;
+  GemmArgs a;
+  a.packed = L.packed;
+  a.M = M;
+  a.NT = L.NT;
+  a.NKB = L.NKB;
+  a.U = L.U;
+  a.grid = L.grid;
+  a.out = reinterpret_cast<__half*>(out);
+  a.out_ld = out_ld;
+  a.ws = L.ws_mm;
+  a.cnt = L.cnt;
+  if (L.G == 128) return launch_mm_g<128>(nb, a, xmap, st);
+  if (L.G == 64) return launch_mm_g<64>(nb, a, xmap, st);
+  if (L.G == 32) return launch_mm_g<32>(nb, a, xmap, st);
   return cudaErrorInvalidValue;
 }
 

@@ -232,3 +232,76 @@ def test_full_size_sampled(shape, M):
     _assert_close(_np(Y1), Y1r[:, P2o], "Y1 (P2 order)")
     _assert_close(_np(Y)[:, cols], Y2r, "Y2 sampled")
     h.close()
+
+
+# ----------------------------------------------------------------------------- A7 (M > 16)
+@pytest.mark.parametrize("G", [32, 64, 128])
+@pytest.mark.parametrize("M", [17, 64, 100, 256, 300])
+def test_a7_tensor_core_path(G, M):
+    """M > 16 runs the A7 tensor-core GEMM (N = 64 / 128 / 256 rows per pass, several passes
+    above 256) on ragged stream-K shapes: Y2 and the staged Y1 against the fp64 oracle."""
+    p = synth.make_problem(1024, 1408, 640, G, M, seed=100 + G + M)
+    P1, P2 = _prep(p)
+    L1, L2 = _olayers(p)
+    Y1r, Y2r = O.dense_mlp(p.X, O.dequantize(L1), O.dequantize(L2))
+    h = tpq.TpMlp(p.w1, p.w2, P1, P2, M_max=512)
+    X = _dev(p.X)
+    Y = _empty(M, p.N2)
+    h.forward(X, M, Y)
+    _assert_close(_np(Y), Y2r, "Y2")
+    Y1 = _empty(M, p.N1)
+    h.layer1(X, M, Y1)
+    P2o, _ = O.alg1_reorder(L2.g)
+    _assert_close(_np(Y1), Y1r[:, P2o], "Y1 (P2 order)")
+    h.close()
+
+
+def test_a7_naive_and_tp_shards():
+    """A7 on the naive variant's staged path and on TP=4 shards summed in rank order."""
+    M, tp = 72, 4
+    p = synth.make_problem(512, 2048, 512, 128, M, seed=7)
+    P1, P2 = _prep(p)
+    L1, L2 = _olayers(p)
+    ref = O.alg3_tp_aware(p.X, L1, L2, tp)
+    X = _dev(p.X)
+    parts = []
+    for r in range(tp):
+        h = tpq.TpMlp(p.w1, p.w2, P1, P2, tp=tp, rank=r, M_max=256)
+        y2 = _empty(M, p.N2)
+        h.forward_local(X, M, y2)
+        _assert_close(_np(y2), ref["Y2_local"][r], f"Y2_local rank {r}")
+        parts.append(y2)
+        h.close()
+    Y = _empty(M, p.N2)
+    tpq.sum_partials(parts, Y)
+    _assert_close(_np(Y), ref["Y2"], "Y2")
+    hn = tpq.TpMlp(p.w1, p.w2, P1, P2, tp=1, variant=tpq.TPQ_NAIVE, M_max=256)
+    Yn = _empty(M, p.N2)
+    hn.forward(X, M, Yn)
+    _assert_close(_np(Yn), ref["Y2"], "Y2 naive tp=1")
+    hn.close()
+
+
+@pytest.mark.parametrize("M", [200, 512])
+def test_a7_full_size_llama_tp8_shard(M):
+    """BASELINE.json configs[3]: Llama-70B MLP at TP=8 (rank 0's shard), M = 200 / 512, in the
+    launch configuration bench.py times; Y1_local in full and 256 sampled columns of Y2_local."""
+    p = synth.make_named("llama70b", M, seed=1)
+    P1, P2 = _prep(p)
+    L1, L2 = _olayers(p)
+    tp, n = 8, p.N1 // 8
+    h = tpq.TpMlp(p.w1, p.w2, P1, P2, tp=tp, rank=0, M_max=512)
+    X = _dev(p.X)
+    Y2 = _empty(M, p.N2)
+    h.forward_local(X, M, Y2)
+    Y1 = _empty(M, n)
+    h.layer1(X, M, Y1)
+    P2o, _ = O.alg1_reorder(L2.g)
+    cols = np.sort(np.random.default_rng(1).choice(p.N2, 256, replace=False))
+    # rank 0: X[:, P1] . W1[P1, P2][:, :n] = X . W1[:, P2[:n]];  Y2_local = Y1_local . W2[P2[:n]]
+    y1r = np.asarray(p.X, np.float64) @ O.dequantize(O.permute_cols(L1, P2o[:n]))
+    L2r = O.permute_rows(L2, P2o[:n])
+    y2r = y1r @ O.dequantize(O.OLayer(q=L2r.q[:, cols], s=L2r.s[:, cols], z=L2r.z[:, cols], g=L2r.g, G=L2r.G))
+    _assert_close(_np(Y1), y1r, "Y1_local")
+    _assert_close(_np(Y2)[:, cols], y2r, "Y2_local sampled")
+    h.close()

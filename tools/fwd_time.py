@@ -20,9 +20,10 @@ p = synth.make_named(a.shape, 16, 0)
 P1, _ = tpq.gptq_reorder(p.w1.g_idx, p.G)
 P2, _ = tpq.gptq_reorder(p.w2.g_idx, p.G)
 R = 2 if a.sim_tp == 1 else 8
-hs = [tpq.TpMlp(p.w1, p.w2, P1, P2, tp=a.sim_tp, rank=0, M_max=16) for _ in range(R)]
-X = torch.from_numpy(p.X).cuda()
-Y = torch.empty(16, p.N2, dtype=torch.float16, device="cuda")
+MM = max(16, max(int(m) for m in a.ms.split(",")))
+hs = [tpq.TpMlp(p.w1, p.w2, P1, P2, tp=a.sim_tp, rank=0, M_max=MM) for _ in range(R)]
+X = torch.from_numpy(synth.make_named(a.shape, MM, 0).X).cuda()
+Y = torch.empty(MM, p.N2, dtype=torch.float16, device="cuda")
 st = torch.cuda.Stream()
 res = {}
 for M in [int(m) for m in a.ms.split(",")]:
