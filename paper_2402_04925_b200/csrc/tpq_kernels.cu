@@ -624,7 +624,10 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_dqgemv(const GemvArgs a, co
 //   * N = NB per tcgen05.mma (M = 128, K = 16); the activation slice of a unit is NB rows x 128 k,
 //     one 3-D tensor TMA (box 64 k x NB rows x 2, 128B swizzle);
 //   * hand-offs per unit (a unit carries 8 MMAs of N = NB: the tensor pipe, not the barriers,
-//     paces it).
+//     paces it);
+//   * a tile split between CTAs leaves fp32 partials (NB x 128 per segment) for k_mm_fixup, a
+//     separate fully parallel kernel that sums them in CTA order (deterministic): one last-arriving
+//     CTA summing up to NB x 128 x 6 values with 128 threads took longer than the GEMM itself.
 // Warps: 0-7 dequant (lane quarter w%4, k-half w/4), 8-11 epilogue, 12 producer, 13 stager,
 // 14 MMA issuer.
 constexpr int kMmWarps = 15;
@@ -668,7 +671,6 @@ __global__ void __launch_bounds__(kMmWarps * 32, 1) k_dqgemm(const GemmArgs a, c
   uint64_t* d_full = done + C::RD;    // segment accumulator final
   uint64_t* d_empty = d_full + 1;     // epilogue read it (4)
   __shared__ uint32_t s_tmem;
-  __shared__ int s_last;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t u0 = cta_start(blockIdx.x, a.U, a.grid);
   const int nu = (int)(cta_start(blockIdx.x + 1, a.U, a.grid) - u0);
@@ -767,26 +769,6 @@ __global__ void __launch_bounds__(kMmWarps * 32, 1) k_dqgemm(const GemmArgs a, c
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(d_empty);
-        if (!full_tile) {
-          __threadfence();
-          named_bar(1, kTileCols);
-          const int c_first = cta_of_unit((int64_t)tile * a.NKB, a.U, a.grid);
-          const int c_last = cta_of_unit((int64_t)(tile + 1) * a.NKB - 1, a.U, a.grid);
-          if (col == 0) s_last = (atomicAdd(a.cnt + tile, 1) == c_last - c_first);
-          named_bar(1, kTileCols);
-          if (s_last) {
-            __threadfence();
-            for (int m = 0; m < a.M; ++m) {
-              float r = 0.f;
-              for (int c = c_first; c <= c_last; ++c) {
-                const int cslot = (cta_start(c, a.U, a.grid) / a.NKB == tile) ? 0 : 1;
-                r += __ldcg(a.ws + ((size_t)c * 2 + cslot) * ((size_t)NB * kTileCols) + (size_t)m * kTileCols + col);
-              }
-              a.out[(int64_t)m * a.out_ld + n] = __float2half_rn(r);
-            }
-            if (col == 0) a.cnt[tile] = 0;
-          }
-        }
         ++seg;
         seg_start = u0 + i + 1;
       }
@@ -912,6 +894,34 @@ __global__ void k_gather_rm(const __half* __restrict__ src, int64_t ld, const in
   }
 }
 
+// A7 stream-K fix-up: tile t split between CTAs c_first..c_last (same partition as k_dqgemm):
+// out[m][t*128 + j] = sum over c of the partial of CTA c (its slot for tile t), in CTA order.
+// Block (t, mb): rows 4 mb + warp, thread j: columns 4 lane .. +3 (float4 loads, 8-byte stores).
+__global__ void k_mm_fixup(const float* __restrict__ ws, int nb, int M, int NKB, int64_t U, int grid,
+                           __half* __restrict__ out, int64_t out_ld) {
+  pdl_launch_dependents();
+  pdl_wait();  // the partials come from the GEMM just before
+  const int t = blockIdx.x;
+  const int c_first = cta_of_unit((int64_t)t * NKB, U, grid), c_last = cta_of_unit((int64_t)(t + 1) * NKB - 1, U, grid);
+  if (c_first == c_last) return;  // the tile lies inside one CTA's range: written by the GEMM
+  const int m = blockIdx.y * 4 + (threadIdx.x >> 5), j = (threadIdx.x & 31) * 4;
+  if (m >= M) return;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int c = c_first; c <= c_last; ++c) {
+    const int slot = (cta_start(c, U, grid) / NKB == t) ? 0 : 1;
+    const float4 v = __ldcg(reinterpret_cast<const float4*>(ws + (((size_t)c * 2 + slot) * nb + m) * kTileCols + j));
+    acc.x += v.x;
+    acc.y += v.y;
+    acc.z += v.z;
+    acc.w += v.w;
+  }
+  const __half2 lo = __floats2half2_rn(acc.x, acc.y), hi = __floats2half2_rn(acc.z, acc.w);
+  uint2 pk;
+  pk.x = *reinterpret_cast<const uint32_t*>(&lo);
+  pk.y = *reinterpret_cast<const uint32_t*>(&hi);
+  *reinterpret_cast<uint2*>(out + (int64_t)m * out_ld + (int64_t)t * kTileCols + j) = pk;
+}
+
 struct PartsArg {
   const __half* p[8];
 };
@@ -1029,10 +1039,13 @@ cudaError_t launch_gemm(const LayerDev& L, const CUtensorMap& xmap, int nb, int 
   a.out_ld = out_ld;
   a.ws = L.ws_mm;
   a.cnt = L.cnt;
-  if (L.G == 128) return launch_mm_g<128>(nb, a, xmap, st);
-  if (L.G == 64) return launch_mm_g<64>(nb, a, xmap, st);
-  if (L.G == 32) return launch_mm_g<32>(nb, a, xmap, st);
-  return cudaErrorInvalidValue;
+  cudaError_t e = L.G == 128 ? launch_mm_g<128>(nb, a, xmap, st)
+                  : L.G == 64 ? launch_mm_g<64>(nb, a, xmap, st)
+                  : L.G == 32 ? launch_mm_g<32>(nb, a, xmap, st)
+                              : cudaErrorInvalidValue;
+  if (e != cudaSuccess) return e;
+  return launch_pdl(k_mm_fixup, dim3((unsigned)L.NT, (unsigned)((M + 3) / 4)), dim3(128), 0, st, (const float*)L.ws_mm,
+                    nb, M, L.NKB, L.U, L.grid, reinterpret_cast<__half*>(out), out_ld);
 }
 
 cudaError_t launch_gather_rowmajor(const void* src, int64_t ld, const int32_t* idx, int mode, int64_t nn, int M,
