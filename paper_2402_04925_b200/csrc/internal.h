@@ -39,6 +39,7 @@ struct LayerDev {
   int grid = 0;            // persistent CTAs (stream-K), one per SM
   float* ws = nullptr;     // [grid][2 slots][16][128] fp32 stream-K partials (GEMV)
   float* ws_mm = nullptr;  // [grid][2 slots][256][128] fp32 stream-K partials (A7 GEMM)
+  float* ws_ss = nullptr;  // [items][128][128] fp32 k-split partials (A7 SS GEMM, M >= 128)
   int* cnt = nullptr;      // [NT] arrival counters (self-resetting)
 };
 
@@ -60,7 +61,22 @@ cudaError_t launch_gemm(const LayerDev& L, const CUtensorMap& xmap, int nb, int 
 // Tensor map of a [16][K] fp16 row-major activation buffer for the GEMV's TMA: box (64 k, 16 rows)
 // with 128-byte swizzle = half a unit's slice in the K-major SW128 operand layout.  Returns false
 // if the driver entry point is unavailable or encoding fails.
-bool make_xmap(CUtensorMap* map, const void* base, int64_t K, int rows);
+bool make_xmap(CUtensorMap* map, const void* base, int64_t K, int rows, int box_rows = 0);
+
+// k-splits of the SS GEMM for `mb` 128-row blocks: as many as keep the work items within one wave
+// of `sms` CTAs, at least 4 k-blocks per split, at most 16 splits.
+inline int ss_splits(int NT, int NKB, int mb, int sms) {
+  const int base = mb * NT;
+  int S = sms / base;
+  const int cap = NKB / 4 < 16 ? NKB / 4 : 16;
+  if (S > cap) S = cap;
+  return S < 1 ? 1 : S;
+}
+
+// A7 for M >= 128 (<= 256 rows per pass): mixed-input SS GEMM, xmap = the [256][K] buffer with
+// 128-row boxes; k-splits chosen to cover `sms` SMs (partials in L.ws_ss, k_ss_fixup).
+cudaError_t launch_gemm_ss(const LayerDev& L, const CUtensorMap& xmap, int M, int sms, void* out, int64_t out_ld,
+                           cudaStream_t st);
 
 // Row-major gather dst[m*K + k] = v(m, k):
 //   GATHER_COLS:      v(m, k) = src[m*ld + (idx ? idx[k] : k)]

@@ -164,6 +164,8 @@ struct tpq_mlp {
   int* d_cnt = nullptr;
   CUtensorMap xmap1 = {}, xmap2 = {};  // TMA views of d_x1 / d_y1 (GEMV activation operand, 16 rows)
   CUtensorMap mm1[3] = {}, mm2[3] = {};  // A7 views of d_x1 / d_y1 with 64 / 128 / 256 rows
+  CUtensorMap ss1 = {}, ss2 = {};        // A7 SS views: 256-row buffers, 128-row boxes
+  int sms = 148;
   int rows = 16;                       // activation rows per pass: 16 (GEMV) or 256 (M_max > 16)
   ncclComm_t comm = nullptr;
   cudaEvent_t ev[6] = {};
@@ -374,12 +376,23 @@ int tp_shard_mlp(const gptq_layer* w1, const gptq_layer* w2, const int32_t* P1, 
         h->rows = M_max > tpq::kMaxM ? kGemmRows : tpq::kMaxM;
         const size_t wm1 = M_max > tpq::kMaxM ? (size_t)h->L1.grid * 2 * kGemmRows * tpq::kTileCols : 0;
         const size_t wm2 = M_max > tpq::kMaxM ? (size_t)h->L2.grid * 2 * kGemmRows * tpq::kTileCols : 0;
+        cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, device);
+        auto ss_ws = [&](const tpq::LayerDev& L) -> size_t {  // largest k-split partial set (M >= 128 passes)
+          if (M_max < 128) return 0;
+          size_t items = 0;
+          for (int mb = 1; mb <= 2; ++mb) {
+            const int S = tpq::ss_splits(L.NT, L.NKB, mb, h->sms);
+            if (S > 1) items = std::max(items, (size_t)mb * L.NT * S);
+          }
+          return items * 128 * 128;
+        };
+        const size_t ws1s = ss_ws(h->L1), ws2s = ss_ws(h->L2);
         const size_t ncnt = (size_t)(h->L1.NT + h->L2.NT);
         if ((r = A(&h->d_w1, h->pk1.size())) || (r = A(&h->d_w2, h->pk2.size())) ||
             (r = A((void**)&h->d_P1, K1 * 4)) || (r = A((void**)&h->d_gcols, n * 4)) || (r = A(&h->d_x1, (size_t)h->rows * K1 * 2)) ||
             (r = A(&h->d_y1, (size_t)h->rows * n * 2)) || (r = A(&h->d_buf, (size_t)tp * h->rows * n * 2)) ||
             (r = A(&h->d_xin, (size_t)M_max * K1 * 2)) || (r = A(&h->d_yout, (size_t)M_max * N2 * 2)) ||
-            (r = A((void**)&h->d_ws, (ws1 + ws2 + wm1 + wm2) * 4)) || (r = A((void**)&h->d_cnt, ncnt * 4)))
+            (r = A((void**)&h->d_ws, (ws1 + ws2 + wm1 + wm2 + ws1s + ws2s) * 4)) || (r = A((void**)&h->d_cnt, ncnt * 4)))
           return r;
         TPQ_CUDA(cudaMemcpy(h->d_w1, h->pk1.data(), h->pk1.size(), cudaMemcpyHostToDevice));
         TPQ_CUDA(cudaMemcpy(h->d_w2, h->pk2.data(), h->pk2.size(), cudaMemcpyHostToDevice));
@@ -387,9 +400,12 @@ int tp_shard_mlp(const gptq_layer* w1, const gptq_layer* w2, const int32_t* P1, 
         TPQ_CUDA(cudaMemcpy(h->d_gcols, h->gather_cols.data(), n * 4, cudaMemcpyHostToDevice));
         TPQ_CUDA(cudaMemset(h->d_cnt, 0, ncnt * 4));
         bool mok = tpq::make_xmap(&h->xmap1, h->d_x1, K1, tpq::kNPad) && tpq::make_xmap(&h->xmap2, h->d_y1, n, tpq::kNPad);
-        if (h->rows > tpq::kMaxM)
+        if (h->rows > tpq::kMaxM) {
           for (int v = 0; v < 3; ++v)
             mok = mok && tpq::make_xmap(&h->mm1[v], h->d_x1, K1, 64 << v) && tpq::make_xmap(&h->mm2[v], h->d_y1, n, 64 << v);
+          mok = mok && tpq::make_xmap(&h->ss1, h->d_x1, K1, kGemmRows, 128) &&
+                tpq::make_xmap(&h->ss2, h->d_y1, n, kGemmRows, 128);
+        }
         if (!mok) return fail(TPQ_ECUDA, "cuTensorMapEncodeTiled failed for the activation buffers");
         h->L1.packed = (const uint8_t*)h->d_w1;
         h->L2.packed = (const uint8_t*)h->d_w2;
@@ -397,6 +413,8 @@ int tp_shard_mlp(const gptq_layer* w1, const gptq_layer* w2, const int32_t* P1, 
         h->L2.ws = h->d_ws + ws1;  // separate partial slots per layer
         h->L1.ws_mm = wm1 ? h->d_ws + ws1 + ws2 : nullptr;
         h->L2.ws_mm = wm2 ? h->d_ws + ws1 + ws2 + wm1 : nullptr;
+        h->L1.ws_ss = ws1s ? h->d_ws + ws1 + ws2 + wm1 + wm2 : nullptr;
+        h->L2.ws_ss = ws2s ? h->d_ws + ws1 + ws2 + wm1 + wm2 + ws1s : nullptr;
         h->L1.cnt = h->d_cnt;
         h->L2.cnt = h->d_cnt + h->L1.NT;
         TPQ_CUDA(cudaDeviceSynchronize());
@@ -508,6 +526,8 @@ static cudaError_t mark_event(cudaEvent_t e, cudaStream_t st) {
 cudaError_t run_layer(tpq_mlp* h, int layer, int mc, void* out, int64_t out_ld, cudaStream_t st) {
   const tpq::LayerDev& L = layer == 1 ? h->L1 : h->L2;
   if (mc <= tpq::kMaxM) return tpq::launch_gemv(L, layer == 1 ? h->xmap1 : h->xmap2, mc, out, out_ld, st);
+  if (mc >= 128 && !getenv("TPQ_NO_SS"))  // compute-bound: activations as the reused A operand
+    return tpq::launch_gemm_ss(L, layer == 1 ? h->ss1 : h->ss2, mc, h->sms, out, out_ld, st);
   const int v = mc <= 64 ? 0 : mc <= 128 ? 1 : 2;
   return tpq::launch_gemm(L, layer == 1 ? h->mm1[v] : h->mm2[v], 64 << v, mc, out, out_ld, st);
 }

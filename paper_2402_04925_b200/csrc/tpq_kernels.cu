@@ -22,6 +22,7 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -843,6 +844,266 @@ __global__ void __launch_bounds__(kMmWarps * 32, 1) k_dqgemm(const GemmArgs a, c
   }
 }
 
+// ------------------------------------------------------------------ A7, large M: mixed-input SS GEMM
+// k_dqgemm_ss<G>: for M >= 128 the activations are the A operand (MMA M = 128 batch rows, TMA from
+// L2, reused across a 128-column weight tile) and the dequantized weights the B operand (N = 128
+// columns), written by 8 warps into shared memory as fp16 s (q - z) in the K-major SWIZZLE_128B
+// layout (fence.proxy.async before the hand-off).  Tile 128 rows x 128 columns, K in 128-row
+// records (8 MMAs of K = 16 each), fp32 accumulator in TMEM (double-buffered across work items).
+// Work items (m-block, n-tile, k-split) round-robin over a persistent grid; with k-splits the
+// fp32 partials are summed by k_ss_fixup in split order (deterministic).
+// Warps: 0-7 dequant, 8-11 epilogue (TMEM lane quarter = 32 batch rows), 12 producer, 13 MMA.
+constexpr int kSsWarps = 14;
+template <int G>
+struct TS {
+  static constexpr int KG = kUnitK / G, GPH = G >= kUnitK / 2 ? 1 : (kUnitK / 2) / G;
+  static constexpr int UB = (int)unit_bytes_c(G), STAGE = (UB + 127) / 128 * 128;
+  static constexpr int BM = 128, BN = kTileCols;
+  static constexpr int XT = BM * kUnitK * 2;  // A tile (activations) per k-block: 32 KB
+  static constexpr int WT = BN * kUnitK * 2;  // B tile (dequantized weights) per k-block: 32 KB
+  static constexpr int NW = 4, NA = 3, NB = 2;  // raw-weight, A (activation) and B (weight) stages
+  static constexpr int KR = 6;                  // k-step done ring: A slot reuse waits t - NA, B slot t - NB;
+                                                // the next k-step on either barrier needs its own A / B first
+  static constexpr int AR = 0, BR = AR + NA * XT, WR = BR + NB * WT;  // A, B 1024-aligned
+  static constexpr int BARS = WR + NW * STAGE;
+  static constexpr int SMEM = BARS + 8 * (2 * NW + NA + NB + KR + 4);  // w_full/empty, a_full, b_full, k_done, d_full/empty
+  static constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+};
+
+struct SsArgs {
+  const uint8_t* packed;
+  int M;              // rows of this pass (<= 256: m-blocks of 128)
+  int MB, NT, NKB, S;
+  int items;          // NT * MB * S: item = (nt * MB + mb) * S + ks
+  int grid;
+  __half* out;        // [M][out_ld]
+  int64_t out_ld;
+  float* ws;          // [items][128][128] k-split partials (S > 1)
+};
+
+template <int G>
+__global__ void __launch_bounds__(kSsWarps * 32, 1) k_dqgemm_ss(const SsArgs a, const __grid_constant__ CUtensorMap xmap) {
+  using C = TS<G>;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BARS);
+  uint64_t* w_full = bars;              // [NW] raw weight record landed
+  uint64_t* w_empty = w_full + C::NW;   // [NW] dequant warps read it (8)
+  uint64_t* a_full = w_empty + C::NW;   // [NA] activation tile landed
+  uint64_t* b_full = a_full + C::NA;    // [NB] dequantized weight tile written (8)
+  uint64_t* k_done = b_full + C::NB;    // [KR] MMAs of k-step t completed: frees its A and B slot
+  uint64_t* d_full = k_done + C::KR;    // [2] item's accumulator final
+  uint64_t* d_empty = d_full + 2;       // [2] epilogue read it (4)
+  __shared__ uint32_t s_tmem;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::NW; ++s) {
+      mbar_init(w_full + s, 1);
+      mbar_init(w_empty + s, 8);
+    }
+    for (int s = 0; s < C::NA; ++s) mbar_init(a_full + s, 1);
+    for (int s = 0; s < C::NB; ++s) mbar_init(b_full + s, 8);
+    for (int s = 0; s < C::KR; ++s) mbar_init(k_done + s, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(d_full + s, 1);
+      mbar_init(d_empty + s, 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 13) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(&s_tmem)) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  pdl_launch_dependents();
+  const uint32_t tmem = __shfl_sync(0xffffffffu, s_tmem, 0);
+  // k-block range of split ks
+  auto krange = [&](int ks, int& k0, int& k1) {
+    k0 = (int)((int64_t)ks * a.NKB / a.S);
+    k1 = (int)((int64_t)(ks + 1) * a.NKB / a.S);
+  };
+
+  if (warp < 8) {
+    // ===================== dequant: record -> fp16 s (q - z) B tile (SW128) =====================
+    const int j = warp * 16 + (lane & 15), kh = lane >> 4;  // weight column (B row), k-half
+    const __half2 k16 = __float2half2_rn(0.0625f);
+    int t = 0;  // k-step counter of this CTA
+    for (int it = blockIdx.x; it < a.items; it += a.grid) {
+      int k0, k1;
+      krange(it % a.S, k0, k1);
+      for (int kb = k0; kb < k1; ++kb, ++t) {
+        const int ws = t % C::NW, ks = t % C::NB;
+        mbar_wait(w_full + ws, (uint32_t)((t / C::NW) & 1));
+        const uint8_t* st = smem + C::WR + ws * C::STAGE;
+        const uint4 c0 = *reinterpret_cast<const uint4*>(st + ((kh * 2 + 0) * kTileCols + j) * 16);
+        const uint4 c1 = *reinterpret_cast<const uint4*>(st + ((kh * 2 + 1) * kTileCols + j) * 16);
+        const uint32_t wv[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+        __half2 zl[C::GPH], zh[C::GPH], sc[C::GPH];
+#pragma unroll
+        for (int g = 0; g < C::GPH; ++g) {
+          const int gi = (kh * (kUnitK / 2)) / G + g;
+          const uint8_t* meta = st + kUnitK * kTileCols / 2;
+          const int z = (meta[C::KG * 256 + gi * 64 + (j >> 1)] >> (4 * (j & 1))) & 0xF;
+          const __half sv = *reinterpret_cast<const __half*>(meta + gi * 256 + 2 * j);
+          zl[g] = __float2half2_rn((float)(1024 + z));
+          zh[g] = __float2half2_rn((float)(-64 - z));
+          sc[g] = __halves2half2(sv, sv);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(w_empty + ws);
+        if (t >= C::NB) mbar_wait(k_done + (t - C::NB) % C::KR, (uint32_t)(((t - C::NB) / C::KR) & 1));  // B slot free
+        uint8_t* brow = smem + C::BR + ks * C::WT + kh * (C::BN * 128) + j * 128;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {  // word w = k 64 kh + 8w .. +7 = 16-byte chunk w of the row
+          const int g = C::GPH == 1 ? 0 : (w * 8) / G;
+          const uint32_t x = wv[w], x8 = x >> 8;
+          uint4 o;
+          o.x = h2u(__hmul2(__hsub2(u2h(lop3_and_or(x, 0x000F000Fu, 0x64006400u)), zl[g]), sc[g]));
+          o.y = h2u(__hmul2(__hfma2(u2h(lop3_and_or(x, 0x00F000F0u, 0x64006400u)), k16, zh[g]), sc[g]));
+          o.z = h2u(__hmul2(__hsub2(u2h(lop3_and_or(x8, 0x000F000Fu, 0x64006400u)), zl[g]), sc[g]));
+          o.w = h2u(__hmul2(__hfma2(u2h(lop3_and_or(x8, 0x00F000F0u, 0x64006400u)), k16, zh[g]), sc[g]));
+          *reinterpret_cast<uint4*>(brow + ((w ^ (j & 7)) << 4)) = o;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core
+        __syncwarp();
+        if (lane == 0) mbar_arrive(b_full + ks);
+      }
+    }
+  } else if (warp < 12) {
+    // ===================== epilogue: one item at a time =====================
+    const int qw = warp - 8;
+    pdl_wait();
+    int n_it = 0;
+    for (int it = blockIdx.x; it < a.items; it += a.grid, ++n_it) {
+      const int db = n_it & 1, ks = it % a.S, mb = (it / a.S) % a.MB, nt = it / (a.S * a.MB);
+      mbar_wait(d_full + db, (uint32_t)((n_it >> 1) & 1));
+      tc_fence_after();
+      const int m = mb * C::BM + qw * 32 + lane;  // batch row of this thread (TMEM lane)
+      for (int c0 = 0; c0 < C::BN; c0 += 32) {
+        uint32_t v[32];
+        tmem_ld16(tmem + ((uint32_t)(qw * 32) << 16) + db * C::BN + c0, v);
+        tmem_ld16(tmem + ((uint32_t)(qw * 32) << 16) + db * C::BN + c0 + 16, v + 16);
+        tmem_wait_ld();
+        if (m < a.M) {
+          if (a.S == 1) {
+            __half* o = a.out + (int64_t)m * a.out_ld + (int64_t)nt * C::BN + c0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              uint4 pk;
+              uint32_t* pw = reinterpret_cast<uint32_t*>(&pk);
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                pw[e] = h2u(__floats2half2_rn(__uint_as_float(v[8 * q + 2 * e]), __uint_as_float(v[8 * q + 2 * e + 1])));
+              *reinterpret_cast<uint4*>(o + 8 * q) = pk;
+            }
+          } else {
+            float* o = a.ws + ((size_t)it * C::BM + (m - mb * C::BM)) * C::BN + c0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              __stcg(reinterpret_cast<float4*>(o + 4 * q),
+                     make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]), __uint_as_float(v[4 * q + 2]),
+                                 __uint_as_float(v[4 * q + 3])));
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(d_empty + db);
+      (void)ks;
+    }
+  } else if (warp == 12) {
+    // ===================== producer: weight records (bulk) + activation tiles (tensor TMA) =====
+    const uint64_t pw = policy_evict_first();
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&xmap)) : "memory");
+    pdl_wait();  // the activations come from the previous kernel in the stream
+    int t = 0;
+    for (int it = blockIdx.x; it < a.items; it += a.grid) {
+      const int mb = (it / a.S) % a.MB, nt = it / (a.S * a.MB);
+      int k0, k1;
+      krange(it % a.S, k0, k1);
+      for (int kb = k0; kb < k1; ++kb, ++t) {
+        const int ws = t % C::NW, ks = t % C::NA;
+        if (t >= C::NW) mbar_wait(w_empty + ws, (uint32_t)(((t - C::NW) / C::NW) & 1));
+        if (elect_one()) {
+          mbar_arrive_expect_tx(w_full + ws, C::UB);
+          bulk_g2s(smem + C::WR + ws * C::STAGE, a.packed + ((int64_t)nt * a.NKB + kb) * C::UB, C::UB, w_full + ws, pw);
+        }
+        __syncwarp();
+        if (t >= C::NA) mbar_wait(k_done + (t - C::NA) % C::KR, (uint32_t)(((t - C::NA) / C::KR) & 1));  // A slot free
+        if (elect_one()) {
+          mbar_arrive_expect_tx(a_full + ks, C::XT);
+          tma_load_3d(smem + C::AR + ks * C::XT, &xmap, 0, mb * C::BM, 2 * kb, a_full + ks);
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    // ===================== MMA issuer =====================
+    int t = 0, n_it = 0;
+    for (int it = blockIdx.x; it < a.items; it += a.grid, ++n_it) {
+      const int db = n_it & 1;
+      int k0, k1;
+      krange(it % a.S, k0, k1);
+      mbar_wait(d_empty + db, (uint32_t)(((n_it >> 1) & 1) ^ 1));
+      for (int kb = k0; kb < k1; ++kb, ++t) {
+        const int sa = t % C::NA, sb = t % C::NB;
+        mbar_wait(a_full + sa, (uint32_t)((t / C::NA) & 1));
+        mbar_wait(b_full + sb, (uint32_t)((t / C::NB) & 1));
+        tc_fence_after();
+        const uint32_t abase = smem_u32(smem + C::AR + sa * C::XT), bbase = smem_u32(smem + C::BR + sb * C::WT);
+        uint64_t ad[8], bd[8];
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {  // k16 block jj: k-half jj / 4, 32-byte step within the 128-byte row
+          ad[jj] = bdesc_sw128(abase + (jj / 4) * (C::BM * 128) + (jj % 4) * 32);
+          bd[jj] = bdesc_sw128(bbase + (jj / 4) * (C::BN * 128) + (jj % 4) * 32);
+        }
+        if (elect_one()) {
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj)
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem + db * C::BN),
+                "l"(ad[jj]), "l"(bd[jj]), "r"(C::IDESC), "r"((kb == k0 && jj == 0) ? 0u : 1u)
+                : "memory");
+          umma_commit1(k_done + t % C::KR);
+          if (kb == k1 - 1) umma_commit1(d_full + db);
+        }
+        __syncwarp();
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 13) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem) : "memory");
+  }
+}
+
+// k-split fix-up of k_dqgemm_ss: out[m][nt 128 + c] = sum over ks of the item's partial (split order).
+// Block (nt * MB + mb, r): rows mb 128 + 4 r + warp, thread = 4 consecutive columns.
+__global__ void k_ss_fixup(const float* __restrict__ ws, int M, int MB, int S, __half* __restrict__ out,
+                           int64_t out_ld) {
+  pdl_launch_dependents();
+  pdl_wait();
+  const int tile = blockIdx.x, mb = tile % MB, nt = tile / MB;
+  const int ml = blockIdx.y * 4 + (threadIdx.x >> 5), m = mb * 128 + ml, c = (threadIdx.x & 31) * 4;
+  if (m >= M) return;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int ks = 0; ks < S; ++ks) {
+    const float4 v = __ldcg(reinterpret_cast<const float4*>(ws + (((size_t)tile * S + ks) * 128 + ml) * 128 + c));
+    acc.x += v.x;
+    acc.y += v.y;
+    acc.z += v.z;
+    acc.w += v.w;
+  }
+  uint2 pk;
+  pk.x = h2u(__floats2half2_rn(acc.x, acc.y));
+  pk.y = h2u(__floats2half2_rn(acc.z, acc.w));
+  *reinterpret_cast<uint2*>(out + (int64_t)m * out_ld + (int64_t)nt * 128 + c) = pk;
+}
+
 template <class Kern, class... Args>
 cudaError_t launch_pdl(Kern k, dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
   cudaLaunchConfig_t cfg = {};
@@ -922,6 +1183,33 @@ __global__ void k_mm_fixup(const float* __restrict__ ws, int nb, int M, int NKB,
   *reinterpret_cast<uint2*>(out + (int64_t)m * out_ld + (int64_t)t * kTileCols + j) = pk;
 }
 
+// X[:, idx] for the layer-1 operand: CTA (m, part) reads row m into shared memory with coalesced
+// 16-byte loads, then gathers part `part` of the k range from there (a direct gather reads a
+// 32-byte sector per 2-byte element).  dst[m][k] = src[m ld + idx[k]].
+__global__ void k_gather_rows(const __half* __restrict__ src, int64_t ld, const int32_t* __restrict__ idx, int64_t K,
+                              __half* __restrict__ dst) {
+  extern __shared__ __align__(16) uint8_t srow_raw[];
+  __half* srow = reinterpret_cast<__half*>(srow_raw);
+  pdl_launch_dependents();
+  pdl_wait();
+  const int m = blockIdx.x;
+  const __half* row = src + (int64_t)m * ld;
+  for (int64_t c = threadIdx.x; c < K / 8; c += blockDim.x)
+    reinterpret_cast<uint4*>(srow)[c] = __ldg(reinterpret_cast<const uint4*>(row) + c);
+  __syncthreads();
+  __half* out = dst + (int64_t)m * K;
+  const int64_t nc = K / 8, c0 = nc * blockIdx.y / gridDim.y, c1 = nc * (blockIdx.y + 1) / gridDim.y;
+  for (int64_t c = c0 + threadIdx.x; c < c1; c += blockDim.x) {
+    const int4 i0 = __ldg(reinterpret_cast<const int4*>(idx) + 2 * c), i1 = __ldg(reinterpret_cast<const int4*>(idx) + 2 * c + 1);
+    uint4 pk;
+    pk.x = (uint32_t)__half_as_ushort(srow[i0.x]) | ((uint32_t)__half_as_ushort(srow[i0.y]) << 16);
+    pk.y = (uint32_t)__half_as_ushort(srow[i0.z]) | ((uint32_t)__half_as_ushort(srow[i0.w]) << 16);
+    pk.z = (uint32_t)__half_as_ushort(srow[i1.x]) | ((uint32_t)__half_as_ushort(srow[i1.y]) << 16);
+    pk.w = (uint32_t)__half_as_ushort(srow[i1.z]) | ((uint32_t)__half_as_ushort(srow[i1.w]) << 16);
+    reinterpret_cast<uint4*>(out)[c] = pk;
+  }
+}
+
 struct PartsArg {
   const __half* p[8];
 };
@@ -959,7 +1247,7 @@ int prof_read(unsigned long long* out) {  // read and reset
   return cudaMemcpyToSymbol(g_tpq_prof, z, sizeof(z)) != cudaSuccess;
 }
 #endif
-bool make_xmap(CUtensorMap* map, const void* base, int64_t K, int rows) {
+bool make_xmap(CUtensorMap* map, const void* base, int64_t K, int rows, int box_rows) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   if (!encode) {
     cudaDriverEntryPointQueryResult q;
@@ -971,7 +1259,7 @@ bool make_xmap(CUtensorMap* map, const void* base, int64_t K, int rows) {
   // dims (64 k, rows, K/64 k-halves); box (64, rows, 2) = one unit's slice: k-half kq at kq * rows * 128
   const cuuint64_t dims[3] = {(cuuint64_t)(kUnitK / 2), (cuuint64_t)rows, (cuuint64_t)(K / (kUnitK / 2))};
   const cuuint64_t strides[2] = {(cuuint64_t)K * 2, (cuuint64_t)kUnitK};  // bytes: row, k-half
-  const cuuint32_t box[3] = {(cuuint32_t)(kUnitK / 2), (cuuint32_t)rows, 2};
+  const cuuint32_t box[3] = {(cuuint32_t)(kUnitK / 2), (cuuint32_t)(box_rows > 0 ? box_rows : rows), 2};
   const cuuint32_t es[3] = {1, 1, 1};
   return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(base), dims, strides, box, es,
                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
@@ -987,7 +1275,9 @@ bool prepare_mm_t() {
 }
 template <int G>
 bool prepare_mm_g() {
-  return prepare_mm_t<G, 64>() && prepare_mm_t<G, 128>() && prepare_mm_t<G, 256>();
+  static_assert(TS<G>::SMEM <= 227 * 1024, "SS GEMM smem over the per-CTA limit");
+  return prepare_mm_t<G, 64>() && prepare_mm_t<G, 128>() && prepare_mm_t<G, 256>() &&
+         cudaFuncSetAttribute(k_dqgemm_ss<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, TS<G>::SMEM) == cudaSuccess;
 }
 
 bool gemv_prepare(int G) {
@@ -1048,8 +1338,40 @@ cudaError_t launch_gemm(const LayerDev& L, const CUtensorMap& xmap, int nb, int 
                     nb, M, L.NKB, L.U, L.grid, reinterpret_cast<__half*>(out), out_ld);
 }
 
+cudaError_t launch_gemm_ss(const LayerDev& L, const CUtensorMap& xmap, int M, int sms, void* out, int64_t out_ld,
+                           cudaStream_t st) {
+  if (M < 1 || M > 256) return cudaErrorInvalidValue;
+  SsArgs a;
+  a.packed = L.packed;
+  a.M = M;
+  a.MB = (M + 127) / 128;
+  a.NT = L.NT;
+  a.NKB = L.NKB;
+  const int base = a.MB * a.NT;
+  const int S = L.ws_ss ? ss_splits(L.NT, L.NKB, a.MB, sms) : 1;
+  a.S = S;
+  a.items = base * S;
+  a.grid = std::min(a.items, sms);
+  a.out = reinterpret_cast<__half*>(out);
+  a.out_ld = out_ld;
+  a.ws = L.ws_ss;
+  cudaError_t e;
+  if (L.G == 128) e = launch_pdl(k_dqgemm_ss<128>, dim3(a.grid), dim3(kSsWarps * 32), TS<128>::SMEM, st, a, xmap);
+  else if (L.G == 64) e = launch_pdl(k_dqgemm_ss<64>, dim3(a.grid), dim3(kSsWarps * 32), TS<64>::SMEM, st, a, xmap);
+  else if (L.G == 32) e = launch_pdl(k_dqgemm_ss<32>, dim3(a.grid), dim3(kSsWarps * 32), TS<32>::SMEM, st, a, xmap);
+  else e = cudaErrorInvalidValue;
+  if (e != cudaSuccess || S == 1) return e;
+  return launch_pdl(k_ss_fixup, dim3((unsigned)base, 32), dim3(128), 0, st, (const float*)L.ws_ss, M, a.MB, S,
+                    reinterpret_cast<__half*>(out), out_ld);
+}
+
 cudaError_t launch_gather_rowmajor(const void* src, int64_t ld, const int32_t* idx, int mode, int64_t nn, int M,
                                    int64_t K, void* dst, cudaStream_t st) {
+  // column gather of rows that fit in shared memory, 16-byte aligned rows: stage each row
+  if (mode == GATHER_COLS && idx && K % 8 == 0 && K * 2 <= 48 * 1024 && ld % 8 == 0 &&
+      reinterpret_cast<uintptr_t>(src) % 16 == 0 && reinterpret_cast<uintptr_t>(idx) % 16 == 0)
+    return launch_pdl(k_gather_rows, dim3((unsigned)M, (unsigned)std::max(1, std::min(16, 256 / M))), dim3(256),
+                      (size_t)K * 2, st, reinterpret_cast<const __half*>(src), ld, idx, K, reinterpret_cast<__half*>(dst));
   const int64_t total = (int64_t)M * K;
   return launch_pdl(k_gather_rm, dim3(grid_for(total, 256)), dim3(256), 0, st, reinterpret_cast<const __half*>(src),
                     ld, idx, mode, nn, M, K, reinterpret_cast<__half*>(dst));
