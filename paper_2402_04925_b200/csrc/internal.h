@@ -20,6 +20,7 @@
 #pragma once
 #include <cuda.h>
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 namespace tpq {
@@ -63,10 +64,21 @@ cudaError_t launch_gemm(const LayerDev& L, const CUtensorMap& xmap, int nb, int 
 // if the driver entry point is unavailable or encoding fails.
 bool make_xmap(CUtensorMap* map, const void* base, int64_t K, int rows, int box_rows = 0);
 
-// k-splits of the SS GEMM for `mb` 128-row blocks: as many as keep the work items within one wave
+// Weight columns per SS GEMM work item.  256 (two tiles, G = 128 only: shared memory) measured
+// slower than 128 on Llama TP=8 (M = 128: 48.0 vs 39.6 us; the 256-column variant has only two
+// activation stages), so it is selectable for experiments only (TPQ_SS_BN=256).
+inline int ss_bn(int NT, int G) {
+  static const bool wide = [] {
+    const char* e = getenv("TPQ_SS_BN");
+    return e && e[0] == '2';
+  }();
+  return wide && NT % 2 == 0 && G == 128 ? 256 : 128;
+}
+
+// k-splits of the SS GEMM for `mb` 128-row blocks and NG column groups: as many as keep the work items within one wave
 // of `sms` CTAs, at least 4 k-blocks per split, at most 16 splits.
-inline int ss_splits(int NT, int NKB, int mb, int sms) {
-  const int base = mb * NT;
+inline int ss_splits(int NG, int NKB, int mb, int sms) {
+  const int base = mb * NG;
   int S = sms / base;
   const int cap = NKB / 4 < 16 ? NKB / 4 : 16;
   if (S > cap) S = cap;

@@ -380,11 +380,12 @@ int tp_shard_mlp(const gptq_layer* w1, const gptq_layer* w2, const int32_t* P1, 
         auto ss_ws = [&](const tpq::LayerDev& L) -> size_t {  // largest k-split partial set (M >= 128 passes)
           if (M_max < 128) return 0;
           size_t items = 0;
+          const int bn = tpq::ss_bn(L.NT, L.G), NG = L.NT * tpq::kTileCols / bn;
           for (int mb = 1; mb <= 2; ++mb) {
-            const int S = tpq::ss_splits(L.NT, L.NKB, mb, h->sms);
-            if (S > 1) items = std::max(items, (size_t)mb * L.NT * S);
+            const int S = tpq::ss_splits(NG, L.NKB, mb, h->sms);
+            if (S > 1) items = std::max(items, (size_t)mb * NG * S);
           }
-          return items * 128 * 128;
+          return items * 128 * bn;
         };
         const size_t ws1s = ss_ws(h->L1), ws2s = ss_ws(h->L2);
         const size_t ncnt = (size_t)(h->L1.NT + h->L2.NT);

@@ -845,51 +845,56 @@ __global__ void __launch_bounds__(kMmWarps * 32, 1) k_dqgemm(const GemmArgs a, c
 }
 
 // ------------------------------------------------------------------ A7, large M: mixed-input SS GEMM
-// k_dqgemm_ss<G>: for M >= 128 the activations are the A operand (MMA M = 128 batch rows, TMA from
-// L2, reused across a 128-column weight tile) and the dequantized weights the B operand (N = 128
-// columns), written by 8 warps into shared memory as fp16 s (q - z) in the K-major SWIZZLE_128B
-// layout (fence.proxy.async before the hand-off).  Tile 128 rows x 128 columns, K in 128-row
-// records (8 MMAs of K = 16 each), fp32 accumulator in TMEM (double-buffered across work items).
-// Work items (m-block, n-tile, k-split) round-robin over a persistent grid; with k-splits the
-// fp32 partials are summed by k_ss_fixup in split order (deterministic).
-// Warps: 0-7 dequant, 8-11 epilogue (TMEM lane quarter = 32 batch rows), 12 producer, 13 MMA.
-constexpr int kSsWarps = 14;
-template <int G>
+// k_dqgemm_ss<G, BN>: for M >= 128 the activations are the A operand (MMA M = 128 batch rows, TMA
+// from L2, reused across BN weight columns) and the dequantized weights the B operand (N = BN
+// columns = BN / 128 tiles), written by warps into shared memory as fp16 s (q - z) in the K-major
+// SWIZZLE_128B layout (fence.proxy.async before the hand-off).  K in 128-row records (8 MMAs of
+// K = 16 per k-step), fp32 accumulator in TMEM (double-buffered across work items).  BN = 256 halves
+// the activation traffic per MMA (the activation TMA, not the tensor pipe, paces BN = 128).
+// Work items (m-block, n-group, k-split) round-robin over one wave; with k-splits the fp32 partials
+// are summed by k_ss_fixup in split order (deterministic).
+// Warps: 0 .. 8 BN/128 - 1 dequant, then 4 epilogue (TMEM lane quarter = 32 batch rows), producer, MMA.
+template <int G, int BN>
 struct TS {
+  static constexpr int TPW = BN / kTileCols;  // weight tiles per item
+  static constexpr int DW = 8 * TPW;          // dequant warps (16 columns x 2 k-halves each)
+  static constexpr int EPI0 = DW, PROD = DW + 4, MMAW = DW + 5, WARPS = DW + 6;
   static constexpr int KG = kUnitK / G, GPH = G >= kUnitK / 2 ? 1 : (kUnitK / 2) / G;
   static constexpr int UB = (int)unit_bytes_c(G), STAGE = (UB + 127) / 128 * 128;
-  static constexpr int BM = 128, BN = kTileCols;
-  static constexpr int XT = BM * kUnitK * 2;  // A tile (activations) per k-block: 32 KB
-  static constexpr int WT = BN * kUnitK * 2;  // B tile (dequantized weights) per k-block: 32 KB
-  static constexpr int NW = 4, NA = 3, NB = 2;  // raw-weight, A (activation) and B (weight) stages
-  static constexpr int KR = 6;                  // k-step done ring: A slot reuse waits t - NA, B slot t - NB;
-                                                // the next k-step on either barrier needs its own A / B first
+  static constexpr int BM = 128;
+  static constexpr int XT = BM * kUnitK * 2;  // A tile (activations) per k-step: 32 KB
+  static constexpr int WT = BN * kUnitK * 2;  // B tile (dequantized weights) per k-step
+  static constexpr int NW = TPW == 1 ? 4 : 2;  // raw-weight k-steps in flight (TPW records each)
+  static constexpr int NA = TPW == 1 ? 3 : 2, NB = 2;  // A (activation) and B (weight) stages
+  static constexpr int KR = 6;  // k-step done ring: A slot reuse waits t - NA, B slot t - NB; the next
+                                // k-step on either barrier needs its own A / B first (KR >= NA + NB)
   static constexpr int AR = 0, BR = AR + NA * XT, WR = BR + NB * WT;  // A, B 1024-aligned
-  static constexpr int BARS = WR + NW * STAGE;
-  static constexpr int SMEM = BARS + 8 * (2 * NW + NA + NB + KR + 4);  // w_full/empty, a_full, b_full, k_done, d_full/empty
+  static constexpr int BARS = WR + NW * TPW * STAGE;
+  static constexpr int SMEM = BARS + 8 * (2 * NW + NA + NB + KR + 4);
   static constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+  static_assert(KR >= NA + NB, "done ring");
 };
 
 struct SsArgs {
   const uint8_t* packed;
   int M;              // rows of this pass (<= 256: m-blocks of 128)
-  int MB, NT, NKB, S;
-  int items;          // NT * MB * S: item = (nt * MB + mb) * S + ks
+  int MB, NG, NKB, S; // m-blocks, column groups of BN, k-blocks, k-splits
+  int items;          // NG * MB * S: item = (ng * MB + mb) * S + ks
   int grid;
   __half* out;        // [M][out_ld]
   int64_t out_ld;
-  float* ws;          // [items][128][128] k-split partials (S > 1)
+  float* ws;          // [items][128][BN] k-split partials (S > 1)
 };
 
-template <int G>
-__global__ void __launch_bounds__(kSsWarps * 32, 1) k_dqgemm_ss(const SsArgs a, const __grid_constant__ CUtensorMap xmap) {
-  using C = TS<G>;
+template <int G, int BN>
+__global__ void __launch_bounds__(TS<G, BN>::WARPS * 32, 1) k_dqgemm_ss(const SsArgs a, const __grid_constant__ CUtensorMap xmap) {
+  using C = TS<G, BN>;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BARS);
-  uint64_t* w_full = bars;              // [NW] raw weight record landed
-  uint64_t* w_empty = w_full + C::NW;   // [NW] dequant warps read it (8)
+  uint64_t* w_full = bars;              // [NW] the k-step's raw weight records landed
+  uint64_t* w_empty = w_full + C::NW;   // [NW] dequant warps read them (DW)
   uint64_t* a_full = w_empty + C::NW;   // [NA] activation tile landed
-  uint64_t* b_full = a_full + C::NA;    // [NB] dequantized weight tile written (8)
+  uint64_t* b_full = a_full + C::NA;    // [NB] dequantized weight tile written (DW)
   uint64_t* k_done = b_full + C::NB;    // [KR] MMAs of k-step t completed: frees its A and B slot
   uint64_t* d_full = k_done + C::KR;    // [2] item's accumulator final
   uint64_t* d_empty = d_full + 2;       // [2] epilogue read it (4)
@@ -898,10 +903,10 @@ __global__ void __launch_bounds__(kSsWarps * 32, 1) k_dqgemm_ss(const SsArgs a, 
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::NW; ++s) {
       mbar_init(w_full + s, 1);
-      mbar_init(w_empty + s, 8);
+      mbar_init(w_empty + s, C::DW);
     }
     for (int s = 0; s < C::NA; ++s) mbar_init(a_full + s, 1);
-    for (int s = 0; s < C::NB; ++s) mbar_init(b_full + s, 8);
+    for (int s = 0; s < C::NB; ++s) mbar_init(b_full + s, C::DW);
     for (int s = 0; s < C::KR; ++s) mbar_init(k_done + s, 1);
     for (int s = 0; s < 2; ++s) {
       mbar_init(d_full + s, 1);
@@ -909,8 +914,10 @@ __global__ void __launch_bounds__(kSsWarps * 32, 1) k_dqgemm_ss(const SsArgs a, 
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 13) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(&s_tmem)) : "memory");
+  if (warp == C::MMAW) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)),
+                 "n"(2 * BN)
+                 : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   tc_fence_before();
@@ -918,15 +925,15 @@ __global__ void __launch_bounds__(kSsWarps * 32, 1) k_dqgemm_ss(const SsArgs a, 
   tc_fence_after();
   pdl_launch_dependents();
   const uint32_t tmem = __shfl_sync(0xffffffffu, s_tmem, 0);
-  // k-block range of split ks
-  auto krange = [&](int ks, int& k0, int& k1) {
+  auto krange = [&](int ks, int& k0, int& k1) {  // k-block range of split ks
     k0 = (int)((int64_t)ks * a.NKB / a.S);
     k1 = (int)((int64_t)(ks + 1) * a.NKB / a.S);
   };
 
-  if (warp < 8) {
-    // ===================== dequant: record -> fp16 s (q - z) B tile (SW128) =====================
-    const int j = warp * 16 + (lane & 15), kh = lane >> 4;  // weight column (B row), k-half
+  if (warp < C::DW) {
+    // ===================== dequant: records -> fp16 s (q - z) B tile (SW128) =====================
+    const int jj = warp * 16 + (lane & 15), kh = lane >> 4;  // B row (column of the item), k-half
+    const int h = jj / kTileCols, j = jj % kTileCols;          // weight tile of the item, its column
     const __half2 k16 = __float2half2_rn(0.0625f);
     int t = 0;  // k-step counter of this CTA
     for (int it = blockIdx.x; it < a.items; it += a.grid) {
@@ -935,7 +942,7 @@ __global__ void __launch_bounds__(kSsWarps * 32, 1) k_dqgemm_ss(const SsArgs a, 
       for (int kb = k0; kb < k1; ++kb, ++t) {
         const int ws = t % C::NW, ks = t % C::NB;
         mbar_wait(w_full + ws, (uint32_t)((t / C::NW) & 1));
-        const uint8_t* st = smem + C::WR + ws * C::STAGE;
+        const uint8_t* st = smem + C::WR + (ws * C::TPW + h) * C::STAGE;
         const uint4 c0 = *reinterpret_cast<const uint4*>(st + ((kh * 2 + 0) * kTileCols + j) * 16);
         const uint4 c1 = *reinterpret_cast<const uint4*>(st + ((kh * 2 + 1) * kTileCols + j) * 16);
         const uint32_t wv[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
@@ -953,7 +960,7 @@ __global__ void __launch_bounds__(kSsWarps * 32, 1) k_dqgemm_ss(const SsArgs a, 
         __syncwarp();
         if (lane == 0) mbar_arrive(w_empty + ws);
         if (t >= C::NB) mbar_wait(k_done + (t - C::NB) % C::KR, (uint32_t)(((t - C::NB) / C::KR) & 1));  // B slot free
-        uint8_t* brow = smem + C::BR + ks * C::WT + kh * (C::BN * 128) + j * 128;
+        uint8_t* brow = smem + C::BR + ks * C::WT + kh * (BN * 128) + jj * 128;
 #pragma unroll
         for (int w = 0; w < 8; ++w) {  // word w = k 64 kh + 8w .. +7 = 16-byte chunk w of the row
           const int g = C::GPH == 1 ? 0 : (w * 8) / G;
@@ -963,31 +970,31 @@ __global__ void __launch_bounds__(kSsWarps * 32, 1) k_dqgemm_ss(const SsArgs a, 
           o.y = h2u(__hmul2(__hfma2(u2h(lop3_and_or(x, 0x00F000F0u, 0x64006400u)), k16, zh[g]), sc[g]));
           o.z = h2u(__hmul2(__hsub2(u2h(lop3_and_or(x8, 0x000F000Fu, 0x64006400u)), zl[g]), sc[g]));
           o.w = h2u(__hmul2(__hfma2(u2h(lop3_and_or(x8, 0x00F000F0u, 0x64006400u)), k16, zh[g]), sc[g]));
-          *reinterpret_cast<uint4*>(brow + ((w ^ (j & 7)) << 4)) = o;
+          *reinterpret_cast<uint4*>(brow + ((w ^ (jj & 7)) << 4)) = o;
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor core
         __syncwarp();
         if (lane == 0) mbar_arrive(b_full + ks);
       }
     }
-  } else if (warp < 12) {
+  } else if (warp < C::PROD) {
     // ===================== epilogue: one item at a time =====================
-    const int qw = warp - 8;
+    const int qw = warp - C::EPI0;
     pdl_wait();
     int n_it = 0;
     for (int it = blockIdx.x; it < a.items; it += a.grid, ++n_it) {
-      const int db = n_it & 1, ks = it % a.S, mb = (it / a.S) % a.MB, nt = it / (a.S * a.MB);
+      const int db = n_it & 1, mb = (it / a.S) % a.MB, ng = it / (a.S * a.MB);
       mbar_wait(d_full + db, (uint32_t)((n_it >> 1) & 1));
       tc_fence_after();
       const int m = mb * C::BM + qw * 32 + lane;  // batch row of this thread (TMEM lane)
-      for (int c0 = 0; c0 < C::BN; c0 += 32) {
+      for (int c0 = 0; c0 < BN; c0 += 32) {
         uint32_t v[32];
-        tmem_ld16(tmem + ((uint32_t)(qw * 32) << 16) + db * C::BN + c0, v);
-        tmem_ld16(tmem + ((uint32_t)(qw * 32) << 16) + db * C::BN + c0 + 16, v + 16);
+        tmem_ld16(tmem + ((uint32_t)(qw * 32) << 16) + db * BN + c0, v);
+        tmem_ld16(tmem + ((uint32_t)(qw * 32) << 16) + db * BN + c0 + 16, v + 16);
         tmem_wait_ld();
         if (m < a.M) {
           if (a.S == 1) {
-            __half* o = a.out + (int64_t)m * a.out_ld + (int64_t)nt * C::BN + c0;
+            __half* o = a.out + (int64_t)m * a.out_ld + (int64_t)ng * BN + c0;
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
               uint4 pk;
@@ -998,7 +1005,7 @@ __global__ void __launch_bounds__(kSsWarps * 32, 1) k_dqgemm_ss(const SsArgs a, 
               *reinterpret_cast<uint4*>(o + 8 * q) = pk;
             }
           } else {
-            float* o = a.ws + ((size_t)it * C::BM + (m - mb * C::BM)) * C::BN + c0;
+            float* o = a.ws + ((size_t)it * C::BM + (m - mb * C::BM)) * BN + c0;
 #pragma unroll
             for (int q = 0; q < 8; ++q)
               __stcg(reinterpret_cast<float4*>(o + 4 * q),
@@ -1010,30 +1017,31 @@ __global__ void __launch_bounds__(kSsWarps * 32, 1) k_dqgemm_ss(const SsArgs a, 
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(d_empty + db);
-      (void)ks;
     }
-  } else if (warp == 12) {
+  } else if (warp == C::PROD) {
     // ===================== producer: weight records (bulk) + activation tiles (tensor TMA) =====
     const uint64_t pw = policy_evict_first();
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&xmap)) : "memory");
     pdl_wait();  // the activations come from the previous kernel in the stream
     int t = 0;
     for (int it = blockIdx.x; it < a.items; it += a.grid) {
-      const int mb = (it / a.S) % a.MB, nt = it / (a.S * a.MB);
+      const int mb = (it / a.S) % a.MB, ng = it / (a.S * a.MB);
       int k0, k1;
       krange(it % a.S, k0, k1);
       for (int kb = k0; kb < k1; ++kb, ++t) {
-        const int ws = t % C::NW, ks = t % C::NA;
+        const int ws = t % C::NW, sa = t % C::NA;
         if (t >= C::NW) mbar_wait(w_empty + ws, (uint32_t)(((t - C::NW) / C::NW) & 1));
         if (elect_one()) {
-          mbar_arrive_expect_tx(w_full + ws, C::UB);
-          bulk_g2s(smem + C::WR + ws * C::STAGE, a.packed + ((int64_t)nt * a.NKB + kb) * C::UB, C::UB, w_full + ws, pw);
+          mbar_arrive_expect_tx(w_full + ws, C::TPW * C::UB);
+          for (int h = 0; h < C::TPW; ++h)
+            bulk_g2s(smem + C::WR + (ws * C::TPW + h) * C::STAGE,
+                     a.packed + ((int64_t)(ng * C::TPW + h) * a.NKB + kb) * C::UB, C::UB, w_full + ws, pw);
         }
         __syncwarp();
         if (t >= C::NA) mbar_wait(k_done + (t - C::NA) % C::KR, (uint32_t)(((t - C::NA) / C::KR) & 1));  // A slot free
         if (elect_one()) {
-          mbar_arrive_expect_tx(a_full + ks, C::XT);
-          tma_load_3d(smem + C::AR + ks * C::XT, &xmap, 0, mb * C::BM, 2 * kb, a_full + ks);
+          mbar_arrive_expect_tx(a_full + sa, C::XT);
+          tma_load_3d(smem + C::AR + sa * C::XT, &xmap, 0, mb * C::BM, 2 * kb, a_full + sa);
         }
         __syncwarp();
       }
@@ -1054,17 +1062,17 @@ __global__ void __launch_bounds__(kSsWarps * 32, 1) k_dqgemm_ss(const SsArgs a, 
         const uint32_t abase = smem_u32(smem + C::AR + sa * C::XT), bbase = smem_u32(smem + C::BR + sb * C::WT);
         uint64_t ad[8], bd[8];
 #pragma unroll
-        for (int jj = 0; jj < 8; ++jj) {  // k16 block jj: k-half jj / 4, 32-byte step within the 128-byte row
-          ad[jj] = bdesc_sw128(abase + (jj / 4) * (C::BM * 128) + (jj % 4) * 32);
-          bd[jj] = bdesc_sw128(bbase + (jj / 4) * (C::BN * 128) + (jj % 4) * 32);
+        for (int q = 0; q < 8; ++q) {  // k16 block q: k-half q / 4, 32-byte step within the 128-byte row
+          ad[q] = bdesc_sw128(abase + (q / 4) * (C::BM * 128) + (q % 4) * 32);
+          bd[q] = bdesc_sw128(bbase + (q / 4) * (BN * 128) + (q % 4) * 32);
         }
         if (elect_one()) {
 #pragma unroll
-          for (int jj = 0; jj < 8; ++jj)
+          for (int q = 0; q < 8; ++q)
             asm volatile(
                 "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-                "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem + db * C::BN),
-                "l"(ad[jj]), "l"(bd[jj]), "r"(C::IDESC), "r"((kb == k0 && jj == 0) ? 0u : 1u)
+                "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem + db * BN),
+                "l"(ad[q]), "l"(bd[q]), "r"(C::IDESC), "r"((kb == k0 && q == 0) ? 0u : 1u)
                 : "memory");
           umma_commit1(k_done + t % C::KR);
           if (kb == k1 - 1) umma_commit1(d_full + db);
@@ -1075,34 +1083,37 @@ __global__ void __launch_bounds__(kSsWarps * 32, 1) k_dqgemm_ss(const SsArgs a, 
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 13) {
+  if (warp == C::MMAW) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * BN) : "memory");
   }
 }
 
-// k-split fix-up of k_dqgemm_ss: out[m][nt 128 + c] = sum over ks of the item's partial (split order).
-// Block (nt * MB + mb, r): rows mb 128 + 4 r + warp, thread = 4 consecutive columns.
-__global__ void k_ss_fixup(const float* __restrict__ ws, int M, int MB, int S, __half* __restrict__ out,
+// k-split fix-up of k_dqgemm_ss: out[m][ng BN + c] = sum over ks of the item's partial (split order).
+// Block (ng * MB + mb, r): rows mb 128 + 4 r + warp, thread = 4 consecutive columns, bn / 128 passes.
+__global__ void k_ss_fixup(const float* __restrict__ ws, int M, int MB, int S, int bn, __half* __restrict__ out,
                            int64_t out_ld) {
   pdl_launch_dependents();
   pdl_wait();
-  const int tile = blockIdx.x, mb = tile % MB, nt = tile / MB;
-  const int ml = blockIdx.y * 4 + (threadIdx.x >> 5), m = mb * 128 + ml, c = (threadIdx.x & 31) * 4;
+  const int grp = blockIdx.x, mb = grp % MB, ng = grp / MB;
+  const int ml = blockIdx.y * 4 + (threadIdx.x >> 5), m = mb * 128 + ml;
   if (m >= M) return;
-  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int ks = 0; ks < S; ++ks) {
-    const float4 v = __ldcg(reinterpret_cast<const float4*>(ws + (((size_t)tile * S + ks) * 128 + ml) * 128 + c));
-    acc.x += v.x;
-    acc.y += v.y;
-    acc.z += v.z;
-    acc.w += v.w;
+  for (int c = (threadIdx.x & 31) * 4; c < bn; c += 128) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int ks = 0; ks < S; ++ks) {
+      const float4 v = __ldcg(reinterpret_cast<const float4*>(ws + (((size_t)grp * S + ks) * 128 + ml) * bn + c));
+      acc.x += v.x;
+      acc.y += v.y;
+      acc.z += v.z;
+      acc.w += v.w;
+    }
+    uint2 pk;
+    pk.x = h2u(__floats2half2_rn(acc.x, acc.y));
+    pk.y = h2u(__floats2half2_rn(acc.z, acc.w));
+    *reinterpret_cast<uint2*>(out + (int64_t)m * out_ld + (int64_t)ng * bn + c) = pk;
   }
-  uint2 pk;
-  pk.x = h2u(__floats2half2_rn(acc.x, acc.y));
-  pk.y = h2u(__floats2half2_rn(acc.z, acc.w));
-  *reinterpret_cast<uint2*>(out + (int64_t)m * out_ld + (int64_t)nt * 128 + c) = pk;
 }
+
 
 template <class Kern, class... Args>
 cudaError_t launch_pdl(Kern k, dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
@@ -1273,11 +1284,17 @@ bool prepare_mm_t() {
   static_assert(2 * smem > 228 * 1024, "GEMM must be one CTA per SM (TMEM 512 columns)");
   return cudaFuncSetAttribute(k_dqgemm<G, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) == cudaSuccess;
 }
+template <int G, int BN>
+bool prepare_ss_t() {
+  static_assert(TS<G, BN>::SMEM + 1024 <= 227 * 1024, "SS GEMM smem (+ static) over the per-CTA limit");
+  return cudaFuncSetAttribute(k_dqgemm_ss<G, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, TS<G, BN>::SMEM) ==
+         cudaSuccess;
+}
 template <int G>
 bool prepare_mm_g() {
-  static_assert(TS<G>::SMEM <= 227 * 1024, "SS GEMM smem over the per-CTA limit");
-  return prepare_mm_t<G, 64>() && prepare_mm_t<G, 128>() && prepare_mm_t<G, 256>() &&
-         cudaFuncSetAttribute(k_dqgemm_ss<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, TS<G>::SMEM) == cudaSuccess;
+  bool ok = prepare_mm_t<G, 64>() && prepare_mm_t<G, 128>() && prepare_mm_t<G, 256>() && prepare_ss_t<G, 128>();
+  if constexpr (G == 128) ok = ok && prepare_ss_t<G, 256>();
+  return ok;
 }
 
 bool gemv_prepare(int G) {
@@ -1338,30 +1355,39 @@ cudaError_t launch_gemm(const LayerDev& L, const CUtensorMap& xmap, int nb, int 
                     nb, M, L.NKB, L.U, L.grid, reinterpret_cast<__half*>(out), out_ld);
 }
 
+template <int G, int BN>
+cudaError_t launch_ss_t(const SsArgs& a, const CUtensorMap& xmap, cudaStream_t st) {
+  return launch_pdl(k_dqgemm_ss<G, BN>, dim3(a.grid), dim3(TS<G, BN>::WARPS * 32), TS<G, BN>::SMEM, st, a, xmap);
+}
+
 cudaError_t launch_gemm_ss(const LayerDev& L, const CUtensorMap& xmap, int M, int sms, void* out, int64_t out_ld,
                            cudaStream_t st) {
   if (M < 1 || M > 256) return cudaErrorInvalidValue;
+  const int bn = ss_bn(L.NT, L.G);
   SsArgs a;
   a.packed = L.packed;
   a.M = M;
   a.MB = (M + 127) / 128;
-  a.NT = L.NT;
+  a.NG = L.NT * kTileCols / bn;
   a.NKB = L.NKB;
-  const int base = a.MB * a.NT;
-  const int S = L.ws_ss ? ss_splits(L.NT, L.NKB, a.MB, sms) : 1;
+  const int base = a.MB * a.NG;
+  const int S = L.ws_ss ? ss_splits(a.NG, L.NKB, a.MB, sms) : 1;
   a.S = S;
   a.items = base * S;
   a.grid = std::min(a.items, sms);
   a.out = reinterpret_cast<__half*>(out);
   a.out_ld = out_ld;
   a.ws = L.ws_ss;
-  cudaError_t e;
-  if (L.G == 128) e = launch_pdl(k_dqgemm_ss<128>, dim3(a.grid), dim3(kSsWarps * 32), TS<128>::SMEM, st, a, xmap);
-  else if (L.G == 64) e = launch_pdl(k_dqgemm_ss<64>, dim3(a.grid), dim3(kSsWarps * 32), TS<64>::SMEM, st, a, xmap);
-  else if (L.G == 32) e = launch_pdl(k_dqgemm_ss<32>, dim3(a.grid), dim3(kSsWarps * 32), TS<32>::SMEM, st, a, xmap);
-  else e = cudaErrorInvalidValue;
+  cudaError_t e = cudaErrorInvalidValue;
+  if (bn == 256) {
+    if (L.G == 128) e = launch_ss_t<128, 256>(a, xmap, st);
+  } else {
+    if (L.G == 128) e = launch_ss_t<128, 128>(a, xmap, st);
+    else if (L.G == 64) e = launch_ss_t<64, 128>(a, xmap, st);
+    else if (L.G == 32) e = launch_ss_t<32, 128>(a, xmap, st);
+  }
   if (e != cudaSuccess || S == 1) return e;
-  return launch_pdl(k_ss_fixup, dim3((unsigned)base, 32), dim3(128), 0, st, (const float*)L.ws_ss, M, a.MB, S,
+  return launch_pdl(k_ss_fixup, dim3((unsigned)base, 32), dim3(128), 0, st, (const float*)L.ws_ss, M, a.MB, S, bn,
                     reinterpret_cast<__half*>(out), out_ld);
 }
 

@@ -305,3 +305,26 @@ def test_a7_full_size_llama_tp8_shard(M):
     _assert_close(_np(Y1), y1r, "Y1_local")
     _assert_close(_np(Y2)[:, cols], y2r, "Y2_local sampled")
     h.close()
+
+
+@pytest.mark.parametrize("G", [64, 128])
+@pytest.mark.parametrize("M", [128, 200])
+def test_a7_ss_wide_tiles(G, M):
+    """M >= 128 runs the SS GEMM (k-splits, fix-up); deterministic across runs."""
+    p = synth.make_problem(1024, 2048, 768, G, M, seed=300 + G + M)
+    P1, P2 = _prep(p)
+    L1, L2 = _olayers(p)
+    Y1r, Y2r = O.dense_mlp(p.X, O.dequantize(L1), O.dequantize(L2))
+    h = tpq.TpMlp(p.w1, p.w2, P1, P2, M_max=256)
+    X = _dev(p.X)
+    Y = _empty(M, p.N2)
+    h.forward(X, M, Y)
+    _assert_close(_np(Y), Y2r, "Y2")
+    Y1 = _empty(M, p.N1)
+    h.layer1(X, M, Y1)
+    P2o, _ = O.alg1_reorder(L2.g)
+    _assert_close(_np(Y1), Y1r[:, P2o], "Y1 (P2 order)")
+    Y2 = _empty(M, p.N2)
+    h.forward(X, M, Y2)
+    assert torch.equal(Y, Y2), "SS GEMM not deterministic"
+    h.close()
