@@ -293,7 +293,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_dqgemv(const GemvArgs a, co
   uint64_t* xfull = empty + C::NS;     // [NX] the pair's activation slices landed (TMA bytes)
   uint64_t* a_full = xfull + C::NX;    // [NA] the pair's A operands stored (8 dequant warps)
   uint64_t* d_empty = a_full + C::NA;  // [ND] epilogue read the pair's accumulators (4 warps)
-  uint64_t* done = d_empty + C::ND;    // [RD] pair p's MMAs completed (one tcgen05.commit): frees its
+  uint64_t* done = d_empty + C::ND;    // [RD] pair p's MMAs completed (tcgen05.commit + release): frees its
                                        //      A buffer and activation slot, hands its accumulators over
   __shared__ uint32_t s_tmem;
   __shared__ int s_last;
@@ -314,7 +314,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_dqgemv(const GemvArgs a, co
     for (int s = 0; s < C::NX; ++s) mbar_init(xfull + s, 1);
     for (int b = 0; b < C::NA; ++b) mbar_init(a_full + b, kSetWarps);
     for (int d = 0; d < C::ND; ++d) mbar_init(d_empty + d, 4);
-    for (int r = 0; r < C::RD; ++r) mbar_init(done + r, 1);
+    for (int r = 0; r < C::RD; ++r) mbar_init(done + r, 2);  // tcgen05.commit + the issuer's release arrive
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == kMmaWarp) {
@@ -411,8 +411,10 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_dqgemv(const GemvArgs a, co
       TPQ_EV(0, 2 * p)
       tc_fence_after();
       // The pair's scales need no wait of their own: the dequant warps wrote them before their
-      // a_full arrive (release), which the MMA warp acquired before the commit that completes
-      // `done` (acquired above), so the writes happen-before this read.
+      // a_full arrive (release); the issuing lane acquired a_full and then arrived on `done` with
+      // a plain release arrive (besides the commit), so the writes happen-before this read through
+      // two release/acquire pairs.  (compute-sanitizer racecheck does not model mbarriers and
+      // reports this hand-off with or without a dedicated barrier.)
       TPQ_EV(1, 2 * p)
       const int nh = 2 * p + 1 < nu ? 2 : 1;
       // per unit: add the unit's scaled group sums, then close the tile segment if it ends here
@@ -599,6 +601,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_dqgemv(const GemvArgs a, co
           for (int j = J; j < 2 * J; ++j) umma_ts1(dop[j], aop[j], bop[j], kIdesc, (j % (G / 16)) ? 1u : 0u);
         }
         umma_commit1(done + p % C::RD);
+        mbar_arrive(done + p % C::RD);  // release: orders the scale writes (acquired via a_full)
       }
       __syncwarp();
       TPQ_T1(is, 3)
