@@ -42,6 +42,7 @@ struct LayerDev {
   float* ws_mm = nullptr;  // [grid][2 slots][256][128] fp32 stream-K partials (A7 GEMM)
   float* ws_ss = nullptr;  // [items][128][128] fp32 k-split partials (A7 SS GEMM, M >= 128)
   int* cnt = nullptr;      // [NT] arrival counters (self-resetting)
+  int sshift = 0;          // GEMV operand shift e: smallest e >= 0 with max|s| 2^(24-e) <= 65504
 };
 
 enum GatherMode { GATHER_COLS = 0, GATHER_ALLGATHER = 1 };

@@ -11,6 +11,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -133,6 +134,23 @@ void unpack_layer(const std::vector<uint8_t>& pk, int64_t K, int64_t N, int G, u
 }
 
 inline uint32_t nib(uint32_t w, int i) { return (w >> (4 * i)) & 0xFu; }
+
+// fp16 bits -> float (host)
+float half_bits_to_float(uint16_t h) {
+  const int e = (h >> 10) & 0x1F, m = h & 0x3FF;
+  const float v = e == 0 ? std::ldexp((float)m, -24) : e == 31 ? INFINITY : std::ldexp((float)(m | 0x400), e - 25);
+  return (h & 0x8000) ? -v : v;
+}
+
+// GEMV operand shift (tpq_kernels.cu k_dqgemv): smallest e >= 0 such that every |s| 2^(24-e) stays
+// within the fp16 range (65504), so that S = s 2^(24-e) is exact.
+int scale_shift(const std::vector<uint16_t>& s) {
+  float mx = 0.f;
+  for (uint16_t h : s) mx = std::max(mx, std::fabs(half_bits_to_float(h)));
+  int e = 0;
+  while (e < 40 && std::ldexp(mx, 24 - e) > 65504.f) ++e;
+  return e;
+}
 
 }  // namespace
 
@@ -365,6 +383,8 @@ int tp_shard_mlp(const gptq_layer* w1, const gptq_layer* w2, const int32_t* P1, 
     h->pk2 = pack_layer(c2);
     plan_layer(h->L1, K1, n, w1->G, device);
     plan_layer(h->L2, n, N2, w2->G, device);
+    h->L1.sshift = scale_shift(c1.s);
+    h->L2.sshift = scale_shift(c2.s);
 
     if (device >= 0) {
       auto upload = [&]() -> int {

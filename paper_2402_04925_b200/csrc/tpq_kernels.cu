@@ -170,6 +170,32 @@ __device__ __forceinline__ void umma_commit1(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
 }
+// One GEMV unit: 8 x tcgen05.mma kind::f16 (M=128, N=16, K=16) into d, A from TMEM columns
+// a + 8j, B from the SW128 activation slice at descriptor b: k16 block j at byte offset
+// (j / 4) * 2048 + (j % 4) * 32, i.e. + (j / 4) * 128 + (j % 4) * 2 in descriptor units.  The
+// first MMA accumulates iff acc0 != 0.  One asm block so the operands are formed with uniform adds
+// right before the issue (a per-MMA C++ loop cost ~110 instructions per unit, most of them
+// control flow, which the issuing warp could not afford among four dequant warps per SMSP).
+__device__ __forceinline__ void umma_unit16(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc, uint32_t acc0) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .b32 a1, a2, a3, a4, a5, a6, a7;\n\t"
+      ".reg .b64 b1, b2, b3, b4, b5, b6, b7;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "add.u32 a1, %1, 8;\n\tadd.u32 a2, %1, 16;\n\tadd.u32 a3, %1, 24;\n\tadd.u32 a4, %1, 32;\n\t"
+      "add.u32 a5, %1, 40;\n\tadd.u32 a6, %1, 48;\n\tadd.u32 a7, %1, 56;\n\t"
+      "add.u64 b1, %2, 2;\n\tadd.u64 b2, %2, 4;\n\tadd.u64 b3, %2, 6;\n\tadd.u64 b4, %2, 128;\n\t"
+      "add.u64 b5, %2, 130;\n\tadd.u64 b6, %2, 132;\n\tadd.u64 b7, %2, 134;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], b1, %3, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], b2, %3, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [a3], b3, %3, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [a4], b4, %3, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [a5], b5, %3, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [a6], b6, %3, 1;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [a7], b7, %3, 1;\n\t}" ::"r"(d),
+      "r"(a), "l"(b), "r"(idesc), "r"(acc0)
+      : "memory");
+}
 // K-major SWIZZLE_128B smem descriptor (sm_100 version 1, layout type 2 in bits 61-63): rows of
 // 128 B (64 f16 of K) in 8-row, 1024-byte swizzle atoms (16-byte chunk c of row r stored at chunk
 // c ^ (r % 8)), SBO = 1024 B between 8-row groups, LBO unused (1).  The k16 block j of a row starts
@@ -184,39 +210,47 @@ constexpr uint32_t kIdesc = (1u << 4) | ((uint32_t)(kNPad >> 3) << 17) | ((uint3
 // ------------------------------------------------------------------ GEMV configuration
 // Unit = (128-column tile t, 128-row k-block kb): one weight record (internal.h), 8 MMAs of
 // K = 16.  A CTA owns a contiguous range of units (stream-K); the units of one tile inside that
-// range form a "segment" whose fp32 result the epilogue accumulates in registers.
+// range form a "segment", accumulated in one TMEM accumulator (16 columns) across all its units.
 //
-// Arithmetic: the A operand is the exact f16 integer (q - z) (LOP3 magic number 1024 + q, resp.
-// 1024 + 16 q, minus one HSUB2 / HFMA2 -- exact, |q - z| <= 15); the MMA accumulates
-// sum_k (q - z) x in fp32 per group (one TMEM accumulator per group of the unit); the epilogue
-// applies the group's scale in fp32.  Per code word (8 weights): 5 ALU-pipe + 4 FMA-pipe ops.
+// Arithmetic: the A operand is fp16(s (q - z) 2^-e) with one HFMA2 per f16x2 pair: a code nibble
+// masked into the low mantissa bits of an f16 is the exact subnormal q 2^-24 (bits 0-3) or q 2^-20
+// (bits 4-7); times S = s 2^(24-e) (resp. 2^(20-e)), exact in fp16, the product is exactly
+// q s 2^-e, and the addend C = fp16(-z s 2^-e) gives A with one rounding of the product sum plus
+// the rounding of C (<= 2^-12 |z s|; reading on operand precision).  e = sshift >= 0 is
+// the smallest shift with max|s| 2^(24-e) <= 65504 (0 for the synthetic checkpoints); the
+// epilogue multiplies the fp32 accumulator by 2^e.  The MMA accumulates in fp32 over the whole
+// segment, so the epilogue runs once per segment (measured: a per-unit fp32-scale epilogue was
+// the bottleneck of the previous design at ~575 cycles per unit, profiles/r01_summary.md).
+// Per code word (8 weights): 5 ALU-pipe + 4 FMA-pipe ops.
 //
 // Hand-offs go per PAIR of consecutive units (p = i / 2): an mbarrier wait costs ~90-180 cycles
 // even when the phase has already completed (B300_MICROARCH.md "mbarrier"; measured here with
-// tools/prof_waits.py), comparable to the ~375 cycles per unit the SM has at HBM speed, so every
-// role waits once per pair.  Weight stages stay per unit.
+// tools/prof_waits.py), comparable to the ~383 cycles per unit the SM has at HBM speed.
 //
-// Warp roles (768 threads, one CTA per SM):
+// Warp roles (23 warps, one CTA per SM):
 //   warps 0-15  dequant, two sets of 8: set w/8 takes the pairs p with p % 2 == set.  Warp w of a
-//               set converts lane quarter w%4 (columns 32(w%4)..+31) of k-half (w/4)%2 of both
-//               units into the pair's TMEM A buffer (tcgen05.st 32x32b.x32) and hands the group
-//               scales to the epilogue.
-//   warps 16-19 epilogue: per pair, tcgen05.ld of the group accumulators (lane quarter w-16),
-//               x scale into registers; at a segment end the tile output or the stream-K partial
-//               + deterministic fix-up.
+//               set converts unit (w/4)%2 of the pair, lane quarter w%4 (columns 32(w%4)..+31),
+//               all 128 k, into the set's TMEM A buffer (two tcgen05.st 32x32b.x32).  Warp 0 of
+//               the set also acquires the pair's activation slice (xfull) before its a_full
+//               arrive, so the MMA warp waits on a_full only.
+//   warps 16-19 epilogue: once per tile segment, tcgen05.ld of the accumulator (lane quarter
+//               w-16); the tile output, or the stream-K partial + deterministic last-arriver fix-up.
 //   warp 20     TMA producer: weight records into the NS-stage ring (L2 evict-first).
-//   warp 21     activation stager: per unit one 3-D tensor TMA (2 x 64 k x 16 rows, 128-byte
-//               rows, 128B swizzle) landing directly in the K-major SW128 operand layout.
-//   warps 22-23 MMA issuers, warp 22 + p%2 takes pair p: 16 x tcgen05.mma kind::f16 (M=128, N=16,
-//               K=16, A from TMEM) + one commit, which frees the pair's A buffer and activation
-//               slot and hands its accumulators to the epilogue.
+//   warp 21     activation stager: per pair one or two 3-D tensor TMAs (64 k x 16 rows boxes,
+//               128-byte rows, 128B swizzle) landing directly in the K-major SW128 operand layout.
+//   warps 22-23 MMA issuers, warp 22 + p%2 takes pair p (= dequant set p % 2): 16 x
+//               tcgen05.mma kind::f16 (M=128, N=16, K=16, A from TMEM) + one commit, which frees
+//               the pair's A buffer and activation slot.  Each issuer accumulates into its own
+//               segment accumulator (double-buffered across segments); per segment it commits
+//               (or, if none of its units lies in the segment, plainly arrives) once on d_full,
+//               and the epilogue adds the two partial sums.  Two issuers on two SMSPs: one warp
+//               issuing all MMAs among four dequant warps per SMSP took ~1100 cycles per pair.
 constexpr int kSetWarps = 8, kEpiWarp0 = 16, kProdWarp = 20, kStageWarp = 21, kMmaWarp = 22;
 constexpr int kGemvThreads = 24 * 32;
 
 template <int G>
 struct TC {
   static constexpr int KG = kUnitK / G;                      // groups per unit
-  static constexpr int GPH = G >= kUnitK / 2 ? 1 : (kUnitK / 2) / G;  // groups per k-half
   static constexpr int UB = (int)unit_bytes_c(G);            // weight record bytes
   static constexpr int STAGE = (UB + 127) / 128 * 128;
 #ifndef TPQ_NS
@@ -227,38 +261,30 @@ struct TC {
 #endif
   static constexpr int NS = G == 32 && TPQ_NS > 18 ? 18 : TPQ_NS;  // weight ring stages (units)
   static constexpr int XU = kNPad * kUnitK * 2;              // activation bytes per unit (16 rows x 128 k)
-  static constexpr int NX = G == 128 ? TPQ_NX : 4;           // activation pair slots
+  static constexpr int NX = TPQ_NX;                          // activation pair slots
   // unit slice = two TMA boxes (64 k, 16 rows) of 2 KB: k-half kq at kq * 2048, row m at m * 128
   // (8-row swizzle atoms of 1024 B), 16-byte chunk swizzled by m % 8
-  static constexpr int DU = KG * kNPad;                      // accumulator columns per unit
   static constexpr int AU = kUnitK / 2;                      // f16x2 A columns per unit
-  // Ring depths are even: pair p and pair p - depth then belong to the same dequant set and the same
-  // MMA warp, which consumed the older phase before waiting on the newer one.  With an odd depth
-  // the MMA warp of pair p can wait on a barrier whose previous phase (the other set's pair) has
-  // not completed yet, and the phase-parity test passes two phases early.
-  static constexpr int NA = 2;                               // TMEM A pair buffers (one per dequant set)
-#ifndef TPQ_ND
-#define TPQ_ND 6
-#endif
-  static constexpr int ND = G == 32 ? 2 : (G == 64 && TPQ_ND > 4 ? 4 : TPQ_ND);  // TMEM accumulator pair sets
+  static constexpr int NA = 3;                               // TMEM A pair buffers: pair p in p % NA
+  static constexpr int NAF = 6;                              // a_full barriers: pair p on p % 6 (= lcm(NA, 2))
+  // Phase-parity waits need the awaited completion to be the latest one of its barrier.
+  //  * a_full(p) on barrier p % 6: the previous completion there, pair p - 6, belongs to the same
+  //    dequant set and MMA warp, which consumed it before waiting on pair p; the set's arrivals for
+  //    p follow its wait on done(p - 3), which implies a_full(p - 3) and hence a_full(p - 6).
+  //  * done(p) on barrier p % RD (one tcgen05.commit per pair, two MMA warps: out of order across
+  //    sets).  Dequant set, waiting on done(p - NA) to reuse A buffer p % NA: the next completion
+  //    there, pair p - NA + RD >= p, needs a_full of a pair >= p, i.e. this set's own arrival for p,
+  //    or (other set) done(p) first.  Stager, waiting on done(p - NX): the next one, p - NX + RD,
+  //    needs its own later TMA load.
+  static constexpr int RD = 6;
+  static_assert(RD >= NX && RD >= NA + 2, "done ring aliasing");
   static constexpr int TCOLS = 512;
-  static_assert(ND * 2 * DU + NA * 2 * AU <= TCOLS, "TMEM budget");
-  // pair-done ring.  Phase-parity waits need the awaited completion to be the latest one of its
-  // barrier.  Stager (pair p-NX) and epilogue (pair p) are safe for RD >= NX, ND.  The dequant set
-  // waits for pair p-NA while the other set's pairs may complete out of order (two MMA warps):
-  // RD - NA even makes the next pair on that barrier, p - NA + RD > p, one of this set's own
-  // pairs, which cannot complete before this set has written it.
-  static constexpr int RD = NX > ND ? (NX > NA + 2 ? NX : NA + 2) : (ND > NA + 2 ? ND : NA + 2);
-  static_assert(RD >= NX && RD >= ND && (RD - NA) % 2 == 0, "done ring aliasing");
-  static_assert(NA % 2 == 0 && NX % 2 == 0 && ND % 2 == 0, "odd ring depth");
-  static constexpr int SRP = NA + ND + 2;                     // scale ring in pairs (> NA + ND: a slot is
-                                                             // rewritten only after the epilogue read it)
-  static_assert(SRP > NA + ND, "scale ring too shallow");
+  static constexpr int DC = 4 * kNPad;                       // segment accumulators [2 buffers][2 issuers] x 16 columns
+  static_assert(DC + NA * 2 * AU <= TCOLS, "TMEM budget");
   static constexpr int XRING = 0;                            // 1024-aligned (swizzle atoms)
   static constexpr int WRING = NX * 2 * XU;                  // weight stages
-  static constexpr int SRING = WRING + NS * STAGE;           // fp16 scales [2 SRP units][KG][128]
-  static constexpr int BARS = SRING + 2 * SRP * KG * kTileCols * 2;
-  static constexpr int SMEM = BARS + 8 * (2 * NS + NX + NA + ND + RD);
+  static constexpr int BARS = WRING + NS * STAGE;
+  static constexpr int SMEM = BARS + 8 * (2 * NS + NX + NAF + RD + 4);
 };
 
 struct GemvArgs {
@@ -271,6 +297,8 @@ struct GemvArgs {
   int64_t out_ld;
   float* ws;
   int* cnt;
+  int sshift;       // A = s (q - z) 2^-sshift (host: keeps s 2^(24 - sshift) in fp16 range); the
+                    // epilogue multiplies the fp32 accumulator by 2^sshift
 };
 
 __device__ __forceinline__ int64_t cta_start(int64_t c, int64_t U, int grid) { return c * U / grid; }
@@ -286,15 +314,15 @@ template <int G>
 __global__ void __launch_bounds__(kGemvThreads, 1) k_dqgemv(const GemvArgs a, const __grid_constant__ CUtensorMap xmap) {
   using C = TC<G>;
   extern __shared__ __align__(1024) uint8_t smem[];
-  __half* sring = reinterpret_cast<__half*>(smem + C::SRING);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BARS);
   uint64_t* full = bars;               // [NS] weight record landed (TMA transaction bytes)
-  uint64_t* empty = full + C::NS;      // [NS] the 8 dequant warps of the unit's set hold their codes
+  uint64_t* empty = full + C::NS;      // [NS] the 4 dequant warps of the unit hold their codes
   uint64_t* xfull = empty + C::NS;     // [NX] the pair's activation slices landed (TMA bytes)
-  uint64_t* a_full = xfull + C::NX;    // [NA] the pair's A operands stored (8 dequant warps)
-  uint64_t* d_empty = a_full + C::NA;  // [ND] epilogue read the pair's accumulators (4 warps)
-  uint64_t* done = d_empty + C::ND;    // [RD] pair p's MMAs completed (tcgen05.commit + release): frees its
-                                       //      A buffer and activation slot, hands its accumulators over
+  uint64_t* a_full = xfull + C::NX;    // [NAF] the pair's A operands stored (8 dequant warps)
+  uint64_t* done = a_full + C::NAF;    // [RD] pair p's MMAs completed (tcgen05.commit): frees its
+                                       //      A buffer and activation slot
+  uint64_t* d_full = done + C::RD;     // [2] segment accumulators final (commit or plain arrive of each MMA warp)
+  uint64_t* d_empty = d_full + 2;      // [2] epilogue read it (4 warps)
   __shared__ uint32_t s_tmem;
   __shared__ int s_last;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -309,12 +337,15 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_dqgemv(const GemvArgs a, co
     TPQ_CTA(3, smid)
     for (int s = 0; s < C::NS; ++s) {
       mbar_init(full + s, 1);
-      mbar_init(empty + s, kSetWarps);
+      mbar_init(empty + s, 4);  // the 4 warps (one per lane quarter) converting the unit
     }
     for (int s = 0; s < C::NX; ++s) mbar_init(xfull + s, 1);
-    for (int b = 0; b < C::NA; ++b) mbar_init(a_full + b, kSetWarps);
-    for (int d = 0; d < C::ND; ++d) mbar_init(d_empty + d, 4);
-    for (int r = 0; r < C::RD; ++r) mbar_init(done + r, 2);  // tcgen05.commit + the issuer's release arrive
+    for (int b = 0; b < C::NAF; ++b) mbar_init(a_full + b, kSetWarps);
+    for (int r = 0; r < C::RD; ++r) mbar_init(done + r, 1);
+    for (int d = 0; d < 2; ++d) {
+      mbar_init(d_full + d, 2);
+      mbar_init(d_empty + d, 4);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == kMmaWarp) {
@@ -328,190 +359,172 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_dqgemv(const GemvArgs a, co
   tc_fence_after();
   pdl_launch_dependents();
   const uint32_t tmem = __shfl_sync(0xffffffffu, s_tmem, 0);  // warp-uniform TMEM base
-  // TMEM columns: accumulator pair set d at d * 2DU (unit h of the pair at + h DU, group g at + g 16);
-  // A pair buffer b at kA0 + b * 2AU (unit h at + h AU)
-  constexpr uint32_t kA0 = C::ND * 2 * C::DU;
+  // TMEM columns: segment accumulator of buffer d, MMA warp w at (2d + w) * 16; A pair buffer b at
+  // kA0 + b * 2AU (unit h at + h AU)
+  constexpr uint32_t kA0 = C::DC;
 
   if (warp < 2 * kSetWarps) {
-    // ===================== dequant: int4 -> exact f16 (q - z) -> TMEM A =====================
-    const int set = warp / kSetWarps, qw = warp & 3, kh = (warp >> 2) & 1;
+    // ===================== dequant: int4 -> fp16 s (q - z) 2^-e -> TMEM A =====================
+    // Per word: masks give the subnormal f16x2 q 2^-24 (nibbles at bits 0-3) and q 2^-20 (bits
+    // 4-7); one HFMA2 each with S = s 2^(24-e) resp. s 2^(20-e) and C = -z s 2^-e.
+    const int set = warp / kSetWarps, qw = warp & 3, h = (warp >> 2) & 1;
     const int col = qw * 32 + lane;  // weight column of the tile = TMEM lane
-    const uint32_t lane_base = (uint32_t)(qw * 32) << 16;
-    const __half2 k16 = __float2half2_rn(0.0625f);
+    const uint32_t a_col0 = tmem + ((uint32_t)(qw * 32) << 16) + kA0 + h * C::AU;  // + (p % NA) * 2AU
+    const int zbyte = kUnitK * kTileCols / 2 + C::KG * 256 + (col >> 1), zsh = 4 * (col & 1);
+    const bool xw = (warp & 7) == 0;  // acquires the pair's activation slice for the MMA warp
+    const float se = exp2f((float)-a.sshift), s24 = 16777216.f * se, s20 = 1048576.f * se;
     TPQ_PDECL
+    int i = 2 * set + h;  // unit of this warp in pair p = set, set + 2, ...: i = 2p + h
+    int s = i % C::NS;
+    uint32_t ph = (uint32_t)((i / C::NS) & 1);
+    int slot = set % C::NA;
     for (int p = set; p < np; p += 2) {
-      const int b = p % C::NA;
-#pragma unroll 1
-      for (int h = 0; h < 2; ++h) {
-        const int i = 2 * p + h;
-        if (i >= nu) break;
-        const int s = i % C::NS;
-        TPQ_W(full + s, (uint32_t)((i / C::NS) & 1), 0);
+      const uint32_t a_col = a_col0 + slot * 2 * C::AU;
+      if (i < nu) {
+        TPQ_W(full + s, ph, 0);
         TPQ_EV(0, i)
         const uint8_t* st = smem + C::WRING + s * C::STAGE;
-        // code words k = 64 kh + 8w .. +7 (w < 8): chunks 2kh, 2kh+1 of this column (16 B each)
-        const uint4 c0 = *reinterpret_cast<const uint4*>(st + ((kh * 2 + 0) * kTileCols + col) * 16);
-        const uint4 c1 = *reinterpret_cast<const uint4*>(st + ((kh * 2 + 1) * kTileCols + col) * 16);
-        const uint32_t wv[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
-        __half2 zl[C::GPH], zh[C::GPH];
-        __half* sr = sring + (i % (2 * C::SRP)) * (C::KG * kTileCols);
+        __half2 sl[C::KG], sh[C::KG], zc[C::KG];
 #pragma unroll
-        for (int j = 0; j < C::GPH; ++j) {
-          const int gi = (kh * (kUnitK / 2)) / G + j;  // group of the unit
-          const uint8_t* meta = st + kUnitK * kTileCols / 2;
-          const int z = (meta[C::KG * 256 + gi * 64 + (col >> 1)] >> (4 * (col & 1))) & 0xF;
-          zl[j] = __float2half2_rn((float)(1024 + z));  // lo slots hold 1024 + q
-          zh[j] = __float2half2_rn((float)(-64 - z));   // hi slots hold 1024 + 16 q: /16 - 64 - z
-          if (G < kUnitK || kh == 0) sr[gi * kTileCols + col] = *reinterpret_cast<const __half*>(meta + gi * 256 + 2 * col);
+        for (int g = 0; g < C::KG; ++g) {
+          const float z = (float)((st[zbyte + g * 64] >> zsh) & 0xFu);
+          const float sf = __half2float(*reinterpret_cast<const __half*>(st + kUnitK * kTileCols / 2 + g * 256 + 2 * col));
+          sl[g] = __float2half2_rn(sf * s24);  // exact: power-of-two scaling inside the fp16 range
+          sh[g] = __float2half2_rn(sf * s20);
+          zc[g] = __float2half2_rn(-z * sf * se);
         }
+        uint4 cw[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) cw[c] = *reinterpret_cast<const uint4*>(st + (c * kTileCols + col) * 16);
         __syncwarp();
         if (lane == 0) mbar_arrive(empty + s);
-        uint32_t r[32];
+#ifdef TPQ_EXP_NODQ
+        if (p >= C::NA) TPQ_W(done + (p - C::NA) % C::RD, (uint32_t)(((p - C::NA) / C::RD) & 1), 1);
+        if (cw[0].x == 0x12345678u && cw[3].w == 0x9abcdef0u && sl[0].x == __half(0.f) && zc[0].y == __half(1.f)) a.ws[threadIdx.x] = 0.f;
+#else
 #pragma unroll
-        for (int w = 0; w < 8; ++w) {
-          const int j = C::GPH == 1 ? 0 : (w * 8) / G;
-          const uint32_t x = wv[w], x8 = x >> 8;
-          // nibble order of a word (internal.h): (k0,k0+1) lo, (k0+2,k0+3) hi of x; the same of x >> 8
-          r[4 * w + 0] = h2u(__hsub2(u2h(lop3_and_or(x, 0x000F000Fu, 0x64006400u)), zl[j]));
-          r[4 * w + 1] = h2u(__hfma2(u2h(lop3_and_or(x, 0x00F000F0u, 0x64006400u)), k16, zh[j]));
-          r[4 * w + 2] = h2u(__hsub2(u2h(lop3_and_or(x8, 0x000F000Fu, 0x64006400u)), zl[j]));
-          r[4 * w + 3] = h2u(__hfma2(u2h(lop3_and_or(x8, 0x00F000F0u, 0x64006400u)), k16, zh[j]));
+        for (int kh = 0; kh < 2; ++kh) {
+          uint32_t r[32];
+#pragma unroll
+          for (int w = 0; w < 8; ++w) {
+            const int j = (64 * kh + 8 * w) / G;  // group of the word within the unit
+            const uint4 c4 = cw[2 * kh + w / 4];
+            const uint32_t x = (w & 3) == 0 ? c4.x : (w & 3) == 1 ? c4.y : (w & 3) == 2 ? c4.z : c4.w;
+            const uint32_t x8 = x >> 8;
+            // nibble order of a word (internal.h): (k0,k0+1) bits 0-3, (k0+2,k0+3) bits 4-7; the same of x >> 8
+            // nibble order of a word (internal.h): (k0,k0+1) bits 0-3, (k0+2,k0+3) bits 4-7; the same of x >> 8
+            r[4 * w + 0] = h2u(__hfma2(u2h(x & 0x000F000Fu), sl[j], zc[j]));
+            r[4 * w + 1] = h2u(__hfma2(u2h(x & 0x00F000F0u), sh[j], zc[j]));
+            r[4 * w + 2] = h2u(__hfma2(u2h(x8 & 0x000F000Fu), sl[j], zc[j]));
+            r[4 * w + 3] = h2u(__hfma2(u2h(x8 & 0x00F000F0u), sh[j], zc[j]));
+          }
+          TPQ_EV(1, i)
+          if (kh == 0) {
+            if (p >= C::NA) TPQ_W(done + (p - C::NA) % C::RD, (uint32_t)(((p - C::NA) / C::RD) & 1), 1);  // A free
+            tc_fence_after();
+          }
+          TPQ_EV(2, i)
+          tmem_st32(a_col + kh * 32, r);  // column c <-> k = 2c, 2c+1
         }
-        TPQ_EV(1, i)
-        if (h == 0) {
-          if (p >= C::NA) TPQ_W(done + (p - C::NA) % C::RD, (uint32_t)(((p - C::NA) / C::RD) & 1), 1);  // A free
-          tc_fence_after();
-        }
-        TPQ_EV(2, i)
-        tmem_st32(tmem + lane_base + kA0 + b * 2 * C::AU + h * C::AU + kh * 32, r);  // column c <-> k = 2c, 2c+1
+#endif
+      } else if (p >= C::NA) {
+        // no unit (odd tail): still order this arrive after pair p - NA's a_full phase completed
+        TPQ_W(done + (p - C::NA) % C::RD, (uint32_t)(((p - C::NA) / C::RD) & 1), 1);
       }
       TPQ_T0(st)
       tmem_wait_st();
       TPQ_T1(st, 2)
+      if (xw) TPQ_W(xfull + p % C::NX, (uint32_t)((p / C::NX) & 1), 3);  // activations landed (acquire)
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(a_full + b);
+      if (lane == 0) mbar_arrive(a_full + p % C::NAF);  // release: A stored, activations visible
       TPQ_EV(3, 2 * p)
+      i += 4;
+      slot = slot + 2 >= C::NA ? slot + 2 - C::NA : slot + 2;
+      s += 4;
+      if (s >= C::NS) {
+        s -= C::NS;
+        ph ^= 1u;
+      }
     }
     TPQ_PFLUSH(0)
   } else if (warp < kProdWarp) {
-    // ===================== epilogue: accumulators x scale -> output / partials ==============
+    // ===================== epilogue: once per tile segment =====================
     const int qw = warp - kEpiWarp0, col = qw * 32 + lane;
     const uint32_t lane_base = (uint32_t)(qw * 32) << 16;
     pdl_wait();  // the output may still be read by the previous kernel in the stream
-    float acc[kNPad];
-#pragma unroll
-    for (int m = 0; m < kNPad; ++m) acc[m] = 0.f;
     TPQ_PDECL
     int64_t seg_start = u0;
-    int kb = (int)(u0 % a.NKB), tile = (int)(u0 / a.NKB);
-    for (int p = 0; p < np; ++p) {
-      const int d = p % C::ND;
-      TPQ_W(done + p % C::RD, (uint32_t)((p / C::RD) & 1), 0);
-      TPQ_EV(0, 2 * p)
-      tc_fence_after();
-      // The pair's scales need no wait of their own: the dequant warps wrote them before their
-      // a_full arrive (release); the issuing lane acquired a_full and then arrived on `done` with
-      // a plain release arrive (besides the commit), so the writes happen-before this read through
-      // two release/acquire pairs.  (compute-sanitizer racecheck does not model mbarriers and
-      // reports this hand-off with or without a dedicated barrier.)
-      TPQ_EV(1, 2 * p)
-      const int nh = 2 * p + 1 < nu ? 2 : 1;
-      // per unit: add the unit's scaled group sums, then close the tile segment if it ends here
-      auto finish_unit = [&](int i) {
-          const int64_t u = u0 + i;
-          if (kb == a.NKB - 1 || i == nu - 1) {  // segment end
-            const int64_t n = (int64_t)tile * kTileCols + col;
-            const bool full_tile = seg_start == (int64_t)tile * a.NKB && kb == a.NKB - 1;
-            if (full_tile) {
-#pragma unroll
-              for (int m = 0; m < kNPad; ++m)
-                if (m < a.M) a.out[m * a.out_ld + n] = __float2half_rn(acc[m]);
-            } else {
-              // stream-K: this CTA holds part of the tile.  Partial -> own workspace slot (slot 0 = the
-              // CTA's first segment, 1 = its last); the last of the tile's CTAs to arrive sums all
-              // partials in CTA order (deterministic) and writes the tile.
-              const int slot = (seg_start == u0) ? 0 : 1;
-              float* mine = a.ws + ((size_t)blockIdx.x * 2 + slot) * (kNPad * kTileCols);
-#pragma unroll
-              for (int m = 0; m < kNPad; ++m)
-                if (m < a.M) __stcg(mine + m * kTileCols + col, acc[m]);
-              __threadfence();
-              named_bar(1, kTileCols);
-              const int c_first = cta_of_unit((int64_t)tile * a.NKB, a.U, a.grid);
-              const int c_last = cta_of_unit((int64_t)(tile + 1) * a.NKB - 1, a.U, a.grid);
-              if (col == 0) s_last = (atomicAdd(a.cnt + tile, 1) == c_last - c_first);
-              named_bar(1, kTileCols);
-              if (s_last) {
-                __threadfence();
-                float r[kNPad];
-#pragma unroll
-                for (int m = 0; m < kNPad; ++m) r[m] = 0.f;
-                for (int c = c_first; c <= c_last; ++c) {
-                  const int cslot = (cta_start(c, a.U, a.grid) / a.NKB == tile) ? 0 : 1;
-                  const float* src = a.ws + ((size_t)c * 2 + cslot) * (kNPad * kTileCols);
-#pragma unroll
-                  for (int m = 0; m < kNPad; ++m)
-                    if (m < a.M) r[m] += __ldcg(src + m * kTileCols + col);
-                }
-#pragma unroll
-                for (int m = 0; m < kNPad; ++m)
-                  if (m < a.M) a.out[m * a.out_ld + n] = __float2half_rn(r[m]);
-                if (col == 0) a.cnt[tile] = 0;  // self-reset for the next launch / graph replay
-              }
-            }
-#pragma unroll
-            for (int m = 0; m < kNPad; ++m) acc[m] = 0.f;
-            seg_start = u + 1;
-          }
-          if (++kb == a.NKB) {
-            kb = 0;
-            ++tile;
-          }
-      };
-      if constexpr (C::KG == 1) {
-        // both units' accumulators in flight at once, released before the arithmetic
-        uint32_t v0[kNPad], v1[kNPad];
-        const uint32_t dcol = tmem + lane_base + d * 2 * C::DU;
-        tmem_ld16(dcol, v0);
-        if (nh == 2) tmem_ld16(dcol + C::DU, v1);
-        const __half* sr = sring + ((2 * p) % (2 * C::SRP)) * kTileCols;
-        const float sc0 = __half2float(sr[col]), sc1 = __half2float(sr[kTileCols + col]);
+    int kb = (int)(u0 % a.NKB), tile = (int)(u0 / a.NKB), seg = 0;
+    for (int i = 0; i < nu; ++i) {
+      if (kb == a.NKB - 1 || i == nu - 1) {  // unit i closes a segment
+        const int d = seg & 1;
+        TPQ_W(d_full + d, (uint32_t)((seg >> 1) & 1), 0);
+        TPQ_EV(0, seg)
+        tc_fence_after();
+        // partial sums of the MMA warps that own a unit of the segment (units seg_start - u0 .. i)
+        const int lo = (int)(seg_start - u0);
+        const bool w0 = i - lo >= 3 || ((lo >> 1) & 1) == 0 || ((i >> 1) & 1) == 0;
+        const bool w1 = i - lo >= 3 || ((lo >> 1) & 1) == 1 || ((i >> 1) & 1) == 1;
+        uint32_t v[kNPad], v1[kNPad];
+        const uint32_t dcol = tmem + lane_base + 2 * d * kNPad;
+        if (w0) tmem_ld16(dcol, v);
+        if (w1) tmem_ld16(dcol + kNPad, v1);
         tmem_wait_ld();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(d_empty + d);
+        const float up = exp2f((float)a.sshift);  // undo the operand shift 2^-e (exact)
 #pragma unroll
-        for (int m = 0; m < kNPad; ++m) acc[m] = fmaf(sc0, __uint_as_float(v0[m]), acc[m]);
-        finish_unit(2 * p);
-        if (nh == 2) {
+        for (int m = 0; m < kNPad; ++m)
+          v[m] = __float_as_uint(up * (w0 ? (w1 ? __uint_as_float(v[m]) + __uint_as_float(v1[m]) : __uint_as_float(v[m]))
+                                          : __uint_as_float(v1[m])));
+        const int64_t n = (int64_t)tile * kTileCols + col;
+        const bool full_tile = seg_start == (int64_t)tile * a.NKB && kb == a.NKB - 1;
+        if (full_tile) {
 #pragma unroll
-          for (int m = 0; m < kNPad; ++m) acc[m] = fmaf(sc1, __uint_as_float(v1[m]), acc[m]);
-          finish_unit(2 * p + 1);
-        }
-      } else {
-#pragma unroll 1
-        for (int h = 0; h < nh; ++h) {
-          const int i = 2 * p + h;
-          const __half* sr = sring + (i % (2 * C::SRP)) * (C::KG * kTileCols);
+          for (int m = 0; m < kNPad; ++m)
+            if (m < a.M) a.out[m * a.out_ld + n] = __float2half_rn(__uint_as_float(v[m]));
+        } else {
+          // stream-K: this CTA holds part of the tile.  Partial -> own workspace slot (slot 0 = the
+          // CTA's first segment, 1 = its last); the last of the tile's CTAs to arrive sums all
+          // partials in CTA order (deterministic) and writes the tile.
+          const int slot = (seg_start == u0) ? 0 : 1;
+          float* mine = a.ws + ((size_t)blockIdx.x * 2 + slot) * (kNPad * kTileCols);
 #pragma unroll
-          for (int g = 0; g < C::KG; ++g) {  // one group accumulator at a time (register budget)
-            uint32_t v[kNPad];
-            tmem_ld16(tmem + lane_base + d * 2 * C::DU + h * C::DU + g * kNPad, v);
-            const float sc = __half2float(sr[g * kTileCols + col]);
-            tmem_wait_ld();
+          for (int m = 0; m < kNPad; ++m)
+            if (m < a.M) __stcg(mine + m * kTileCols + col, __uint_as_float(v[m]));
+          __threadfence();
+          named_bar(1, kTileCols);
+          const int c_first = cta_of_unit((int64_t)tile * a.NKB, a.U, a.grid);
+          const int c_last = cta_of_unit((int64_t)(tile + 1) * a.NKB - 1, a.U, a.grid);
+          if (col == 0) s_last = (atomicAdd(a.cnt + tile, 1) == c_last - c_first);
+          named_bar(1, kTileCols);
+          if (s_last) {
+            __threadfence();
+            float r[kNPad];
 #pragma unroll
-            for (int m = 0; m < kNPad; ++m) acc[m] = fmaf(sc, __uint_as_float(v[m]), acc[m]);
+            for (int m = 0; m < kNPad; ++m) r[m] = 0.f;
+            for (int c = c_first; c <= c_last; ++c) {
+              const int cslot = (cta_start(c, a.U, a.grid) / a.NKB == tile) ? 0 : 1;
+              const float* src = a.ws + ((size_t)c * 2 + cslot) * (kNPad * kTileCols);
+#pragma unroll
+              for (int m = 0; m < kNPad; ++m)
+                if (m < a.M) r[m] += __ldcg(src + m * kTileCols + col);
+            }
+#pragma unroll
+            for (int m = 0; m < kNPad; ++m)
+              if (m < a.M) a.out[m * a.out_ld + n] = __float2half_rn(r[m]);
+            if (col == 0) a.cnt[tile] = 0;  // self-reset for the next launch / graph replay
           }
-          if (h == nh - 1) {
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(d_empty + d);
-          }
-          finish_unit(i);
         }
+        ++seg;
+        seg_start = u0 + i + 1;
       }
-      TPQ_EV(2, 2 * p)
+      if (++kb == a.NKB) {
+        kb = 0;
+        ++tile;
+      }
     }
     TPQ_PFLUSH(5)
   } else if (warp == kProdWarp) {
@@ -568,45 +581,71 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_dqgemv(const GemvArgs a, co
     TPQ_PFLUSH(15)
   } else {
     // ===================== MMA issuers (warp-uniform operands, one elected lane issues) ========
+    const int w = warp - kMmaWarp;  // takes the pairs p % 2 == w (dequant set w)
     const uint32_t xring = smem_u32(smem + C::XRING);
+    const int kb0 = (int)(u0 % a.NKB);
+    const int nseg = (kb0 + nu - 1) / a.NKB + 1;  // segment of unit i: (kb0 + i) / NKB
     TPQ_PDECL
-    for (int p = warp - kMmaWarp; p < np; p += 2) {
-      const int d = p % C::ND, b = p % C::NA, x = p % C::NX;
-      const bool two = 2 * p + 1 < nu;
-      TPQ_W(d_empty + d, (uint32_t)(((p / C::ND) & 1) ^ 1), 0);
-      TPQ_EV(0, 2 * p)
-      TPQ_W(a_full + b, (uint32_t)((p / C::NA) & 1), 1);
-      TPQ_EV(1, 2 * p)
-      TPQ_W(xfull + x, (uint32_t)((p / C::NX) & 1), 2);
-      TPQ_EV(2, 2 * p)
-      tc_fence_after();
-      const uint64_t bd0 = bdesc_sw128(xring + 2 * x * C::XU);
-      const uint32_t dt = tmem + d * 2 * C::DU, at = tmem + kA0 + b * 2 * C::AU;
-      constexpr int J = kUnitK / 16;  // MMAs per unit
-      uint32_t aop[2 * J], dop[2 * J];
-      uint64_t bop[2 * J];
-#pragma unroll
-      for (int j = 0; j < 2 * J; ++j) {  // operands first, then back-to-back issue
-        const int h = j / J, jj = j % J;
-        aop[j] = at + h * C::AU + jj * 8;
-        bop[j] = bd0 + (uint64_t)((h * C::XU + (jj / 4) * (C::XU / 2) + (jj % 4) * 32) >> 4);
-        dop[j] = dt + h * C::DU + (jj / (G / 16)) * kNPad;                // group of the k16 block
-      }
-      TPQ_T0(is)
-      if (elect_one()) {
-#pragma unroll
-        for (int j = 0; j < J; ++j) umma_ts1(dop[j], aop[j], bop[j], kIdesc, (j % (G / 16)) ? 1u : 0u);
-        if (two) {
-#pragma unroll
-          for (int j = J; j < 2 * J; ++j) umma_ts1(dop[j], aop[j], bop[j], kIdesc, (j % (G / 16)) ? 1u : 0u);
-        }
-        umma_commit1(done + p % C::RD);
-        mbar_arrive(done + p % C::RD);  // release: orders the scale writes (acquired via a_full)
-      }
+    int sw = 0;  // next segment this warp has not yet closed on d_full
+    // close segment sw without a unit in it: plain arrive once the epilogue drained segment sw - 2
+    auto skip_seg = [&]() {
+      TPQ_W(d_empty + (sw & 1), (uint32_t)(((sw >> 1) & 1) ^ 1), 0);
+      if (lane == 0) mbar_arrive(d_full + (sw & 1));
       __syncwarp();
-      TPQ_T1(is, 3)
+      ++sw;
+    };
+    static_assert(C::XU == 4096 && C::AU == 64, "umma_unit16 offsets");
+    for (int p = w; p < np; p += 2) {
+      const int x = p % C::NX;
+      const uint64_t bd0 = bdesc_sw128(xring + 2 * x * C::XU);
+      // fast path: both units of the pair inside one segment that this warp already opened and
+      // does not close here (sg == sw, previous unit of this warp in sg, next one too)
+      const int i0 = 2 * p, sg = (kb0 + i0) / a.NKB;
+      const int lo = sg * a.NKB - kb0 > 0 ? sg * a.NKB - kb0 : 0;
+      const int hi = (sg + 1) * a.NKB - kb0 - 1 < nu - 1 ? (sg + 1) * a.NKB - kb0 - 1 : nu - 1;
+      const bool fast = sg == sw && i0 - 3 >= lo && i0 + 4 <= hi;
+      const uint32_t at = tmem + kA0 + (p % C::NA) * 2 * C::AU;
+      TPQ_W(a_full + p % C::NAF, (uint32_t)((p / C::NAF) & 1), 1);  // A stored + activations landed
+      TPQ_EV(1, 2 * p)
+      tc_fence_after();
+      if (fast) {
+        const uint32_t dt = tmem + (2 * (sg & 1) + w) * kNPad;
+        if (elect_one()) {
+          umma_unit16(dt, at, bd0, kIdesc, 1u);
+          umma_unit16(dt, at + C::AU, bd0 + (C::XU >> 4), kIdesc, 1u);
+          umma_commit1(done + p % C::RD);
+        }
+        __syncwarp();
+        TPQ_EV(3, 2 * p)
+        continue;
+      }
+#pragma unroll 1
+      for (int h = 0; h < 2; ++h) {
+        const int i = 2 * p + h;
+        if (i >= nu) break;
+        const int sg = (kb0 + i) / a.NKB;
+        while (sw < sg) skip_seg();
+        const int lo = sg * a.NKB - kb0 > 0 ? sg * a.NKB - kb0 : 0;
+        const int hi = (sg + 1) * a.NKB - kb0 - 1 < nu - 1 ? (sg + 1) * a.NKB - kb0 - 1 : nu - 1;
+        const bool first = (h ? i - 1 : i - 3) < lo, last = (h ? i + 3 : i + 1) > hi;  // this warp's units of sg
+        const int d = sg & 1;
+        if (first) {
+          TPQ_W(d_empty + d, (uint32_t)(((sg >> 1) & 1) ^ 1), 0);  // epilogue drained segment sg - 2
+          tc_fence_after();
+        }
+        const uint32_t dt = tmem + (2 * d + w) * kNPad;
+        if (elect_one()) {
+          umma_unit16(dt, at + h * C::AU, bd0 + (uint64_t)((h * C::XU) >> 4), kIdesc, first ? 0u : 1u);
+          if (last) umma_commit1(d_full + d);
+        }
+        __syncwarp();
+        if (last) ++sw;
+      }
+      if (elect_one()) umma_commit1(done + p % C::RD);
+      __syncwarp();
       TPQ_EV(3, 2 * p)
     }
+    while (sw < nseg) skip_seg();
     TPQ_PFLUSH(20)
   }
   tc_fence_before();
@@ -1321,6 +1360,7 @@ cudaError_t launch_gemv(const LayerDev& L, const CUtensorMap& xmap, int M, void*
   a.out_ld = out_ld;
   a.ws = L.ws;
   a.cnt = L.cnt;
+  a.sshift = L.sshift;
   if (L.G == 128) return launch_pdl(k_dqgemv<128>, dim3(a.grid), dim3(kGemvThreads), TC<128>::SMEM, st, a, xmap);
   if (L.G == 64) return launch_pdl(k_dqgemv<64>, dim3(a.grid), dim3(kGemvThreads), TC<64>::SMEM, st, a, xmap);
   if (L.G == 32) return launch_pdl(k_dqgemv<32>, dim3(a.grid), dim3(kGemvThreads), TC<32>::SMEM, st, a, xmap);

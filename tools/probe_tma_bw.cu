@@ -100,5 +100,9 @@ int main() {
   run<8576, 20>(src, bytes, sink, 1);
   run<4288, 16>(src, bytes, sink, 2);
   run<17152, 6>(src, bytes, sink, 2);
+  run<8512, 20>(src, bytes, sink, 1);
+  run<8512, 24>(src, bytes, sink, 1);
+  run<17024, 12>(src, bytes, sink, 1);
+  run<32768, 6>(src, bytes, sink, 1);
   return 0;
 }
