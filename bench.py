@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--sweep", action="store_true", help="also time M=1,4 (extra 'sweep' key)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-naive", action="store_true", help="N > 1: skip timing the naive AllGather path")
     ap.add_argument("--no-graph", action="store_true", help="launch every step eagerly (no CUDA graph)")
     ap.add_argument("--sim-tp", type=int, default=0,
                     help="single GPU: time one rank's shard of a TP=k MLP (no collective)")
@@ -331,19 +332,24 @@ def main():
     t_mid = statistics.mean(e[2].elapsed_time(e[3]) for e in evs) * 1e3
 
     # ---------------- e2e through the public host-buffer API (pinned host memory)
+    # (--sim-tp has no host-buffer path: one rank's shard alone is not a complete forward)
     Xh = torch.from_numpy(p.X[:M].copy()).pin_memory()
     Yh = torch.empty(M, N2, dtype=torch.float16).pin_memory()
     Ke = max(20, min(K // 10, 2000))
-    for i in range(5):
-        hs[i % R].forward_host(Xh.numpy(), Yh.numpy(), stream=stream)
-    sync_all()
     es, ee = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    es.record(stream)
-    for i in range(Ke):
-        hs[i % R].forward_host(Xh.numpy(), Yh.numpy(), stream=stream)
-    ee.record(stream)
+    if not sim_tp:
+        for i in range(5):
+            hs[i % R].forward_host(Xh.numpy(), Yh.numpy(), stream=stream)
+        sync_all()
+        es.record(stream)
+        for i in range(Ke):
+            hs[i % R].forward_host(Xh.numpy(), Yh.numpy(), stream=stream)
+        ee.record(stream)
+    else:
+        es.record(stream)
+        ee.record(stream)
     sync_all()
-    e2e_ms = es.elapsed_time(ee) / Ke
+    e2e_ms = es.elapsed_time(ee) / Ke if not sim_tp else float("nan")
     if world > 1:
         t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -374,11 +380,19 @@ def main():
                          "allreduce": t_coll},
         "step_roofline": {"bytes": step_bytes, "GBps": step_bytes / (ms_per_step * 1e-3) / 1e9,
                           "frac": step_bytes / (ms_per_step * 1e-3) / 1e9 / peak},
-        "e2e": {"value": e2e_ms * 1e3, "unit": "us", "h2d_bytes_per_step": 2 * M * K1,
-                "d2h_bytes_per_step": 2 * M * N2},
+        "e2e": None if sim_tp else {"value": e2e_ms * 1e3, "unit": "us", "h2d_bytes_per_step": 2 * M * K1,
+                                    "d2h_bytes_per_step": 2 * M * N2},
         "gpu_launches": K * 3 + (K if variant == tpq.TPQ_NAIVE else 0),
         "clocks": clk,
     }
+    if world > 1 and variant == tpq.TPQ_TP_AWARE and not a.no_naive:
+        # the paper's comparison on the same box, same kernels, same graph timing: Alg. 2 (naive
+        # act_order TP, AllGather of Y1 + global P2 permute between the layers)
+        try:
+            line["naive_allgather"] = time_naive(a, p, P1, P2, shard_tp, rank, local, R, comm, X, Y, stream,
+                                                 sync_all, world, dev, ms_per_step)
+        except Exception as e:  # report, keep the TP-aware line
+            line["naive_allgather"] = {"error": f"{type(e).__name__}: {e}"}
     if rank == 0 and a.sweep:
         line["sweep"] = sweep_m(hs, p, R, stream, dev, sim_tp)
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
@@ -396,6 +410,48 @@ def main():
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def time_naive(a, p, P1, P2, tp, rank, local, R, comm, X, Y, stream, sync_all, world, dev, ours_ms):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2402_04925_b200 as tpq
+    M = a.m
+    hn = [tpq.TpMlp(p.w1, p.w2, P1, P2, tp=tp, rank=rank, variant=tpq.TPQ_NAIVE, M_max=16, device=local)
+          for _ in range(R)]
+    for h in hn:
+        h.set_comm(comm)
+    with torch.cuda.stream(stream):
+        for i in range(max(3, a.warmup)):
+            hn[i % R].forward(X, M, Y, stream=stream)
+    sync_all()
+    per = R * max(1, 16 // R)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream):
+        for i in range(per):
+            hn[i % R].forward(X, M, Y, stream=stream)
+    for _ in range(3):
+        g.replay()
+    sync_all()
+    reps = max(1, a.steps // per)
+    s_, e_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        s_.record(stream)
+        for _ in range(reps):
+            g.replay()
+        e_.record(stream)
+    sync_all()
+    ms = s_.elapsed_time(e_) / (reps * per)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    for h in hn:
+        h.close()
+    return {"value": ms * 1e3, "unit": "us", "steps": reps * per,
+            "speedup_tp_aware": ms / ours_ms,
+            "what": "Alg. 2: layer 1, ncclAllGather(Y1), P2 gather + CHUNK, layer 2, ncclAllReduce; "
+                    "same kernels, CUDA-graph timed, max over ranks"}
 
 
 def sweep_m(hs, p, R, stream, dev, sim_tp):

@@ -6,8 +6,8 @@
 // Packed layer shard (K rows in Alg.-1 order, N columns): 128-column TILES x 128-row K-BLOCKS.
 // Unit (t, kb) is one contiguous record of unit_bytes(G) = 8192 + 320 * (128 / G) bytes,
 // tile-major at offset (t * NKB + kb) * unit_bytes(G):
-//   [0, 8192)                 int4 codes: chunk c (k = 128 kb + 32c .. +31) x column j (0..127)
-//                             x 16 bytes; u32 word w of a chunk holds k0 = 32c + 8w .. k0+7 as
+//   [0, 8192)                 int4 codes: 16-byte block code_block(c, j) = c * 128 + (j ^ 2c) holds
+//                             chunk c (k = 128 kb + 32c .. +31) of column j (0..127); u32 word w of a chunk holds k0 = 32c + 8w .. k0+7 as
 //                             nibbles n0=q[k0] n4=q[k0+1] n1=q[k0+2] n5=q[k0+3] n2=q[k0+4]
 //                             n6=q[k0+5] n3=q[k0+6] n7=q[k0+7]  (LOP3 magic-number extraction
 //                             yields f16x2 pairs of consecutive k = one TMEM column of the MMA
@@ -29,8 +29,19 @@ constexpr int kTileCols = 128;      // weight columns per tile (= TMEM lanes = M
 constexpr int kUnitK = 128;         // weight rows per unit (8 MMAs of K = 16)
 constexpr int kNPad = 16;           // batch rows per MMA (tcgen05 M=128 needs N % 16 == 0)
 constexpr int kMaxM = 16;           // rows per forward chunk
+constexpr int kGemvParts = 4;       // max stream-K participants per GEMV CTA (workspace sizing)
 constexpr int64_t unit_bytes_c(int G) { return (int64_t)kUnitK * kTileCols / 2 + 320LL * (kUnitK / G); }
 inline int64_t unit_bytes(int G) { return unit_bytes_c(G); }
+#ifdef __CUDACC__
+#define TPQ_HD __host__ __device__
+#else
+#define TPQ_HD
+#endif
+// 16-byte code block of (chunk c, column j) inside a record: column XOR-swizzled by 2c within its
+// aligned group of 8, so that a quarter-warp reading columns g, g+1 of chunks 0..3 (the mma.sync
+// GEMV fragment order) hits 8 distinct bank groups; still a permutation inside each aligned 8-column
+// group, so lanes reading 8 consecutive columns of one chunk stay conflict-free.
+TPQ_HD constexpr int code_block(int c, int j) { return c * kTileCols + (j ^ (2 * c)); }
 
 struct LayerDev {
   const uint8_t* packed = nullptr;  // device
@@ -38,10 +49,11 @@ struct LayerDev {
   int G = 0, NT = 0, NKB = 0;
   int64_t U = 0;           // NT * NKB units
   int grid = 0;            // persistent CTAs (stream-K), one per SM
-  float* ws = nullptr;     // [grid][2 slots][16][128] fp32 stream-K partials (GEMV)
+  float* ws = nullptr;     // [grid * kGemvParts][2 slots][16 * 128] fp32 stream-K partials (GEMV)
   float* ws_mm = nullptr;  // [grid][2 slots][256][128] fp32 stream-K partials (A7 GEMM)
   float* ws_ss = nullptr;  // [items][128][128] fp32 k-split partials (A7 SS GEMM, M >= 128)
   int* cnt = nullptr;      // [NT] arrival counters (self-resetting)
+  int gemv = 0;            // GEMV kernel: 0 = from the TPQ_GEMV environment variable (default tcgen05), 1 = tcgen05, 2 = register-dequant
   int sshift = 0;          // GEMV operand shift e: smallest e >= 0 with max|s| 2^(24-e) <= 65504
 };
 
@@ -52,8 +64,10 @@ bool gemv_prepare(int G);
 
 // out[m][n] = sum_k x[m][k] deq(W)[k][n] for M <= 16 rows; x is a [16][K] fp16 row-major buffer
 // described by `xmap` (make_xmap), out is [M][out_ld] fp16 row-major.
-cudaError_t launch_gemv(const LayerDev& L, const CUtensorMap& xmap, int M, void* out, int64_t out_ld,
-                        cudaStream_t st);
+// described by `xmap` (make_xmap, 16-row boxes; tcgen05 GEMV) and by x / ldx (register-dequant GEMV,
+// the default).  TPQ_GEMV=tc selects the tcgen05 GEMV (k_dqgemv) instead.
+cudaError_t launch_gemv(const LayerDev& L, const CUtensorMap& xmap, const void* x, int64_t ldx, int M, void* out,
+                        int64_t out_ld, cudaStream_t st);
 
 // A7 (M > 16): out[m][n] = sum_k x[m][k] deq(W)[k][n] for M <= nb rows (nb in {64, 128, 256}), x a
 // [nb][K] fp16 row-major buffer described by xmap (make_xmap with rows = nb), out [M][out_ld].

@@ -94,7 +94,7 @@ std::vector<uint8_t> pack_layer(const Canon& c) {
           const int64_t k0 = kb * tpq::kUnitK + 32 * ch + 8 * w;
           uint32_t word = 0;
           for (int i = 0; i < 8; ++i) word |= (uint32_t)c.q[(size_t)((k0 + i) * c.N + n)] << (4 * kNibbleOfK[i]);
-          words[(ch * tpq::kTileCols + j) * 4 + w] = word;
+          words[tpq::code_block(ch, j) * 4 + w] = word;
         }
       for (int gi = 0; gi < KG; ++gi) {
         const int64_t g = kb * KG + gi;
@@ -120,7 +120,7 @@ void unpack_layer(const std::vector<uint8_t>& pk, int64_t K, int64_t N, int G, u
       const int64_t n = t * tpq::kTileCols + j;
       for (int ch = 0; ch < tpq::kUnitK / 32; ++ch)
         for (int w = 0; w < 4; ++w) {
-          const uint32_t word = words[(ch * tpq::kTileCols + j) * 4 + w];
+          const uint32_t word = words[tpq::code_block(ch, j) * 4 + w];
           const int64_t k0 = kb * tpq::kUnitK + 32 * ch + 8 * w;
           for (int i = 0; i < 8; ++i) q[(k0 + i) * N + n] = (word >> (4 * kNibbleOfK[i])) & 0xF;
         }
@@ -391,8 +391,8 @@ int tp_shard_mlp(const gptq_layer* w1, const gptq_layer* w2, const int32_t* P1, 
         TPQ_CUDA(cudaSetDevice(device));
         int r;
         auto A = [&](void** p, size_t b) { return dev_alloc(p, b); };
-        const size_t ws1 = (size_t)h->L1.grid * 2 * tpq::kNPad * tpq::kTileCols;
-        const size_t ws2 = (size_t)h->L2.grid * 2 * tpq::kNPad * tpq::kTileCols;
+        const size_t ws1 = (size_t)h->L1.grid * tpq::kGemvParts * 2 * tpq::kNPad * tpq::kTileCols;
+        const size_t ws2 = (size_t)h->L2.grid * tpq::kGemvParts * 2 * tpq::kNPad * tpq::kTileCols;
         h->rows = M_max > tpq::kMaxM ? kGemmRows : tpq::kMaxM;
         const size_t wm1 = M_max > tpq::kMaxM ? (size_t)h->L1.grid * 2 * kGemmRows * tpq::kTileCols : 0;
         const size_t wm2 = M_max > tpq::kMaxM ? (size_t)h->L2.grid * 2 * kGemmRows * tpq::kTileCols : 0;
@@ -546,7 +546,9 @@ static cudaError_t mark_event(cudaEvent_t e, cudaStream_t st) {
 // One dequant-GEMM layer for mc rows: the GEMV (mc <= 16) or the A7 tensor-core GEMM (mc <= 256).
 cudaError_t run_layer(tpq_mlp* h, int layer, int mc, void* out, int64_t out_ld, cudaStream_t st) {
   const tpq::LayerDev& L = layer == 1 ? h->L1 : h->L2;
-  if (mc <= tpq::kMaxM) return tpq::launch_gemv(L, layer == 1 ? h->xmap1 : h->xmap2, mc, out, out_ld, st);
+  if (mc <= tpq::kMaxM)
+    return tpq::launch_gemv(L, layer == 1 ? h->xmap1 : h->xmap2, layer == 1 ? h->d_x1 : h->d_y1, layer == 1 ? h->K1 : h->n,
+                            mc, out, out_ld, st);
   if (mc >= 128 && !getenv("TPQ_NO_SS"))  // compute-bound: activations as the reused A operand
     return tpq::launch_gemm_ss(L, layer == 1 ? h->ss1 : h->ss2, mc, h->sms, out, out_ld, st);
   const int v = mc <= 64 ? 0 : mc <= 128 ? 1 : 2;
@@ -694,6 +696,13 @@ int tpq_mlp_set_timing(tpq_mlp* h, void* const* events) {
     h->ev[i] = (cudaEvent_t)events[i];
   }
   h->timing = true;
+  return TPQ_OK;
+}
+
+int tpq_mlp_set_gemv_kernel(tpq_mlp* h, int kind) {
+  if (!h) return fail(TPQ_EINVAL, "NULL handle");
+  if (kind < TPQ_GEMV_AUTO || kind > TPQ_GEMV_REG) return fail(TPQ_EINVAL, "unknown GEMV kernel kind %d", kind);
+  h->L1.gemv = h->L2.gemv = kind;
   return TPQ_OK;
 }
 

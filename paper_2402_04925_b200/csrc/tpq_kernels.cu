@@ -60,6 +60,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// Wait with a suspend-time hint: the warp sleeps until the phase completes (or the hint, in ns,
+// expires) instead of spinning try_wait / branch / yield through the issue slots of busy warps.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "TPQ_WAITS_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra TPQ_WAITS_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(1000000)
+      : "memory");
+}
 // Per-CTA timeline (build with -DTPQ_PROF; profiling aid, not in the product build): entry,
 // work start, end (globaltimer ns) and SM id per CTA, per layer (N > K selects the slot).
 #ifdef TPQ_PROF
@@ -289,6 +300,8 @@ struct TC {
 
 struct GemvArgs {
   const uint8_t* packed;
+  const __half* x;  // activations [>= M rows][ldx] fp16 row-major (register-dequant GEMV)
+  int64_t ldx;
   int M;
   int NT, NKB;      // tiles, k-blocks per tile
   int64_t U;        // NT * NKB units
@@ -395,7 +408,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_dqgemv(const GemvArgs a, co
         }
         uint4 cw[4];
 #pragma unroll
-        for (int c = 0; c < 4; ++c) cw[c] = *reinterpret_cast<const uint4*>(st + (c * kTileCols + col) * 16);
+        for (int c = 0; c < 4; ++c) cw[c] = *reinterpret_cast<const uint4*>(st + code_block(c, col) * 16);
         __syncwarp();
         if (lane == 0) mbar_arrive(empty + s);
 #ifdef TPQ_EXP_NODQ
@@ -657,6 +670,310 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_dqgemv(const GemvArgs a, co
   }
 }
 
+// ------------------------------------------------------------------ GEMV, register-dequant path (M <= 16)
+// k_dqgemv_r<G, NB, NSETS, WPS>: the product path for M <= 16.  Same weight records, same operand
+// arithmetic (A = fp16(s (q - z) 2^-e) from one HFMA2 per f16x2 pair, fp32 accumulation over a whole
+// tile segment, x 2^e in the epilogue), but the dequantized operand never leaves registers: each
+// warp turns its columns' codes into mma.sync.m16n8k16 A fragments and multiplies them with the
+// activation fragments right away.  The tcgen05 GEMV above spends most of its time in the
+// dequant -> TMEM -> MMA -> commit -> dequant hand-off chain (profiles/r01_summary.md: dequant warps
+// wait 63-73 % on "A free", MMA warps 71-82 % on "A full"); at M <= 16 (3.8-61 flop/B, HBM-bound)
+// the contraction needs < 3 % of the tensor pipe, and the register path has no cross-warp hand-off
+// besides the TMA ring (tools/probe_hmma_gemv.cu: 214-300 cycles per 128 x 128 unit per SM from
+// shared memory, against ~350-378 cycles of HBM time per unit).
+//
+// Fragment mapping.  m16n8k16 "row.col": A rows = 16 weight columns (c0 = 16 b + g, c1 = c0 + 8 of
+// the warp's CW columns), B columns = batch rows n = 8 nb + g, k = 16 per step.  The k order inside
+// a step is free as long as A and B agree: thread (g = lane / 4, t = lane % 4) holds, for k-step
+// s = 2e + h (e, h in 0..3, 0..1), the physical k = 32 t + 4 s + {0, 1} (virtual 2t, 2t+1) and
+// 32 t + 4 s + {2, 3} (virtual 2t+8, 2t+9).  So a thread reads one 16-byte code chunk per column
+// (chunk t of the record, internal.h: word e = k 32t + 8e .. +7) and 64 contiguous activation bytes
+// per batch row (k 32 t .. 32 t + 31), both with 128-bit shared loads.
+//
+// Work split.  A CTA per SM holds NSETS independent stream-K participants (sets of WPS warps, each
+// warp CW = 128 / WPS columns of every unit), p = blockIdx.x * NSETS + set, over contiguous unit
+// ranges [p U / P, (p + 1) U / P).  One producer warp fills every set's ring of D stages (weight
+// record by 1-D bulk TMA, L2 evict-first; the unit's activation slice, XR = 8 NB rows x 128 k, by
+// one 3-D tensor TMA with 128-byte swizzle).  A tile split between participants leaves fp32
+// partials in fragment order; the last arriver sums them in participant order (deterministic).
+template <int G, int NB, int NSETS, int WPS>
+struct TR {
+  static constexpr int CW = kTileCols / WPS;  // columns per warp
+  static constexpr int BLK = CW / 16;         // 16-column MMA blocks per warp
+  static constexpr int KG = kUnitK / G;       // groups per unit
+  static constexpr int UB = (int)unit_bytes_c(G);
+  static constexpr int STAGE = (UB + 127) / 128 * 128;
+#ifndef TPQ_RD
+#define TPQ_RD 16
+#endif
+  static constexpr int D0 = (222 * 1024) / (NSETS * STAGE);
+  static constexpr int D = D0 > TPQ_RD ? TPQ_RD : D0;  // ring stages per set
+  static_assert(D >= 2, "GEMV ring needs >= 2 stages per set");
+  static constexpr int BARS = NSETS * D * STAGE;
+  static constexpr int SMEM = BARS + 16 * NSETS * D;
+  static constexpr int WARPS = NSETS * (WPS + 1);     // WPS consumers + one producer per set
+  static constexpr int PART = WPS * BLK * NB * 128;  // fp32 partial floats per participant slot
+  static_assert(PART <= kNPad * kTileCols, "partial slot size");
+};
+
+__device__ __forceinline__ void hmma16816(float* d, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                                          uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t u4w(const uint4& v, int e) { return e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w; }
+
+template <int G, int NB, int NSETS, int WPS>
+__global__ void __launch_bounds__(TR<G, NB, NSETS, WPS>::WARPS * 32, 1)
+    k_dqgemv_r(const GemvArgs a) {
+  using C = TR<G, NB, NSETS, WPS>;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::BARS);  // [NSETS][D] record + slice landed
+  uint64_t* empty = full + NSETS * C::D;                          // [NSETS][D] the set's WPS warps read it
+  __shared__ int s_last[NSETS];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int P = a.grid * NSETS;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < NSETS * C::D; ++i) {
+      mbar_init(full + i, 1);
+      mbar_init(empty + i, WPS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  pdl_launch_dependents();
+
+  if (warp >= NSETS * WPS) {
+    // ===================== producers: one lane per set feeds the set's ring =====================
+    const int s = warp - NSETS * WPS;
+    if (lane == 0) {
+      const uint64_t pw = policy_evict_first();
+      const int p = blockIdx.x * NSETS + s;
+      const int64_t ub = cta_start(p, a.U, P);
+      const int nu = (int)(cta_start(p + 1, a.U, P) - ub);
+      uint64_t* full_s = full + s * C::D;
+      // weight records do not depend on the previous kernel: no griddepcontrol.wait here, so the
+      // first D of them overlap its tail (PDL)
+      uint64_t* empty_s = empty + s * C::D;
+      uint8_t* ring = smem + s * C::D * C::STAGE;
+      const uint8_t* src = a.packed + ub * C::UB;
+      for (int r = 0, d = 0, lap = 0; r < nu; ++r, src += C::UB) {
+#ifdef TPQ_RPSLEEP
+        if (lap) mbar_wait_sleep(empty_s + d, (uint32_t)((lap - 1) & 1));
+#else
+        if (lap) mbar_wait(empty_s + d, (uint32_t)((lap - 1) & 1));
+#endif
+        mbar_arrive_expect_tx(full_s + d, C::UB);
+        bulk_g2s(ring + d * C::STAGE, src, C::UB, full_s + d, pw);
+        if (++d == C::D) {
+          d = 0;
+          ++lap;
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    // ===================== consumers: dequant to A fragments + mma.sync =====================
+    const int set = warp / WPS, wi = warp % WPS, g = lane >> 2, t = lane & 3;
+    const int p = blockIdx.x * NSETS + set;
+    const int64_t ub = cta_start(p, a.U, P);
+    const int nu = (int)(cta_start(p + 1, a.U, P) - ub);
+    const float se = exp2f((float)-a.sshift), s24 = 16777216.f * se, s20 = 1048576.f * se;
+    const float up = exp2f((float)a.sshift);
+    const int jg = (32 * t) / G;  // group (within the unit) of this thread's k range
+    uint64_t* full_s = full + set * C::D;
+    uint64_t* empty_s = empty + set * C::D;
+    float acc[C::BLK][NB][4];
+#pragma unroll
+    for (int b = 0; b < C::BLK; ++b)
+#pragma unroll
+      for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[b][nb][e] = 0.f;
+    int tile = (int)(ub / a.NKB), kb = (int)(ub % a.NKB);
+    int64_t seg_start = ub;
+    pdl_wait();  // outputs / partials may still be read by the previous kernel in the stream
+    // activation fragments straight from global memory (X is <= 16 x K fp16, L2-resident): row
+    // g + 8 nb, k = 128 kb + 32 t .. + 31, four 16-byte loads per row
+    const __half* xp = a.x + (int64_t)g * a.ldx + 32 * t + (int64_t)kb * kUnitK;
+    const int64_t x8 = 8 * a.ldx;
+    const uint8_t* ring = smem + set * C::D * C::STAGE;
+    uint32_t fph = 0;  // phase parity of the set's full barriers in lap r / D
+    for (int r = 0, d = 0; r < nu; ++r) {
+      uint4 xb[NB][4];
+#pragma unroll
+      for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) xb[nb][i] = *reinterpret_cast<const uint4*>(xp + nb * x8 + 8 * i);
+#ifdef TPQ_RSLEEP
+      mbar_wait_sleep(full_s + d, fph);
+#else
+      mbar_wait(full_s + d, fph);
+#endif
+      const uint8_t* rec = ring + d * C::STAGE;
+      uint4 wc[C::BLK][2];
+      __half2 sl[C::BLK][2], sh[C::BLK][2], zc[C::BLK][2];
+#pragma unroll
+      for (int b = 0; b < C::BLK; ++b)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) wc[b][h] = *reinterpret_cast<const uint4*>(rec + code_block(t, wi * C::CW + 16 * b + 8 * h + g) * 16);
+      auto opnd = [&](int c, uint32_t& vl, uint32_t& vh, uint32_t& vz) {  // S = s 2^(24|20 - e), C = -z s 2^-e
+        const float sf = __half2float(*reinterpret_cast<const __half*>(rec + kUnitK * kTileCols / 2 + jg * 256 + 2 * c));
+        const float z = (float)((rec[kUnitK * kTileCols / 2 + C::KG * 256 + jg * 64 + (c >> 1)] >> (4 * (c & 1))) & 0xFu);
+        vl = h2u(__float2half2_rn(sf * s24));  // exact: power-of-two scaling inside the fp16 range
+        vh = h2u(__float2half2_rn(sf * s20));
+        vz = h2u(__float2half2_rn(-z * sf * se));
+      };
+#ifdef TPQ_RSHFL
+      if constexpr (C::KG == 1 && C::BLK == 2) {
+#else
+      if constexpr (false) {
+#endif
+        // one group per unit: the four threads t of group g need the same four columns; each computes
+        // one (b = t / 2, h = t % 2) and the others read it by shuffle
+        uint32_t vl, vh, vz;
+        opnd(wi * C::CW + 16 * (t >> 1) + 8 * (t & 1) + g, vl, vh, vz);
+#pragma unroll
+        for (int b = 0; b < 2; ++b)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int src = (lane & ~3) | (2 * b + h);
+            sl[b][h] = u2h(__shfl_sync(0xffffffffu, vl, src));
+            sh[b][h] = u2h(__shfl_sync(0xffffffffu, vh, src));
+            zc[b][h] = u2h(__shfl_sync(0xffffffffu, vz, src));
+          }
+      } else {
+#pragma unroll
+        for (int b = 0; b < C::BLK; ++b)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            uint32_t vl, vh, vz;
+            opnd(wi * C::CW + 16 * b + 8 * h + g, vl, vh, vz);
+            sl[b][h] = u2h(vl);
+            sh[b][h] = u2h(vh);
+            zc[b][h] = u2h(vz);
+          }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty_s + d);  // release: the stage is in registers
+      if (++d == C::D) {
+        d = 0;
+        fph ^= 1u;
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+#pragma unroll
+        for (int hs = 0; hs < 2; ++hs)
+#pragma unroll
+          for (int b = 0; b < C::BLK; ++b) {
+            const uint32_t y0 = hs ? u4w(wc[b][0], e) >> 8 : u4w(wc[b][0], e);
+            const uint32_t y1 = hs ? u4w(wc[b][1], e) >> 8 : u4w(wc[b][1], e);
+            const uint32_t a0 = h2u(__hfma2(u2h(y0 & 0x000F000Fu), sl[b][0], zc[b][0]));
+            const uint32_t a1 = h2u(__hfma2(u2h(y1 & 0x000F000Fu), sl[b][1], zc[b][1]));
+            const uint32_t a2 = h2u(__hfma2(u2h(y0 & 0x00F000F0u), sh[b][0], zc[b][0]));
+            const uint32_t a3 = h2u(__hfma2(u2h(y1 & 0x00F000F0u), sh[b][1], zc[b][1]));
+#pragma unroll
+            for (int nb = 0; nb < NB; ++nb)
+              hmma16816(acc[b][nb], a0, a1, a2, a3, u4w(xb[nb][e], 2 * hs), u4w(xb[nb][e], 2 * hs + 1));
+          }
+      if (kb == a.NKB - 1 || r == nu - 1) {  // unit r closes a tile segment
+        const bool full_tile = seg_start == (int64_t)tile * a.NKB && kb == a.NKB - 1;
+        if (full_tile) {
+#pragma unroll
+          for (int b = 0; b < C::BLK; ++b)
+#pragma unroll
+            for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const int m = 8 * nb + 2 * t + (e & 1);
+                const int64_t col = (int64_t)tile * kTileCols + wi * C::CW + 16 * b + 8 * (e >> 1) + g;
+                if (m < a.M) a.out[m * a.out_ld + col] = __float2half_rn(up * acc[b][nb][e]);
+              }
+        } else {
+          // stream-K: partial (fragment order) -> own slot (0 = the participant's first segment,
+          // 1 = its last); the last of the tile's participants sums all partials in order.
+          const int slot = (seg_start == ub) ? 0 : 1;
+          float* mine = a.ws + ((size_t)p * 2 + slot) * (kNPad * kTileCols) + wi * (C::BLK * NB * 128) + lane;
+#pragma unroll
+          for (int b = 0; b < C::BLK; ++b)
+#pragma unroll
+            for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+              for (int e = 0; e < 4; ++e) __stcg(mine + ((b * NB + nb) * 4 + e) * 32, up * acc[b][nb][e]);
+          __threadfence();
+          named_bar(1 + set, WPS * 32);
+          const int c_first = cta_of_unit((int64_t)tile * a.NKB, a.U, P);
+          const int c_last = cta_of_unit((int64_t)(tile + 1) * a.NKB - 1, a.U, P);
+          if (wi == 0 && lane == 0) s_last[set] = (atomicAdd(a.cnt + tile, 1) == c_last - c_first);
+          named_bar(1 + set, WPS * 32);
+          if (s_last[set]) {
+            __threadfence();
+            float rs[C::BLK][NB][4];
+#pragma unroll
+            for (int b = 0; b < C::BLK; ++b)
+#pragma unroll
+              for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) rs[b][nb][e] = 0.f;
+            // participants in order; Q in flight per batch (independent L2 loads)
+            constexpr int Q = 8 / (C::BLK * NB) > 1 ? 8 / (C::BLK * NB) : 1;
+            for (int c0 = c_first; c0 <= c_last; c0 += Q) {
+              float v[Q][C::BLK][NB][4];
+#pragma unroll
+              for (int q = 0; q < Q; ++q) {
+                const int c = c0 + q <= c_last ? c0 + q : c_last;
+                const int cslot = (cta_start(c, a.U, P) / a.NKB == tile) ? 0 : 1;
+                const float* src = a.ws + ((size_t)c * 2 + cslot) * (kNPad * kTileCols) + wi * (C::BLK * NB * 128) + lane;
+#pragma unroll
+                for (int b = 0; b < C::BLK; ++b)
+#pragma unroll
+                  for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) v[q][b][nb][e] = __ldcg(src + ((b * NB + nb) * 4 + e) * 32);
+              }
+#pragma unroll
+              for (int q = 0; q < Q; ++q)
+                if (c0 + q <= c_last)
+#pragma unroll
+                  for (int b = 0; b < C::BLK; ++b)
+#pragma unroll
+                    for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+                      for (int e = 0; e < 4; ++e) rs[b][nb][e] += v[q][b][nb][e];
+            }
+#pragma unroll
+            for (int b = 0; b < C::BLK; ++b)
+#pragma unroll
+              for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const int m = 8 * nb + 2 * t + (e & 1);
+                  const int64_t col = (int64_t)tile * kTileCols + wi * C::CW + 16 * b + 8 * (e >> 1) + g;
+                  if (m < a.M) a.out[m * a.out_ld + col] = __float2half_rn(rs[b][nb][e]);
+                }
+            if (wi == 0 && lane == 0) a.cnt[tile] = 0;  // self-reset for the next launch / graph replay
+          }
+        }
+#pragma unroll
+        for (int b = 0; b < C::BLK; ++b)
+#pragma unroll
+          for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) acc[b][nb][e] = 0.f;
+        seg_start = ub + r + 1;
+      }
+      xp += kUnitK;
+      if (++kb == a.NKB) {
+        kb = 0;
+        ++tile;
+        xp -= (int64_t)a.NKB * kUnitK;
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------ A7: tensor-core path, M > 16
 // k_dqgemm<G, NB>: the same product for NB (64 / 128 / 256) activation rows per launch, where the
 // tensor pipe, not HBM, is the limit.  Same weight records and stream-K split
@@ -749,8 +1066,8 @@ __global__ void __launch_bounds__(kMmWarps * 32, 1) k_dqgemm(const GemmArgs a, c
       const int s = i % C::NS, b = i % C::NA;
       mbar_wait(full + s, (uint32_t)((i / C::NS) & 1));
       const uint8_t* st = smem + C::WRING + s * C::STAGE;
-      const uint4 c0 = *reinterpret_cast<const uint4*>(st + ((kh * 2 + 0) * kTileCols + col) * 16);
-      const uint4 c1 = *reinterpret_cast<const uint4*>(st + ((kh * 2 + 1) * kTileCols + col) * 16);
+      const uint4 c0 = *reinterpret_cast<const uint4*>(st + code_block(kh * 2 + 0, col) * 16);
+      const uint4 c1 = *reinterpret_cast<const uint4*>(st + code_block(kh * 2 + 1, col) * 16);
       const uint32_t wv[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
       __half2 zl[C::GPH], zh[C::GPH], sc[C::GPH];
 #pragma unroll
@@ -985,8 +1302,8 @@ __global__ void __launch_bounds__(TS<G, BN>::WARPS * 32, 1) k_dqgemm_ss(const Ss
         const int ws = t % C::NW, ks = t % C::NB;
         mbar_wait(w_full + ws, (uint32_t)((t / C::NW) & 1));
         const uint8_t* st = smem + C::WR + (ws * C::TPW + h) * C::STAGE;
-        const uint4 c0 = *reinterpret_cast<const uint4*>(st + ((kh * 2 + 0) * kTileCols + j) * 16);
-        const uint4 c1 = *reinterpret_cast<const uint4*>(st + ((kh * 2 + 1) * kTileCols + j) * 16);
+        const uint4 c0 = *reinterpret_cast<const uint4*>(st + code_block(kh * 2 + 0, j) * 16);
+        const uint4 c1 = *reinterpret_cast<const uint4*>(st + code_block(kh * 2 + 1, j) * 16);
         const uint32_t wv[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
         __half2 zl[C::GPH], zh[C::GPH], sc[C::GPH];
 #pragma unroll
@@ -1172,8 +1489,35 @@ cudaError_t launch_pdl(Kern k, dim3 grid, dim3 block, size_t smem, cudaStream_t 
   return cudaLaunchKernelEx(&cfg, k, args...);
 }
 
+#ifndef TPQ_RSETS
+#define TPQ_RSETS 4
+#endif
+#ifndef TPQ_RWPS
+#define TPQ_RWPS 4
+#endif
+constexpr int kRSets = TPQ_RSETS, kRWps = TPQ_RWPS;  // register-dequant GEMV: participants per CTA, warps per set
+static_assert(kRSets <= kGemvParts, "GEMV workspace holds kGemvParts participants per CTA");
+
+template <int G, int NB>
+bool prepare_r() {
+  using C = TR<G, NB, kRSets, kRWps>;
+  static_assert(C::SMEM + 64 <= 227 * 1024, "GEMV smem over the per-CTA limit");
+  static_assert(2 * C::SMEM > 228 * 1024, "GEMV is one CTA per SM");
+  if (cudaFuncSetAttribute(k_dqgemv_r<G, NB, kRSets, kRWps>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM) !=
+      cudaSuccess)
+    return false;
+  if (getenv("TPQ_VERBOSE")) {
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, k_dqgemv_r<G, NB, kRSets, kRWps>);
+    fprintf(stderr, "[tpq] k_dqgemv_r<%d,%d,%d,%d>: regs %d, local %zu, smem dyn %d (D=%d)\n", G, NB, kRSets, kRWps,
+            fa.numRegs, fa.localSizeBytes, C::SMEM, C::D);
+  }
+  return true;
+}
+
 template <int G>
 bool prepare_t() {
+  if (!prepare_r<G, 1>() || !prepare_r<G, 2>()) return false;
   constexpr int smem = TC<G>::SMEM;
   static_assert(smem <= 227 * 1024, "GEMV smem over the per-CTA limit");
   static_assert(2 * smem > 228 * 1024, "GEMV must be one CTA per SM (TMEM 512 columns)");
@@ -1339,18 +1683,50 @@ bool prepare_mm_g() {
   return ok;
 }
 
+// Every kernel of the forward prefers the maximum shared-memory carveout: consecutive kernels with
+// different L1/shared splits make the SM drain and reconfigure between them, which also defeats the
+// programmatic-dependent-launch overlap (the GEMV / GEMM kernels need ~210 KB anyway).
+template <class Kern>
+bool max_carveout(Kern k) {
+  return getenv("TPQ_NO_CARVEOUT") ||
+         cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared) ==
+             cudaSuccess;
+}
+template <int G>
+bool carveout_g() {
+  return max_carveout(k_dqgemv<G>) && max_carveout(k_dqgemv_r<G, 1, kRSets, kRWps>) &&
+         max_carveout(k_dqgemv_r<G, 2, kRSets, kRWps>) && max_carveout(k_dqgemm<G, 64>) &&
+         max_carveout(k_dqgemm<G, 128>) && max_carveout(k_dqgemm<G, 256>) && max_carveout(k_dqgemm_ss<G, 128>);
+}
+
 bool gemv_prepare(int G) {
+  if (!(max_carveout(k_gather_rm) && max_carveout(k_gather_rows) && max_carveout(k_mm_fixup) &&
+        max_carveout(k_ss_fixup) && max_carveout(k_sum_partials)))
+    return false;
+  if (!(G == 128 ? carveout_g<128>() : G == 64 ? carveout_g<64>() : G == 32 ? carveout_g<32>() : false)) return false;
   if (G == 128) return prepare_t<128>() && prepare_mm_g<128>();
   if (G == 64) return prepare_t<64>() && prepare_mm_g<64>();
   if (G == 32) return prepare_t<32>() && prepare_mm_g<32>();
   return false;
 }
 
-cudaError_t launch_gemv(const LayerDev& L, const CUtensorMap& xmap, int M, void* out, int64_t out_ld,
-                        cudaStream_t st) {
+template <int G>
+cudaError_t launch_r(const GemvArgs& a, cudaStream_t st) {
+  if (a.M <= 8) {
+    using C = TR<G, 1, kRSets, kRWps>;
+    return launch_pdl(k_dqgemv_r<G, 1, kRSets, kRWps>, dim3(a.grid), dim3(C::WARPS * 32), C::SMEM, st, a);
+  }
+  using C = TR<G, 2, kRSets, kRWps>;
+  return launch_pdl(k_dqgemv_r<G, 2, kRSets, kRWps>, dim3(a.grid), dim3(C::WARPS * 32), C::SMEM, st, a);
+}
+
+cudaError_t launch_gemv(const LayerDev& L, const CUtensorMap& xmap, const void* x, int64_t ldx, int M, void* out,
+                        int64_t out_ld, cudaStream_t st) {
   if (M < 1 || M > kMaxM) return cudaErrorInvalidValue;
   GemvArgs a;
   a.packed = L.packed;
+  a.x = reinterpret_cast<const __half*>(x);
+  a.ldx = ldx;
   a.M = M;
   a.NT = L.NT;
   a.NKB = L.NKB;
@@ -1361,6 +1737,19 @@ cudaError_t launch_gemv(const LayerDev& L, const CUtensorMap& xmap, int M, void*
   a.ws = L.ws;
   a.cnt = L.cnt;
   a.sshift = L.sshift;
+  // GEMV kernel choice: TPQ_GEMV=r / tc forces one; default tc (measured faster at every Llama /
+  // Granite shard size so far, profiles/r01_summary.md)
+  static const int pick = [] {
+    const char* e = getenv("TPQ_GEMV");
+    return !e ? 0 : e[0] == 'r' ? 1 : 2;
+  }();
+  const bool use_r = L.gemv == 2 || (L.gemv == 0 && pick == 1);
+  if (use_r) {
+    if (L.G == 128) return launch_r<128>(a, st);
+    if (L.G == 64) return launch_r<64>(a, st);
+    if (L.G == 32) return launch_r<32>(a, st);
+    return cudaErrorInvalidValue;
+  }
   if (L.G == 128) return launch_pdl(k_dqgemv<128>, dim3(a.grid), dim3(kGemvThreads), TC<128>::SMEM, st, a, xmap);
   if (L.G == 64) return launch_pdl(k_dqgemv<64>, dim3(a.grid), dim3(kGemvThreads), TC<64>::SMEM, st, a, xmap);
   if (L.G == 32) return launch_pdl(k_dqgemv<32>, dim3(a.grid), dim3(kGemvThreads), TC<32>::SMEM, st, a, xmap);

@@ -15,15 +15,17 @@ import synth  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--shape", default="llama70b")
 ap.add_argument("--m", type=int, default=1)
+ap.add_argument("--sim-tp", type=int, default=1)
 a = ap.parse_args()
 p = synth.make_named(a.shape, 16, 0)
 P1, _ = tpq.gptq_reorder(p.w1.g_idx, p.G)
 P2, _ = tpq.gptq_reorder(p.w2.g_idx, p.G)
-h = tpq.TpMlp(p.w1, p.w2, P1, P2, tp=1, M_max=16)
+R = 2 if a.sim_tp == 1 else 8  # rotate replicas: cold L2 as in bench.py
+hs = [tpq.TpMlp(p.w1, p.w2, P1, P2, tp=a.sim_tp, rank=0, M_max=16) for _ in range(R)]
 X = torch.from_numpy(p.X).cuda()
 Y = torch.empty(16, p.N2, dtype=torch.float16, device="cuda")
-for _ in range(10):
-    h.forward_local(X, a.m, Y)
+for i in range(10 * R + 1):
+    hs[i % R].forward_local(X, a.m, Y)
 torch.cuda.synchronize()
 L = tpq.lib()
 L.tpq_debug_cta.argtypes = [C.c_void_p]

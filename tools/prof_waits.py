@@ -15,12 +15,13 @@ import synth  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--shape", default="llama70b")
 ap.add_argument("--m", type=int, default=1)
+ap.add_argument("--sim-tp", type=int, default=1)
 ap.add_argument("--iters", type=int, default=20)
 a = ap.parse_args()
 p = synth.make_named(a.shape, 16, 0)
 P1, _ = tpq.gptq_reorder(p.w1.g_idx, p.G)
 P2, _ = tpq.gptq_reorder(p.w2.g_idx, p.G)
-h = tpq.TpMlp(p.w1, p.w2, P1, P2, tp=1, M_max=16)
+h = tpq.TpMlp(p.w1, p.w2, P1, P2, tp=a.sim_tp, rank=0, M_max=16)
 X = torch.from_numpy(p.X).cuda()
 Y = torch.empty(16, p.N2, dtype=torch.float16, device="cuda")
 L = tpq.lib()
