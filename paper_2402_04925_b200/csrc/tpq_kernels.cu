@@ -133,6 +133,21 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+// Stage release by lane 0 once every lane's shared-memory loads of the stage have returned: the
+// warp reduction reads each lane's `dep` (an XOR over all registers loaded from the stage), which
+// waits on those loads; the never-taken store keeps the reduction.  A plain __syncwarp + arrive
+// right after the loads let the producer's TMA overwrite a stage whose loads were still in flight
+// (run-to-run mismatches at M = 16, tools/stress_reg.py).
+__device__ __forceinline__ void release_loaded(uint64_t* bar, uint32_t dep, int lane, float* sink, int never) {
+  const uint32_t all = __reduce_or_sync(0xffffffffu, dep);
+  if (all == 0x9e3779b9u && never < 0) sink[threadIdx.x] = 0.f;
+  if (lane == 0) mbar_arrive(bar);
+}
+__device__ __forceinline__ int atom_add_acq_rel_gpu(int* p, int v) {
+  int old;
+  asm volatile("atom.add.acq_rel.gpu.global.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -409,8 +424,13 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_dqgemv(const GemvArgs a, co
         uint4 cw[4];
 #pragma unroll
         for (int c = 0; c < 4; ++c) cw[c] = *reinterpret_cast<const uint4*>(st + code_block(c, col) * 16);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(empty + s);
+        {
+          // release the weight stage early (releasing it after the dequant costs ~2 us per forward)
+          uint32_t dep = cw[0].x ^ cw[1].y ^ cw[2].z ^ cw[3].w;
+#pragma unroll
+          for (int g = 0; g < C::KG; ++g) dep ^= h2u(sl[g]) ^ h2u(zc[g]);
+          release_loaded(empty + s, dep, lane, a.ws, a.M);
+        }
 #ifdef TPQ_EXP_NODQ
         if (p >= C::NA) TPQ_W(done + (p - C::NA) % C::RD, (uint32_t)(((p - C::NA) / C::RD) & 1), 1);
         if (cw[0].x == 0x12345678u && cw[3].w == 0x9abcdef0u && sl[0].x == __half(0.f) && zc[0].y == __half(1.f)) a.ws[threadIdx.x] = 0.f;
@@ -507,14 +527,15 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_dqgemv(const GemvArgs a, co
 #pragma unroll
           for (int m = 0; m < kNPad; ++m)
             if (m < a.M) __stcg(mine + m * kTileCols + col, __uint_as_float(v[m]));
-          __threadfence();
+          // the 128 threads' partial stores are ordered before one acq_rel atomic by the named
+          // barrier (release cumulativity); the last arriver's acquire is passed on by the second
+          // barrier (the semaphore pattern of CUTLASS's generic barrier)
           named_bar(1, kTileCols);
           const int c_first = cta_of_unit((int64_t)tile * a.NKB, a.U, a.grid);
           const int c_last = cta_of_unit((int64_t)(tile + 1) * a.NKB - 1, a.U, a.grid);
-          if (col == 0) s_last = (atomicAdd(a.cnt + tile, 1) == c_last - c_first);
+          if (col == 0) s_last = (atom_add_acq_rel_gpu(a.cnt + tile, 1) == c_last - c_first);
           named_bar(1, kTileCols);
           if (s_last) {
-            __threadfence();
             float r[kNPad];
 #pragma unroll
             for (int m = 0; m < kNPad; ++m) r[m] = 0.f;
@@ -856,8 +877,7 @@ __global__ void __launch_bounds__(TR<G, NB, NSETS, WPS>::WARPS * 32, 1)
             zc[b][h] = u2h(vz);
           }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(empty_s + d);  // release: the stage is in registers
+      const int d_rel = d;
       if (++d == C::D) {
         d = 0;
         fph ^= 1u;
@@ -878,6 +898,11 @@ __global__ void __launch_bounds__(TR<G, NB, NSETS, WPS>::WARPS * 32, 1)
             for (int nb = 0; nb < NB; ++nb)
               hmma16816(acc[b][nb], a0, a1, a2, a3, u4w(xb[nb][e], 2 * hs), u4w(xb[nb][e], 2 * hs + 1));
           }
+      // release the stage only now: every value read from it has been consumed by an instruction
+      // above, so no shared-memory load of this warp can still be in flight when the producer's
+      // TMA overwrites it (releasing right after the loads raced at M = 16, tools/stress_reg.py)
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty_s + d_rel);
       if (kb == a.NKB - 1 || r == nu - 1) {  // unit r closes a tile segment
         const bool full_tile = seg_start == (int64_t)tile * a.NKB && kb == a.NKB - 1;
         if (full_tile) {
@@ -1080,8 +1105,12 @@ __global__ void __launch_bounds__(kMmWarps * 32, 1) k_dqgemm(const GemmArgs a, c
         zh[j] = __float2half2_rn((float)(-64 - z));
         sc[j] = __halves2half2(sv, sv);
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(empty + s);
+      {
+        uint32_t dep = c0.x ^ c0.w ^ c1.x ^ c1.w;
+#pragma unroll
+        for (int j = 0; j < C::GPH; ++j) dep ^= h2u(zl[j]) ^ h2u(sc[j]);
+        release_loaded(empty + s, dep, lane, a.ws, a.M);
+      }
       uint32_t r[32];
 #pragma unroll
       for (int w = 0; w < 8; ++w) {
@@ -1316,8 +1345,12 @@ __global__ void __launch_bounds__(TS<G, BN>::WARPS * 32, 1) k_dqgemm_ss(const Ss
           zh[g] = __float2half2_rn((float)(-64 - z));
           sc[g] = __halves2half2(sv, sv);
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(w_empty + ws);
+        {
+          uint32_t dep = c0.x ^ c0.w ^ c1.x ^ c1.w;
+#pragma unroll
+          for (int g = 0; g < C::GPH; ++g) dep ^= h2u(zl[g]) ^ h2u(sc[g]);
+          release_loaded(w_empty + ws, dep, lane, a.ws, a.M);
+        }
         if (t >= C::NB) mbar_wait(k_done + (t - C::NB) % C::KR, (uint32_t)(((t - C::NB) / C::KR) & 1));  // B slot free
         uint8_t* brow = smem + C::BR + ks * C::WT + kh * (BN * 128) + jj * 128;
 #pragma unroll

@@ -66,3 +66,31 @@ for layer in (0, 1):
         hi_ = np.array([x[1] for x in pairs])
         print(f"   SM pairs: {len(pairs)}; |dt| med {np.median(d):.2f} max {d.max():.2f}; first-finisher med "
               f"{np.median(lo_):.2f}, second med {np.median(hi_):.2f} max {hi_.max():.2f}")
+
+# correlate layer-1 end times with the CTA's stream-K range: offset of its first unit in its tile,
+# number of tile segments, whether it is the last arriver (fix-up) of its first / last tile
+if os.environ.get("TPQ_CTA_CORR"):
+    K1, N1 = p.K1, p.N1 // a.sim_tp
+    NKB, NT = K1 // 128, N1 // 128
+    U = NKB * NT
+    v = t[0]
+    grid = int((v[:, 0] > 0).sum())
+    t0 = v[:grid, 1].min()
+    ends = (v[:grid, 2] - t0) / 1e3
+    rows = []
+    for c in range(grid):
+        u0, u1 = c * U // grid, (c + 1) * U // grid
+        off = u0 % NKB
+        nseg = (u1 - 1) // NKB - u0 // NKB + 1
+        rows.append((ends[c], c, off, nseg, u1 - u0, (u1 - 1) % NKB))
+    rows.sort()
+    import collections
+    by = collections.defaultdict(list)
+    for e, c, off, nseg, n, last in rows:
+        by[nseg].append(e)
+    print("layer 1 end by #segments:", {k: (len(x), round(float(np.median(x)), 2)) for k, x in sorted(by.items())})
+    for e, c, off, nseg, n, last in rows[:8] + rows[-12:]:
+        print(f"  cta {c:3d} end {e:6.2f} first-kb {off:2d} last-kb {last:2d} segs {nseg} units {n}")
+    offs = np.array([r[2] for r in rows]); es = np.array([r[0] for r in rows])
+    print("corr(end, first-kb) =", round(float(np.corrcoef(offs, es)[0, 1]), 3),
+          " corr(end, last-kb) =", round(float(np.corrcoef(np.array([r[5] for r in rows]), es)[0, 1]), 3))
