@@ -539,12 +539,23 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_dqgemv(const GemvArgs a, co
             float r[kNPad];
 #pragma unroll
             for (int m = 0; m < kNPad; ++m) r[m] = 0.f;
+            // per contributor, all 16 row loads are issued before any add (rows >= M of a slot are
+            // allocated and ignored): predicated loads were compiled into two reused registers,
+            // i.e. 8 dependent L2 round trips per contributor at M = 16
             for (int c = c_first; c <= c_last; ++c) {
               const int cslot = (cta_start(c, a.U, a.grid) / a.NKB == tile) ? 0 : 1;
-              const float* src = a.ws + ((size_t)c * 2 + cslot) * (kNPad * kTileCols);
+              const float* src = a.ws + ((size_t)c * 2 + cslot) * (kNPad * kTileCols) + col;
+              float v2[kNPad];
+              if (a.M > 4) {
+#pragma unroll
+                for (int m = 0; m < kNPad; ++m) v2[m] = __ldcg(src + m * kTileCols);
+              } else {
+#pragma unroll
+                for (int m = 0; m < 4; ++m) v2[m] = __ldcg(src + m * kTileCols);
+              }
 #pragma unroll
               for (int m = 0; m < kNPad; ++m)
-                if (m < a.M) r[m] += __ldcg(src + m * kTileCols + col);
+                if (m < a.M) r[m] += v2[m];
             }
 #pragma unroll
             for (int m = 0; m < kNPad; ++m)

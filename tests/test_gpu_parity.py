@@ -250,6 +250,29 @@ def test_full_size_sampled(shape, M, kind):
     h.close()
 
 
+@KINDS
+def test_full_size_repeat_bit_identical(kind):
+    """Llama-70B layer 1 at M = 16, interleaved with full forwards: every repeat must be
+    bit-identical (fixed split-K order, reading c20).  Catches ring races: a stage released
+    before its loads returned made 24 of 60 repeats differ in the register GEMV."""
+    M = 16
+    p = synth.make_named("llama70b", M, seed=0)
+    P1, P2 = _prep(p)
+    h = _mlp(kind, p.w1, p.w2, P1, P2, M_max=16)
+    X = _dev(p.X)
+    Y = _empty(M, p.N2)
+    ref = _empty(M, p.N1)
+    h.layer1(X, M, ref)
+    for it in range(24):
+        if it % 2 == 0:
+            h.forward(X, M, Y)
+        Y1 = _empty(M, p.N1)
+        h.layer1(X, M, Y1)
+        torch.cuda.synchronize()
+        assert torch.equal(Y1, ref), f"repeat {it}: {(Y1 != ref).sum().item()} elements differ"
+    h.close()
+
+
 # ----------------------------------------------------------------------------- A7 (M > 16)
 @pytest.mark.parametrize("G", [32, 64, 128])
 @pytest.mark.parametrize("M", [17, 64, 100, 256, 300])
