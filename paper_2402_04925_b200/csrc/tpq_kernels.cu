@@ -539,23 +539,44 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_dqgemv(const GemvArgs a, co
             float r[kNPad];
 #pragma unroll
             for (int m = 0; m < kNPad; ++m) r[m] = 0.f;
-            // per contributor, all 16 row loads are issued before any add (rows >= M of a slot are
-            // allocated and ignored): predicated loads were compiled into two reused registers,
-            // i.e. 8 dependent L2 round trips per contributor at M = 16
-            for (int c = c_first; c <= c_last; ++c) {
-              const int cslot = (cta_start(c, a.U, a.grid) / a.NKB == tile) ? 0 : 1;
-              const float* src = a.ws + ((size_t)c * 2 + cslot) * (kNPad * kTileCols) + col;
-              float v2[kNPad];
-              if (a.M > 4) {
+            // Contributors in CTA order; every load of a batch is issued before any add (rows >= M
+            // of a slot are allocated and ignored): predicated per-row loads were compiled into two
+            // reused registers (8 dependent L2 round trips per contributor at M = 16), and one
+            // contributor per iteration costs one round trip each.  Batches: 4 contributors x 4
+            // rows for M <= 4, 2 x 16 rows otherwise.
+            auto slot_ptr = [&](int c) {
+              return a.ws + ((size_t)c * 2 + ((cta_start(c, a.U, a.grid) / a.NKB == tile) ? 0 : 1)) * (kNPad * kTileCols) + col;
+            };
+            if (a.M <= 4) {
+              for (int c = c_first; c <= c_last; c += 4) {
+                float v2[4][4];
 #pragma unroll
-                for (int m = 0; m < kNPad; ++m) v2[m] = __ldcg(src + m * kTileCols);
-              } else {
+                for (int q = 0; q < 4; ++q) {
+                  const float* src = slot_ptr(c + q <= c_last ? c + q : c_last);
 #pragma unroll
-                for (int m = 0; m < 4; ++m) v2[m] = __ldcg(src + m * kTileCols);
+                  for (int m = 0; m < 4; ++m) v2[q][m] = __ldcg(src + m * kTileCols);
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                  if (c + q <= c_last)
+#pragma unroll
+                    for (int m = 0; m < 4; ++m) r[m] += v2[q][m];
               }
+            } else {
+              for (int c = c_first; c <= c_last; c += 2) {
+                float v2[2][kNPad];
 #pragma unroll
-              for (int m = 0; m < kNPad; ++m)
-                if (m < a.M) r[m] += v2[m];
+                for (int q = 0; q < 2; ++q) {
+                  const float* src = slot_ptr(c + q <= c_last ? c + q : c_last);
+#pragma unroll
+                  for (int m = 0; m < kNPad; ++m) v2[q][m] = __ldcg(src + m * kTileCols);
+                }
+#pragma unroll
+                for (int q = 0; q < 2; ++q)
+                  if (c + q <= c_last)
+#pragma unroll
+                    for (int m = 0; m < kNPad; ++m) r[m] += v2[q][m];
+              }
             }
 #pragma unroll
             for (int m = 0; m < kNPad; ++m)
