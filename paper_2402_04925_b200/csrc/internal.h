@@ -30,6 +30,8 @@ constexpr int kUnitK = 128;         // weight rows per unit (8 MMAs of K = 16)
 constexpr int kNPad = 16;           // batch rows per MMA (tcgen05 M=128 needs N % 16 == 0)
 constexpr int kMaxM = 16;           // rows per forward chunk
 constexpr int kGemvParts = 4;       // max stream-K participants per GEMV CTA (workspace sizing)
+constexpr int kCntStride = 32;      // ints between stream-K tile counters: one 128-byte line each (the CTAs of
+                                    // all tiles hitting one line serialised their atomics: ~5 us per layer)
 constexpr int64_t unit_bytes_c(int G) { return (int64_t)kUnitK * kTileCols / 2 + 320LL * (kUnitK / G); }
 inline int64_t unit_bytes(int G) { return unit_bytes_c(G); }
 #ifdef __CUDACC__
@@ -52,7 +54,7 @@ struct LayerDev {
   float* ws = nullptr;     // [grid * kGemvParts][2 slots][16 * 128] fp32 stream-K partials (GEMV)
   float* ws_mm = nullptr;  // [grid][2 slots][256][128] fp32 stream-K partials (A7 GEMM)
   float* ws_ss = nullptr;  // [items][128][128] fp32 k-split partials (A7 SS GEMM, M >= 128)
-  int* cnt = nullptr;      // [NT] arrival counters (self-resetting)
+  int* cnt = nullptr;      // [NT * kCntStride] arrival counters, one per 128-byte line (self-resetting)
   int gemv = 0;            // GEMV kernel: 0 = from the TPQ_GEMV environment variable (default tcgen05), 1 = tcgen05, 2 = register-dequant
   int sshift = 0;          // GEMV operand shift e: smallest e >= 0 with max|s| 2^(24-e) <= 65504
 };

@@ -408,7 +408,7 @@ int tp_shard_mlp(const gptq_layer* w1, const gptq_layer* w2, const int32_t* P1, 
           return items * 128 * bn;
         };
         const size_t ws1s = ss_ws(h->L1), ws2s = ss_ws(h->L2);
-        const size_t ncnt = (size_t)(h->L1.NT + h->L2.NT);
+        const size_t ncnt = (size_t)(h->L1.NT + h->L2.NT) * tpq::kCntStride;
         if ((r = A(&h->d_w1, h->pk1.size())) || (r = A(&h->d_w2, h->pk2.size())) ||
             (r = A((void**)&h->d_P1, K1 * 4)) || (r = A((void**)&h->d_gcols, n * 4)) || (r = A(&h->d_x1, (size_t)h->rows * K1 * 2)) ||
             (r = A(&h->d_y1, (size_t)h->rows * n * 2)) || (r = A(&h->d_buf, (size_t)tp * h->rows * n * 2)) ||
@@ -437,7 +437,7 @@ int tp_shard_mlp(const gptq_layer* w1, const gptq_layer* w2, const int32_t* P1, 
         h->L1.ws_ss = ws1s ? h->d_ws + ws1 + ws2 + wm1 + wm2 : nullptr;
         h->L2.ws_ss = ws2s ? h->d_ws + ws1 + ws2 + wm1 + wm2 + ws1s : nullptr;
         h->L1.cnt = h->d_cnt;
-        h->L2.cnt = h->d_cnt + h->L1.NT;
+        h->L2.cnt = h->d_cnt + (size_t)h->L1.NT * tpq::kCntStride;
         TPQ_CUDA(cudaDeviceSynchronize());
         return TPQ_OK;
       };

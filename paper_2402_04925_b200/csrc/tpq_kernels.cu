@@ -325,6 +325,7 @@ struct GemvArgs {
   int64_t out_ld;
   float* ws;
   int* cnt;
+  int fixk;         // tcgen05 GEMV: 1 = split tiles are reduced by k_mm_fixup after the kernel (no atomics)
   int sshift;       // A = s (q - z) 2^-sshift (host: keeps s 2^(24 - sshift) in fp16 range); the
                     // epilogue multiplies the fp32 accumulator by 2^sshift
 };
@@ -527,14 +528,31 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_dqgemv(const GemvArgs a, co
 #pragma unroll
           for (int m = 0; m < kNPad; ++m)
             if (m < a.M) __stcg(mine + m * kTileCols + col, __uint_as_float(v[m]));
+          if (a.fixk) {  // reduced by k_mm_fixup after this kernel (its griddepcontrol.wait orders the stores)
+            ++seg;
+            seg_start = u0 + i + 1;
+            if (++kb == a.NKB) {
+              kb = 0;
+              ++tile;
+            }
+            continue;
+          }
           // the 128 threads' partial stores are ordered before one acq_rel atomic by the named
           // barrier (release cumulativity); the last arriver's acquire is passed on by the second
           // barrier (the semaphore pattern of CUTLASS's generic barrier)
           named_bar(1, kTileCols);
           const int c_first = cta_of_unit((int64_t)tile * a.NKB, a.U, a.grid);
           const int c_last = cta_of_unit((int64_t)(tile + 1) * a.NKB - 1, a.U, a.grid);
-          if (col == 0) s_last = (atom_add_acq_rel_gpu(a.cnt + tile, 1) == c_last - c_first);
+#ifdef TPQ_EXP_RELAXED
+          TPQ_EV(1, seg)
+          if (col == 0) s_last = 0;  // timing experiment only: no arrival count (wrong results)
+#else
+          if (col == 0) s_last = (atom_add_acq_rel_gpu(a.cnt + tile * kCntStride, 1) == c_last - c_first);
+#endif
           named_bar(1, kTileCols);
+#ifndef TPQ_EXP_RELAXED
+          TPQ_EV(1, seg)
+#endif
           if (s_last) {
             float r[kNPad];
 #pragma unroll
@@ -581,9 +599,10 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_dqgemv(const GemvArgs a, co
 #pragma unroll
             for (int m = 0; m < kNPad; ++m)
               if (m < a.M) a.out[m * a.out_ld + n] = __float2half_rn(r[m]);
-            if (col == 0) a.cnt[tile] = 0;  // self-reset for the next launch / graph replay
+            if (col == 0) a.cnt[tile * kCntStride] = 0;  // self-reset for the next launch / graph replay
           }
         }
+        TPQ_EV(2, seg)
         ++seg;
         seg_start = u0 + i + 1;
       }
@@ -599,8 +618,12 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_dqgemv(const GemvArgs a, co
     // griddepcontrol.wait, so they overlap the tail of the previous kernel (PDL).
     const uint64_t pw = policy_evict_first();
     TPQ_PDECL
+#ifndef TPQ_PRE
+#define TPQ_PRE 64
+#endif
     const int pre = nu < C::NS ? nu : C::NS;
     for (int i = 0; i < pre; ++i) {
+      if (i == TPQ_PRE) pdl_wait();  // records issued before the previous kernel completed: at most TPQ_PRE
       if (elect_one()) {
         mbar_arrive_expect_tx(full + i, C::UB);
         bulk_g2s(smem + C::WRING + i * C::STAGE, a.packed + (u0 + i) * C::UB, C::UB, full + i, pw);
@@ -963,7 +986,7 @@ __global__ void __launch_bounds__(TR<G, NB, NSETS, WPS>::WARPS * 32, 1)
           named_bar(1 + set, WPS * 32);
           const int c_first = cta_of_unit((int64_t)tile * a.NKB, a.U, P);
           const int c_last = cta_of_unit((int64_t)(tile + 1) * a.NKB - 1, a.U, P);
-          if (wi == 0 && lane == 0) s_last[set] = (atomicAdd(a.cnt + tile, 1) == c_last - c_first);
+          if (wi == 0 && lane == 0) s_last[set] = (atomicAdd(a.cnt + tile * kCntStride, 1) == c_last - c_first);
           named_bar(1 + set, WPS * 32);
           if (s_last[set]) {
             __threadfence();
@@ -1010,7 +1033,7 @@ __global__ void __launch_bounds__(TR<G, NB, NSETS, WPS>::WARPS * 32, 1)
                   const int64_t col = (int64_t)tile * kTileCols + wi * C::CW + 16 * b + 8 * (e >> 1) + g;
                   if (m < a.M) a.out[m * a.out_ld + col] = __float2half_rn(rs[b][nb][e]);
                 }
-            if (wi == 0 && lane == 0) a.cnt[tile] = 0;  // self-reset for the next launch / graph replay
+            if (wi == 0 && lane == 0) a.cnt[tile * kCntStride] = 0;  // self-reset for the next launch / graph replay
           }
         }
 #pragma unroll
@@ -1630,13 +1653,23 @@ __global__ void k_mm_fixup(const float* __restrict__ ws, int nb, int M, int NKB,
   const int m = blockIdx.y * 4 + (threadIdx.x >> 5), j = (threadIdx.x & 31) * 4;
   if (m >= M) return;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int c = c_first; c <= c_last; ++c) {
-    const int slot = (cta_start(c, U, grid) / NKB == t) ? 0 : 1;
-    const float4 v = __ldcg(reinterpret_cast<const float4*>(ws + (((size_t)c * 2 + slot) * nb + m) * kTileCols + j));
-    acc.x += v.x;
-    acc.y += v.y;
-    acc.z += v.z;
-    acc.w += v.w;
+  // contributors in CTA order, eight loads in flight per batch (one L2 round trip per batch)
+  for (int c0 = c_first; c0 <= c_last; c0 += 8) {
+    float4 v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int c = c0 + q <= c_last ? c0 + q : c_last;
+      const int slot = (cta_start(c, U, grid) / NKB == t) ? 0 : 1;
+      v[q] = __ldcg(reinterpret_cast<const float4*>(ws + (((size_t)c * 2 + slot) * nb + m) * kTileCols + j));
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (c0 + q <= c_last) {
+        acc.x += v[q].x;
+        acc.y += v[q].y;
+        acc.z += v[q].z;
+        acc.w += v[q].w;
+      }
   }
   const __half2 lo = __floats2half2_rn(acc.x, acc.y), hi = __floats2half2_rn(acc.z, acc.w);
   uint2 pk;
@@ -1790,6 +1823,7 @@ cudaError_t launch_gemv(const LayerDev& L, const CUtensorMap& xmap, const void* 
   if (M < 1 || M > kMaxM) return cudaErrorInvalidValue;
   GemvArgs a;
   a.packed = L.packed;
+  a.fixk = 0;
   a.x = reinterpret_cast<const __half*>(x);
   a.ldx = ldx;
   a.M = M;
@@ -1815,10 +1849,17 @@ cudaError_t launch_gemv(const LayerDev& L, const CUtensorMap& xmap, const void* 
     if (L.G == 32) return launch_r<32>(a, st);
     return cudaErrorInvalidValue;
   }
-  if (L.G == 128) return launch_pdl(k_dqgemv<128>, dim3(a.grid), dim3(kGemvThreads), TC<128>::SMEM, st, a, xmap);
-  if (L.G == 64) return launch_pdl(k_dqgemv<64>, dim3(a.grid), dim3(kGemvThreads), TC<64>::SMEM, st, a, xmap);
-  if (L.G == 32) return launch_pdl(k_dqgemv<32>, dim3(a.grid), dim3(kGemvThreads), TC<32>::SMEM, st, a, xmap);
-  return cudaErrorInvalidValue;
+  // split tiles: reduced by k_mm_fixup after the GEMV (default) or by the last-arriving CTA inside
+  // it (TPQ_INKERNEL_FIXUP=1): the in-kernel arrival atomic measured ~5 us at the end of each CTA
+  static const bool inkernel = getenv("TPQ_INKERNEL_FIXUP") != nullptr;
+  a.fixk = inkernel ? 0 : 1;
+  cudaError_t e = L.G == 128 ? launch_pdl(k_dqgemv<128>, dim3(a.grid), dim3(kGemvThreads), TC<128>::SMEM, st, a, xmap)
+                  : L.G == 64 ? launch_pdl(k_dqgemv<64>, dim3(a.grid), dim3(kGemvThreads), TC<64>::SMEM, st, a, xmap)
+                  : L.G == 32 ? launch_pdl(k_dqgemv<32>, dim3(a.grid), dim3(kGemvThreads), TC<32>::SMEM, st, a, xmap)
+                              : cudaErrorInvalidValue;
+  if (e != cudaSuccess || !a.fixk) return e;
+  return launch_pdl(k_mm_fixup, dim3((unsigned)L.NT, (unsigned)((M + 3) / 4)), dim3(128), 0, st, (const float*)L.ws, kNPad,
+                    M, L.NKB, L.U, L.grid, reinterpret_cast<__half*>(out), out_ld);
 }
 
 template <int G>

@@ -48,13 +48,18 @@ L.tpq_debug_trace.argtypes = [C.c_void_p]
 tr = (C.c_longlong * (24 * 64 * 4))()
 L.tpq_debug_trace(C.cast(tr, C.c_void_p))
 t = np.array(tr, dtype=np.int64).reshape(24, 64, 4)
-t0 = t[22, 16, 1] or t[22, 16, 0] or 1
+nz = t[t > 0]
+t0 = int(nz.min()) if nz.size else 1  # cycles relative to the first recorded event of CTA 0
 def f(w, i, e):
     return f"{t[w, i, e] - t0:7d}" if t[w, i, e] else "      -"
 print("pair | prod W(2p) | stage | deq(set p%2 w0, unit 2p): full computed Afree | arrive | mma: d_empty a_full xfull issued | epi: done s_full d_empty_arr")
-for pp in range(5, 22):
+for pp in range(0 if a.sim_tp > 1 else 5, 8 if a.sim_tp > 1 else 22):
     i = 2 * pp
     dw = 0 if pp % 2 == 0 else 8
     mw = 22 + pp % 2
     print(f"{pp:4d} | {f(20, i, 0)} | {f(21, i, 0)} | {f(dw, i, 0)} {f(dw, i, 1)} {f(dw, i, 2)} | {f(dw, i, 3)} | "
           f"{f(mw, i, 0)} {f(mw, i, 1)} {f(mw, i, 2)} {f(mw, i, 3)} | {f(16, i, 0)} {f(16, i, 1)} {f(16, i, 2)}")
+
+print("epilogue (warp 16) per segment: d_full landed | partial+atomic done | segment done")
+for sg in range(4):
+    print(f"  seg {sg}: {f(16, sg, 0)} {f(16, sg, 1)} {f(16, sg, 2)}")
