@@ -382,7 +382,7 @@ def main():
                           "frac": step_bytes / (ms_per_step * 1e-3) / 1e9 / peak},
         "e2e": None if sim_tp else {"value": e2e_ms * 1e3, "unit": "us", "h2d_bytes_per_step": 2 * M * K1,
                                     "d2h_bytes_per_step": 2 * M * N2},
-        "gpu_launches": K * 3 + (K if variant == tpq.TPQ_NAIVE else 0),
+        "gpu_launches": K * launches_per_step(M, variant == tpq.TPQ_NAIVE),
         "clocks": clk,
     }
     if world > 1 and variant == tpq.TPQ_TP_AWARE and not a.no_naive:
@@ -410,6 +410,15 @@ def main():
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def launches_per_step(M, naive):
+    """Our kernels per forward (M <= 16): X[:, P1] gather, per layer the GEMV plus (tcgen05 GEMV)
+    its split-tile fix-up kernel, and the naive path's P2 gather; NCCL kernels not counted."""
+    reg = os.environ.get("TPQ_GEMV", "").startswith("r")
+    fix = 0 if (reg or os.environ.get("TPQ_INKERNEL_FIXUP")) else 1
+    per_layer = 1 + fix if M <= 16 else 2
+    return 1 + 2 * per_layer + (1 if naive else 0)
 
 
 def time_naive(a, p, P1, P2, tp, rank, local, R, comm, X, Y, stream, sync_all, world, dev, ours_ms):
