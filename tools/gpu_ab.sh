@@ -1,3 +1,3 @@
-for e in "" 1; do for tp in 1 8; do
-echo "inkernel=$e tp=$tp $(env ${e:+TPQ_INKERNEL_FIXUP=1} timeout 200 python tools/fwd_time.py --sim-tp $tp --ms 1,2,3,4,5,8,12,16 2>&1 | tail -1)"
-done; done
+for rep in 1 2; do for v in "" _evn; do for tp in 1 8; do
+echo "$v tp=$tp $(TPQ_LIB_PATH=paper_2402_04925_b200/libtpq$v.so timeout 200 python tools/fwd_time.py --sim-tp $tp --ms 1,16 2>&1 | tail -1)"
+done; done; done
