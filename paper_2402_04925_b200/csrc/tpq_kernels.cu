@@ -1653,13 +1653,14 @@ __global__ void k_mm_fixup(const float* __restrict__ ws, int nb, int M, int NKB,
   const int m = blockIdx.y * 4 + (threadIdx.x >> 5), j = (threadIdx.x & 31) * 4;
   if (m >= M) return;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  const int s_first = cta_start(c_first, U, grid) == (int64_t)t * NKB ? 0 : 1;  // see k_gemv_fixup
   // contributors in CTA order, eight loads in flight per batch (one L2 round trip per batch)
   for (int c0 = c_first; c0 <= c_last; c0 += 8) {
     float4 v[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const int c = c0 + q <= c_last ? c0 + q : c_last;
-      const int slot = (cta_start(c, U, grid) / NKB == t) ? 0 : 1;
+      const int slot = c > c_first ? 0 : s_first;
       v[q] = __ldcg(reinterpret_cast<const float4*>(ws + (((size_t)c * 2 + slot) * nb + m) * kTileCols + j));
     }
 #pragma unroll
@@ -1676,6 +1677,70 @@ __global__ void k_mm_fixup(const float* __restrict__ ws, int nb, int M, int NKB,
   pk.x = *reinterpret_cast<const uint32_t*>(&lo);
   pk.y = *reinterpret_cast<const uint32_t*>(&hi);
   *reinterpret_cast<uint2*>(out + (int64_t)m * out_ld + (int64_t)t * kTileCols + j) = pk;
+}
+
+// GEMV stream-K fix-up (tcgen05 GEMV, partial slots [grid][2][16][128]): block t sums tile t's
+// contributors in CTA order, one thread per column, every load of a batch in flight before any add
+// (16 contributors for M = 1, 4 contributors x 4 rows for M <= 4, else 2 x 16).  Used for M <= 4,
+// where k_mm_fixup (one warp per row) cost ~1 us per extra row; k_mm_fixup is faster for M > 4.
+__global__ void __launch_bounds__(128) k_gemv_fixup(const float* __restrict__ ws, int M, int NKB, int64_t U, int grid,
+                                                    __half* __restrict__ out, int64_t out_ld) {
+  pdl_launch_dependents();
+  pdl_wait();  // the partials come from the GEMV just before
+  const int t = blockIdx.x, col = threadIdx.x;
+  const int c_first = cta_of_unit((int64_t)t * NKB, U, grid), c_last = cta_of_unit((int64_t)(t + 1) * NKB - 1, U, grid);
+  if (c_first == c_last) return;  // the tile lies inside one CTA's range: written by the GEMV
+  // slot of contributor c: every CTA after c_first starts inside tile t (slot 0, its first segment);
+  // c_first's slot is 0 only if its range starts exactly at the tile (no 64-bit division per load)
+  const int s_first = cta_start(c_first, U, grid) == (int64_t)t * NKB ? 0 : 1;
+  auto slot_ptr = [&](int c) { return ws + ((size_t)c * 2 + (c > c_first ? 0 : s_first)) * (kNPad * kTileCols) + col; };
+  float r[kNPad];
+#pragma unroll
+  for (int m = 0; m < kNPad; ++m) r[m] = 0.f;
+  if (M == 1) {
+    for (int c = c_first; c <= c_last; c += 16) {
+      float v[16];
+#pragma unroll
+      for (int q = 0; q < 16; ++q) v[q] = __ldcg(slot_ptr(c + q <= c_last ? c + q : c_last));
+#pragma unroll
+      for (int q = 0; q < 16; ++q)
+        if (c + q <= c_last) r[0] += v[q];
+    }
+  } else if (M <= 4) {
+    for (int c = c_first; c <= c_last; c += 4) {
+      float v[4][4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float* src = slot_ptr(c + q <= c_last ? c + q : c_last);
+#pragma unroll
+        for (int m = 0; m < 4; ++m) v[q][m] = __ldcg(src + m * kTileCols);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (c + q <= c_last)
+#pragma unroll
+          for (int m = 0; m < 4; ++m) r[m] += v[q][m];
+    }
+  } else {
+    for (int c = c_first; c <= c_last; c += 2) {
+      float v[2][kNPad];
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const float* src = slot_ptr(c + q <= c_last ? c + q : c_last);
+#pragma unroll
+        for (int m = 0; m < kNPad; ++m) v[q][m] = __ldcg(src + m * kTileCols);
+      }
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+        if (c + q <= c_last)
+#pragma unroll
+          for (int m = 0; m < kNPad; ++m) r[m] += v[q][m];
+    }
+  }
+  __half* o = out + (int64_t)t * kTileCols + col;
+#pragma unroll
+  for (int m = 0; m < kNPad; ++m)
+    if (m < M) o[m * out_ld] = __float2half_rn(r[m]);
 }
 
 // X[:, idx] for the layer-1 operand: CTA (m, part) reads row m into shared memory with coalesced
@@ -1798,7 +1863,7 @@ bool carveout_g() {
 }
 
 bool gemv_prepare(int G) {
-  if (!(max_carveout(k_gather_rm) && max_carveout(k_gather_rows) && max_carveout(k_mm_fixup) &&
+  if (!(max_carveout(k_gather_rm) && max_carveout(k_gather_rows) && max_carveout(k_mm_fixup) && max_carveout(k_gemv_fixup) &&
         max_carveout(k_ss_fixup) && max_carveout(k_sum_partials)))
     return false;
   if (!(G == 128 ? carveout_g<128>() : G == 64 ? carveout_g<64>() : G == 32 ? carveout_g<32>() : false)) return false;
@@ -1858,6 +1923,11 @@ cudaError_t launch_gemv(const LayerDev& L, const CUtensorMap& xmap, const void* 
                   : L.G == 32 ? launch_pdl(k_dqgemv<32>, dim3(a.grid), dim3(kGemvThreads), TC<32>::SMEM, st, a, xmap)
                               : cudaErrorInvalidValue;
   if (e != cudaSuccess || !a.fixk) return e;
+  // M <= 4: one thread per column, all contributors' rows in flight (k_gemv_fixup); M > 4: one warp
+  // per row, float4 per lane (k_mm_fixup), measured faster there
+  if (M <= 4)
+    return launch_pdl(k_gemv_fixup, dim3((unsigned)L.NT), dim3(128), 0, st, (const float*)L.ws, M, L.NKB, L.U, L.grid,
+                      reinterpret_cast<__half*>(out), out_ld);
   return launch_pdl(k_mm_fixup, dim3((unsigned)L.NT, (unsigned)((M + 3) / 4)), dim3(128), 0, st, (const float*)L.ws, kNPad,
                     M, L.NKB, L.U, L.grid, reinterpret_cast<__half*>(out), out_ld);
 }
