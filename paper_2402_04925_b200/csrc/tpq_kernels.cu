@@ -1754,13 +1754,22 @@ __global__ void k_gather_rows(const __half* __restrict__ src, int64_t ld, const 
   pdl_wait();
   const int m = blockIdx.x;
   const __half* row = src + (int64_t)m * ld;
+  const int64_t nc = K / 8, c0 = nc * blockIdx.y / gridDim.y, c1 = nc * (blockIdx.y + 1) / gridDim.y;
+  // the first chunk's indices are requested before the row stage and the barrier, so the two L2
+  // round trips overlap (usually the only chunk of a thread)
+  int4 n0 = make_int4(0, 0, 0, 0), n1 = n0;
+  if (c0 + threadIdx.x < c1) {
+    n0 = __ldg(reinterpret_cast<const int4*>(idx) + 2 * (c0 + threadIdx.x));
+    n1 = __ldg(reinterpret_cast<const int4*>(idx) + 2 * (c0 + threadIdx.x) + 1);
+  }
   for (int64_t c = threadIdx.x; c < K / 8; c += blockDim.x)
     reinterpret_cast<uint4*>(srow)[c] = __ldg(reinterpret_cast<const uint4*>(row) + c);
   __syncthreads();
   __half* out = dst + (int64_t)m * K;
-  const int64_t nc = K / 8, c0 = nc * blockIdx.y / gridDim.y, c1 = nc * (blockIdx.y + 1) / gridDim.y;
   for (int64_t c = c0 + threadIdx.x; c < c1; c += blockDim.x) {
-    const int4 i0 = __ldg(reinterpret_cast<const int4*>(idx) + 2 * c), i1 = __ldg(reinterpret_cast<const int4*>(idx) + 2 * c + 1);
+    const bool first = c == c0 + threadIdx.x;
+    const int4 i0 = first ? n0 : __ldg(reinterpret_cast<const int4*>(idx) + 2 * c);
+    const int4 i1 = first ? n1 : __ldg(reinterpret_cast<const int4*>(idx) + 2 * c + 1);
     uint4 pk;
     pk.x = (uint32_t)__half_as_ushort(srow[i0.x]) | ((uint32_t)__half_as_ushort(srow[i0.y]) << 16);
     pk.y = (uint32_t)__half_as_ushort(srow[i0.z]) | ((uint32_t)__half_as_ushort(srow[i0.w]) << 16);
