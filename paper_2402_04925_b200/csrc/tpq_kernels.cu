@@ -543,16 +543,9 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_dqgemv(const GemvArgs a, co
           named_bar(1, kTileCols);
           const int c_first = cta_of_unit((int64_t)tile * a.NKB, a.U, a.grid);
           const int c_last = cta_of_unit((int64_t)(tile + 1) * a.NKB - 1, a.U, a.grid);
-#ifdef TPQ_EXP_RELAXED
-          TPQ_EV(1, seg)
-          if (col == 0) s_last = 0;  // timing experiment only: no arrival count (wrong results)
-#else
           if (col == 0) s_last = (atom_add_acq_rel_gpu(a.cnt + tile * kCntStride, 1) == c_last - c_first);
-#endif
           named_bar(1, kTileCols);
-#ifndef TPQ_EXP_RELAXED
           TPQ_EV(1, seg)
-#endif
           if (s_last) {
             float r[kNPad];
 #pragma unroll
