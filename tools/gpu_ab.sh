@@ -1,4 +1,3 @@
-timeout 800 python -m pytest tests -q -m gpu 2>&1 | tail -1
-for rep in 1 2; do for v in "" _old; do for tp in 1 8; do
-echo "$v tp=$tp $(TPQ_LIB_PATH=paper_2402_04925_b200/libtpq$v.so timeout 200 python tools/fwd_time.py --sim-tp $tp --ms 1,16 2>&1 | tail -1)"
-done; done; done
+for g in 148 120 96 74; do for tp in 4 8; do
+echo "grid=$g tp=$tp $(TPQ_GRID=$g timeout 200 python tools/fwd_time.py --sim-tp $tp --ms 1,16 2>&1 | tail -1)"
+done; done
