@@ -50,9 +50,10 @@ struct LayerDev {
   int64_t K = 0, N = 0;
   int G = 0, NT = 0, NKB = 0;
   int64_t U = 0;           // NT * NKB units
-  int grid = 0;            // persistent CTAs (stream-K), one per SM
+  int grid = 0;            // persistent CTAs of the M <= 16 GEMV (stream-K), at most one per SM
+  int grid_mm = 0;         // persistent CTAs of the A7 k_dqgemm (every SM)
   float* ws = nullptr;     // [grid * kGemvParts][2 slots][16 * 128] fp32 stream-K partials (GEMV)
-  float* ws_mm = nullptr;  // [grid][2 slots][256][128] fp32 stream-K partials (A7 GEMM)
+  float* ws_mm = nullptr;  // [grid_mm][2 slots][256][128] fp32 stream-K partials (A7 GEMM)
   float* ws_ss = nullptr;  // [items][128][128] fp32 k-split partials (A7 SS GEMM, M >= 128)
   int* cnt = nullptr;      // [NT * kCntStride] arrival counters, one per 128-byte line (self-resetting)
   int gemv = 0;            // GEMV kernel: 0 = from the TPQ_GEMV environment variable (default tcgen05), 1 = tcgen05, 2 = register-dequant

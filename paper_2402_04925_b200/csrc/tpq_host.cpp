@@ -251,9 +251,16 @@ void plan_layer(tpq::LayerDev& L, int64_t K, int64_t N, int G, int device) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     tpq::gemv_prepare(G);
   }
-  if (const char* e = getenv("TPQ_GRID")) sms = std::max(1, std::min(sms, atoi(e)));  // tuning aid
   const int64_t cap = std::max<int64_t>(1, L.U / 4);
-  L.grid = (int)std::min<int64_t>((int64_t)sms, cap);
+  // Small shards (< 64 units per SM: Llama / Granite at TP >= 2) are latency-bound, not
+  // bandwidth-bound: 128 of 148 CTAs measured 1-3.5 us faster per forward there (the next kernel
+  // can start on SMs the previous one has already left), while full-size layers need every SM
+  // (profiles/r01_summary.md, grid sweep).
+  int g = sms;
+  if (L.U < 64LL * sms) g = std::max(1, sms * 128 / 148);
+  if (const char* e = getenv("TPQ_GRID")) g = std::max(1, std::min(sms, atoi(e)));  // tuning aid
+  L.grid = (int)std::min<int64_t>((int64_t)g, cap);
+  L.grid_mm = (int)std::min<int64_t>((int64_t)sms, cap);
   if (getenv("TPQ_VERBOSE"))
     fprintf(stderr, "[tpq] layer K=%lld N=%lld G=%d: grid %d over %lld units\n", (long long)K, (long long)N, G,
             L.grid, (long long)L.U);
@@ -394,8 +401,8 @@ int tp_shard_mlp(const gptq_layer* w1, const gptq_layer* w2, const int32_t* P1, 
         const size_t ws1 = (size_t)h->L1.grid * tpq::kGemvParts * 2 * tpq::kNPad * tpq::kTileCols;
         const size_t ws2 = (size_t)h->L2.grid * tpq::kGemvParts * 2 * tpq::kNPad * tpq::kTileCols;
         h->rows = M_max > tpq::kMaxM ? kGemmRows : tpq::kMaxM;
-        const size_t wm1 = M_max > tpq::kMaxM ? (size_t)h->L1.grid * 2 * kGemmRows * tpq::kTileCols : 0;
-        const size_t wm2 = M_max > tpq::kMaxM ? (size_t)h->L2.grid * 2 * kGemmRows * tpq::kTileCols : 0;
+        const size_t wm1 = M_max > tpq::kMaxM ? (size_t)h->L1.grid_mm * 2 * kGemmRows * tpq::kTileCols : 0;
+        const size_t wm2 = M_max > tpq::kMaxM ? (size_t)h->L2.grid_mm * 2 * kGemmRows * tpq::kTileCols : 0;
         cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, device);
         auto ss_ws = [&](const tpq::LayerDev& L) -> size_t {  // largest k-split partial set (M >= 128 passes)
           if (M_max < 128) return 0;

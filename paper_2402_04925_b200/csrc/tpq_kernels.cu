@@ -1951,7 +1951,7 @@ cudaError_t launch_gemm(const LayerDev& L, const CUtensorMap& xmap, int nb, int 
   a.NT = L.NT;
   a.NKB = L.NKB;
   a.U = L.U;
-  a.grid = L.grid;
+  a.grid = L.grid_mm;
   a.out = reinterpret_cast<__half*>(out);
   a.out_ld = out_ld;
   a.ws = L.ws_mm;
@@ -1962,7 +1962,7 @@ cudaError_t launch_gemm(const LayerDev& L, const CUtensorMap& xmap, int nb, int 
                               : cudaErrorInvalidValue;
   if (e != cudaSuccess) return e;
   return launch_pdl(k_mm_fixup, dim3((unsigned)L.NT, (unsigned)((M + 3) / 4)), dim3(128), 0, st, (const float*)L.ws_mm,
-                    nb, M, L.NKB, L.U, L.grid, reinterpret_cast<__half*>(out), out_ld);
+                    nb, M, L.NKB, L.U, L.grid_mm, reinterpret_cast<__half*>(out), out_ld);
 }
 
 template <int G, int BN>
