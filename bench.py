@@ -45,7 +45,9 @@ def parse():
     ap.add_argument("--variant", default="tp_aware", choices=["tp_aware", "naive"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--seed", type=int, default=0)
-    ap.add_argument("--sweep", action="store_true", help="also time M=1,4 (extra 'sweep' key)")
+    ap.add_argument("--sweep", action="store_true",
+                    help="N = 1: add graph-timed step latencies at M = 1/4/8/16 (key sweep_us_by_M; runs after "
+                         "the timed region, so power-capped boxes may report it slower)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-naive", action="store_true", help="N > 1: skip timing the naive AllGather path")
     ap.add_argument("--no-graph", action="store_true", help="launch every step eagerly (no CUDA graph)")
@@ -393,8 +395,8 @@ def main():
                                                  sync_all, world, dev, ms_per_step)
         except Exception as e:  # report, keep the TP-aware line
             line["naive_allgather"] = {"error": f"{type(e).__name__}: {e}"}
-    if rank == 0 and a.sweep:
-        line["sweep"] = sweep_m(hs, p, R, stream, dev, sim_tp)
+    if world == 1 and a.sweep:  # (collective forwards at N > 1 would need every rank)
+        line["sweep_us_by_M"] = sweep_m(hs, p, R, stream, dev, sim_tp)
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         den = 4 if a.shape != "tiny" else 1
         t = oracle_sample_time(synth.make_named(a.shape, M, a.seed), den)
@@ -464,22 +466,32 @@ def time_naive(a, p, P1, P2, tp, rank, local, R, comm, X, Y, stream, sync_all, w
 
 
 def sweep_m(hs, p, R, stream, dev, sim_tp):
+    """Step latency (us) at M = 1, 4, 8, 16 on the same handles: CUDA graphs of R * k forwards
+    (rotating the cold weight replicas) replayed after warm-up, as in the main timed region."""
     import torch
     out = {}
+    per = R * max(1, 16 // R)
     for M in (1, 4, 8, 16):
         X = torch.from_numpy(p.X[:M].copy()).to(dev)
         Y = torch.empty(M, p.N2, dtype=torch.float16, device=dev)
         f = (lambda h: h.forward_local(X, M, Y, stream=stream)) if sim_tp else (lambda h: h.forward(X, M, Y, stream=stream))
         with torch.cuda.stream(stream):
-            for i in range(50):
+            for i in range(per):
                 f(hs[i % R])
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=stream):
+                for i in range(per):
+                    f(hs[i % R])
+            for _ in range(5):
+                g.replay()
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            reps = max(1, 2000 // per)
             s.record(stream)
-            for i in range(1000):
-                f(hs[i % R])
+            for _ in range(reps):
+                g.replay()
             e.record(stream)
         torch.cuda.synchronize(dev)
-        out[str(M)] = s.elapsed_time(e)  # ms per 1000 = us per step
+        out[str(M)] = s.elapsed_time(e) * 1e3 / (reps * per)
     return out
 
 
