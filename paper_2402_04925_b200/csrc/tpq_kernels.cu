@@ -992,12 +992,14 @@ __global__ void __launch_bounds__(TR<G, NB, NSETS, WPS>::WARPS * 32, 1)
                 for (int e = 0; e < 4; ++e) rs[b][nb][e] = 0.f;
             // participants in order; Q in flight per batch (independent L2 loads)
             constexpr int Q = 8 / (C::BLK * NB) > 1 ? 8 / (C::BLK * NB) : 1;
+            // slot of participant c: every participant after c_first starts inside the tile (slot 0)
+            const int s_first = cta_start(c_first, a.U, P) == (int64_t)tile * a.NKB ? 0 : 1;
             for (int c0 = c_first; c0 <= c_last; c0 += Q) {
               float v[Q][C::BLK][NB][4];
 #pragma unroll
               for (int q = 0; q < Q; ++q) {
                 const int c = c0 + q <= c_last ? c0 + q : c_last;
-                const int cslot = (cta_start(c, a.U, P) / a.NKB == tile) ? 0 : 1;
+                const int cslot = c > c_first ? 0 : s_first;
                 const float* src = a.ws + ((size_t)c * 2 + cslot) * (kNPad * kTileCols) + wi * (C::BLK * NB * 128) + lane;
 #pragma unroll
                 for (int b = 0; b < C::BLK; ++b)
