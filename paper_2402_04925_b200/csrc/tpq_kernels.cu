@@ -63,6 +63,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 // Wait with a suspend-time hint: the warp sleeps until the phase completes (or the hint, in ns,
 // expires) instead of spinning try_wait / branch / yield through the issue slots of busy warps.
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+#ifdef TPQ_NOSLEEP
+  mbar_wait(bar, parity);
+  return;
+#endif
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "TPQ_WAITS_%=:\n\t"
@@ -71,6 +75,35 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
       "r"(parity), "r"(1000000)
       : "memory");
 }
+// Wait for a phase expected to take many microseconds (e.g. a whole tile segment): back off with
+// __nanosleep between try_waits.  A plain try_wait loop returns after a short hardware window whatever
+// the suspend hint, and its retries compete for issue slots with the warps doing the work
+// (profiles/r02_summary.md: the epilogue's d_full loop was 12 % of all issued instructions).
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity, unsigned ns) {
+  if (ns == 0) {
+    mbar_wait(bar, parity);
+    return;
+  }
+  while (!mbar_try(bar, parity)) __nanosleep(ns);
+}
+#ifndef TPQ_EPI_NS
+#define TPQ_EPI_NS 256
+#endif
+#ifndef TPQ_MMA_NS
+#define TPQ_MMA_NS 0
+#endif
+#ifndef TPQ_DONE_NS
+#define TPQ_DONE_NS 0
+#endif
 // Per-CTA timeline (build with -DTPQ_PROF; profiling aid, not in the product build): entry,
 // work start, end (globaltimer ns) and SM id per CTA, per layer (N > K selects the slot).
 #ifdef TPQ_PROF
@@ -734,6 +767,333 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_dqgemv(const GemvArgs a, co
   __syncthreads();
   if (threadIdx.x == 0) { TPQ_CTA(2, gtime()) }
   if (warp == kMmaWarp) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::TCOLS) : "memory");
+  }
+}
+
+// ------------------------------------------------------------------ GEMV v2 (M <= 16), lean issue
+// Same records, operand arithmetic, MMA issue and stream-K split as k_dqgemv; what changes is the
+// instruction count per unit, which ncu showed to be the limit (profiles/r02_summary.md: 1521 warp
+// instructions per 128 x 128 unit = 380 per SMSP against the ~378 cycles one unit may take at HBM
+// speed; the dequant loop alone ~250 per warp-unit for ~150 of conversion):
+//   * dequant in THREE sets of FOUR warps (one per SMSP / TMEM lane quarter); a warp converts its
+//     32 columns of BOTH units of a pair per iteration, so waits, hand-offs and index arithmetic are
+//     paid once per pair; set s owns TMEM A buffer s and the pairs p = s, s + 3, ...;
+//   * a weight stage is released right after the warp's last tcgen05.st of the unit (every loaded
+//     register has been consumed by then: no reduction guard);
+//   * the epilogue walks tile segments, not units.
+// Warps 0-3 epilogue, 4-15 dequant, 16 TMA producer, 17 activation stager, 18-19 MMA issuers: the
+// SMSP arbiter prefers higher warp ids, so the warps that only wait sit lowest.
+constexpr int kV2Sets = 3, kV2Deq0 = 4, kV2Prod = 16, kV2Stage = 17, kV2Mma = 18;
+constexpr int kV2Threads = 20 * 32;
+
+template <int G>
+struct TC2 {
+  static constexpr int KG = kUnitK / G;
+  static constexpr int UB = (int)unit_bytes_c(G);
+  static constexpr int STAGE = (UB + 127) / 128 * 128;
+  static constexpr int NS = 18;                   // weight ring stages (units)
+  static constexpr int XU = kNPad * kUnitK * 2;   // activation bytes per unit
+  static constexpr int NX = 6;                    // activation pair slots
+  static constexpr int AU = kUnitK / 2;           // TMEM columns per unit of A
+  static constexpr int RD = 6;                    // done ring: pair p on p % 6
+  // a_full(p) on barrier p % NAF: the previous completion there, pair p - 6, had the same MMA issuer
+  // (p % 2) and dequant set (p % 3), so the waiter consumed it before; with 3 barriers the issuer of
+  // pair p could find pair p - 3's phase (other issuer) still open and read the one before it.
+  static constexpr int NAF = 6;
+  // done(p) on barrier p % RD.  Dequant set p % 3 waits done(p - 3) before overwriting its buffer:
+  // the next completion there, p + 3, needs this set's own a_full(p + 3).  The stager waits
+  // done(p - NX) before reusing slot p % NX: the next one, p - NX + RD >= p, needs its own later load.
+  static_assert(RD % kV2Sets == 0 && RD >= NX, "done ring aliasing");
+  static constexpr int TCOLS = 512;
+  static constexpr int DC = 4 * kNPad;            // [2 segment buffers][2 issuers] x 16 columns
+  static_assert(DC + kV2Sets * 2 * AU <= TCOLS, "TMEM budget");
+  static constexpr int XRING = 0;
+  static constexpr int WRING = NX * 2 * XU;
+  static constexpr int BARS = WRING + NS * STAGE;
+  static constexpr int SMEM = BARS + 8 * (2 * NS + NX + NAF + RD + 4);
+};
+
+template <int G>
+__global__ void __launch_bounds__(kV2Threads, 1) k_dqgemv2(const GemvArgs a, const __grid_constant__ CUtensorMap xmap) {
+  using C = TC2<G>;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BARS);
+  uint64_t* full = bars;                // [NS] weight record landed
+  uint64_t* empty = full + C::NS;       // [NS] the 4 warps converting the unit are done with it
+  uint64_t* xfull = empty + C::NS;      // [NX] the pair's activation slices landed
+  uint64_t* a_full = xfull + C::NX;     // [NAF] pair p's A operands stored (the 4 warps of set p % 3)
+  uint64_t* done = a_full + C::NAF;     // [RD] pair p's MMAs completed (tcgen05.commit)
+  uint64_t* d_full = done + C::RD;      // [2] segment accumulators final (both issuers)
+  uint64_t* d_empty = d_full + 2;       // [2] epilogue read them (4 warps)
+  __shared__ uint32_t s_tmem;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t u0 = cta_start(blockIdx.x, a.U, a.grid);
+  const int nu = (int)(cta_start(blockIdx.x + 1, a.U, a.grid) - u0);
+  const int np = (nu + 1) / 2;
+
+  if (threadIdx.x == 0) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    TPQ_CTA(0, gtime())
+    TPQ_CTA(3, smid)
+    for (int s = 0; s < C::NS; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, 4);
+    }
+    for (int s = 0; s < C::NX; ++s) mbar_init(xfull + s, 1);
+    for (int s = 0; s < C::NAF; ++s) mbar_init(a_full + s, 4);
+    for (int r = 0; r < C::RD; ++r) mbar_init(done + r, 1);
+    for (int d = 0; d < 2; ++d) {
+      mbar_init(d_full + d, 2);
+      mbar_init(d_empty + d, 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == kV2Mma) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)),
+                 "n"(C::TCOLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  pdl_launch_dependents();
+  const uint32_t tmem = __shfl_sync(0xffffffffu, s_tmem, 0);
+  constexpr uint32_t kA0 = C::DC;  // A buffer of set s at kA0 + s * 2AU (unit h of the pair at + h AU)
+
+  if (warp >= kV2Deq0 && warp < kV2Prod) {
+    // ===================== dequant: set = warp / 4 - 1 takes pairs p = set, set + 3, ... =========
+    const int set = (warp - kV2Deq0) >> 2, qw = warp & 3;
+    const int col = qw * 32 + lane;
+    const uint32_t a_buf = tmem + ((uint32_t)(qw * 32) << 16) + kA0 + set * 2 * C::AU;
+    const int zbyte = kUnitK * kTileCols / 2 + C::KG * 256 + (col >> 1), zsh = 4 * (col & 1);
+    const int sbyte = kUnitK * kTileCols / 2 + 2 * col;
+    const bool xw = qw == 0;
+    const float se = exp2f((float)-a.sshift), s24 = 16777216.f * se, s20 = 1048576.f * se;
+    int st = (2 * set) % C::NS;                       // stage of unit 2p
+    uint32_t ph = (uint32_t)(((2 * set) / C::NS) & 1);
+    for (int p = set; p < np; p += kV2Sets) {
+      TPQ_EV(0, p)
+#pragma unroll 1
+      for (int h = 0; h < 2; ++h) {
+        const int i = 2 * p + h;
+        const int sh_ = st + h >= C::NS ? st + h - C::NS : st + h;
+        const uint32_t phh = st + h >= C::NS ? ph ^ 1u : ph;
+        if (i >= nu) break;
+        mbar_wait(full + sh_, phh);
+        if (h == 0) { TPQ_EV(1, p) }
+        const uint8_t* sp = smem + C::WRING + sh_ * C::STAGE;
+        __half2 sl[C::KG], shh[C::KG], zc[C::KG];
+#pragma unroll
+        for (int g = 0; g < C::KG; ++g) {
+          const float z = (float)((sp[zbyte + g * 64] >> zsh) & 0xFu);
+          const float sf = __half2float(*reinterpret_cast<const __half*>(sp + sbyte + g * 256));
+          sl[g] = __float2half2_rn(sf * s24);
+          shh[g] = __float2half2_rn(sf * s20);
+          zc[g] = __float2half2_rn(-z * sf * se);
+        }
+        uint4 cw[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) cw[c] = *reinterpret_cast<const uint4*>(sp + code_block(c, col) * 16);
+#pragma unroll
+        for (int kh = 0; kh < 2; ++kh) {
+          uint32_t r[32];
+#pragma unroll
+          for (int w = 0; w < 8; ++w) {
+            const int j = (64 * kh + 8 * w) / G;
+            const uint4 c4 = cw[2 * kh + w / 4];
+            const uint32_t x = (w & 3) == 0 ? c4.x : (w & 3) == 1 ? c4.y : (w & 3) == 2 ? c4.z : c4.w;
+            const uint32_t x8 = x >> 8;
+            r[4 * w + 0] = h2u(__hfma2(u2h(x & 0x000F000Fu), sl[j], zc[j]));
+            r[4 * w + 1] = h2u(__hfma2(u2h(x & 0x00F000F0u), shh[j], zc[j]));
+            r[4 * w + 2] = h2u(__hfma2(u2h(x8 & 0x000F000Fu), sl[j], zc[j]));
+            r[4 * w + 3] = h2u(__hfma2(u2h(x8 & 0x00F000F0u), shh[j], zc[j]));
+          }
+          if (h == 0 && kh == 0 && p >= kV2Sets) {
+            // own buffer free: pair p - 3's MMAs completed
+            const int q = p - kV2Sets;
+            mbar_wait_backoff(done + q % C::RD, (uint32_t)((q / C::RD) & 1), TPQ_DONE_NS);
+            TPQ_EV(2, p)
+            tc_fence_after();
+          }
+          tmem_st32(a_buf + h * C::AU + kh * 32, r);
+        }
+        // every register loaded from the stage fed the tcgen05.st just issued (in-order issue)
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + sh_);
+      }
+      tmem_wait_st();
+      if (xw) mbar_wait(xfull + p % C::NX, (uint32_t)((p / C::NX) & 1));
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(a_full + p % C::NAF);
+      TPQ_EV(3, p)
+      st += 2 * kV2Sets;
+      if (st >= C::NS) {
+        st -= C::NS;
+        ph ^= 1u;
+      }
+    }
+  } else if (warp < kV2Deq0) {
+    // ===================== epilogue: once per tile segment =====================
+    const int qw = warp, col = qw * 32 + lane;
+    const uint32_t lane_base = (uint32_t)(qw * 32) << 16;
+    pdl_wait();
+    const float up = exp2f((float)a.sshift);
+    int tile = (int)(u0 / a.NKB);
+    int64_t seg_start = u0;
+    const int64_t uend = u0 + nu;
+    for (int seg = 0; seg_start < uend; ++seg, ++tile) {
+      const int64_t tile_end = (int64_t)(tile + 1) * a.NKB;
+      const int64_t seg_end = tile_end < uend ? tile_end : uend;  // exclusive
+      const int lo = (int)(seg_start - u0), hi = (int)(seg_end - 1 - u0);
+      const int d = seg & 1;
+      mbar_wait_backoff(d_full + d, (uint32_t)((seg >> 1) & 1), TPQ_EPI_NS);
+      tc_fence_after();
+      const bool w0 = hi - lo >= 3 || ((lo >> 1) & 1) == 0 || ((hi >> 1) & 1) == 0;
+      const bool w1 = hi - lo >= 3 || ((lo >> 1) & 1) == 1 || ((hi >> 1) & 1) == 1;
+      uint32_t v[kNPad], v1[kNPad];
+      const uint32_t dcol = tmem + lane_base + 2 * d * kNPad;
+      if (w0) tmem_ld16(dcol, v);
+      if (w1) tmem_ld16(dcol + kNPad, v1);
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(d_empty + d);
+#pragma unroll
+      for (int m = 0; m < kNPad; ++m)
+        v[m] = __float_as_uint(up * (w0 ? (w1 ? __uint_as_float(v[m]) + __uint_as_float(v1[m]) : __uint_as_float(v[m]))
+                                        : __uint_as_float(v1[m])));
+      const int64_t n = (int64_t)tile * kTileCols + col;
+      if (seg_start == (int64_t)tile * a.NKB && seg_end == tile_end) {
+#pragma unroll
+        for (int m = 0; m < kNPad; ++m)
+          if (m < a.M) a.out[m * a.out_ld + n] = __float2half_rn(__uint_as_float(v[m]));
+      } else {
+        // split tile: partial into this CTA's slot (0 = its first segment, 1 = its last), summed by
+        // the fix-up kernel in CTA order after this kernel
+        float* mine = a.ws + ((size_t)blockIdx.x * 2 + (seg_start == u0 ? 0 : 1)) * (kNPad * kTileCols);
+#pragma unroll
+        for (int m = 0; m < kNPad; ++m)
+          if (m < a.M) __stcg(mine + m * kTileCols + col, __uint_as_float(v[m]));
+      }
+      seg_start = seg_end;
+    }
+  } else if (warp == kV2Prod) {
+    // ===================== TMA producer =====================
+    const uint64_t pw = policy_evict_first();
+    const int pre = nu < C::NS ? nu : C::NS;
+    for (int i = 0; i < pre; ++i) {
+      if (elect_one()) {
+        mbar_arrive_expect_tx(full + i, C::UB);
+        bulk_g2s(smem + C::WRING + i * C::STAGE, a.packed + (u0 + i) * C::UB, C::UB, full + i, pw);
+      }
+      __syncwarp();
+    }
+    for (int i = 0, s = 0, ph = 0; i + C::NS < nu; ++i) {
+      TPQ_EV(0, i)
+      mbar_wait_sleep(empty + s, (uint32_t)ph);
+      TPQ_EV(1, i)
+      if (elect_one()) {
+        mbar_arrive_expect_tx(full + s, C::UB);
+        bulk_g2s(smem + C::WRING + s * C::STAGE, a.packed + (u0 + i + C::NS) * C::UB, C::UB, full + s, pw);
+      }
+      __syncwarp();
+      if (++s == C::NS) {
+        s = 0;
+        ph ^= 1;
+      }
+    }
+  } else if (warp == kV2Stage) {
+    // ===================== activation stager =====================
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&xmap)) : "memory");
+    pdl_wait();
+    if (lane == 0) { TPQ_CTA(1, gtime()) }
+    int kb = (int)(u0 % a.NKB);
+    for (int p = 0; p < np; ++p) {
+      const int x = p % C::NX, nh = (2 * p + 1 < nu) ? 2 : 1;
+      const int kb1 = kb + 1 == a.NKB ? 0 : kb + 1;
+      if (p >= C::NX) mbar_wait_sleep(done + (p - C::NX) % C::RD, (uint32_t)(((p - C::NX) / C::RD) & 1));
+      if (elect_one()) {
+        mbar_arrive_expect_tx(xfull + x, nh * C::XU);
+        tma_load_3d(smem + C::XRING + 2 * x * C::XU, &xmap, 0, 0, 2 * kb, xfull + x);
+        if (nh == 2) tma_load_3d(smem + C::XRING + (2 * x + 1) * C::XU, &xmap, 0, 0, 2 * kb1, xfull + x);
+      }
+      __syncwarp();
+      kb = nh == 2 ? (kb1 + 1 == a.NKB ? 0 : kb1 + 1) : kb1;
+    }
+  } else {
+    // ===================== MMA issuers: warp kV2Mma + w takes the pairs p % 2 == w ===============
+    const int w = warp - kV2Mma;
+    const uint32_t xring = smem_u32(smem + C::XRING);
+    const int kb0 = (int)(u0 % a.NKB);
+    const int nseg = (kb0 + nu - 1) / a.NKB + 1;
+    int sw = 0;
+    auto skip_seg = [&]() {
+      mbar_wait(d_empty + (sw & 1), (uint32_t)(((sw >> 1) & 1) ^ 1));
+      if (lane == 0) mbar_arrive(d_full + (sw & 1));
+      __syncwarp();
+      ++sw;
+    };
+    static_assert(C::XU == 4096 && C::AU == 64, "umma_unit16 offsets");
+    for (int p = w; p < np; p += 2) {
+      const int x = p % C::NX, b = p % kV2Sets;
+      const uint64_t bd0 = bdesc_sw128(xring + 2 * x * C::XU);
+      const int i0 = 2 * p, sg = (kb0 + i0) / a.NKB;
+      const int lo = sg * a.NKB - kb0 > 0 ? sg * a.NKB - kb0 : 0;
+      const int hi = (sg + 1) * a.NKB - kb0 - 1 < nu - 1 ? (sg + 1) * a.NKB - kb0 - 1 : nu - 1;
+      const bool fast = sg == sw && i0 - 3 >= lo && i0 + 4 <= hi;
+      const uint32_t at = tmem + kA0 + b * 2 * C::AU;
+      TPQ_EV(0, p)
+      mbar_wait_backoff(a_full + p % C::NAF, (uint32_t)((p / C::NAF) & 1), TPQ_MMA_NS);
+      TPQ_EV(1, p)
+      tc_fence_after();
+      if (fast) {
+        const uint32_t dt = tmem + (2 * (sg & 1) + w) * kNPad;
+        if (elect_one()) {
+          umma_unit16(dt, at, bd0, kIdesc, 1u);
+          umma_unit16(dt, at + C::AU, bd0 + (C::XU >> 4), kIdesc, 1u);
+          umma_commit1(done + p % C::RD);
+        }
+        __syncwarp();
+        TPQ_EV(3, p)
+        continue;
+      }
+#pragma unroll 1
+      for (int h = 0; h < 2; ++h) {
+        const int i = 2 * p + h;
+        if (i >= nu) break;
+        const int sg = (kb0 + i) / a.NKB;
+        while (sw < sg) skip_seg();
+        const int lo = sg * a.NKB - kb0 > 0 ? sg * a.NKB - kb0 : 0;
+        const int hi = (sg + 1) * a.NKB - kb0 - 1 < nu - 1 ? (sg + 1) * a.NKB - kb0 - 1 : nu - 1;
+        const bool first = (h ? i - 1 : i - 3) < lo, last = (h ? i + 3 : i + 1) > hi;
+        const int d = sg & 1;
+        if (first) {
+          mbar_wait(d_empty + d, (uint32_t)(((sg >> 1) & 1) ^ 1));
+          tc_fence_after();
+        }
+        const uint32_t dt = tmem + (2 * d + w) * kNPad;
+        if (elect_one()) {
+          umma_unit16(dt, at + h * C::AU, bd0 + (uint64_t)((h * C::XU) >> 4), kIdesc, first ? 0u : 1u);
+          if (last) umma_commit1(d_full + d);
+        }
+        __syncwarp();
+        if (last) ++sw;
+      }
+      if (elect_one()) umma_commit1(done + p % C::RD);
+      __syncwarp();
+      TPQ_EV(3, p)
+    }
+    while (sw < nseg) skip_seg();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x == 0) { TPQ_CTA(2, gtime()) }
+  if (warp == kV2Mma) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::TCOLS) : "memory");
   }
@@ -1606,6 +1966,9 @@ bool prepare_t() {
   static_assert(2 * smem > 228 * 1024, "GEMV must be one CTA per SM (TMEM 512 columns)");
   if (cudaFuncSetAttribute(k_dqgemv<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
     return false;
+  static_assert(TC2<G>::SMEM <= 227 * 1024 && 2 * TC2<G>::SMEM > 228 * 1024, "GEMV v2: one CTA per SM");
+  if (cudaFuncSetAttribute(k_dqgemv2<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC2<G>::SMEM) != cudaSuccess)
+    return false;
   if (getenv("TPQ_VERBOSE")) {
     cudaFuncAttributes fa;
     cudaFuncGetAttributes(&fa, k_dqgemv<G>);
@@ -1861,7 +2224,7 @@ bool max_carveout(Kern k) {
 }
 template <int G>
 bool carveout_g() {
-  return max_carveout(k_dqgemv<G>) && max_carveout(k_dqgemv_r<G, 1, kRSets, kRWps>) &&
+  return max_carveout(k_dqgemv<G>) && max_carveout(k_dqgemv2<G>) && max_carveout(k_dqgemv_r<G, 1, kRSets, kRWps>) &&
          max_carveout(k_dqgemv_r<G, 2, kRSets, kRWps>) && max_carveout(k_dqgemm<G, 64>) &&
          max_carveout(k_dqgemm<G, 128>) && max_carveout(k_dqgemm<G, 256>) && max_carveout(k_dqgemm_ss<G, 128>);
 }
@@ -1922,7 +2285,16 @@ cudaError_t launch_gemv(const LayerDev& L, const CUtensorMap& xmap, const void* 
   // it (TPQ_INKERNEL_FIXUP=1): the in-kernel arrival atomic measured ~5 us at the end of each CTA
   static const bool inkernel = getenv("TPQ_INKERNEL_FIXUP") != nullptr;
   a.fixk = inkernel ? 0 : 1;
-  cudaError_t e = L.G == 128 ? launch_pdl(k_dqgemv<128>, dim3(a.grid), dim3(kGemvThreads), TC<128>::SMEM, st, a, xmap)
+  static const bool v1 = getenv("TPQ_GEMV_V1") != nullptr;
+  cudaError_t e;
+  if (!v1) {
+    a.fixk = 1;
+    e = L.G == 128 ? launch_pdl(k_dqgemv2<128>, dim3(a.grid), dim3(kV2Threads), TC2<128>::SMEM, st, a, xmap)
+        : L.G == 64 ? launch_pdl(k_dqgemv2<64>, dim3(a.grid), dim3(kV2Threads), TC2<64>::SMEM, st, a, xmap)
+        : L.G == 32 ? launch_pdl(k_dqgemv2<32>, dim3(a.grid), dim3(kV2Threads), TC2<32>::SMEM, st, a, xmap)
+                    : cudaErrorInvalidValue;
+  } else
+  e = L.G == 128 ? launch_pdl(k_dqgemv<128>, dim3(a.grid), dim3(kGemvThreads), TC<128>::SMEM, st, a, xmap)
                   : L.G == 64 ? launch_pdl(k_dqgemv<64>, dim3(a.grid), dim3(kGemvThreads), TC<64>::SMEM, st, a, xmap)
                   : L.G == 32 ? launch_pdl(k_dqgemv<32>, dim3(a.grid), dim3(kGemvThreads), TC<32>::SMEM, st, a, xmap)
                               : cudaErrorInvalidValue;

@@ -1,3 +1,5 @@
-for rep in 1 2; do for v in "" _ns16 _ns12 _nx6; do for tp in 1 8; do
-echo "$v tp=$tp $(TPQ_LIB_PATH=paper_2402_04925_b200/libtpq$v.so timeout 200 python tools/fwd_time.py --sim-tp $tp --ms 1,16 2>&1 | tail -1)"
-done; done; done
+mkdir -p gpurun_out
+export TPQ_LIB_PATH=paper_2402_04925_b200/libtpq_prof.so
+timeout 120 python tools/trace_v2.py --m 16 > gpurun_out/trace_v2_m16.log 2>&1
+timeout 120 python tools/trace_v2.py --m 1 > gpurun_out/trace_v2_m1.log 2>&1
+for cfg in "1 1" "1 16" "8 1"; do set -- $cfg; echo "== tp=$1 M=$2"; timeout 120 python tools/cta_times.py --sim-tp $1 --m $2; done > gpurun_out/cta_times.log 2>&1
