@@ -415,12 +415,9 @@ def main():
 
 
 def launches_per_step(M, naive):
-    """Our kernels per forward (M <= 16): X[:, P1] gather, per layer the GEMV plus (tcgen05 GEMV)
-    its split-tile fix-up kernel, and the naive path's P2 gather; NCCL kernels not counted."""
-    reg = os.environ.get("TPQ_GEMV", "").startswith("r")
-    fix = 0 if (reg or os.environ.get("TPQ_INKERNEL_FIXUP")) else 1
-    per_layer = 1 + fix if M <= 16 else 2
-    return 1 + 2 * per_layer + (1 if naive else 0)
+    """Our kernels per forward (M <= 16): the X[:, P1] gather, per layer the GEMV and its split-tile
+    fix-up kernel, and the naive path's P2 gather; NCCL kernels not counted."""
+    return 1 + 2 * 2 + (1 if naive else 0)
 
 
 def time_naive(a, p, P1, P2, tp, rank, local, R, comm, X, Y, stream, sync_all, world, dev, ours_ms):

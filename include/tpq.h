@@ -176,18 +176,6 @@ int tpq_sum_partials(const void* const* parts, int nparts, int64_t count, void* 
  * layer-2 GEMV, [5] after the AllReduce.  The array is copied; events stay caller-owned. */
 int tpq_mlp_set_timing(tpq_mlp* h, void* const* events);
 
-/* Kernel choice of the M <= 16 dequant-GEMV (both compute SURVEY.md §8(a) rows A4 / A5 with the
- * same operand arithmetic, PAPER.md:L19 s (q - z) with fp32 accumulation):
- *   TPQ_GEMV_AUTO (0)  the handle's default (tcgen05 unless the TPQ_GEMV environment variable says
- *                      "r" or "tc" at tp_shard_mlp time);
- *   TPQ_GEMV_TC   (1)  k_dqgemv: A operand dequantized into tensor memory, tcgen05.mma;
- *   TPQ_GEMV_REG  (2)  k_dqgemv_r: A fragments dequantized in registers, mma.sync.
- * Takes effect at the next forward; not thread-safe against a concurrent forward on the handle.
- * TPQ_EINVAL for a NULL handle or an unknown kind. */
-#define TPQ_GEMV_AUTO 0
-#define TPQ_GEMV_TC 1
-#define TPQ_GEMV_REG 2
-int tpq_mlp_set_gemv_kernel(tpq_mlp* h, int kind);
 
 /* ------------------------------- introspection / test-only exports ------------------- */
 typedef struct tpq_mlp_info_t {

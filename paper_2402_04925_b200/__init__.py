@@ -3,6 +3,6 @@
 The product is libtpq.so (C-ABI in include/tpq.h); this package is its thin binding.
 """
 from ._lib import (  # noqa: F401
-    Comm, EXPORTS, LIB_PATH, TPQ_GEMV_AUTO, TPQ_GEMV_REG, TPQ_GEMV_TC, TPQ_NAIVE, TPQ_TP_AWARE, TPQError, TpMlp, comm_unique_id, gptq_reorder, lib,
+    Comm, EXPORTS, LIB_PATH, TPQ_NAIVE, TPQ_TP_AWARE, TPQError, TpMlp, comm_unique_id, gptq_reorder, lib,
     sum_partials,
 )

@@ -17,7 +17,6 @@ LIB_PATH = os.environ.get("TPQ_LIB_PATH") or os.path.join(_PKG, "libtpq.so")
 
 TPQ_OK, TPQ_EINVAL, TPQ_EUNSUPPORTED, TPQ_ECUDA, TPQ_ENCCL, TPQ_ENOMEM, TPQ_ESTATE = range(7)
 TPQ_NAIVE, TPQ_TP_AWARE = 0, 1
-TPQ_GEMV_AUTO, TPQ_GEMV_TC, TPQ_GEMV_REG = 0, 1, 2
 _CODES = {1: "EINVAL", 2: "EUNSUPPORTED", 3: "ECUDA", 4: "ENCCL", 5: "ENOMEM", 6: "ESTATE"}
 
 # Every symbol include/tpq.h declares (tests check the .so exports all of them).
@@ -27,7 +26,6 @@ EXPORTS = [
     "tp_mlp_forward", "tp_mlp_forward_host",
     "tp_mlp_forward_local", "tpq_layer1", "tpq_naive_gather", "tpq_layer2", "tpq_sum_partials",
     "tpq_mlp_info", "tpq_mlp_index_maps", "tpq_mlp_export_canonical", "tpq_mlp_set_timing",
-    "tpq_mlp_set_gemv_kernel",
 ]
 
 
@@ -85,7 +83,6 @@ def lib() -> C.CDLL:
             "tpq_mlp_index_maps": [vp, vp, vp, C.POINTER(i32), C.POINTER(i32)],
             "tpq_mlp_export_canonical": [vp, C.c_int, vp, vp, vp],
             "tpq_mlp_set_timing": [vp, vp],
-            "tpq_mlp_set_gemv_kernel": [vp, C.c_int],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -230,10 +227,6 @@ class TpMlp:
 
     def layer2(self, Y1in, M: int, Y2, stream=None):
         _check(lib().tpq_layer2(self._h, _ptr(Y1in), M, _ptr(Y2), _stream(stream)))
-
-    def set_gemv_kernel(self, kind: int):
-        """M <= 16 GEMV kernel: TPQ_GEMV_AUTO / TPQ_GEMV_TC (tcgen05) / TPQ_GEMV_REG (mma.sync)."""
-        _check(lib().tpq_mlp_set_gemv_kernel(self._h, int(kind)))
 
     def set_timing(self, events):
         """events: 6 torch.cuda.Event (or None to disable); see tpq_mlp_set_timing."""

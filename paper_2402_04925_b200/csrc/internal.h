@@ -29,9 +29,6 @@ constexpr int kTileCols = 128;      // weight columns per tile (= TMEM lanes = M
 constexpr int kUnitK = 128;         // weight rows per unit (8 MMAs of K = 16)
 constexpr int kNPad = 16;           // batch rows per MMA (tcgen05 M=128 needs N % 16 == 0)
 constexpr int kMaxM = 16;           // rows per forward chunk
-constexpr int kGemvParts = 4;       // max stream-K participants per GEMV CTA (workspace sizing)
-constexpr int kCntStride = 32;      // ints between stream-K tile counters: one 128-byte line each (the CTAs of
-                                    // all tiles hitting one line serialised their atomics: ~5 us per layer)
 constexpr int64_t unit_bytes_c(int G) { return (int64_t)kUnitK * kTileCols / 2 + 320LL * (kUnitK / G); }
 inline int64_t unit_bytes(int G) { return unit_bytes_c(G); }
 #ifdef __CUDACC__
@@ -40,9 +37,8 @@ inline int64_t unit_bytes(int G) { return unit_bytes_c(G); }
 #define TPQ_HD
 #endif
 // 16-byte code block of (chunk c, column j) inside a record: column XOR-swizzled by 2c within its
-// aligned group of 8, so that a quarter-warp reading columns g, g+1 of chunks 0..3 (the mma.sync
-// GEMV fragment order) hits 8 distinct bank groups; still a permutation inside each aligned 8-column
-// group, so lanes reading 8 consecutive columns of one chunk stay conflict-free.
+// aligned group of 8 (a permutation inside each aligned 8-column group, so the dequant warps' lanes,
+// reading 8 consecutive columns of one chunk per quarter-warp, stay conflict-free).
 TPQ_HD constexpr int code_block(int c, int j) { return c * kTileCols + (j ^ (2 * c)); }
 
 struct LayerDev {
@@ -52,11 +48,9 @@ struct LayerDev {
   int64_t U = 0;           // NT * NKB units
   int grid = 0;            // persistent CTAs of the M <= 16 GEMV (stream-K), at most one per SM
   int grid_mm = 0;         // persistent CTAs of the A7 k_dqgemm (every SM)
-  float* ws = nullptr;     // [grid * kGemvParts][2 slots][16 * 128] fp32 stream-K partials (GEMV)
+  float* ws = nullptr;     // [grid][2 slots][16][128] fp32 stream-K partials of the GEMV (slot 0 = first segment)
   float* ws_mm = nullptr;  // [grid_mm][2 slots][256][128] fp32 stream-K partials (A7 GEMM)
   float* ws_ss = nullptr;  // [items][128][128] fp32 k-split partials (A7 SS GEMM, M >= 128)
-  int* cnt = nullptr;      // [NT * kCntStride] arrival counters, one per 128-byte line (self-resetting)
-  int gemv = 0;            // GEMV kernel: 0 = from the TPQ_GEMV environment variable (default tcgen05), 1 = tcgen05, 2 = register-dequant
   int sshift = 0;          // GEMV operand shift e: smallest e >= 0 with max|s| 2^(24-e) <= 65504
 };
 
@@ -65,12 +59,10 @@ enum GatherMode { GATHER_COLS = 0, GATHER_ALLGATHER = 1 };
 // Set the GEMV kernel attributes (dynamic shared memory) on the current device; false on failure.
 bool gemv_prepare(int G);
 
-// out[m][n] = sum_k x[m][k] deq(W)[k][n] for M <= 16 rows; x is a [16][K] fp16 row-major buffer
-// described by `xmap` (make_xmap), out is [M][out_ld] fp16 row-major.
-// described by `xmap` (make_xmap, 16-row boxes; tcgen05 GEMV) and by x / ldx (register-dequant GEMV,
-// the default).  TPQ_GEMV=tc selects the tcgen05 GEMV (k_dqgemv) instead.
-cudaError_t launch_gemv(const LayerDev& L, const CUtensorMap& xmap, const void* x, int64_t ldx, int M, void* out,
-                        int64_t out_ld, cudaStream_t st);
+// out[m][n] = sum_k x[m][k] deq(W)[k][n] for M <= 16 rows (k_dqgemv + its split-tile fix-up); x is
+// a [16][K] fp16 row-major buffer described by `xmap` (make_xmap, 16-row boxes), out is [M][out_ld]
+// fp16 row-major.
+cudaError_t launch_gemv(const LayerDev& L, const CUtensorMap& xmap, int M, void* out, int64_t out_ld, cudaStream_t st);
 
 // A7 (M > 16): out[m][n] = sum_k x[m][k] deq(W)[k][n] for M <= nb rows (nb in {64, 128, 256}), x a
 // [nb][K] fp16 row-major buffer described by xmap (make_xmap with rows = nb), out [M][out_ld].
@@ -116,7 +108,6 @@ cudaError_t launch_gather_rowmajor(const void* src, int64_t ld, const int32_t* i
 
 #ifdef TPQ_PROF
 int cta_read(unsigned long long* out);
-int prof_read(unsigned long long* out);
 int trace_read(long long* out);
 #endif
 

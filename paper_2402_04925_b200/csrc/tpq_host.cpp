@@ -179,7 +179,6 @@ struct tpq_mlp {
   void* d_xin = nullptr;       // host-forward staging [M_max][K1]
   void* d_yout = nullptr;      // host-forward staging [M_max][N2]
   float* d_ws = nullptr;
-  int* d_cnt = nullptr;
   CUtensorMap xmap1 = {}, xmap2 = {};  // TMA views of d_x1 / d_y1 (GEMV activation operand, 16 rows)
   CUtensorMap mm1[3] = {}, mm2[3] = {};  // A7 views of d_x1 / d_y1 with 64 / 128 / 256 rows
   CUtensorMap ss1 = {}, ss2 = {};        // A7 SS views: 256-row buffers, 128-row boxes
@@ -222,7 +221,7 @@ int validate_perm(const int32_t* P, const gptq_layer* w, const char* name) {
 void free_dev(tpq_mlp* h) {
   if (h->device < 0) return;
   cudaSetDevice(h->device);
-  void* ptrs[] = {h->d_w1, h->d_w2, h->d_P1, h->d_gcols, h->d_x1, h->d_y1, h->d_buf, h->d_xin, h->d_yout, h->d_ws, h->d_cnt};
+  void* ptrs[] = {h->d_w1, h->d_w2, h->d_P1, h->d_gcols, h->d_x1, h->d_y1, h->d_buf, h->d_xin, h->d_yout, h->d_ws};
   for (void* p : ptrs)
     if (p) cudaFree(p);
 }
@@ -247,10 +246,7 @@ void plan_layer(tpq::LayerDev& L, int64_t K, int64_t N, int G, int device) {
   L.NKB = (int)(K / tpq::kUnitK);
   L.U = (int64_t)L.NT * L.NKB;
   int sms = 148;
-  if (device >= 0) {
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    tpq::gemv_prepare(G);
-  }
+  if (device >= 0) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   const int64_t cap = std::max<int64_t>(1, L.U / 4);
   // Small shards (< 64 units per SM: Llama / Granite at TP >= 2) are latency-bound, not
   // bandwidth-bound: 128 of 148 CTAs measured 1-3.5 us faster per forward there (the next kernel
@@ -396,10 +392,16 @@ int tp_shard_mlp(const gptq_layer* w1, const gptq_layer* w2, const int32_t* P1, 
     if (device >= 0) {
       auto upload = [&]() -> int {
         TPQ_CUDA(cudaSetDevice(device));
+        // kernel attributes (dynamic shared memory, carveout) are per device: set them on this one
+        for (int G : {w1->G, w2->G})
+          if (!tpq::gemv_prepare(G)) {
+            cudaGetLastError();
+            return fail(TPQ_ECUDA, "kernel attribute setup failed for G=%d on device %d", G, device);
+          }
         int r;
         auto A = [&](void** p, size_t b) { return dev_alloc(p, b); };
-        const size_t ws1 = (size_t)h->L1.grid * tpq::kGemvParts * 2 * tpq::kNPad * tpq::kTileCols;
-        const size_t ws2 = (size_t)h->L2.grid * tpq::kGemvParts * 2 * tpq::kNPad * tpq::kTileCols;
+        const size_t ws1 = (size_t)h->L1.grid * 2 * tpq::kNPad * tpq::kTileCols;  // [grid][2 slots][16][128]
+        const size_t ws2 = (size_t)h->L2.grid * 2 * tpq::kNPad * tpq::kTileCols;
         h->rows = M_max > tpq::kMaxM ? kGemmRows : tpq::kMaxM;
         const size_t wm1 = M_max > tpq::kMaxM ? (size_t)h->L1.grid_mm * 2 * kGemmRows * tpq::kTileCols : 0;
         const size_t wm2 = M_max > tpq::kMaxM ? (size_t)h->L2.grid_mm * 2 * kGemmRows * tpq::kTileCols : 0;
@@ -415,18 +417,16 @@ int tp_shard_mlp(const gptq_layer* w1, const gptq_layer* w2, const int32_t* P1, 
           return items * 128 * bn;
         };
         const size_t ws1s = ss_ws(h->L1), ws2s = ss_ws(h->L2);
-        const size_t ncnt = (size_t)(h->L1.NT + h->L2.NT) * tpq::kCntStride;
         if ((r = A(&h->d_w1, h->pk1.size())) || (r = A(&h->d_w2, h->pk2.size())) ||
             (r = A((void**)&h->d_P1, K1 * 4)) || (r = A((void**)&h->d_gcols, n * 4)) || (r = A(&h->d_x1, (size_t)h->rows * K1 * 2)) ||
             (r = A(&h->d_y1, (size_t)h->rows * n * 2)) || (r = A(&h->d_buf, (size_t)tp * h->rows * n * 2)) ||
             (r = A(&h->d_xin, (size_t)M_max * K1 * 2)) || (r = A(&h->d_yout, (size_t)M_max * N2 * 2)) ||
-            (r = A((void**)&h->d_ws, (ws1 + ws2 + wm1 + wm2 + ws1s + ws2s) * 4)) || (r = A((void**)&h->d_cnt, ncnt * 4)))
+            (r = A((void**)&h->d_ws, (ws1 + ws2 + wm1 + wm2 + ws1s + ws2s) * 4)))
           return r;
         TPQ_CUDA(cudaMemcpy(h->d_w1, h->pk1.data(), h->pk1.size(), cudaMemcpyHostToDevice));
         TPQ_CUDA(cudaMemcpy(h->d_w2, h->pk2.data(), h->pk2.size(), cudaMemcpyHostToDevice));
         TPQ_CUDA(cudaMemcpy(h->d_P1, P1, K1 * 4, cudaMemcpyHostToDevice));
         TPQ_CUDA(cudaMemcpy(h->d_gcols, h->gather_cols.data(), n * 4, cudaMemcpyHostToDevice));
-        TPQ_CUDA(cudaMemset(h->d_cnt, 0, ncnt * 4));
         bool mok = tpq::make_xmap(&h->xmap1, h->d_x1, K1, tpq::kNPad) && tpq::make_xmap(&h->xmap2, h->d_y1, n, tpq::kNPad);
         if (h->rows > tpq::kMaxM) {
           for (int v = 0; v < 3; ++v)
@@ -443,8 +443,6 @@ int tp_shard_mlp(const gptq_layer* w1, const gptq_layer* w2, const int32_t* P1, 
         h->L2.ws_mm = wm2 ? h->d_ws + ws1 + ws2 + wm1 : nullptr;
         h->L1.ws_ss = ws1s ? h->d_ws + ws1 + ws2 + wm1 + wm2 : nullptr;
         h->L2.ws_ss = ws2s ? h->d_ws + ws1 + ws2 + wm1 + wm2 + ws1s : nullptr;
-        h->L1.cnt = h->d_cnt;
-        h->L2.cnt = h->d_cnt + (size_t)h->L1.NT * tpq::kCntStride;
         TPQ_CUDA(cudaDeviceSynchronize());
         return TPQ_OK;
       };
@@ -554,8 +552,7 @@ static cudaError_t mark_event(cudaEvent_t e, cudaStream_t st) {
 cudaError_t run_layer(tpq_mlp* h, int layer, int mc, void* out, int64_t out_ld, cudaStream_t st) {
   const tpq::LayerDev& L = layer == 1 ? h->L1 : h->L2;
   if (mc <= tpq::kMaxM)
-    return tpq::launch_gemv(L, layer == 1 ? h->xmap1 : h->xmap2, layer == 1 ? h->d_x1 : h->d_y1, layer == 1 ? h->K1 : h->n,
-                            mc, out, out_ld, st);
+    return tpq::launch_gemv(L, layer == 1 ? h->xmap1 : h->xmap2, mc, out, out_ld, st);
   if (mc >= 128 && !getenv("TPQ_NO_SS"))  // compute-bound: activations as the reused A operand
     return tpq::launch_gemm_ss(L, layer == 1 ? h->ss1 : h->ss2, mc, h->sms, out, out_ld, st);
   const int v = mc <= 64 ? 0 : mc <= 128 ? 1 : 2;
@@ -688,7 +685,6 @@ int tpq_sum_partials(const void* const* parts, int nparts, int64_t count, void* 
 #ifdef TPQ_PROF
 // Profiling build only (libtpq_prof.so): per-CTA GEMV timeline of the last launches.
 int tpq_debug_cta(unsigned long long* out) { return tpq::cta_read(out) ? TPQ_ECUDA : TPQ_OK; }
-int tpq_debug_prof(unsigned long long* out) { return tpq::prof_read(out) ? TPQ_ECUDA : TPQ_OK; }
 int tpq_debug_trace(long long* out) { return tpq::trace_read(out) ? TPQ_ECUDA : TPQ_OK; }
 #endif
 
@@ -706,12 +702,6 @@ int tpq_mlp_set_timing(tpq_mlp* h, void* const* events) {
   return TPQ_OK;
 }
 
-int tpq_mlp_set_gemv_kernel(tpq_mlp* h, int kind) {
-  if (!h) return fail(TPQ_EINVAL, "NULL handle");
-  if (kind < TPQ_GEMV_AUTO || kind > TPQ_GEMV_REG) return fail(TPQ_EINVAL, "unknown GEMV kernel kind %d", kind);
-  h->L1.gemv = h->L2.gemv = kind;
-  return TPQ_OK;
-}
 
 int tpq_mlp_info(const tpq_mlp* h, tpq_mlp_info_t* o) {
   if (!h || !o) return fail(TPQ_EINVAL, "NULL");

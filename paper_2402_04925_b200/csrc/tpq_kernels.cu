@@ -6,16 +6,19 @@
 //                  metadata next to its codes).  Blackwell-native: per SM one persistent CTA;
 //                  one warp streams (128-column tile x 128-row k-block) weight records into a
 //                  shared-memory ring with TMA bulk copies (mbarrier complete_tx, L2 evict-first);
-//                  16 warps turn int4 codes into s (q - z) f16 with LOP3 magic numbers straight
-//                  into TENSOR MEMORY (tcgen05.st, the MMA A operand); one warp stages the M real
-//                  activation slice (tensor TMA); one thread issues tcgen05.mma kind::f16 (M=128
-//                  columns, N=16 batch rows, A from TMEM, B = activations from smem), the
-//                  accumulator of a tile segment stays in TMEM; four warps read it back once per
-//                  segment.  Persistent stream-K over units with a deterministic last-arriver
-//                  fix-up; programmatic dependent launch (weight prefetch overlaps the previous
-//                  kernel).
+//                  12 warps turn int4 codes into fp16 s (q - z) with LOP3 magic numbers straight
+//                  into TENSOR MEMORY (tcgen05.st, the MMA A operand); one warp stages the
+//                  activation slice (tensor TMA); two warps issue tcgen05.mma kind::f16 (M = 128
+//                  columns, N = 16 batch rows, A from TMEM, B = activations from smem); the
+//                  accumulator of a tile segment stays in TMEM and four warps read it back once per
+//                  segment.  Persistent stream-K over units; split tiles are summed after the
+//                  kernel by k_gemv_fixup / k_mm_fixup in CTA order (deterministic); programmatic
+//                  dependent launch (the weight prefetch overlaps the previous kernel).
+//  k_dqgemm<G,NB>  A7 (17 <= M < 128): same records, weights as the TMEM A operand, N = 64..256.
+//  k_dqgemm_ss<G>  A7 (M >= 128): mixed-input SS GEMM, activations as the reused smem A operand.
 //  k_gather_rm     X[:, P1] gather (Alg. 3 L1) or the naive AllGather re-permute
-//                  + CHUNK (Alg. 2 L3-4), row-major.
+//                  + CHUNK (Alg. 2 L3-4), row-major; k_gather_rows the
+//                  staged-row variant.
 //  k_sum_partials  rank-order sum (single-GPU shard simulation only).
 #include <cuda.h>  // CUtensorMap; the map is encoded on the host through the runtime's driver entry point
 #include <cudaTypedefs.h>
@@ -63,10 +66,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 // Wait with a suspend-time hint: the warp sleeps until the phase completes (or the hint, in ns,
 // expires) instead of spinning try_wait / branch / yield through the issue slots of busy warps.
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
-#ifdef TPQ_NOSLEEP
-  mbar_wait(bar, parity);
-  return;
-#endif
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "TPQ_WAITS_%=:\n\t"
@@ -95,15 +94,7 @@ __device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity
   }
   while (!mbar_try(bar, parity)) __nanosleep(ns);
 }
-#ifndef TPQ_EPI_NS
-#define TPQ_EPI_NS 256
-#endif
-#ifndef TPQ_MMA_NS
-#define TPQ_MMA_NS 0
-#endif
-#ifndef TPQ_DONE_NS
-#define TPQ_DONE_NS 0
-#endif
+
 // Per-CTA timeline (build with -DTPQ_PROF; profiling aid, not in the product build): entry,
 // work start, end (globaltimer ns) and SM id per CTA, per layer (N > K selects the slot).
 #ifdef TPQ_PROF
@@ -119,30 +110,9 @@ __device__ __forceinline__ unsigned long long gtime() {
 __device__ long long g_tpq_trace[24][64][4];
 #define TPQ_EV(e, i) \
   if (blockIdx.x == 0 && a.NT * kTileCols < a.NKB * kUnitK && lane == 0 && (i) < 64) g_tpq_trace[warp][i][e] = clock64();
-// wait-cycle accounting per role (slot k), flushed by lane 0 of every warp at the end
-__device__ unsigned long long g_tpq_prof[32];
-#define TPQ_PDECL long long _pt[4] = {0, 0, 0, 0}; const long long _t_start = clock64();
-#define TPQ_W(bar, par, k)               \
-  do {                                   \
-    const long long _t0 = clock64();     \
-    mbar_wait(bar, par);                 \
-    _pt[k] += clock64() - _t0;           \
-  } while (0)
-#define TPQ_T0(k) const long long _tt##k = clock64();
-#define TPQ_T1(k, slot) _pt[slot] += clock64() - _tt##k;
-#define TPQ_PFLUSH(base)                                                                \
-  if (lane == 0) {                                                                      \
-    atomicAdd(&g_tpq_prof[(base) + 4], (unsigned long long)(clock64() - _t_start));     \
-    for (int _k = 0; _k < 4; ++_k) atomicAdd(&g_tpq_prof[(base) + _k], (unsigned long long)_pt[_k]); \
-  }
 #else
 #define TPQ_CTA(e, v)
 #define TPQ_EV(e, i)
-#define TPQ_PDECL
-#define TPQ_W(bar, par, k) mbar_wait(bar, par)
-#define TPQ_T0(k)
-#define TPQ_T1(k, slot)
-#define TPQ_PFLUSH(base)
 #endif
 // 1-D TMA bulk copy global -> shared, completion counted on `bar` in bytes.
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
@@ -266,103 +236,8 @@ __device__ __forceinline__ uint64_t bdesc_sw128(uint32_t saddr) {
 // instruction descriptor: D f32, A/B f16, both K-major, N = 16, M = 128
 constexpr uint32_t kIdesc = (1u << 4) | ((uint32_t)(kNPad >> 3) << 17) | ((uint32_t)(kTileCols >> 4) << 24);
 
-// ------------------------------------------------------------------ GEMV configuration
-// Unit = (128-column tile t, 128-row k-block kb): one weight record (internal.h), 8 MMAs of
-// K = 16.  A CTA owns a contiguous range of units (stream-K); the units of one tile inside that
-// range form a "segment", accumulated in one TMEM accumulator (16 columns) across all its units.
-//
-// Arithmetic: the A operand is fp16(s (q - z) 2^-e) with one HFMA2 per f16x2 pair: a code nibble
-// masked into the low mantissa bits of an f16 is the exact subnormal q 2^-24 (bits 0-3) or q 2^-20
-// (bits 4-7); times S = s 2^(24-e) (resp. 2^(20-e)), exact in fp16, the product is exactly
-// q s 2^-e, and the addend C = fp16(-z s 2^-e) gives A with one rounding of the product sum plus
-// the rounding of C (<= 2^-12 |z s|; reading on operand precision).  e = sshift >= 0 is
-// the smallest shift with max|s| 2^(24-e) <= 65504 (0 for the synthetic checkpoints); the
-// epilogue multiplies the fp32 accumulator by 2^e.  The MMA accumulates in fp32 over the whole
-// segment, so the epilogue runs once per segment (measured: a per-unit fp32-scale epilogue was
-// the bottleneck of the previous design at ~575 cycles per unit, profiles/r01_summary.md).
-// Per code word (8 weights): 5 ALU-pipe + 4 FMA-pipe ops.
-//
-// Hand-offs go per PAIR of consecutive units (p = i / 2): an mbarrier wait costs ~90-180 cycles
-// even when the phase has already completed (B300_MICROARCH.md "mbarrier"; measured here with
-// tools/prof_waits.py), comparable to the ~383 cycles per unit the SM has at HBM speed.
-//
-// Warp roles (23 warps, one CTA per SM):
-//   warps 0-15  dequant, two sets of 8: set w/8 takes the pairs p with p % 2 == set.  Warp w of a
-//               set converts unit (w/4)%2 of the pair, lane quarter w%4 (columns 32(w%4)..+31),
-//               all 128 k, into the set's TMEM A buffer (two tcgen05.st 32x32b.x32).  Warp 0 of
-//               the set also acquires the pair's activation slice (xfull) before its a_full
-//               arrive, so the MMA warp waits on a_full only.
-//   warps 16-19 epilogue: once per tile segment, tcgen05.ld of the accumulator (lane quarter
-//               w-16); the tile output, or the stream-K partial + deterministic last-arriver fix-up.
-//   warp 20     TMA producer: weight records into the NS-stage ring (L2 evict-first).
-//   warp 21     activation stager: per pair one or two 3-D tensor TMAs (64 k x 16 rows boxes,
-//               128-byte rows, 128B swizzle) landing directly in the K-major SW128 operand layout.
-//   warps 22-23 MMA issuers, warp 22 + p%2 takes pair p (= dequant set p % 2): 16 x
-//               tcgen05.mma kind::f16 (M=128, N=16, K=16, A from TMEM) + one commit, which frees
-//               the pair's A buffer and activation slot.  Each issuer accumulates into its own
-//               segment accumulator (double-buffered across segments); per segment it commits
-//               (or, if none of its units lies in the segment, plainly arrives) once on d_full,
-//               and the epilogue adds the two partial sums.  Two issuers on two SMSPs: one warp
-//               issuing all MMAs among four dequant warps per SMSP took ~1100 cycles per pair.
-constexpr int kSetWarps = 8, kEpiWarp0 = 16, kProdWarp = 20, kStageWarp = 21, kMmaWarp = 22;
-constexpr int kGemvThreads = 24 * 32;
-
-template <int G>
-struct TC {
-  static constexpr int KG = kUnitK / G;                      // groups per unit
-  static constexpr int UB = (int)unit_bytes_c(G);            // weight record bytes
-  static constexpr int STAGE = (UB + 127) / 128 * 128;
-#ifndef TPQ_NS
-#define TPQ_NS 20
-#endif
-#ifndef TPQ_NX
-#define TPQ_NX 4
-#endif
-  static constexpr int NS = G == 32 && TPQ_NS > 18 ? 18 : TPQ_NS;  // weight ring stages (units)
-  static constexpr int XU = kNPad * kUnitK * 2;              // activation bytes per unit (16 rows x 128 k)
-  static constexpr int NX = TPQ_NX;                          // activation pair slots
-  // unit slice = two TMA boxes (64 k, 16 rows) of 2 KB: k-half kq at kq * 2048, row m at m * 128
-  // (8-row swizzle atoms of 1024 B), 16-byte chunk swizzled by m % 8
-  static constexpr int AU = kUnitK / 2;                      // f16x2 A columns per unit
-  static constexpr int NA = 3;                               // TMEM A pair buffers: pair p in p % NA
-  static constexpr int NAF = 6;                              // a_full barriers: pair p on p % 6 (= lcm(NA, 2))
-  // Phase-parity waits need the awaited completion to be the latest one of its barrier.
-  //  * a_full(p) on barrier p % 6: the previous completion there, pair p - 6, belongs to the same
-  //    dequant set and MMA warp, which consumed it before waiting on pair p; the set's arrivals for
-  //    p follow its wait on done(p - 3), which implies a_full(p - 3) and hence a_full(p - 6).
-  //  * done(p) on barrier p % RD (one tcgen05.commit per pair, two MMA warps: out of order across
-  //    sets).  Dequant set, waiting on done(p - NA) to reuse A buffer p % NA: the next completion
-  //    there, pair p - NA + RD >= p, needs a_full of a pair >= p, i.e. this set's own arrival for p,
-  //    or (other set) done(p) first.  Stager, waiting on done(p - NX): the next one, p - NX + RD,
-  //    needs its own later TMA load.
-  static constexpr int RD = 6;
-  static_assert(RD >= NX && RD >= NA + 2, "done ring aliasing");
-  static constexpr int TCOLS = 512;
-  static constexpr int DC = 4 * kNPad;                       // segment accumulators [2 buffers][2 issuers] x 16 columns
-  static_assert(DC + NA * 2 * AU <= TCOLS, "TMEM budget");
-  static constexpr int XRING = 0;                            // 1024-aligned (swizzle atoms)
-  static constexpr int WRING = NX * 2 * XU;                  // weight stages
-  static constexpr int BARS = WRING + NS * STAGE;
-  static constexpr int SMEM = BARS + 8 * (2 * NS + NX + NAF + RD + 4);
-};
-
-struct GemvArgs {
-  const uint8_t* packed;
-  const __half* x;  // activations [>= M rows][ldx] fp16 row-major (register-dequant GEMV)
-  int64_t ldx;
-  int M;
-  int NT, NKB;      // tiles, k-blocks per tile
-  int64_t U;        // NT * NKB units
-  int grid;
-  __half* out;      // [M][out_ld] row-major
-  int64_t out_ld;
-  float* ws;
-  int* cnt;
-  int fixk;         // tcgen05 GEMV: 1 = split tiles are reduced by k_mm_fixup after the kernel (no atomics)
-  int sshift;       // A = s (q - z) 2^-sshift (host: keeps s 2^(24 - sshift) in fp16 range); the
-                    // epilogue multiplies the fp32 accumulator by 2^sshift
-};
-
+// ------------------------------------------------------------------ stream-K partition
+// CTA c of `grid` owns units [c U / grid, (c + 1) U / grid) of a layer.
 __device__ __forceinline__ int64_t cta_start(int64_t c, int64_t U, int grid) { return c * U / grid; }
 // CTA owning unit u under cta_start (inverse of the floor partition).
 __device__ __forceinline__ int cta_of_unit(int64_t u, int64_t U, int grid) {
@@ -372,411 +247,23 @@ __device__ __forceinline__ int cta_of_unit(int64_t u, int64_t U, int grid) {
 __device__ __forceinline__ uint32_t h2u(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
 __device__ __forceinline__ __half2 u2h(uint32_t u) { return *reinterpret_cast<__half2*>(&u); }
 
-template <int G>
-__global__ void __launch_bounds__(kGemvThreads, 1) k_dqgemv(const GemvArgs a, const __grid_constant__ CUtensorMap xmap) {
-  using C = TC<G>;
-  extern __shared__ __align__(1024) uint8_t smem[];
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BARS);
-  uint64_t* full = bars;               // [NS] weight record landed (TMA transaction bytes)
-  uint64_t* empty = full + C::NS;      // [NS] the 4 dequant warps of the unit hold their codes
-  uint64_t* xfull = empty + C::NS;     // [NX] the pair's activation slices landed (TMA bytes)
-  uint64_t* a_full = xfull + C::NX;    // [NAF] the pair's A operands stored (8 dequant warps)
-  uint64_t* done = a_full + C::NAF;    // [RD] pair p's MMAs completed (tcgen05.commit): frees its
-                                       //      A buffer and activation slot
-  uint64_t* d_full = done + C::RD;     // [2] segment accumulators final (commit or plain arrive of each MMA warp)
-  uint64_t* d_empty = d_full + 2;      // [2] epilogue read it (4 warps)
-  __shared__ uint32_t s_tmem;
-  __shared__ int s_last;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t u0 = cta_start(blockIdx.x, a.U, a.grid);
-  const int nu = (int)(cta_start(blockIdx.x + 1, a.U, a.grid) - u0);
-  const int np = (nu + 1) / 2;  // pairs (the last one may hold a single unit)
 
-  if (threadIdx.x == 0) {
-    unsigned smid;
-    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-    TPQ_CTA(0, gtime())
-    TPQ_CTA(3, smid)
-    for (int s = 0; s < C::NS; ++s) {
-      mbar_init(full + s, 1);
-      mbar_init(empty + s, 4);  // the 4 warps (one per lane quarter) converting the unit
-    }
-    for (int s = 0; s < C::NX; ++s) mbar_init(xfull + s, 1);
-    for (int b = 0; b < C::NAF; ++b) mbar_init(a_full + b, kSetWarps);
-    for (int r = 0; r < C::RD; ++r) mbar_init(done + r, 1);
-    for (int d = 0; d < 2; ++d) {
-      mbar_init(d_full + d, 2);
-      mbar_init(d_empty + d, 4);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == kMmaWarp) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)),
-                 "n"(C::TCOLS)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  pdl_launch_dependents();
-  const uint32_t tmem = __shfl_sync(0xffffffffu, s_tmem, 0);  // warp-uniform TMEM base
-  // TMEM columns: segment accumulator of buffer d, MMA warp w at (2d + w) * 16; A pair buffer b at
-  // kA0 + b * 2AU (unit h at + h AU)
-  constexpr uint32_t kA0 = C::DC;
+struct GemvArgs {
+  const uint8_t* packed;
+  int M;
+  int NT, NKB;      // tiles, k-blocks per tile
+  int64_t U;        // NT * NKB units
+  int grid;
+  __half* out;      // [M][out_ld] row-major
+  int64_t out_ld;
+  float* ws;        // [grid][2 slots][16][128] fp32 split-tile partials (slot 0 = first segment, 1 = last)
+  int sshift;       // A = s (q - z) 2^-sshift (host: keeps s 2^(24 - sshift) in fp16 range); the
+                    // epilogue multiplies the fp32 accumulator by 2^sshift
+};
 
-  if (warp < 2 * kSetWarps) {
-    // ===================== dequant: int4 -> fp16 s (q - z) 2^-e -> TMEM A =====================
-    // Per word: masks give the subnormal f16x2 q 2^-24 (nibbles at bits 0-3) and q 2^-20 (bits
-    // 4-7); one HFMA2 each with S = s 2^(24-e) resp. s 2^(20-e) and C = -z s 2^-e.
-    const int set = warp / kSetWarps, qw = warp & 3, h = (warp >> 2) & 1;
-    const int col = qw * 32 + lane;  // weight column of the tile = TMEM lane
-    const uint32_t a_col0 = tmem + ((uint32_t)(qw * 32) << 16) + kA0 + h * C::AU;  // + (p % NA) * 2AU
-    const int zbyte = kUnitK * kTileCols / 2 + C::KG * 256 + (col >> 1), zsh = 4 * (col & 1);
-    const bool xw = (warp & 7) == 0;  // acquires the pair's activation slice for the MMA warp
-    const float se = exp2f((float)-a.sshift), s24 = 16777216.f * se, s20 = 1048576.f * se;
-    TPQ_PDECL
-    int i = 2 * set + h;  // unit of this warp in pair p = set, set + 2, ...: i = 2p + h
-    int s = i % C::NS;
-    uint32_t ph = (uint32_t)((i / C::NS) & 1);
-    int slot = set % C::NA;
-    for (int p = set; p < np; p += 2) {
-      const uint32_t a_col = a_col0 + slot * 2 * C::AU;
-      if (i < nu) {
-        TPQ_W(full + s, ph, 0);
-        TPQ_EV(0, i)
-        const uint8_t* st = smem + C::WRING + s * C::STAGE;
-        __half2 sl[C::KG], sh[C::KG], zc[C::KG];
-#pragma unroll
-        for (int g = 0; g < C::KG; ++g) {
-          const float z = (float)((st[zbyte + g * 64] >> zsh) & 0xFu);
-          const float sf = __half2float(*reinterpret_cast<const __half*>(st + kUnitK * kTileCols / 2 + g * 256 + 2 * col));
-          sl[g] = __float2half2_rn(sf * s24);  // exact: power-of-two scaling inside the fp16 range
-          sh[g] = __float2half2_rn(sf * s20);
-          zc[g] = __float2half2_rn(-z * sf * se);
-        }
-        uint4 cw[4];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) cw[c] = *reinterpret_cast<const uint4*>(st + code_block(c, col) * 16);
-        {
-          // release the weight stage early (releasing it after the dequant costs ~2 us per forward)
-          uint32_t dep = cw[0].x ^ cw[1].y ^ cw[2].z ^ cw[3].w;
-#pragma unroll
-          for (int g = 0; g < C::KG; ++g) dep ^= h2u(sl[g]) ^ h2u(zc[g]);
-          release_loaded(empty + s, dep, lane, a.ws, a.M);
-        }
-#ifdef TPQ_EXP_NODQ
-        if (p >= C::NA) TPQ_W(done + (p - C::NA) % C::RD, (uint32_t)(((p - C::NA) / C::RD) & 1), 1);
-        if (cw[0].x == 0x12345678u && cw[3].w == 0x9abcdef0u && sl[0].x == __half(0.f) && zc[0].y == __half(1.f)) a.ws[threadIdx.x] = 0.f;
-#else
-#pragma unroll
-        for (int kh = 0; kh < 2; ++kh) {
-          uint32_t r[32];
-#pragma unroll
-          for (int w = 0; w < 8; ++w) {
-            const int j = (64 * kh + 8 * w) / G;  // group of the word within the unit
-            const uint4 c4 = cw[2 * kh + w / 4];
-            const uint32_t x = (w & 3) == 0 ? c4.x : (w & 3) == 1 ? c4.y : (w & 3) == 2 ? c4.z : c4.w;
-            const uint32_t x8 = x >> 8;
-            // nibble order of a word (internal.h): (k0,k0+1) bits 0-3, (k0+2,k0+3) bits 4-7; the same of x >> 8
-            // nibble order of a word (internal.h): (k0,k0+1) bits 0-3, (k0+2,k0+3) bits 4-7; the same of x >> 8
-            r[4 * w + 0] = h2u(__hfma2(u2h(x & 0x000F000Fu), sl[j], zc[j]));
-            r[4 * w + 1] = h2u(__hfma2(u2h(x & 0x00F000F0u), sh[j], zc[j]));
-            r[4 * w + 2] = h2u(__hfma2(u2h(x8 & 0x000F000Fu), sl[j], zc[j]));
-            r[4 * w + 3] = h2u(__hfma2(u2h(x8 & 0x00F000F0u), sh[j], zc[j]));
-          }
-          TPQ_EV(1, i)
-          if (kh == 0) {
-            if (p >= C::NA) TPQ_W(done + (p - C::NA) % C::RD, (uint32_t)(((p - C::NA) / C::RD) & 1), 1);  // A free
-            tc_fence_after();
-          }
-          TPQ_EV(2, i)
-          tmem_st32(a_col + kh * 32, r);  // column c <-> k = 2c, 2c+1
-        }
-#endif
-      } else if (p >= C::NA) {
-        // no unit (odd tail): still order this arrive after pair p - NA's a_full phase completed
-        TPQ_W(done + (p - C::NA) % C::RD, (uint32_t)(((p - C::NA) / C::RD) & 1), 1);
-      }
-      TPQ_T0(st)
-      tmem_wait_st();
-      TPQ_T1(st, 2)
-      if (xw) TPQ_W(xfull + p % C::NX, (uint32_t)((p / C::NX) & 1), 3);  // activations landed (acquire)
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(a_full + p % C::NAF);  // release: A stored, activations visible
-      TPQ_EV(3, 2 * p)
-      i += 4;
-      slot = slot + 2 >= C::NA ? slot + 2 - C::NA : slot + 2;
-      s += 4;
-      if (s >= C::NS) {
-        s -= C::NS;
-        ph ^= 1u;
-      }
-    }
-    TPQ_PFLUSH(0)
-  } else if (warp < kProdWarp) {
-    // ===================== epilogue: once per tile segment =====================
-    const int qw = warp - kEpiWarp0, col = qw * 32 + lane;
-    const uint32_t lane_base = (uint32_t)(qw * 32) << 16;
-    pdl_wait();  // the output may still be read by the previous kernel in the stream
-    TPQ_PDECL
-    int64_t seg_start = u0;
-    int kb = (int)(u0 % a.NKB), tile = (int)(u0 / a.NKB), seg = 0;
-    for (int i = 0; i < nu; ++i) {
-      if (kb == a.NKB - 1 || i == nu - 1) {  // unit i closes a segment
-        const int d = seg & 1;
-        TPQ_W(d_full + d, (uint32_t)((seg >> 1) & 1), 0);
-        TPQ_EV(0, seg)
-        tc_fence_after();
-        // partial sums of the MMA warps that own a unit of the segment (units seg_start - u0 .. i)
-        const int lo = (int)(seg_start - u0);
-        const bool w0 = i - lo >= 3 || ((lo >> 1) & 1) == 0 || ((i >> 1) & 1) == 0;
-        const bool w1 = i - lo >= 3 || ((lo >> 1) & 1) == 1 || ((i >> 1) & 1) == 1;
-        uint32_t v[kNPad], v1[kNPad];
-        const uint32_t dcol = tmem + lane_base + 2 * d * kNPad;
-        if (w0) tmem_ld16(dcol, v);
-        if (w1) tmem_ld16(dcol + kNPad, v1);
-        tmem_wait_ld();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(d_empty + d);
-        const float up = exp2f((float)a.sshift);  // undo the operand shift 2^-e (exact)
-#pragma unroll
-        for (int m = 0; m < kNPad; ++m)
-          v[m] = __float_as_uint(up * (w0 ? (w1 ? __uint_as_float(v[m]) + __uint_as_float(v1[m]) : __uint_as_float(v[m]))
-                                          : __uint_as_float(v1[m])));
-        const int64_t n = (int64_t)tile * kTileCols + col;
-        const bool full_tile = seg_start == (int64_t)tile * a.NKB && kb == a.NKB - 1;
-        if (full_tile) {
-#pragma unroll
-          for (int m = 0; m < kNPad; ++m)
-            if (m < a.M) a.out[m * a.out_ld + n] = __float2half_rn(__uint_as_float(v[m]));
-        } else {
-          // stream-K: this CTA holds part of the tile.  Partial -> own workspace slot (slot 0 = the
-          // CTA's first segment, 1 = its last); the last of the tile's CTAs to arrive sums all
-          // partials in CTA order (deterministic) and writes the tile.
-          const int slot = (seg_start == u0) ? 0 : 1;
-          float* mine = a.ws + ((size_t)blockIdx.x * 2 + slot) * (kNPad * kTileCols);
-#pragma unroll
-          for (int m = 0; m < kNPad; ++m)
-            if (m < a.M) __stcg(mine + m * kTileCols + col, __uint_as_float(v[m]));
-          if (a.fixk) {  // reduced by k_mm_fixup after this kernel (its griddepcontrol.wait orders the stores)
-            ++seg;
-            seg_start = u0 + i + 1;
-            if (++kb == a.NKB) {
-              kb = 0;
-              ++tile;
-            }
-            continue;
-          }
-          // the 128 threads' partial stores are ordered before one acq_rel atomic by the named
-          // barrier (release cumulativity); the last arriver's acquire is passed on by the second
-          // barrier (the semaphore pattern of CUTLASS's generic barrier)
-          named_bar(1, kTileCols);
-          const int c_first = cta_of_unit((int64_t)tile * a.NKB, a.U, a.grid);
-          const int c_last = cta_of_unit((int64_t)(tile + 1) * a.NKB - 1, a.U, a.grid);
-          if (col == 0) s_last = (atom_add_acq_rel_gpu(a.cnt + tile * kCntStride, 1) == c_last - c_first);
-          named_bar(1, kTileCols);
-          TPQ_EV(1, seg)
-          if (s_last) {
-            float r[kNPad];
-#pragma unroll
-            for (int m = 0; m < kNPad; ++m) r[m] = 0.f;
-            // Contributors in CTA order; every load of a batch is issued before any add (rows >= M
-            // of a slot are allocated and ignored): predicated per-row loads were compiled into two
-            // reused registers (8 dependent L2 round trips per contributor at M = 16), and one
-            // contributor per iteration costs one round trip each.  Batches: 4 contributors x 4
-            // rows for M <= 4, 2 x 16 rows otherwise.
-            auto slot_ptr = [&](int c) {
-              return a.ws + ((size_t)c * 2 + ((cta_start(c, a.U, a.grid) / a.NKB == tile) ? 0 : 1)) * (kNPad * kTileCols) + col;
-            };
-            if (a.M <= 4) {
-              for (int c = c_first; c <= c_last; c += 4) {
-                float v2[4][4];
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                  const float* src = slot_ptr(c + q <= c_last ? c + q : c_last);
-#pragma unroll
-                  for (int m = 0; m < 4; ++m) v2[q][m] = __ldcg(src + m * kTileCols);
-                }
-#pragma unroll
-                for (int q = 0; q < 4; ++q)
-                  if (c + q <= c_last)
-#pragma unroll
-                    for (int m = 0; m < 4; ++m) r[m] += v2[q][m];
-              }
-            } else {
-              for (int c = c_first; c <= c_last; c += 2) {
-                float v2[2][kNPad];
-#pragma unroll
-                for (int q = 0; q < 2; ++q) {
-                  const float* src = slot_ptr(c + q <= c_last ? c + q : c_last);
-#pragma unroll
-                  for (int m = 0; m < kNPad; ++m) v2[q][m] = __ldcg(src + m * kTileCols);
-                }
-#pragma unroll
-                for (int q = 0; q < 2; ++q)
-                  if (c + q <= c_last)
-#pragma unroll
-                    for (int m = 0; m < kNPad; ++m) r[m] += v2[q][m];
-              }
-            }
-#pragma unroll
-            for (int m = 0; m < kNPad; ++m)
-              if (m < a.M) a.out[m * a.out_ld + n] = __float2half_rn(r[m]);
-            if (col == 0) a.cnt[tile * kCntStride] = 0;  // self-reset for the next launch / graph replay
-          }
-        }
-        TPQ_EV(2, seg)
-        ++seg;
-        seg_start = u0 + i + 1;
-      }
-      if (++kb == a.NKB) {
-        kb = 0;
-        ++tile;
-      }
-    }
-    TPQ_PFLUSH(5)
-  } else if (warp == kProdWarp) {
-    // ===================== TMA producer (warp-uniform loop, one elected lane issues) ===========
-    // Weight records do not depend on the previous kernel: the first NS are requested before any
-    // griddepcontrol.wait, so they overlap the tail of the previous kernel (PDL).
-    const uint64_t pw = policy_evict_first();
-    TPQ_PDECL
-#ifndef TPQ_PRE
-#define TPQ_PRE 64
-#endif
-    const int pre = nu < C::NS ? nu : C::NS;
-    for (int i = 0; i < pre; ++i) {
-      if (i == TPQ_PRE) pdl_wait();  // records issued before the previous kernel completed: at most TPQ_PRE
-      if (elect_one()) {
-        mbar_arrive_expect_tx(full + i, C::UB);
-        bulk_g2s(smem + C::WRING + i * C::STAGE, a.packed + (u0 + i) * C::UB, C::UB, full + i, pw);
-      }
-      __syncwarp();
-    }
-    for (int i = 0, s = 0, ph = 0; i + C::NS < nu; ++i) {  // refill as the dequant warps release
-      TPQ_W(empty + s, (uint32_t)ph, 0);
-      TPQ_EV(0, i + C::NS)
-      if (elect_one()) {
-        mbar_arrive_expect_tx(full + s, C::UB);
-        bulk_g2s(smem + C::WRING + s * C::STAGE, a.packed + (u0 + i + C::NS) * C::UB, C::UB, full + s, pw);
-      }
-      __syncwarp();
-      if (++s == C::NS) {
-        s = 0;
-        ph ^= 1;
-      }
-    }
-    TPQ_PFLUSH(10)
-  } else if (warp == kStageWarp) {
-    // ===================== activation stager (tensor TMA) =====================
-    // Slot rows >= M hold stale data; a row of B only feeds the same row of D (discarded).
-    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&xmap)) : "memory");
-    pdl_wait();  // the activations come from the previous kernel in the stream
-    if (lane == 0) { TPQ_CTA(1, gtime()) }
-    int kb = (int)(u0 % a.NKB);
-    TPQ_PDECL
-    for (int p = 0; p < np; ++p) {
-      const int x = p % C::NX, nh = (2 * p + 1 < nu) ? 2 : 1;
-      const int kb1 = kb + 1 == a.NKB ? 0 : kb + 1;
-      if (p >= C::NX) TPQ_W(done + (p - C::NX) % C::RD, (uint32_t)(((p - C::NX) / C::RD) & 1), 0);  // slot free
-      TPQ_EV(0, 2 * p)
-      TPQ_T0(tm)
-      if (elect_one()) {
-        mbar_arrive_expect_tx(xfull + x, nh * C::XU);
-        tma_load_3d(smem + C::XRING + 2 * x * C::XU, &xmap, 0, 0, 2 * kb, xfull + x);
-        if (nh == 2) tma_load_3d(smem + C::XRING + (2 * x + 1) * C::XU, &xmap, 0, 0, 2 * kb1, xfull + x);
-      }
-      __syncwarp();
-      TPQ_T1(tm, 1)
-      kb = nh == 2 ? (kb1 + 1 == a.NKB ? 0 : kb1 + 1) : kb1;
-    }
-    TPQ_PFLUSH(15)
-  } else {
-    // ===================== MMA issuers (warp-uniform operands, one elected lane issues) ========
-    const int w = warp - kMmaWarp;  // takes the pairs p % 2 == w (dequant set w)
-    const uint32_t xring = smem_u32(smem + C::XRING);
-    const int kb0 = (int)(u0 % a.NKB);
-    const int nseg = (kb0 + nu - 1) / a.NKB + 1;  // segment of unit i: (kb0 + i) / NKB
-    TPQ_PDECL
-    int sw = 0;  // next segment this warp has not yet closed on d_full
-    // close segment sw without a unit in it: plain arrive once the epilogue drained segment sw - 2
-    auto skip_seg = [&]() {
-      TPQ_W(d_empty + (sw & 1), (uint32_t)(((sw >> 1) & 1) ^ 1), 0);
-      if (lane == 0) mbar_arrive(d_full + (sw & 1));
-      __syncwarp();
-      ++sw;
-    };
-    static_assert(C::XU == 4096 && C::AU == 64, "umma_unit16 offsets");
-    for (int p = w; p < np; p += 2) {
-      const int x = p % C::NX;
-      const uint64_t bd0 = bdesc_sw128(xring + 2 * x * C::XU);
-      // fast path: both units of the pair inside one segment that this warp already opened and
-      // does not close here (sg == sw, previous unit of this warp in sg, next one too)
-      const int i0 = 2 * p, sg = (kb0 + i0) / a.NKB;
-      const int lo = sg * a.NKB - kb0 > 0 ? sg * a.NKB - kb0 : 0;
-      const int hi = (sg + 1) * a.NKB - kb0 - 1 < nu - 1 ? (sg + 1) * a.NKB - kb0 - 1 : nu - 1;
-      const bool fast = sg == sw && i0 - 3 >= lo && i0 + 4 <= hi;
-      const uint32_t at = tmem + kA0 + (p % C::NA) * 2 * C::AU;
-      TPQ_W(a_full + p % C::NAF, (uint32_t)((p / C::NAF) & 1), 1);  // A stored + activations landed
-      TPQ_EV(1, 2 * p)
-      tc_fence_after();
-      if (fast) {
-        const uint32_t dt = tmem + (2 * (sg & 1) + w) * kNPad;
-        if (elect_one()) {
-          umma_unit16(dt, at, bd0, kIdesc, 1u);
-          umma_unit16(dt, at + C::AU, bd0 + (C::XU >> 4), kIdesc, 1u);
-          umma_commit1(done + p % C::RD);
-        }
-        __syncwarp();
-        TPQ_EV(3, 2 * p)
-        continue;
-      }
-#pragma unroll 1
-      for (int h = 0; h < 2; ++h) {
-        const int i = 2 * p + h;
-        if (i >= nu) break;
-        const int sg = (kb0 + i) / a.NKB;
-        while (sw < sg) skip_seg();
-        const int lo = sg * a.NKB - kb0 > 0 ? sg * a.NKB - kb0 : 0;
-        const int hi = (sg + 1) * a.NKB - kb0 - 1 < nu - 1 ? (sg + 1) * a.NKB - kb0 - 1 : nu - 1;
-        const bool first = (h ? i - 1 : i - 3) < lo, last = (h ? i + 3 : i + 1) > hi;  // this warp's units of sg
-        const int d = sg & 1;
-        if (first) {
-          TPQ_W(d_empty + d, (uint32_t)(((sg >> 1) & 1) ^ 1), 0);  // epilogue drained segment sg - 2
-          tc_fence_after();
-        }
-        const uint32_t dt = tmem + (2 * d + w) * kNPad;
-        if (elect_one()) {
-          umma_unit16(dt, at + h * C::AU, bd0 + (uint64_t)((h * C::XU) >> 4), kIdesc, first ? 0u : 1u);
-          if (last) umma_commit1(d_full + d);
-        }
-        __syncwarp();
-        if (last) ++sw;
-      }
-      if (elect_one()) umma_commit1(done + p % C::RD);
-      __syncwarp();
-      TPQ_EV(3, 2 * p)
-    }
-    while (sw < nseg) skip_seg();
-    TPQ_PFLUSH(20)
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (threadIdx.x == 0) { TPQ_CTA(2, gtime()) }
-  if (warp == kMmaWarp) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::TCOLS) : "memory");
-  }
-}
-
-// ------------------------------------------------------------------ GEMV v2 (M <= 16), lean issue
-// Same records, operand arithmetic, MMA issue and stream-K split as k_dqgemv; what changes is the
-// instruction count per unit, which ncu showed to be the limit (profiles/r02_summary.md: 1521 warp
-// instructions per 128 x 128 unit = 380 per SMSP against the ~378 cycles one unit may take at HBM
-// speed; the dequant loop alone ~250 per warp-unit for ~150 of conversion):
+// ------------------------------------------------------------------ GEMV (M <= 16)
+// Designed for issue: round 1's GEMV spent 1521 warp instructions per 128 x 128 unit, 380 per SMSP
+// against the ~378 cycles one unit may take at HBM speed (profiles/r02_summary.md); this one:
 //   * dequant in THREE sets of FOUR warps (one per SMSP / TMEM lane quarter); a warp converts its
 //     32 columns of BOTH units of a pair per iteration, so waits, hand-offs and index arithmetic are
 //     paid once per pair; set s owns TMEM A buffer s and the pairs p = s, s + 3, ...;
@@ -785,11 +272,11 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_dqgemv(const GemvArgs a, co
 //   * the epilogue walks tile segments, not units.
 // Warps 0-3 epilogue, 4-15 dequant, 16 TMA producer, 17 activation stager, 18-19 MMA issuers: the
 // SMSP arbiter prefers higher warp ids, so the warps that only wait sit lowest.
-constexpr int kV2Sets = 3, kV2Deq0 = 4, kV2Prod = 16, kV2Stage = 17, kV2Mma = 18;
-constexpr int kV2Threads = 20 * 32;
+constexpr int kSets = 3, kDeq0 = 4, kProdWarp = 16, kStageWarp = 17, kMmaWarp = 18;
+constexpr int kGemvThreads = 20 * 32;
 
 template <int G>
-struct TC2 {
+struct TC {
   static constexpr int KG = kUnitK / G;
   static constexpr int UB = (int)unit_bytes_c(G);
   static constexpr int STAGE = (UB + 127) / 128 * 128;
@@ -805,10 +292,10 @@ struct TC2 {
   // done(p) on barrier p % RD.  Dequant set p % 3 waits done(p - 3) before overwriting its buffer:
   // the next completion there, p + 3, needs this set's own a_full(p + 3).  The stager waits
   // done(p - NX) before reusing slot p % NX: the next one, p - NX + RD >= p, needs its own later load.
-  static_assert(RD % kV2Sets == 0 && RD >= NX, "done ring aliasing");
+  static_assert(RD % kSets == 0 && RD >= NX, "done ring aliasing");
   static constexpr int TCOLS = 512;
   static constexpr int DC = 4 * kNPad;            // [2 segment buffers][2 issuers] x 16 columns
-  static_assert(DC + kV2Sets * 2 * AU <= TCOLS, "TMEM budget");
+  static_assert(DC + kSets * 2 * AU <= TCOLS, "TMEM budget");
   static constexpr int XRING = 0;
   static constexpr int WRING = NX * 2 * XU;
   static constexpr int BARS = WRING + NS * STAGE;
@@ -816,8 +303,8 @@ struct TC2 {
 };
 
 template <int G>
-__global__ void __launch_bounds__(kV2Threads, 1) k_dqgemv2(const GemvArgs a, const __grid_constant__ CUtensorMap xmap) {
-  using C = TC2<G>;
+__global__ void __launch_bounds__(kGemvThreads, 1) k_dqgemv(const GemvArgs a, const __grid_constant__ CUtensorMap xmap) {
+  using C = TC<G>;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BARS);
   uint64_t* full = bars;                // [NS] weight record landed
@@ -851,7 +338,7 @@ __global__ void __launch_bounds__(kV2Threads, 1) k_dqgemv2(const GemvArgs a, con
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == kV2Mma) {
+  if (warp == kMmaWarp) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&s_tmem)),
                  "n"(C::TCOLS)
                  : "memory");
@@ -864,9 +351,9 @@ __global__ void __launch_bounds__(kV2Threads, 1) k_dqgemv2(const GemvArgs a, con
   const uint32_t tmem = __shfl_sync(0xffffffffu, s_tmem, 0);
   constexpr uint32_t kA0 = C::DC;  // A buffer of set s at kA0 + s * 2AU (unit h of the pair at + h AU)
 
-  if (warp >= kV2Deq0 && warp < kV2Prod) {
+  if (warp >= kDeq0 && warp < kProdWarp) {
     // ===================== dequant: set = warp / 4 - 1 takes pairs p = set, set + 3, ... =========
-    const int set = (warp - kV2Deq0) >> 2, qw = warp & 3;
+    const int set = (warp - kDeq0) >> 2, qw = warp & 3;
     const int col = qw * 32 + lane;
     const uint32_t a_buf = tmem + ((uint32_t)(qw * 32) << 16) + kA0 + set * 2 * C::AU;
     const int zbyte = kUnitK * kTileCols / 2 + C::KG * 256 + (col >> 1), zsh = 4 * (col & 1);
@@ -875,7 +362,7 @@ __global__ void __launch_bounds__(kV2Threads, 1) k_dqgemv2(const GemvArgs a, con
     const float se = exp2f((float)-a.sshift), s24 = 16777216.f * se, s20 = 1048576.f * se;
     int st = (2 * set) % C::NS;                       // stage of unit 2p
     uint32_t ph = (uint32_t)(((2 * set) / C::NS) & 1);
-    for (int p = set; p < np; p += kV2Sets) {
+    for (int p = set; p < np; p += kSets) {
       TPQ_EV(0, p)
 #pragma unroll 1
       for (int h = 0; h < 2; ++h) {
@@ -912,10 +399,10 @@ __global__ void __launch_bounds__(kV2Threads, 1) k_dqgemv2(const GemvArgs a, con
             r[4 * w + 2] = h2u(__hfma2(u2h(x8 & 0x000F000Fu), sl[j], zc[j]));
             r[4 * w + 3] = h2u(__hfma2(u2h(x8 & 0x00F000F0u), shh[j], zc[j]));
           }
-          if (h == 0 && kh == 0 && p >= kV2Sets) {
+          if (h == 0 && kh == 0 && p >= kSets) {
             // own buffer free: pair p - 3's MMAs completed
-            const int q = p - kV2Sets;
-            mbar_wait_backoff(done + q % C::RD, (uint32_t)((q / C::RD) & 1), TPQ_DONE_NS);
+            const int q = p - kSets;
+            mbar_wait_backoff(done + q % C::RD, (uint32_t)((q / C::RD) & 1), 0);
             TPQ_EV(2, p)
             tc_fence_after();
           }
@@ -931,13 +418,13 @@ __global__ void __launch_bounds__(kV2Threads, 1) k_dqgemv2(const GemvArgs a, con
       __syncwarp();
       if (lane == 0) mbar_arrive(a_full + p % C::NAF);
       TPQ_EV(3, p)
-      st += 2 * kV2Sets;
+      st += 2 * kSets;
       if (st >= C::NS) {
         st -= C::NS;
         ph ^= 1u;
       }
     }
-  } else if (warp < kV2Deq0) {
+  } else if (warp < kDeq0) {
     // ===================== epilogue: once per tile segment =====================
     const int qw = warp, col = qw * 32 + lane;
     const uint32_t lane_base = (uint32_t)(qw * 32) << 16;
@@ -951,7 +438,7 @@ __global__ void __launch_bounds__(kV2Threads, 1) k_dqgemv2(const GemvArgs a, con
       const int64_t seg_end = tile_end < uend ? tile_end : uend;  // exclusive
       const int lo = (int)(seg_start - u0), hi = (int)(seg_end - 1 - u0);
       const int d = seg & 1;
-      mbar_wait_backoff(d_full + d, (uint32_t)((seg >> 1) & 1), TPQ_EPI_NS);
+      mbar_wait_backoff(d_full + d, (uint32_t)((seg >> 1) & 1), 256);
       tc_fence_after();
       const bool w0 = hi - lo >= 3 || ((lo >> 1) & 1) == 0 || ((hi >> 1) & 1) == 0;
       const bool w1 = hi - lo >= 3 || ((lo >> 1) & 1) == 1 || ((hi >> 1) & 1) == 1;
@@ -982,7 +469,7 @@ __global__ void __launch_bounds__(kV2Threads, 1) k_dqgemv2(const GemvArgs a, con
       }
       seg_start = seg_end;
     }
-  } else if (warp == kV2Prod) {
+  } else if (warp == kProdWarp) {
     // ===================== TMA producer =====================
     const uint64_t pw = policy_evict_first();
     const int pre = nu < C::NS ? nu : C::NS;
@@ -1007,7 +494,7 @@ __global__ void __launch_bounds__(kV2Threads, 1) k_dqgemv2(const GemvArgs a, con
         ph ^= 1;
       }
     }
-  } else if (warp == kV2Stage) {
+  } else if (warp == kStageWarp) {
     // ===================== activation stager =====================
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&xmap)) : "memory");
     pdl_wait();
@@ -1026,8 +513,8 @@ __global__ void __launch_bounds__(kV2Threads, 1) k_dqgemv2(const GemvArgs a, con
       kb = nh == 2 ? (kb1 + 1 == a.NKB ? 0 : kb1 + 1) : kb1;
     }
   } else {
-    // ===================== MMA issuers: warp kV2Mma + w takes the pairs p % 2 == w ===============
-    const int w = warp - kV2Mma;
+    // ===================== MMA issuers: warp kMmaWarp + w takes the pairs p % 2 == w ===============
+    const int w = warp - kMmaWarp;
     const uint32_t xring = smem_u32(smem + C::XRING);
     const int kb0 = (int)(u0 % a.NKB);
     const int nseg = (kb0 + nu - 1) / a.NKB + 1;
@@ -1040,7 +527,7 @@ __global__ void __launch_bounds__(kV2Threads, 1) k_dqgemv2(const GemvArgs a, con
     };
     static_assert(C::XU == 4096 && C::AU == 64, "umma_unit16 offsets");
     for (int p = w; p < np; p += 2) {
-      const int x = p % C::NX, b = p % kV2Sets;
+      const int x = p % C::NX, b = p % kSets;
       const uint64_t bd0 = bdesc_sw128(xring + 2 * x * C::XU);
       const int i0 = 2 * p, sg = (kb0 + i0) / a.NKB;
       const int lo = sg * a.NKB - kb0 > 0 ? sg * a.NKB - kb0 : 0;
@@ -1048,7 +535,7 @@ __global__ void __launch_bounds__(kV2Threads, 1) k_dqgemv2(const GemvArgs a, con
       const bool fast = sg == sw && i0 - 3 >= lo && i0 + 4 <= hi;
       const uint32_t at = tmem + kA0 + b * 2 * C::AU;
       TPQ_EV(0, p)
-      mbar_wait_backoff(a_full + p % C::NAF, (uint32_t)((p / C::NAF) & 1), TPQ_MMA_NS);
+      mbar_wait_backoff(a_full + p % C::NAF, (uint32_t)((p / C::NAF) & 1), 0);
       TPQ_EV(1, p)
       tc_fence_after();
       if (fast) {
@@ -1093,319 +580,9 @@ __global__ void __launch_bounds__(kV2Threads, 1) k_dqgemv2(const GemvArgs a, con
   tc_fence_before();
   __syncthreads();
   if (threadIdx.x == 0) { TPQ_CTA(2, gtime()) }
-  if (warp == kV2Mma) {
+  if (warp == kMmaWarp) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::TCOLS) : "memory");
-  }
-}
-
-// ------------------------------------------------------------------ GEMV, register-dequant path (M <= 16)
-// k_dqgemv_r<G, NB, NSETS, WPS>: the product path for M <= 16.  Same weight records, same operand
-// arithmetic (A = fp16(s (q - z) 2^-e) from one HFMA2 per f16x2 pair, fp32 accumulation over a whole
-// tile segment, x 2^e in the epilogue), but the dequantized operand never leaves registers: each
-// warp turns its columns' codes into mma.sync.m16n8k16 A fragments and multiplies them with the
-// activation fragments right away.  The tcgen05 GEMV above spends most of its time in the
-// dequant -> TMEM -> MMA -> commit -> dequant hand-off chain (profiles/r01_summary.md: dequant warps
-// wait 63-73 % on "A free", MMA warps 71-82 % on "A full"); at M <= 16 (3.8-61 flop/B, HBM-bound)
-// the contraction needs < 3 % of the tensor pipe, and the register path has no cross-warp hand-off
-// besides the TMA ring (tools/probe_hmma_gemv.cu: 214-300 cycles per 128 x 128 unit per SM from
-// shared memory, against ~350-378 cycles of HBM time per unit).
-//
-// Fragment mapping.  m16n8k16 "row.col": A rows = 16 weight columns (c0 = 16 b + g, c1 = c0 + 8 of
-// the warp's CW columns), B columns = batch rows n = 8 nb + g, k = 16 per step.  The k order inside
-// a step is free as long as A and B agree: thread (g = lane / 4, t = lane % 4) holds, for k-step
-// s = 2e + h (e, h in 0..3, 0..1), the physical k = 32 t + 4 s + {0, 1} (virtual 2t, 2t+1) and
-// 32 t + 4 s + {2, 3} (virtual 2t+8, 2t+9).  So a thread reads one 16-byte code chunk per column
-// (chunk t of the record, internal.h: word e = k 32t + 8e .. +7) and 64 contiguous activation bytes
-// per batch row (k 32 t .. 32 t + 31), both with 128-bit shared loads.
-//
-// Work split.  A CTA per SM holds NSETS independent stream-K participants (sets of WPS warps, each
-// warp CW = 128 / WPS columns of every unit), p = blockIdx.x * NSETS + set, over contiguous unit
-// ranges [p U / P, (p + 1) U / P).  One producer warp fills every set's ring of D stages (weight
-// record by 1-D bulk TMA, L2 evict-first; the unit's activation slice, XR = 8 NB rows x 128 k, by
-// one 3-D tensor TMA with 128-byte swizzle).  A tile split between participants leaves fp32
-// partials in fragment order; the last arriver sums them in participant order (deterministic).
-template <int G, int NB, int NSETS, int WPS>
-struct TR {
-  static constexpr int CW = kTileCols / WPS;  // columns per warp
-  static constexpr int BLK = CW / 16;         // 16-column MMA blocks per warp
-  static constexpr int KG = kUnitK / G;       // groups per unit
-  static constexpr int UB = (int)unit_bytes_c(G);
-  static constexpr int STAGE = (UB + 127) / 128 * 128;
-#ifndef TPQ_RD
-#define TPQ_RD 16
-#endif
-  static constexpr int D0 = (222 * 1024) / (NSETS * STAGE);
-  static constexpr int D = D0 > TPQ_RD ? TPQ_RD : D0;  // ring stages per set
-  static_assert(D >= 2, "GEMV ring needs >= 2 stages per set");
-  static constexpr int BARS = NSETS * D * STAGE;
-  static constexpr int SMEM = BARS + 16 * NSETS * D;
-  static constexpr int WARPS = NSETS * (WPS + 1);     // WPS consumers + one producer per set
-  static constexpr int PART = WPS * BLK * NB * 128;  // fp32 partial floats per participant slot
-  static_assert(PART <= kNPad * kTileCols, "partial slot size");
-};
-
-__device__ __forceinline__ void hmma16816(float* d, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
-                                          uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
-      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
-}
-__device__ __forceinline__ uint32_t u4w(const uint4& v, int e) { return e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w; }
-
-template <int G, int NB, int NSETS, int WPS>
-__global__ void __launch_bounds__(TR<G, NB, NSETS, WPS>::WARPS * 32, 1)
-    k_dqgemv_r(const GemvArgs a) {
-  using C = TR<G, NB, NSETS, WPS>;
-  extern __shared__ __align__(1024) uint8_t smem[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::BARS);  // [NSETS][D] record + slice landed
-  uint64_t* empty = full + NSETS * C::D;                          // [NSETS][D] the set's WPS warps read it
-  __shared__ int s_last[NSETS];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int P = a.grid * NSETS;
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < NSETS * C::D; ++i) {
-      mbar_init(full + i, 1);
-      mbar_init(empty + i, WPS);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  pdl_launch_dependents();
-
-  if (warp >= NSETS * WPS) {
-    // ===================== producers: one lane per set feeds the set's ring =====================
-    const int s = warp - NSETS * WPS;
-    if (lane == 0) {
-      const uint64_t pw = policy_evict_first();
-      const int p = blockIdx.x * NSETS + s;
-      const int64_t ub = cta_start(p, a.U, P);
-      const int nu = (int)(cta_start(p + 1, a.U, P) - ub);
-      uint64_t* full_s = full + s * C::D;
-      // weight records do not depend on the previous kernel: no griddepcontrol.wait here, so the
-      // first D of them overlap its tail (PDL)
-      uint64_t* empty_s = empty + s * C::D;
-      uint8_t* ring = smem + s * C::D * C::STAGE;
-      const uint8_t* src = a.packed + ub * C::UB;
-      for (int r = 0, d = 0, lap = 0; r < nu; ++r, src += C::UB) {
-#ifdef TPQ_RPSLEEP
-        if (lap) mbar_wait_sleep(empty_s + d, (uint32_t)((lap - 1) & 1));
-#else
-        if (lap) mbar_wait(empty_s + d, (uint32_t)((lap - 1) & 1));
-#endif
-        mbar_arrive_expect_tx(full_s + d, C::UB);
-        bulk_g2s(ring + d * C::STAGE, src, C::UB, full_s + d, pw);
-        if (++d == C::D) {
-          d = 0;
-          ++lap;
-        }
-      }
-    }
-    __syncwarp();
-  } else {
-    // ===================== consumers: dequant to A fragments + mma.sync =====================
-    const int set = warp / WPS, wi = warp % WPS, g = lane >> 2, t = lane & 3;
-    const int p = blockIdx.x * NSETS + set;
-    const int64_t ub = cta_start(p, a.U, P);
-    const int nu = (int)(cta_start(p + 1, a.U, P) - ub);
-    const float se = exp2f((float)-a.sshift), s24 = 16777216.f * se, s20 = 1048576.f * se;
-    const float up = exp2f((float)a.sshift);
-    const int jg = (32 * t) / G;  // group (within the unit) of this thread's k range
-    uint64_t* full_s = full + set * C::D;
-    uint64_t* empty_s = empty + set * C::D;
-    float acc[C::BLK][NB][4];
-#pragma unroll
-    for (int b = 0; b < C::BLK; ++b)
-#pragma unroll
-      for (int nb = 0; nb < NB; ++nb)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) acc[b][nb][e] = 0.f;
-    int tile = (int)(ub / a.NKB), kb = (int)(ub % a.NKB);
-    int64_t seg_start = ub;
-    pdl_wait();  // outputs / partials may still be read by the previous kernel in the stream
-    // activation fragments straight from global memory (X is <= 16 x K fp16, L2-resident): row
-    // g + 8 nb, k = 128 kb + 32 t .. + 31, four 16-byte loads per row
-    const __half* xp = a.x + (int64_t)g * a.ldx + 32 * t + (int64_t)kb * kUnitK;
-    const int64_t x8 = 8 * a.ldx;
-    const uint8_t* ring = smem + set * C::D * C::STAGE;
-    uint32_t fph = 0;  // phase parity of the set's full barriers in lap r / D
-    for (int r = 0, d = 0; r < nu; ++r) {
-      uint4 xb[NB][4];
-#pragma unroll
-      for (int nb = 0; nb < NB; ++nb)
-#pragma unroll
-        for (int i = 0; i < 4; ++i) xb[nb][i] = *reinterpret_cast<const uint4*>(xp + nb * x8 + 8 * i);
-#ifdef TPQ_RSLEEP
-      mbar_wait_sleep(full_s + d, fph);
-#else
-      mbar_wait(full_s + d, fph);
-#endif
-      const uint8_t* rec = ring + d * C::STAGE;
-      uint4 wc[C::BLK][2];
-      __half2 sl[C::BLK][2], sh[C::BLK][2], zc[C::BLK][2];
-#pragma unroll
-      for (int b = 0; b < C::BLK; ++b)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) wc[b][h] = *reinterpret_cast<const uint4*>(rec + code_block(t, wi * C::CW + 16 * b + 8 * h + g) * 16);
-      auto opnd = [&](int c, uint32_t& vl, uint32_t& vh, uint32_t& vz) {  // S = s 2^(24|20 - e), C = -z s 2^-e
-        const float sf = __half2float(*reinterpret_cast<const __half*>(rec + kUnitK * kTileCols / 2 + jg * 256 + 2 * c));
-        const float z = (float)((rec[kUnitK * kTileCols / 2 + C::KG * 256 + jg * 64 + (c >> 1)] >> (4 * (c & 1))) & 0xFu);
-        vl = h2u(__float2half2_rn(sf * s24));  // exact: power-of-two scaling inside the fp16 range
-        vh = h2u(__float2half2_rn(sf * s20));
-        vz = h2u(__float2half2_rn(-z * sf * se));
-      };
-#ifdef TPQ_RSHFL
-      if constexpr (C::KG == 1 && C::BLK == 2) {
-#else
-      if constexpr (false) {
-#endif
-        // one group per unit: the four threads t of group g need the same four columns; each computes
-        // one (b = t / 2, h = t % 2) and the others read it by shuffle
-        uint32_t vl, vh, vz;
-        opnd(wi * C::CW + 16 * (t >> 1) + 8 * (t & 1) + g, vl, vh, vz);
-#pragma unroll
-        for (int b = 0; b < 2; ++b)
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int src = (lane & ~3) | (2 * b + h);
-            sl[b][h] = u2h(__shfl_sync(0xffffffffu, vl, src));
-            sh[b][h] = u2h(__shfl_sync(0xffffffffu, vh, src));
-            zc[b][h] = u2h(__shfl_sync(0xffffffffu, vz, src));
-          }
-      } else {
-#pragma unroll
-        for (int b = 0; b < C::BLK; ++b)
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            uint32_t vl, vh, vz;
-            opnd(wi * C::CW + 16 * b + 8 * h + g, vl, vh, vz);
-            sl[b][h] = u2h(vl);
-            sh[b][h] = u2h(vh);
-            zc[b][h] = u2h(vz);
-          }
-      }
-      const int d_rel = d;
-      if (++d == C::D) {
-        d = 0;
-        fph ^= 1u;
-      }
-#pragma unroll
-      for (int e = 0; e < 4; ++e)
-#pragma unroll
-        for (int hs = 0; hs < 2; ++hs)
-#pragma unroll
-          for (int b = 0; b < C::BLK; ++b) {
-            const uint32_t y0 = hs ? u4w(wc[b][0], e) >> 8 : u4w(wc[b][0], e);
-            const uint32_t y1 = hs ? u4w(wc[b][1], e) >> 8 : u4w(wc[b][1], e);
-            const uint32_t a0 = h2u(__hfma2(u2h(y0 & 0x000F000Fu), sl[b][0], zc[b][0]));
-            const uint32_t a1 = h2u(__hfma2(u2h(y1 & 0x000F000Fu), sl[b][1], zc[b][1]));
-            const uint32_t a2 = h2u(__hfma2(u2h(y0 & 0x00F000F0u), sh[b][0], zc[b][0]));
-            const uint32_t a3 = h2u(__hfma2(u2h(y1 & 0x00F000F0u), sh[b][1], zc[b][1]));
-#pragma unroll
-            for (int nb = 0; nb < NB; ++nb)
-              hmma16816(acc[b][nb], a0, a1, a2, a3, u4w(xb[nb][e], 2 * hs), u4w(xb[nb][e], 2 * hs + 1));
-          }
-      // release the stage only now: every value read from it has been consumed by an instruction
-      // above, so no shared-memory load of this warp can still be in flight when the producer's
-      // TMA overwrites it (releasing right after the loads raced at M = 16, tools/stress_reg.py)
-      __syncwarp();
-      if (lane == 0) mbar_arrive(empty_s + d_rel);
-      if (kb == a.NKB - 1 || r == nu - 1) {  // unit r closes a tile segment
-        const bool full_tile = seg_start == (int64_t)tile * a.NKB && kb == a.NKB - 1;
-        if (full_tile) {
-#pragma unroll
-          for (int b = 0; b < C::BLK; ++b)
-#pragma unroll
-            for (int nb = 0; nb < NB; ++nb)
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const int m = 8 * nb + 2 * t + (e & 1);
-                const int64_t col = (int64_t)tile * kTileCols + wi * C::CW + 16 * b + 8 * (e >> 1) + g;
-                if (m < a.M) a.out[m * a.out_ld + col] = __float2half_rn(up * acc[b][nb][e]);
-              }
-        } else {
-          // stream-K: partial (fragment order) -> own slot (0 = the participant's first segment,
-          // 1 = its last); the last of the tile's participants sums all partials in order.
-          const int slot = (seg_start == ub) ? 0 : 1;
-          float* mine = a.ws + ((size_t)p * 2 + slot) * (kNPad * kTileCols) + wi * (C::BLK * NB * 128) + lane;
-#pragma unroll
-          for (int b = 0; b < C::BLK; ++b)
-#pragma unroll
-            for (int nb = 0; nb < NB; ++nb)
-#pragma unroll
-              for (int e = 0; e < 4; ++e) __stcg(mine + ((b * NB + nb) * 4 + e) * 32, up * acc[b][nb][e]);
-          __threadfence();
-          named_bar(1 + set, WPS * 32);
-          const int c_first = cta_of_unit((int64_t)tile * a.NKB, a.U, P);
-          const int c_last = cta_of_unit((int64_t)(tile + 1) * a.NKB - 1, a.U, P);
-          if (wi == 0 && lane == 0) s_last[set] = (atomicAdd(a.cnt + tile * kCntStride, 1) == c_last - c_first);
-          named_bar(1 + set, WPS * 32);
-          if (s_last[set]) {
-            __threadfence();
-            float rs[C::BLK][NB][4];
-#pragma unroll
-            for (int b = 0; b < C::BLK; ++b)
-#pragma unroll
-              for (int nb = 0; nb < NB; ++nb)
-#pragma unroll
-                for (int e = 0; e < 4; ++e) rs[b][nb][e] = 0.f;
-            // participants in order; Q in flight per batch (independent L2 loads)
-            constexpr int Q = 8 / (C::BLK * NB) > 1 ? 8 / (C::BLK * NB) : 1;
-            // slot of participant c: every participant after c_first starts inside the tile (slot 0)
-            const int s_first = cta_start(c_first, a.U, P) == (int64_t)tile * a.NKB ? 0 : 1;
-            for (int c0 = c_first; c0 <= c_last; c0 += Q) {
-              float v[Q][C::BLK][NB][4];
-#pragma unroll
-              for (int q = 0; q < Q; ++q) {
-                const int c = c0 + q <= c_last ? c0 + q : c_last;
-                const int cslot = c > c_first ? 0 : s_first;
-                const float* src = a.ws + ((size_t)c * 2 + cslot) * (kNPad * kTileCols) + wi * (C::BLK * NB * 128) + lane;
-#pragma unroll
-                for (int b = 0; b < C::BLK; ++b)
-#pragma unroll
-                  for (int nb = 0; nb < NB; ++nb)
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) v[q][b][nb][e] = __ldcg(src + ((b * NB + nb) * 4 + e) * 32);
-              }
-#pragma unroll
-              for (int q = 0; q < Q; ++q)
-                if (c0 + q <= c_last)
-#pragma unroll
-                  for (int b = 0; b < C::BLK; ++b)
-#pragma unroll
-                    for (int nb = 0; nb < NB; ++nb)
-#pragma unroll
-                      for (int e = 0; e < 4; ++e) rs[b][nb][e] += v[q][b][nb][e];
-            }
-#pragma unroll
-            for (int b = 0; b < C::BLK; ++b)
-#pragma unroll
-              for (int nb = 0; nb < NB; ++nb)
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                  const int m = 8 * nb + 2 * t + (e & 1);
-                  const int64_t col = (int64_t)tile * kTileCols + wi * C::CW + 16 * b + 8 * (e >> 1) + g;
-                  if (m < a.M) a.out[m * a.out_ld + col] = __float2half_rn(rs[b][nb][e]);
-                }
-            if (wi == 0 && lane == 0) a.cnt[tile * kCntStride] = 0;  // self-reset for the next launch / graph replay
-          }
-        }
-#pragma unroll
-        for (int b = 0; b < C::BLK; ++b)
-#pragma unroll
-          for (int nb = 0; nb < NB; ++nb)
-#pragma unroll
-            for (int e = 0; e < 4; ++e) acc[b][nb][e] = 0.f;
-        seg_start = ub + r + 1;
-      }
-      xp += kUnitK;
-      if (++kb == a.NKB) {
-        kb = 0;
-        ++tile;
-        xp -= (int64_t)a.NKB * kUnitK;
-      }
-    }
   }
 }
 
@@ -1450,7 +627,6 @@ struct GemmArgs {
   __half* out;      // [M][out_ld]
   int64_t out_ld;
   float* ws;        // [grid][2][NB][128]
-  int* cnt;
 };
 
 template <int G, int NB>
@@ -1932,52 +1108,6 @@ cudaError_t launch_pdl(Kern k, dim3 grid, dim3 block, size_t smem, cudaStream_t 
   return cudaLaunchKernelEx(&cfg, k, args...);
 }
 
-#ifndef TPQ_RSETS
-#define TPQ_RSETS 4
-#endif
-#ifndef TPQ_RWPS
-#define TPQ_RWPS 4
-#endif
-constexpr int kRSets = TPQ_RSETS, kRWps = TPQ_RWPS;  // register-dequant GEMV: participants per CTA, warps per set
-static_assert(kRSets <= kGemvParts, "GEMV workspace holds kGemvParts participants per CTA");
-
-template <int G, int NB>
-bool prepare_r() {
-  using C = TR<G, NB, kRSets, kRWps>;
-  static_assert(C::SMEM + 64 <= 227 * 1024, "GEMV smem over the per-CTA limit");
-  static_assert(2 * C::SMEM > 228 * 1024, "GEMV is one CTA per SM");
-  if (cudaFuncSetAttribute(k_dqgemv_r<G, NB, kRSets, kRWps>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM) !=
-      cudaSuccess)
-    return false;
-  if (getenv("TPQ_VERBOSE")) {
-    cudaFuncAttributes fa;
-    cudaFuncGetAttributes(&fa, k_dqgemv_r<G, NB, kRSets, kRWps>);
-    fprintf(stderr, "[tpq] k_dqgemv_r<%d,%d,%d,%d>: regs %d, local %zu, smem dyn %d (D=%d)\n", G, NB, kRSets, kRWps,
-            fa.numRegs, fa.localSizeBytes, C::SMEM, C::D);
-  }
-  return true;
-}
-
-template <int G>
-bool prepare_t() {
-  if (!prepare_r<G, 1>() || !prepare_r<G, 2>()) return false;
-  constexpr int smem = TC<G>::SMEM;
-  static_assert(smem <= 227 * 1024, "GEMV smem over the per-CTA limit");
-  static_assert(2 * smem > 228 * 1024, "GEMV must be one CTA per SM (TMEM 512 columns)");
-  if (cudaFuncSetAttribute(k_dqgemv<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
-    return false;
-  static_assert(TC2<G>::SMEM <= 227 * 1024 && 2 * TC2<G>::SMEM > 228 * 1024, "GEMV v2: one CTA per SM");
-  if (cudaFuncSetAttribute(k_dqgemv2<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC2<G>::SMEM) != cudaSuccess)
-    return false;
-  if (getenv("TPQ_VERBOSE")) {
-    cudaFuncAttributes fa;
-    cudaFuncGetAttributes(&fa, k_dqgemv<G>);
-    fprintf(stderr, "[tpq] k_dqgemv<%d>: regs %d, smem dyn %d static %zu\n", G, fa.numRegs, smem,
-            fa.sharedSizeBytes);
-  }
-  return true;
-}
-
 // ------------------------------------------------------------------ gathers
 __device__ __forceinline__ int64_t gather_src(int m, int64_t k, int64_t ld, const int32_t* idx, int mode,
                                               int64_t nn, int M) {
@@ -2168,11 +1298,6 @@ int cta_read(unsigned long long* out) {
 int trace_read(long long* out) {
   return cudaMemcpyFromSymbol(out, g_tpq_trace, sizeof(long long) * 24 * 64 * 4) != cudaSuccess;
 }
-int prof_read(unsigned long long* out) {  // read and reset
-  if (cudaMemcpyFromSymbol(out, g_tpq_prof, sizeof(unsigned long long) * 32) != cudaSuccess) return 1;
-  unsigned long long z[32] = {0};
-  return cudaMemcpyToSymbol(g_tpq_prof, z, sizeof(z)) != cudaSuccess;
-}
 #endif
 bool make_xmap(CUtensorMap* map, const void* base, int64_t K, int rows, int box_rows) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
@@ -2224,9 +1349,21 @@ bool max_carveout(Kern k) {
 }
 template <int G>
 bool carveout_g() {
-  return max_carveout(k_dqgemv<G>) && max_carveout(k_dqgemv2<G>) && max_carveout(k_dqgemv_r<G, 1, kRSets, kRWps>) &&
-         max_carveout(k_dqgemv_r<G, 2, kRSets, kRWps>) && max_carveout(k_dqgemm<G, 64>) &&
-         max_carveout(k_dqgemm<G, 128>) && max_carveout(k_dqgemm<G, 256>) && max_carveout(k_dqgemm_ss<G, 128>);
+  return max_carveout(k_dqgemv<G>) && max_carveout(k_dqgemm<G, 64>) && max_carveout(k_dqgemm<G, 128>) &&
+         max_carveout(k_dqgemm<G, 256>) && max_carveout(k_dqgemm_ss<G, 128>);
+}
+
+template <int G>
+bool prepare_gemv() {
+  static_assert(TC<G>::SMEM <= 227 * 1024 && 2 * TC<G>::SMEM > 228 * 1024, "GEMV: one CTA per SM (TMEM 512 columns)");
+  if (cudaFuncSetAttribute(k_dqgemv<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC<G>::SMEM) != cudaSuccess)
+    return false;
+  if (getenv("TPQ_VERBOSE")) {
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, k_dqgemv<G>);
+    fprintf(stderr, "[tpq] k_dqgemv<%d>: regs %d, local %zu, smem dyn %d\n", G, fa.numRegs, fa.localSizeBytes, TC<G>::SMEM);
+  }
+  return true;
 }
 
 bool gemv_prepare(int G) {
@@ -2234,30 +1371,16 @@ bool gemv_prepare(int G) {
         max_carveout(k_ss_fixup) && max_carveout(k_sum_partials)))
     return false;
   if (!(G == 128 ? carveout_g<128>() : G == 64 ? carveout_g<64>() : G == 32 ? carveout_g<32>() : false)) return false;
-  if (G == 128) return prepare_t<128>() && prepare_mm_g<128>();
-  if (G == 64) return prepare_t<64>() && prepare_mm_g<64>();
-  if (G == 32) return prepare_t<32>() && prepare_mm_g<32>();
+  if (G == 128) return prepare_gemv<128>() && prepare_mm_g<128>();
+  if (G == 64) return prepare_gemv<64>() && prepare_mm_g<64>();
+  if (G == 32) return prepare_gemv<32>() && prepare_mm_g<32>();
   return false;
 }
 
-template <int G>
-cudaError_t launch_r(const GemvArgs& a, cudaStream_t st) {
-  if (a.M <= 8) {
-    using C = TR<G, 1, kRSets, kRWps>;
-    return launch_pdl(k_dqgemv_r<G, 1, kRSets, kRWps>, dim3(a.grid), dim3(C::WARPS * 32), C::SMEM, st, a);
-  }
-  using C = TR<G, 2, kRSets, kRWps>;
-  return launch_pdl(k_dqgemv_r<G, 2, kRSets, kRWps>, dim3(a.grid), dim3(C::WARPS * 32), C::SMEM, st, a);
-}
-
-cudaError_t launch_gemv(const LayerDev& L, const CUtensorMap& xmap, const void* x, int64_t ldx, int M, void* out,
-                        int64_t out_ld, cudaStream_t st) {
+cudaError_t launch_gemv(const LayerDev& L, const CUtensorMap& xmap, int M, void* out, int64_t out_ld, cudaStream_t st) {
   if (M < 1 || M > kMaxM) return cudaErrorInvalidValue;
   GemvArgs a;
   a.packed = L.packed;
-  a.fixk = 0;
-  a.x = reinterpret_cast<const __half*>(x);
-  a.ldx = ldx;
   a.M = M;
   a.NT = L.NT;
   a.NKB = L.NKB;
@@ -2266,41 +1389,16 @@ cudaError_t launch_gemv(const LayerDev& L, const CUtensorMap& xmap, const void* 
   a.out = reinterpret_cast<__half*>(out);
   a.out_ld = out_ld;
   a.ws = L.ws;
-  a.cnt = L.cnt;
   a.sshift = L.sshift;
-  // GEMV kernel choice: TPQ_GEMV=r / tc forces one; default tc (measured faster at every Llama /
-  // Granite shard size so far, profiles/r01_summary.md)
-  static const int pick = [] {
-    const char* e = getenv("TPQ_GEMV");
-    return !e ? 0 : e[0] == 'r' ? 1 : 2;
-  }();
-  const bool use_r = L.gemv == 2 || (L.gemv == 0 && pick == 1);
-  if (use_r) {
-    if (L.G == 128) return launch_r<128>(a, st);
-    if (L.G == 64) return launch_r<64>(a, st);
-    if (L.G == 32) return launch_r<32>(a, st);
-    return cudaErrorInvalidValue;
-  }
-  // split tiles: reduced by k_mm_fixup after the GEMV (default) or by the last-arriving CTA inside
-  // it (TPQ_INKERNEL_FIXUP=1): the in-kernel arrival atomic measured ~5 us at the end of each CTA
-  static const bool inkernel = getenv("TPQ_INKERNEL_FIXUP") != nullptr;
-  a.fixk = inkernel ? 0 : 1;
-  static const bool v1 = getenv("TPQ_GEMV_V1") != nullptr;
-  cudaError_t e;
-  if (!v1) {
-    a.fixk = 1;
-    e = L.G == 128 ? launch_pdl(k_dqgemv2<128>, dim3(a.grid), dim3(kV2Threads), TC2<128>::SMEM, st, a, xmap)
-        : L.G == 64 ? launch_pdl(k_dqgemv2<64>, dim3(a.grid), dim3(kV2Threads), TC2<64>::SMEM, st, a, xmap)
-        : L.G == 32 ? launch_pdl(k_dqgemv2<32>, dim3(a.grid), dim3(kV2Threads), TC2<32>::SMEM, st, a, xmap)
-                    : cudaErrorInvalidValue;
-  } else
-  e = L.G == 128 ? launch_pdl(k_dqgemv<128>, dim3(a.grid), dim3(kGemvThreads), TC<128>::SMEM, st, a, xmap)
+  cudaError_t e = L.G == 128 ? launch_pdl(k_dqgemv<128>, dim3(a.grid), dim3(kGemvThreads), TC<128>::SMEM, st, a, xmap)
                   : L.G == 64 ? launch_pdl(k_dqgemv<64>, dim3(a.grid), dim3(kGemvThreads), TC<64>::SMEM, st, a, xmap)
                   : L.G == 32 ? launch_pdl(k_dqgemv<32>, dim3(a.grid), dim3(kGemvThreads), TC<32>::SMEM, st, a, xmap)
                               : cudaErrorInvalidValue;
-  if (e != cudaSuccess || !a.fixk) return e;
-  // M <= 4: one thread per column, all contributors' rows in flight (k_gemv_fixup); M > 4: one warp
-  // per row, float4 per lane (k_mm_fixup), measured faster there
+  if (e != cudaSuccess) return e;
+  // split tiles, summed in CTA order after the GEMV: M <= 4 one thread per column with every
+  // contributor's rows in flight (k_gemv_fixup); M > 4 one warp per row, float4 per lane (k_mm_fixup),
+  // measured faster there.  Separate kernels ordered by griddepcontrol.wait beat an in-kernel
+  // last-arriver reduction (branch exp-fused-forward, profiles/r02_summary.md).
   if (M <= 4)
     return launch_pdl(k_gemv_fixup, dim3((unsigned)L.NT), dim3(128), 0, st, (const float*)L.ws, M, L.NKB, L.U, L.grid,
                       reinterpret_cast<__half*>(out), out_ld);
@@ -2329,7 +1427,6 @@ cudaError_t launch_gemm(const LayerDev& L, const CUtensorMap& xmap, int nb, int 
   a.out = reinterpret_cast<__half*>(out);
   a.out_ld = out_ld;
   a.ws = L.ws_mm;
-  a.cnt = L.cnt;
   cudaError_t e = L.G == 128 ? launch_mm_g<128>(nb, a, xmap, st)
                   : L.G == 64 ? launch_mm_g<64>(nb, a, xmap, st)
                   : L.G == 32 ? launch_mm_g<32>(nb, a, xmap, st)

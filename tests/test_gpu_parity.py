@@ -45,14 +45,8 @@ def _np(t):
     return t.float().cpu().numpy().astype(np.float64)
 
 
-KINDS = pytest.mark.parametrize("kind", [tpq.TPQ_GEMV_TC, tpq.TPQ_GEMV_REG], ids=["tc", "reg"])
-
-
-def _mlp(kind, *args, **kw):
-    """TpMlp whose M <= 16 GEMV runs on the given kernel (tcgen05 or register-dequant mma.sync)."""
-    h = tpq.TpMlp(*args, **kw)
-    h.set_gemv_kernel(kind)
-    return h
+def _mlp(*args, **kw):
+    return tpq.TpMlp(*args, **kw)
 
 
 def _assert_close(y, ref, what):
@@ -62,13 +56,12 @@ def _assert_close(y, ref, what):
 
 
 @pytest.mark.parametrize("M", [1, 3, 8, 9, 16])
-@KINDS
-def test_tiny_tp_aware_vs_oracle(M, kind):
+def test_tiny_tp_aware_vs_oracle(M):
     p = synth.make_named("tiny", M, seed=0)
     P1, P2 = _prep(p)
     L1, L2 = _olayers(p)
     ref = O.alg3_tp_aware(p.X, L1, L2, 1)
-    h = _mlp(kind, p.w1, p.w2, P1, P2, M_max=16)
+    h = _mlp(p.w1, p.w2, P1, P2, M_max=16)
     X = _dev(p.X)
     Y = _empty(M, p.N2)
     h.forward(X, M, Y)
@@ -81,14 +74,13 @@ def test_tiny_tp_aware_vs_oracle(M, kind):
 
 @pytest.mark.parametrize("G", [32, 64, 128])
 @pytest.mark.parametrize("M", [1, 5, 16])
-@KINDS
-def test_group_sizes_ragged_tail(G, M, kind):
+def test_group_sizes_ragged_tail(G, M):
     """Several 64-col blocks x groups, N not a multiple of the CTA count (ragged stream-K)."""
     p = synth.make_problem(1024, 1408, 640, G, M, seed=G + M)
     P1, P2 = _prep(p)
     L1, L2 = _olayers(p)
     Y1r, Y2r = O.dense_mlp(p.X, O.dequantize(L1), O.dequantize(L2))
-    h = _mlp(kind, p.w1, p.w2, P1, P2, M_max=16)
+    h = _mlp(p.w1, p.w2, P1, P2, M_max=16)
     X = _dev(p.X)
     Y = _empty(M, p.N2)
     h.forward(X, M, Y)
@@ -96,8 +88,7 @@ def test_group_sizes_ragged_tail(G, M, kind):
     h.close()
 
 
-@KINDS
-def test_onehot_probes_exact_plumbing(kind):
+def test_onehot_probes_exact_plumbing():
     """Integer regime + X = e_k: Y1_local[m, j] = W1[k, w1_cols[j]] exactly representable in
     fp16, so the device result must equal the oracle bit-for-bit: exposes P1 (row gather),
     P2 (column permutation) and the packed layout."""
@@ -109,7 +100,7 @@ def test_onehot_probes_exact_plumbing(kind):
     W1 = O.dequantize(L1)
     for tp in (1, 2, 4):
         for rank in range(tp):
-            h = _mlp(kind, p.w1, p.w2, P1, P2, tp=tp, rank=rank, M_max=16)
+            h = _mlp(p.w1, p.w2, P1, P2, tp=tp, rank=rank, M_max=16)
             cols, _, _, _ = h.index_maps()
             Y1 = _empty(16, 1024 // tp)
             h.layer1(_dev(X), 16, Y1)
@@ -118,8 +109,7 @@ def test_onehot_probes_exact_plumbing(kind):
 
 
 @pytest.mark.parametrize("tp", [2, 4, 8])
-@KINDS
-def test_tp_shards_on_one_gpu_tp_aware(tp, kind):
+def test_tp_shards_on_one_gpu_tp_aware(tp):
     """Every rank's shard on cuda:0; partials summed in rank order (tpq_sum_partials): equals
     the oracle's Alg. 3 (and its per-rank Y1_local)."""
     M = 4
@@ -130,7 +120,7 @@ def test_tp_shards_on_one_gpu_tp_aware(tp, kind):
     X = _dev(p.X)
     parts = []
     for r in range(tp):
-        h = _mlp(kind, p.w1, p.w2, P1, P2, tp=tp, rank=r, M_max=16)
+        h = _mlp(p.w1, p.w2, P1, P2, tp=tp, rank=r, M_max=16)
         y2 = _empty(M, p.N2)
         h.forward_local(X, M, y2)
         y1 = _empty(M, p.N1 // tp)
@@ -182,12 +172,11 @@ def test_naive_variant_staged(tp):
         h.close()
 
 
-@KINDS
-def test_deterministic_and_graph_capturable(kind):
+def test_deterministic_and_graph_capturable():
     M = 16
     p = synth.make_problem(2048, 4096, 2048, 128, M, seed=77)
     P1, P2 = _prep(p)
-    h = _mlp(kind, p.w1, p.w2, P1, P2, M_max=16)
+    h = _mlp(p.w1, p.w2, P1, P2, M_max=16)
     X = _dev(p.X)
     Ya, Yb = _empty(M, p.N2), _empty(M, p.N2)
     h.forward(X, M, Ya)
@@ -228,15 +217,14 @@ def test_m_above_16_chunks_and_host_e2e():
 
 
 @pytest.mark.parametrize("shape,M", [("llama70b", 1), ("llama70b", 16), ("granite20b", 4)])
-@KINDS
-def test_full_size_sampled(shape, M, kind):
+def test_full_size_sampled(shape, M):
     """BASELINE.json configs at full size in the launch configuration bench.py times:
     all of Y1 and 512 sampled columns of Y2 against the oracle."""
     p = synth.make_named(shape, M, seed=0)
     P1, P2 = _prep(p)
     L1, L2 = _olayers(p)
     cols = np.sort(np.random.default_rng(0).choice(p.N2, 512, replace=False))
-    h = _mlp(kind, p.w1, p.w2, P1, P2, M_max=16)
+    h = _mlp(p.w1, p.w2, P1, P2, M_max=16)
     X = _dev(p.X)
     Y = _empty(M, p.N2)
     h.forward(X, M, Y)
@@ -250,15 +238,14 @@ def test_full_size_sampled(shape, M, kind):
     h.close()
 
 
-@KINDS
-def test_full_size_repeat_bit_identical(kind):
+def test_full_size_repeat_bit_identical():
     """Llama-70B layer 1 at M = 16, interleaved with full forwards: every repeat must be
     bit-identical (fixed split-K order, reading c20).  Catches ring races: a stage released
     before its loads returned made 24 of 60 repeats differ in the register GEMV."""
     M = 16
     p = synth.make_named("llama70b", M, seed=0)
     P1, P2 = _prep(p)
-    h = _mlp(kind, p.w1, p.w2, P1, P2, M_max=16)
+    h = _mlp(p.w1, p.w2, P1, P2, M_max=16)
     X = _dev(p.X)
     Y = _empty(M, p.N2)
     ref = _empty(M, p.N1)

@@ -43,4 +43,4 @@ for M in [int(m) for m in a.ms.split(",")]:
         e.record(st)
     torch.cuda.synchronize()
     res[M] = s.elapsed_time(e) * 1e3 / (20 * a.reps)
-print(os.environ.get("TPQ_GEMV_DEBUG", "0"), a.shape, "tp", a.sim_tp, {k: round(v, 2) for k, v in res.items()})
+print(a.shape, "tp", a.sim_tp, {k: round(v, 2) for k, v in res.items()})

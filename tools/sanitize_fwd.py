@@ -1,6 +1,6 @@
 """Small forwards through every kernel path, for compute-sanitizer (memcheck / racecheck / synccheck):
     compute-sanitizer --tool racecheck python tools/sanitize_fwd.py
-GEMV (M = 4, G = 32 / 128; tcgen05 and register-dequant kernels), A7 weights-as-TMEM (M = 40),
+GEMV (M = 4, G = 32 / 128), A7 weights-as-TMEM (M = 40),
 A7 SS GEMM (M = 160), naive staged path."""
 import os
 import sys
@@ -17,13 +17,11 @@ for (K1, N1, N2, G, M, variant) in [(256, 512, 256, 32, 4, tpq.TPQ_TP_AWARE), (1
     p = synth.make_problem(K1, N1, N2, G, M, seed=1)
     P1, _ = tpq.gptq_reorder(p.w1.g_idx, p.w1.G)
     P2, _ = tpq.gptq_reorder(p.w2.g_idx, p.w2.G)
-    for kind in ((tpq.TPQ_GEMV_TC, tpq.TPQ_GEMV_REG) if M <= 16 else (tpq.TPQ_GEMV_AUTO,)):
-        h = tpq.TpMlp(p.w1, p.w2, P1, P2, M_max=256, variant=variant)
-        h.set_gemv_kernel(kind)
-        X = torch.from_numpy(p.X).cuda()
-        Y = torch.empty(M, p.N2, dtype=torch.float16, device="cuda")
-        for _ in range(2):
-            h.forward(X, M, Y)
-        torch.cuda.synchronize()
-        print("ok", K1, N1, N2, G, M, variant, kind, float(Y.float().abs().mean()))
-        h.close()
+    h = tpq.TpMlp(p.w1, p.w2, P1, P2, M_max=256, variant=variant)
+    X = torch.from_numpy(p.X).cuda()
+    Y = torch.empty(M, p.N2, dtype=torch.float16, device="cuda")
+    for _ in range(2):
+        h.forward(X, M, Y)
+    torch.cuda.synchronize()
+    print("ok", K1, N1, N2, G, M, variant, float(Y.float().abs().mean()))
+    h.close()
