@@ -12,7 +12,8 @@
 //                             n6=q[k0+5] n3=q[k0+6] n7=q[k0+7]  (LOP3 magic-number extraction
 //                             yields f16x2 pairs of consecutive k = one TMEM column of the MMA
 //                             A operand)
-//   [8192 + 256 gi, +256)     fp16 scale of column j, group gi of the block (gi < 128 / G)
+//   [8192 + 256 gi, +256)     fp16 s' = s 2^E of column j, group gi of the block (gi < 128 / G);
+//                             E >= 0 per column (tpq_host.cpp column_exponents, LayerDev::colf)
 //   [8192 + 256 (128/G) + 64 gi, +64)   int4 zero of column j, group gi (byte j/2, nibble j%2)
 //
 // Activations (GEMV input) and outputs are plain row-major fp16 [M][ld]; the layer-1 input is the
@@ -51,7 +52,7 @@ struct LayerDev {
   float* ws = nullptr;     // [grid][2 slots][16][128] fp32 stream-K partials of the GEMV (slot 0 = first segment)
   float* ws_mm = nullptr;  // [grid_mm][2 slots][256][128] fp32 stream-K partials (A7 GEMM)
   float* ws_ss = nullptr;  // [items][128][128] fp32 k-split partials (A7 SS GEMM, M >= 128)
-  int sshift = 0;          // GEMV operand shift e: smallest e >= 0 with max|s| 2^(24-e) <= 65504
+  const float* colf = nullptr;  // [N] 2^(24 - E_n): records hold s' = s 2^E_n (tpq_host.cpp column_exponents)
 };
 
 enum GatherMode { GATHER_COLS = 0, GATHER_ALLGATHER = 1 };

@@ -73,12 +73,58 @@ struct Canon {
   std::vector<uint16_t> s;
 };
 
+// Per-column scale exponent of the device records (reading c22): E_n >= 0 is the largest
+// shift with max_g |s[g][n]| 2^E_n < 2^16, so that the stored s' = s 2^E_n is exact in fp16 (a
+// power-of-two scale-up of finite fp16 values below the range limit) and the column's largest
+// scale lands in [2^14, 2^16).  The kernels multiply their fp32 accumulators by 2^(c - E_n).
+std::vector<int> column_exponents(const Canon& c) {
+  std::vector<int> E((size_t)c.N, 0);
+  const int64_t ng = c.K / c.G;
+  for (int64_t n = 0; n < c.N; ++n) {
+    int emax = -100;  // binary exponent of the largest |s| of the column
+    for (int64_t g = 0; g < ng; ++g) {
+      const uint16_t h = c.s[(size_t)(g * c.N + n)] & 0x7FFF;
+      if (h == 0) continue;
+      const int be = (h >> 10) ? (int)(h >> 10) - 15 : 7 - __builtin_clz((unsigned)h);  // subnormal: m 2^-24
+      emax = std::max(emax, be);
+    }
+    E[(size_t)n] = emax == -100 ? 0 : std::max(0, 14 - emax);
+  }
+  return E;
+}
+
+// fp16 bits times 2^e (e >= 0), exact: the result stays finite by the choice of E
+uint16_t half_scale_up(uint16_t h, int e) {
+  if ((h & 0x7FFF) == 0 || e == 0) return h;
+  const uint16_t sign = h & 0x8000;
+  uint32_t ex = (h >> 10) & 0x1F, m = h & 0x3FF;
+  while (e > 0 && ex == 0) {  // subnormal: shift the mantissa until it normalises
+    m <<= 1;
+    --e;
+    if (m & 0x400) {
+      ex = 1;
+      m &= 0x3FF;
+    }
+  }
+  return (uint16_t)(sign | ((ex + e) << 10) | m);
+}
+uint16_t half_scale_down(uint16_t h, int e) {  // inverse of half_scale_up on its outputs
+  if ((h & 0x7FFF) == 0 || e == 0) return h;
+  const uint16_t sign = h & 0x8000;
+  int ex = (h >> 10) & 0x1F;
+  uint32_t m = h & 0x3FF;
+  if (ex - e >= 1) return (uint16_t)(sign | ((ex - e) << 10) | m);
+  m |= 0x400;  // becomes subnormal: shift right by 1 - (ex - e) (exact for values produced by scale-up)
+  m >>= (1 - (ex - e));
+  return (uint16_t)(sign | m);
+}
+
 // Pack a canonical shard into the device layout of internal.h.
 // Nibble slot (0..7) of k0 + i inside a code word (internal.h): k0,k0+1 -> n0,n4; k0+2,k0+3 -> n1,n5;
 // k0+4,k0+5 -> n2,n6; k0+6,k0+7 -> n3,n7.
 constexpr int kNibbleOfK[8] = {0, 4, 1, 5, 2, 6, 3, 7};
 
-std::vector<uint8_t> pack_layer(const Canon& c) {
+std::vector<uint8_t> pack_layer(const Canon& c, const std::vector<int>& E) {
   const int G = c.G, KG = tpq::kUnitK / G;
   const int64_t NT = c.N / tpq::kTileCols, NKB = c.K / tpq::kUnitK, UB = tpq::unit_bytes(G);
   constexpr int64_t kCodes = tpq::kUnitK * tpq::kTileCols / 2;
@@ -98,7 +144,8 @@ std::vector<uint8_t> pack_layer(const Canon& c) {
         }
       for (int gi = 0; gi < KG; ++gi) {
         const int64_t g = kb * KG + gi;
-        memcpy(rec + kCodes + 256 * gi + 2 * j, &c.s[(size_t)(g * c.N + n)], 2);
+        const uint16_t sp = half_scale_up(c.s[(size_t)(g * c.N + n)], E[(size_t)n]);  // s' = s 2^E_n
+        memcpy(rec + kCodes + 256 * gi + 2 * j, &sp, 2);
         rec[kCodes + 256 * KG + 64 * gi + j / 2] |= (uint8_t)(c.z[(size_t)(g * c.N + n)] << (4 * (j & 1)));
       }
     }
@@ -107,8 +154,8 @@ std::vector<uint8_t> pack_layer(const Canon& c) {
 }
 
 // Inverse of pack_layer (test export).
-void unpack_layer(const std::vector<uint8_t>& pk, int64_t K, int64_t N, int G, uint8_t* q, uint16_t* s,
-                  uint8_t* z) {
+void unpack_layer(const std::vector<uint8_t>& pk, const std::vector<int>& E, int64_t K, int64_t N, int G, uint8_t* q,
+                  uint16_t* s, uint8_t* z) {
   const int KG = tpq::kUnitK / G;
   const int64_t NT = N / tpq::kTileCols, NKB = K / tpq::kUnitK, UB = tpq::unit_bytes(G);
   constexpr int64_t kCodes = tpq::kUnitK * tpq::kTileCols / 2;
@@ -126,7 +173,9 @@ void unpack_layer(const std::vector<uint8_t>& pk, int64_t K, int64_t N, int G, u
         }
       for (int gi = 0; gi < KG; ++gi) {
         const int64_t g = kb * KG + gi;
-        memcpy(&s[g * N + n], rec + kCodes + 256 * gi + 2 * j, 2);
+        uint16_t sp;
+        memcpy(&sp, rec + kCodes + 256 * gi + 2 * j, 2);
+        s[g * N + n] = half_scale_down(sp, E[(size_t)n]);
         z[g * N + n] = (rec[kCodes + 256 * KG + 64 * gi + j / 2] >> (4 * (j & 1))) & 0xF;
       }
     }
@@ -135,22 +184,7 @@ void unpack_layer(const std::vector<uint8_t>& pk, int64_t K, int64_t N, int G, u
 
 inline uint32_t nib(uint32_t w, int i) { return (w >> (4 * i)) & 0xFu; }
 
-// fp16 bits -> float (host)
-float half_bits_to_float(uint16_t h) {
-  const int e = (h >> 10) & 0x1F, m = h & 0x3FF;
-  const float v = e == 0 ? std::ldexp((float)m, -24) : e == 31 ? INFINITY : std::ldexp((float)(m | 0x400), e - 25);
-  return (h & 0x8000) ? -v : v;
-}
 
-// GEMV operand shift (tpq_kernels.cu k_dqgemv): smallest e >= 0 such that every |s| 2^(24-e) stays
-// within the fp16 range (65504), so that S = s 2^(24-e) is exact.
-int scale_shift(const std::vector<uint16_t>& s) {
-  float mx = 0.f;
-  for (uint16_t h : s) mx = std::max(mx, std::fabs(half_bits_to_float(h)));
-  int e = 0;
-  while (e < 40 && std::ldexp(mx, 24 - e) > 65504.f) ++e;
-  return e;
-}
 
 }  // namespace
 
@@ -167,6 +201,7 @@ struct tpq_mlp {
   std::vector<int32_t> P1, P2, w1_cols, w2_rows, gather_cols;
   int32_t w2_group_lo = 0, w2_group_hi = 0;
   std::vector<uint8_t> pk1, pk2;  // packed host copies
+  std::vector<int> E1, E2;        // per-column scale exponents of the records (column_exponents)
   tpq::LayerDev L1, L2;
   // device buffers
   void* d_w1 = nullptr;
@@ -179,6 +214,7 @@ struct tpq_mlp {
   void* d_xin = nullptr;       // host-forward staging [M_max][K1]
   void* d_yout = nullptr;      // host-forward staging [M_max][N2]
   float* d_ws = nullptr;
+  float* d_colf = nullptr;     // per-column 2^(24 - E) of layer 1 [n] then layer 2 [N2]
   CUtensorMap xmap1 = {}, xmap2 = {};  // TMA views of d_x1 / d_y1 (GEMV activation operand, 16 rows)
   CUtensorMap mm1[3] = {}, mm2[3] = {};  // A7 views of d_x1 / d_y1 with 64 / 128 / 256 rows
   CUtensorMap ss1 = {}, ss2 = {};        // A7 SS views: 256-row buffers, 128-row boxes
@@ -221,7 +257,7 @@ int validate_perm(const int32_t* P, const gptq_layer* w, const char* name) {
 void free_dev(tpq_mlp* h) {
   if (h->device < 0) return;
   cudaSetDevice(h->device);
-  void* ptrs[] = {h->d_w1, h->d_w2, h->d_P1, h->d_gcols, h->d_x1, h->d_y1, h->d_buf, h->d_xin, h->d_yout, h->d_ws};
+  void* ptrs[] = {h->d_w1, h->d_w2, h->d_P1, h->d_gcols, h->d_x1, h->d_y1, h->d_buf, h->d_xin, h->d_yout, h->d_ws, h->d_colf};
   for (void* p : ptrs)
     if (p) cudaFree(p);
 }
@@ -382,12 +418,12 @@ int tp_shard_mlp(const gptq_layer* w1, const gptq_layer* w2, const int32_t* P1, 
         c2.z[(size_t)(lg * N2 + j)] = (uint8_t)nib(w2->qzeros[(size_t)(g * (N2 / 8) + j / 8)], j % 8);
       }
     }
-    h->pk1 = pack_layer(c1);
-    h->pk2 = pack_layer(c2);
+    h->E1 = column_exponents(c1);
+    h->E2 = column_exponents(c2);
+    h->pk1 = pack_layer(c1, h->E1);
+    h->pk2 = pack_layer(c2, h->E2);
     plan_layer(h->L1, K1, n, w1->G, device);
     plan_layer(h->L2, n, N2, w2->G, device);
-    h->L1.sshift = scale_shift(c1.s);
-    h->L2.sshift = scale_shift(c2.s);
 
     if (device >= 0) {
       auto upload = [&]() -> int {
@@ -421,11 +457,18 @@ int tp_shard_mlp(const gptq_layer* w1, const gptq_layer* w2, const int32_t* P1, 
             (r = A((void**)&h->d_P1, K1 * 4)) || (r = A((void**)&h->d_gcols, n * 4)) || (r = A(&h->d_x1, (size_t)h->rows * K1 * 2)) ||
             (r = A(&h->d_y1, (size_t)h->rows * n * 2)) || (r = A(&h->d_buf, (size_t)tp * h->rows * n * 2)) ||
             (r = A(&h->d_xin, (size_t)M_max * K1 * 2)) || (r = A(&h->d_yout, (size_t)M_max * N2 * 2)) ||
-            (r = A((void**)&h->d_ws, (ws1 + ws2 + wm1 + wm2 + ws1s + ws2s) * 4)))
+            (r = A((void**)&h->d_ws, (ws1 + ws2 + wm1 + wm2 + ws1s + ws2s) * 4)) ||
+            (r = A((void**)&h->d_colf, (size_t)(n + N2) * 4)))
           return r;
         TPQ_CUDA(cudaMemcpy(h->d_w1, h->pk1.data(), h->pk1.size(), cudaMemcpyHostToDevice));
         TPQ_CUDA(cudaMemcpy(h->d_w2, h->pk2.data(), h->pk2.size(), cudaMemcpyHostToDevice));
         TPQ_CUDA(cudaMemcpy(h->d_P1, P1, K1 * 4, cudaMemcpyHostToDevice));
+        {
+          std::vector<float> cf((size_t)(n + N2));
+          for (int64_t j = 0; j < n; ++j) cf[(size_t)j] = std::ldexp(1.f, 24 - h->E1[(size_t)j]);
+          for (int64_t j = 0; j < N2; ++j) cf[(size_t)(n + j)] = std::ldexp(1.f, 24 - h->E2[(size_t)j]);
+          TPQ_CUDA(cudaMemcpy(h->d_colf, cf.data(), cf.size() * 4, cudaMemcpyHostToDevice));
+        }
         TPQ_CUDA(cudaMemcpy(h->d_gcols, h->gather_cols.data(), n * 4, cudaMemcpyHostToDevice));
         bool mok = tpq::make_xmap(&h->xmap1, h->d_x1, K1, tpq::kNPad) && tpq::make_xmap(&h->xmap2, h->d_y1, n, tpq::kNPad);
         if (h->rows > tpq::kMaxM) {
@@ -435,6 +478,8 @@ int tp_shard_mlp(const gptq_layer* w1, const gptq_layer* w2, const int32_t* P1, 
                 tpq::make_xmap(&h->ss2, h->d_y1, n, kGemmRows, 128);
         }
         if (!mok) return fail(TPQ_ECUDA, "cuTensorMapEncodeTiled failed for the activation buffers");
+        h->L1.colf = h->d_colf;
+        h->L2.colf = h->d_colf + n;
         h->L1.packed = (const uint8_t*)h->d_w1;
         h->L2.packed = (const uint8_t*)h->d_w2;
         h->L1.ws = h->d_ws;
@@ -728,8 +773,8 @@ int tpq_mlp_index_maps(const tpq_mlp* h, int32_t* w1_cols, int32_t* w2_rows, int
 
 int tpq_mlp_export_canonical(const tpq_mlp* h, int layer, uint8_t* q, uint16_t* s, uint8_t* z) {
   if (!h || !q || !s || !z) return fail(TPQ_EINVAL, "NULL");
-  if (layer == 1) unpack_layer(h->pk1, h->K1, h->n, h->G1, q, s, z);
-  else if (layer == 2) unpack_layer(h->pk2, h->n, h->N2, h->G2, q, s, z);
+  if (layer == 1) unpack_layer(h->pk1, h->E1, h->K1, h->n, h->G1, q, s, z);
+  else if (layer == 2) unpack_layer(h->pk2, h->E2, h->n, h->N2, h->G2, q, s, z);
   else return fail(TPQ_EINVAL, "layer=%d", layer);
   return TPQ_OK;
 }

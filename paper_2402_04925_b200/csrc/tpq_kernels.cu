@@ -257,8 +257,7 @@ struct GemvArgs {
   __half* out;      // [M][out_ld] row-major
   int64_t out_ld;
   float* ws;        // [grid][2 slots][16][128] fp32 split-tile partials (slot 0 = first segment, 1 = last)
-  int sshift;       // A = s (q - z) 2^-sshift (host: keeps s 2^(24 - sshift) in fp16 range); the
-                    // epilogue multiplies the fp32 accumulator by 2^sshift
+  const float* colf;  // [N] 2^(24 - E_n): the records hold s' = s 2^E_n per column n
 };
 
 // ------------------------------------------------------------------ GEMV (M <= 16)
@@ -359,7 +358,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_dqgemv(const GemvArgs a, co
     const int zbyte = kUnitK * kTileCols / 2 + C::KG * 256 + (col >> 1), zsh = 4 * (col & 1);
     const int sbyte = kUnitK * kTileCols / 2 + 2 * col;
     const bool xw = qw == 0;
-    const float se = exp2f((float)-a.sshift), s24 = 16777216.f * se, s20 = 1048576.f * se;
+    // S = s' for the nibbles at bits 0-3 (q 2^-24) and s' / 16 for bits 4-7 (q 2^-20), C = -z s' 2^-24
     int st = (2 * set) % C::NS;                       // stage of unit 2p
     uint32_t ph = (uint32_t)(((2 * set) / C::NS) & 1);
     for (int p = set; p < np; p += kSets) {
@@ -378,9 +377,9 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_dqgemv(const GemvArgs a, co
         for (int g = 0; g < C::KG; ++g) {
           const float z = (float)((sp[zbyte + g * 64] >> zsh) & 0xFu);
           const float sf = __half2float(*reinterpret_cast<const __half*>(sp + sbyte + g * 256));
-          sl[g] = __float2half2_rn(sf * s24);
-          shh[g] = __float2half2_rn(sf * s20);
-          zc[g] = __float2half2_rn(-z * sf * se);
+          sl[g] = __float2half2_rn(sf);
+          shh[g] = __float2half2_rn(sf * 0.0625f);
+          zc[g] = __float2half2_rn(-z * sf * 5.9604644775390625e-8f);
         }
         uint4 cw[4];
 #pragma unroll
@@ -429,7 +428,6 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_dqgemv(const GemvArgs a, co
     const int qw = warp, col = qw * 32 + lane;
     const uint32_t lane_base = (uint32_t)(qw * 32) << 16;
     pdl_wait();
-    const float up = exp2f((float)a.sshift);
     int tile = (int)(u0 / a.NKB);
     int64_t seg_start = u0;
     const int64_t uend = u0 + nu;
@@ -438,6 +436,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_dqgemv(const GemvArgs a, co
       const int64_t seg_end = tile_end < uend ? tile_end : uend;  // exclusive
       const int lo = (int)(seg_start - u0), hi = (int)(seg_end - 1 - u0);
       const int d = seg & 1;
+      const float up = __ldg(a.colf + (int64_t)tile * kTileCols + col);  // 2^(24 - E) of this column
       mbar_wait_backoff(d_full + d, (uint32_t)((seg >> 1) & 1), 256);
       tc_fence_after();
       const bool w0 = hi - lo >= 3 || ((lo >> 1) & 1) == 0 || ((hi >> 1) & 1) == 0;
@@ -627,6 +626,7 @@ struct GemmArgs {
   __half* out;      // [M][out_ld]
   int64_t out_ld;
   float* ws;        // [grid][2][NB][128]
+  const float* colf;  // [N] 2^(24 - E_n) (records hold s' = s 2^E_n); the operand is fp16(s' 2^-12 (q - z))
 };
 
 template <int G, int NB>
@@ -689,7 +689,7 @@ __global__ void __launch_bounds__(kMmWarps * 32, 1) k_dqgemm(const GemmArgs a, c
         const __half sv = *reinterpret_cast<const __half*>(meta + gi * 256 + 2 * col);
         zl[j] = __float2half2_rn((float)(1024 + z));
         zh[j] = __float2half2_rn((float)(-64 - z));
-        sc[j] = __halves2half2(sv, sv);
+        sc[j] = __float2half2_rn(__half2float(sv) * 2.44140625e-4f);  // s' 2^-12 (exact: power of two)
       }
       {
         uint32_t dep = c0.x ^ c0.w ^ c1.x ^ c1.w;
@@ -730,6 +730,7 @@ __global__ void __launch_bounds__(kMmWarps * 32, 1) k_dqgemm(const GemmArgs a, c
         tc_fence_after();
         const int slot = (seg_start == u0) ? 0 : 1;
         float* mine = a.ws + ((size_t)blockIdx.x * 2 + slot) * ((size_t)NB * kTileCols);
+        const float up = __ldg(a.colf + n) * 2.44140625e-4f;  // 2^(12 - E): undo s' 2^-12 (exact)
         for (int m0 = 0; m0 < a.M; m0 += 16) {  // 16 rows per tcgen05.ld
           uint32_t v[16];
           tmem_ld16(tmem + lane_base + m0, v);
@@ -737,8 +738,9 @@ __global__ void __launch_bounds__(kMmWarps * 32, 1) k_dqgemm(const GemmArgs a, c
 #pragma unroll
           for (int m = 0; m < 16; ++m) {
             if (m0 + m >= a.M) break;
-            if (full_tile) a.out[(int64_t)(m0 + m) * a.out_ld + n] = __float2half_rn(__uint_as_float(v[m]));
-            else __stcg(mine + (size_t)(m0 + m) * kTileCols + col, __uint_as_float(v[m]));
+            const float y = up * __uint_as_float(v[m]);
+            if (full_tile) a.out[(int64_t)(m0 + m) * a.out_ld + n] = __float2half_rn(y);
+            else __stcg(mine + (size_t)(m0 + m) * kTileCols + col, y);
           }
         }
         tc_fence_before();
@@ -858,6 +860,7 @@ struct SsArgs {
   __half* out;        // [M][out_ld]
   int64_t out_ld;
   float* ws;          // [items][128][BN] k-split partials (S > 1)
+  const float* colf;  // [N] 2^(24 - E_n) (records hold s' = s 2^E_n); the operand is fp16(s' 2^-12 (q - z))
 };
 
 template <int G, int BN>
@@ -929,7 +932,7 @@ __global__ void __launch_bounds__(TS<G, BN>::WARPS * 32, 1) k_dqgemm_ss(const Ss
           const __half sv = *reinterpret_cast<const __half*>(meta + gi * 256 + 2 * j);
           zl[g] = __float2half2_rn((float)(1024 + z));
           zh[g] = __float2half2_rn((float)(-64 - z));
-          sc[g] = __halves2half2(sv, sv);
+          sc[g] = __float2half2_rn(__half2float(sv) * 2.44140625e-4f);  // s' 2^-12
         }
         {
           uint32_t dep = c0.x ^ c0.w ^ c1.x ^ c1.w;
@@ -970,6 +973,11 @@ __global__ void __launch_bounds__(TS<G, BN>::WARPS * 32, 1) k_dqgemm_ss(const Ss
         tmem_ld16(tmem + ((uint32_t)(qw * 32) << 16) + db * BN + c0, v);
         tmem_ld16(tmem + ((uint32_t)(qw * 32) << 16) + db * BN + c0 + 16, v + 16);
         tmem_wait_ld();
+        {
+          const float* cf = a.colf + (int64_t)ng * BN + c0;  // same 32 columns for every lane (broadcast)
+#pragma unroll
+          for (int q = 0; q < 32; ++q) v[q] = __float_as_uint(__uint_as_float(v[q]) * (__ldg(cf + q) * 2.44140625e-4f));
+        }
         if (m < a.M) {
           if (a.S == 1) {
             __half* o = a.out + (int64_t)m * a.out_ld + (int64_t)ng * BN + c0;
@@ -1389,7 +1397,7 @@ cudaError_t launch_gemv(const LayerDev& L, const CUtensorMap& xmap, int M, void*
   a.out = reinterpret_cast<__half*>(out);
   a.out_ld = out_ld;
   a.ws = L.ws;
-  a.sshift = L.sshift;
+  a.colf = L.colf;
   cudaError_t e = L.G == 128 ? launch_pdl(k_dqgemv<128>, dim3(a.grid), dim3(kGemvThreads), TC<128>::SMEM, st, a, xmap)
                   : L.G == 64 ? launch_pdl(k_dqgemv<64>, dim3(a.grid), dim3(kGemvThreads), TC<64>::SMEM, st, a, xmap)
                   : L.G == 32 ? launch_pdl(k_dqgemv<32>, dim3(a.grid), dim3(kGemvThreads), TC<32>::SMEM, st, a, xmap)
@@ -1427,6 +1435,7 @@ cudaError_t launch_gemm(const LayerDev& L, const CUtensorMap& xmap, int nb, int 
   a.out = reinterpret_cast<__half*>(out);
   a.out_ld = out_ld;
   a.ws = L.ws_mm;
+  a.colf = L.colf;
   cudaError_t e = L.G == 128 ? launch_mm_g<128>(nb, a, xmap, st)
                   : L.G == 64 ? launch_mm_g<64>(nb, a, xmap, st)
                   : L.G == 32 ? launch_mm_g<32>(nb, a, xmap, st)
@@ -1459,6 +1468,7 @@ cudaError_t launch_gemm_ss(const LayerDev& L, const CUtensorMap& xmap, int M, in
   a.out = reinterpret_cast<__half*>(out);
   a.out_ld = out_ld;
   a.ws = L.ws_ss;
+  a.colf = L.colf;
   cudaError_t e = cudaErrorInvalidValue;
   if (bn == 256) {
     if (L.G == 128) e = launch_ss_t<128, 256>(a, xmap, st);

@@ -18,6 +18,9 @@ inputs.  Recipe:
 * s = fp16(U[0.5, 1.5] / (6.52 * sqrt(K_l))) per (group, col): 6.52 ~ sqrt(42.5)
   is the rms of (q - z), so std(Y1) ~ std(Y2) ~ 1 and fp16 never overflows.
 * X = fp16(N(0, 1)), shape [M][K1].
+* wide_scales=True (precision tests only): s = fp16(2^-2 * 10^-(1.5 u + 4 v)), u ~ U[0, 1) per
+  (group, col) and v ~ U[0, 1) per column: 5.5 decades across the layer (whole columns up to 4
+  decades below the largest), 1.5 within a column.
 
 GPTQ packing (reading c4): ``qweight[K/8][N]`` uint32 with row k's
 nibble at bits 4*(k%8) of word k//8; ``qzeros[ceil(K/G)][N/8]`` uint32 with
@@ -85,7 +88,7 @@ def pack_cols_u4(z: np.ndarray) -> np.ndarray:
 
 
 def make_layer(K: int, N: int, G: int, ss_phi, ss_q, ss_z, ss_s, *, identity_phi=False,
-               integer_regime=False) -> Layer:
+               integer_regime=False, wide_scales=False) -> Layer:
     rng_phi = np.random.Generator(np.random.PCG64(ss_phi))
     phi = np.arange(K, dtype=np.int64) if identity_phi else rng_phi.permutation(K).astype(np.int64)
     g_idx = (phi // G).astype(np.int32)
@@ -98,6 +101,10 @@ def make_layer(K: int, N: int, G: int, ss_phi, ss_q, ss_z, ss_s, *, identity_phi
         # an exactly representable dyadic rational.
         e = rng_s.integers(0, 4, size=(ng, N))
         s = np.ldexp(1.0, -e).astype(np.float16)
+    elif wide_scales:
+        u = rng_s.uniform(0.0, 1.0, size=(ng, N))
+        v = rng_s.uniform(0.0, 1.0, size=(1, N))
+        s = (0.25 * 10.0 ** -(1.5 * u + 4.0 * v)).astype(np.float16)
     else:
         s = (rng_s.uniform(0.5, 1.5, size=(ng, N)) / (6.52 * np.sqrt(K))).astype(np.float16)
     lay = Layer(K=K, N=N, G=G, phi=phi, g_idx=g_idx, q=q, z=z, scales_f16=s)
@@ -122,14 +129,14 @@ class Problem:
 
 
 def make_problem(K1: int, N1: int, N2: int, G: int, M: int, seed: int = 0, *,
-                 G2: int | None = None, identity_phi=False, integer_regime=False) -> Problem:
+                 G2: int | None = None, identity_phi=False, integer_regime=False, wide_scales=False) -> Problem:
     """Build the seeded synthetic MLP problem Y = (X.W1).W2 (PAPER.md:L151 shapes)."""
     G2 = G if G2 is None else G2
     ss = np.random.SeedSequence(seed).spawn(9)
     w1 = make_layer(K1, N1, G, ss[0], ss[2], ss[4], ss[6], identity_phi=identity_phi,
-                    integer_regime=integer_regime)
+                    integer_regime=integer_regime, wide_scales=wide_scales)
     w2 = make_layer(N1, N2, G2, ss[1], ss[3], ss[5], ss[7], identity_phi=identity_phi,
-                    integer_regime=integer_regime)
+                    integer_regime=integer_regime, wide_scales=wide_scales)
     rng_x = np.random.Generator(np.random.PCG64(ss[8]))
     if integer_regime:
         X = rng_x.integers(-2, 3, size=(M, K1)).astype(np.float16)

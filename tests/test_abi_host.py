@@ -166,3 +166,28 @@ def test_forward_on_host_only_handle_is_estate():
         h.forward_host(X, Y, stream=0)
     assert e.value.code == 6
     h.close()
+
+
+def test_export_exact_over_wide_and_extreme_scales():
+    """The device records hold s' = s 2^E per column (reading c22); the canonical export must give
+    back every scale bit-exactly, over 4.5 decades (synth wide_scales) plus hand-set extremes:
+    subnormal scales, the largest finite fp16, an all-zero column and negative zeros."""
+    p = synth.make_problem(256, 1024, 256, 32, 1, seed=9, wide_scales=True)
+    s1 = p.w1.scales_f16
+    s1[:, 0] = np.float16(2.0 ** -24)            # smallest subnormal everywhere in column 0
+    s1[0, 1] = np.float16(65504.0)               # largest finite next to tiny ones
+    s1[1:, 1] = np.float16(2.0 ** -20)
+    s1[:, 2] = np.float16(0.0)                   # all-zero column
+    s1[3, 3] = np.float16(-0.0)
+    p.w2.scales_f16[:, 5] = np.float16(6.1e-5)   # just below the smallest normal
+    P1, P2 = _prep(p)
+    L1, L2 = _olayers(p)
+    for tp, rank in ((1, 0), (4, 3)):
+        h = tpq.TpMlp(p.w1, p.w2, P1, P2, tp=tp, rank=rank, M_max=4, device=-1)
+        ref = O.canonical_shard(L1, L2, tp, rank, "tp_aware")
+        _, s_1, _ = h.export_canonical(1)
+        _, s_2, _ = h.export_canonical(2)
+        want1 = np.asarray(p.w1.scales_bits)[:, ref["w1_cols"]]
+        assert (s_1 == want1).all()
+        assert (s_2 == np.asarray(p.w2.scales_bits)[ref["w2_group_lo"]:ref["w2_group_hi"]]).all()
+        h.close()

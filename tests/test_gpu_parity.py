@@ -354,3 +354,73 @@ def test_a7_ss_wide_tiles(G, M):
     h.forward(X, M, Y2)
     assert torch.equal(Y, Y2), "SS GEMM not deterministic"
     h.close()
+
+
+def _check_elementwise(y, ref, absref, tol, what):
+    """|y - ref| <= tol * absref element by element, absref = |inputs| . |W| (the worst-case
+    rounding bound of a dot product: each term carries its own relative error, so a column made of
+    small scales is held to its own magnitude, and cancellation in the output does not matter)."""
+    ratio = np.abs(y - ref) / np.where(absref > 0, absref, 1.0)
+    worst = np.unravel_index(int(np.argmax(ratio)), ratio.shape)
+    assert np.all(ratio <= tol), f"{what}: element {worst} error {ratio[worst]:.3e} x |inputs|.|W| > {tol}"
+    return float(ratio.max())
+
+
+@pytest.mark.parametrize("M", [1, 8, 40, 160])
+def test_wide_scale_range_per_column(M):
+    """Scales log-uniform over 5.5 decades (whole columns up to 4 decades below the largest, 1.5
+    within a column; synth wide_scales): every output element within 2e-3 (layer 1) / 4e-3
+    (layer 2, fp16 Y1 input) of |inputs| . |W|.  A single operand shift per layer (round 1) leaves
+    the fp16 A operand of the small-scale columns subnormal: emulated in numpy it reaches 1.0e-2 on
+    this recipe, against 1.8e-4 for the per-column exponent of the records (reading c22).  M covers
+    the GEMV and both A7 kernels."""
+    p = synth.make_problem(1024, 2048, 1024, 128, M, seed=5, wide_scales=True)
+    P1, P2 = _prep(p)
+    L1, L2 = _olayers(p)
+    h = tpq.TpMlp(p.w1, p.w2, P1, P2, M_max=256)
+    X = _dev(p.X)
+    Y1 = _empty(M, p.N1)
+    h.layer1(X, M, Y1)
+    Y = _empty(M, p.N2)
+    h.forward(X, M, Y)
+    P2o, _ = O.alg1_reorder(L2.g)
+    W1, W2 = O.dequantize(L1), O.dequantize(L2)
+    Xf = p.X.astype(np.float64)
+    Y1r, Y2r = O.dense_mlp(Xf, W1, W2)
+    b1 = np.abs(Xf) @ np.abs(W1)
+    b2 = np.abs(Y1r) @ np.abs(W2)
+    _check_elementwise(_np(Y1), Y1r[:, P2o], b1[:, P2o], 2e-3, "Y1 (P2 order)")
+    _check_elementwise(_np(Y), Y2r, b2, 4e-3, "Y2")
+    h.close()
+
+
+@pytest.mark.parametrize("tp", [2, 4, 8])
+@pytest.mark.parametrize("M", [1, 16])
+def test_full_size_tp_shards(tp, M):
+    """Llama-70B shards at TP = 2/4/8 in the launch configuration of a TP-rank (the small-shard
+    grid, 5-6 stream-K contributors per layer-1 tile), first and last rank: Y1_local in full and
+    512 sampled columns of Y2_local against the oracle's Alg. 3 L1-L2 for that rank."""
+    p = synth.make_named("llama70b", M, seed=1)
+    P1, P2 = _prep(p)
+    L1, L2 = _olayers(p)
+    n = p.N1 // tp
+    X = _dev(p.X)
+    cols = np.sort(np.random.default_rng(tp).choice(p.N2, 512, replace=False))
+    for r in (0, tp - 1):
+        mp = O.shard_maps(O.alg1_reorder(L2.g)[0], p.N1, tp, r, "tp_aware", p.G)
+        # Alg. 3 L1 for rank r: X[:, P1] W1[P1, P2][:, r n:(r+1) n] = X W1[:, w1_cols]
+        Xf = p.X.astype(np.float64)
+        c1 = mp["w1_cols"]
+        Y1r = np.concatenate([Xf @ O.dequantize(O.permute_cols(L1, c1[lo:lo + 2048])) for lo in range(0, n, 2048)], axis=1)
+        # Alg. 3 L2 for rank r: Y1_local W2[P2][r n:(r+1) n]
+        W2r = O.permute_rows(L2, mp["w2_rows"])
+        W2rc = O.OLayer(q=W2r.q[:, cols], s=W2r.s[:, cols], z=W2r.z[:, cols], g=W2r.g, G=W2r.G)
+        Y2r = Y1r @ O.dequantize(W2rc)
+        h = tpq.TpMlp(p.w1, p.w2, P1, P2, tp=tp, rank=r, M_max=16)
+        Y1 = _empty(M, n)
+        h.layer1(X, M, Y1)
+        Y2 = _empty(M, p.N2)
+        h.forward_local(X, M, Y2)
+        _assert_close(_np(Y1), Y1r, f"tp={tp} rank {r} Y1_local")
+        _assert_close(_np(Y2)[:, cols], Y2r, f"tp={tp} rank {r} Y2_local sampled")
+        h.close()

@@ -360,3 +360,72 @@ def test_dense_mlp_columns_equals_dense():
     cols = np.array([47, 0, 5])
     _, Y2s = O.dense_mlp_columns(X, L1, L2, cols2=cols, chunk=7)
     assert (Y2s == Y2[:, cols]).all()
+
+
+# ----------------------------------------------------------------------------- fp16 decode
+def test_fp16_bits_golden():
+    """fp16_bits_to_f64 against binary16 values written out by hand (tests/golden/fp16_bits.json,
+    IEEE 754 definition): normal, subnormal, extreme and signed patterns.  This is the decode every
+    scale of the checkpoint goes through in layer_from_checkpoint."""
+    g = golden("fp16_bits.json")
+    for c in g["cases"]:
+        v = O.fp16_bits_to_f64(np.array([int(c["bits"], 16)], dtype=np.uint16))[0]
+        want = math.inf if c["value"] == "inf" else float(c["value"])
+        assert v == want and math.copysign(1.0, v) == math.copysign(1.0, want), (c, v)
+
+
+def test_layer_from_checkpoint_scales_decode():
+    """The decoded scale of a checkpoint entry is its binary16 value (bits chosen by hand)."""
+    bits = np.array([[0x3C00, 0x0001], [0x7BFF, 0x3555]], dtype=np.uint16)
+    K, N, G = 16, 16, 8
+    qw = np.zeros((K // 8, N), np.uint32)
+    qz = np.zeros((K // G, N // 8), np.uint32)
+    sb = np.tile(bits, (1, N // 2))
+    L = O.layer_from_checkpoint(qw, sb, qz, np.arange(K) // G, K, N, G)
+    assert L.s[0, 0] == 1.0 and L.s[0, 1] == 2.0 ** -24 and L.s[1, 0] == 65504.0 and L.s[1, 1] == 1365 / 4096
+
+
+# ----------------------------------------------------------------------------- canonical shard
+def _hand_shard_layers():
+    """Hand example (non-identity phi): K1 = N1 = 4, N2 = 2, G = 2.
+    phi1 = [2, 0, 1, 3] -> g1 = [1, 0, 0, 1] (Eq. 3); phi2 = [3, 1, 2, 0] -> g2 = [1, 0, 1, 0].
+    q1[k][n] = 4k + n, s1[g][n] = 10 (g + 1) + n, z1[g][n] = g + n;
+    q2[k][n] = 3k + n, s2 = [[1, 2], [3, 4]], z2 = [[5, 6], [7, 8]]."""
+    q1 = np.arange(16, dtype=np.int64).reshape(4, 4)
+    s1 = np.array([[10, 11, 12, 13], [20, 21, 22, 23]], dtype=np.float64)
+    z1 = np.array([[0, 1, 2, 3], [1, 2, 3, 4]], dtype=np.int64)
+    q2 = np.array([[0, 1], [3, 4], [6, 7], [9, 10]], dtype=np.int64)
+    s2 = np.array([[1, 2], [3, 4]], dtype=np.float64)
+    z2 = np.array([[5, 6], [7, 8]], dtype=np.int64)
+    L1 = O.OLayer(q=q1, s=s1, z=z1, g=O.eq3_g_idx_actorder([2, 0, 1, 3], 2), G=2)
+    L2 = O.OLayer(q=q2, s=s2, z=z2, g=O.eq3_g_idx_actorder([3, 1, 2, 0], 2), G=2)
+    return L1, L2
+
+
+def test_canonical_shard_hand_example():
+    """canonical_shard at tp = 2 against values derived by hand:
+    P1 = stable argsort([1,0,0,1]) = [1,2,0,3]; P2 = stable argsort([1,0,1,0]) = [1,3,0,2]; n = 2.
+    TP-aware rank 0 keeps W1[P1, P2] columns P2[0:2] = [1, 3] and W2 rows [1, 3] (group 0);
+    rank 1 columns [0, 2], rows [0, 2] (group 1).  Naive rank 0 keeps W1[P1] columns [0, 1]."""
+    L1, L2 = _hand_shard_layers()
+    a0 = O.canonical_shard(L1, L2, 2, 0, "tp_aware")
+    assert a0["P1"].tolist() == [1, 2, 0, 3] and a0["P2"].tolist() == [1, 3, 0, 2]
+    assert a0["w1_cols"].tolist() == [1, 3] and a0["w2_rows"].tolist() == [1, 3]
+    assert a0["w1_q"].tolist() == [[5, 7], [9, 11], [1, 3], [13, 15]]
+    assert a0["w1_s"].tolist() == [[11, 13], [21, 23]] and a0["w1_z"].tolist() == [[1, 3], [2, 4]]
+    assert a0["w1_g"].tolist() == [0, 0, 1, 1]
+    assert a0["w2_q"].tolist() == [[3, 4], [9, 10]] and a0["w2_g"].tolist() == [0, 0]
+    assert a0["w2_s"].tolist() == [[1, 2]] and a0["w2_z"].tolist() == [[5, 6]]
+    assert (a0["w2_group_lo"], a0["w2_group_hi"]) == (0, 1)
+    assert a0["gather_src"].tolist() == [[0, 1], [1, 1]]
+    a1 = O.canonical_shard(L1, L2, 2, 1, "tp_aware")
+    assert a1["w1_cols"].tolist() == [0, 2] and a1["w2_rows"].tolist() == [0, 2]
+    assert a1["w1_q"].tolist() == [[4, 6], [8, 10], [0, 2], [12, 14]]
+    assert a1["w1_s"].tolist() == [[10, 12], [20, 22]] and a1["w1_z"].tolist() == [[0, 2], [1, 3]]
+    assert a1["w2_q"].tolist() == [[0, 1], [6, 7]] and a1["w2_g"].tolist() == [0, 0]
+    assert a1["w2_s"].tolist() == [[3, 4]] and a1["w2_z"].tolist() == [[7, 8]]
+    assert (a1["w2_group_lo"], a1["w2_group_hi"]) == (1, 2)
+    assert a1["gather_src"].tolist() == [[0, 0], [1, 0]]
+    n0 = O.canonical_shard(L1, L2, 2, 0, "naive")
+    assert n0["w1_cols"].tolist() == [0, 1] and n0["w1_q"].tolist() == [[4, 5], [8, 9], [0, 1], [12, 13]]
+    assert n0["w2_q"].tolist() == a0["w2_q"].tolist()
