@@ -38,16 +38,15 @@ METRIC = ("MLP fwd latency (µs) & HBM GB/s vs roofline, M=1..16, TP=1/2/4/8 vs 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5000)
-    ap.add_argument("--warmup", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=50)
     ap.add_argument("--shape", default="llama70b", choices=sorted(synth.SHAPES))
     ap.add_argument("--m", type=int, default=16)
     ap.add_argument("--variant", default="tp_aware", choices=["tp_aware", "naive"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--seed", type=int, default=0)
-    ap.add_argument("--sweep", action="store_true",
-                    help="N = 1: add graph-timed step latencies at M = 1/4/8/16 (key sweep_us_by_M; runs after "
-                         "the timed region, so power-capped boxes may report it slower)")
+    ap.add_argument("--quick", action="store_true",
+                    help="N = 1: skip the extra lines (M sweep, Granite TP=1, Llama TP=8 shard)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-naive", action="store_true", help="N > 1: skip timing the naive AllGather path")
     ap.add_argument("--no-graph", action="store_true", help="launch every step eagerly (no CUDA graph)")
@@ -138,27 +137,55 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------------ oracle
-def oracle_sample_time(p, frac_den: int = 8, reps: int = 1):
-    """Time the oracle (as it stands: checkpoint unpack, Alg. 1, Alg. 3 at tp=1, fp64) on the
-    sub-MLP made of the first N1/frac_den intermediate columns (W1[:, :c], W2[:c, :]), which
-    is 1/frac_den of the full forward's work; returns seconds per FULL forward."""
+def oracle_prepare(p):
+    """Offline part of the oracle (timed once, reported apart from the forward): checkpoint
+    unpack (layer_from_checkpoint) and Alg. 1 (alg1_reorder, PAPER.md:L44-54)."""
     import oracle as O
-    c = p.N1 // frac_den
-    w1, w2 = p.w1, p.w2
-    qw1, sc1, qz1 = w1.qweight[:, :c], w1.scales_bits[:, :c], w1.qzeros[:, :c // 8]
-    qw2, g2 = w2.qweight[:c // 8, :], w2.g_idx[:c]
-    # the sub-MLP keeps W2's rows 0..c-1 whose act_order groups are re-indexed densely
-    ug, g2d = np.unique(g2, return_inverse=True)
-    sc2, qz2 = w2.scales_bits[ug], w2.qzeros[ug]
-    best = None
-    for _ in range(reps):
-        t0 = time.perf_counter()
-        L1 = O.layer_from_checkpoint(qw1, sc1, qz1, w1.g_idx, p.K1, c, p.G)
-        L2 = O.layer_from_checkpoint(qw2, sc2, qz2, g2d, c, p.N2, p.G)
-        O.alg3_tp_aware(p.X, L1, L2, 1)
-        dt = time.perf_counter() - t0
-        best = dt if best is None else min(best, dt)
-    return best * frac_den
+    t0 = time.perf_counter()
+    L1 = O.layer_from_checkpoint(p.w1.qweight, p.w1.scales_bits, p.w1.qzeros, p.w1.g_idx, p.K1, p.N1, p.G)
+    L2 = O.layer_from_checkpoint(p.w2.qweight, p.w2.scales_bits, p.w2.qzeros, p.w2.g_idx, p.N1, p.N2, p.G)
+    t1 = time.perf_counter()
+    O.alg1_reorder(L1.g)
+    O.alg1_reorder(L2.g)
+    t2 = time.perf_counter()
+    return L1, L2, {"unpack_s": t1 - t0, "alg1_s": t2 - t1}
+
+
+def oracle_forward(X, L1, L2, chunk=2048):
+    """One full forward of the oracle as it stands (fp64, TP = 1, so Alg. 3 = the plain definition
+    Y2 = (X . deq(W1)) . deq(W2), reading c9): dequantize (oracle.dequantize, PAPER.md:L19 with the
+    unordered g) and matmul, column block by column block so the fp64 weights fit in host memory.
+    Returns (Y2, seconds in dequantize, seconds in matmul)."""
+    import oracle as O
+    X = np.asarray(X, dtype=np.float64)
+    td = tm = 0.0
+
+    def block(L, lo, hi):
+        return O.OLayer(q=L.q[:, lo:hi], s=L.s[:, lo:hi], z=L.z[:, lo:hi], g=L.g, G=L.G)
+
+    Y = []
+    for L, inp in ((L1, X), (L2, None)):
+        src = inp if inp is not None else Y[0]
+        out = np.empty((src.shape[0], L.N))
+        for lo in range(0, L.N, chunk):
+            hi = min(L.N, lo + chunk)
+            t0 = time.perf_counter()
+            W = O.dequantize(block(L, lo, hi))
+            t1 = time.perf_counter()
+            out[:, lo:hi] = src @ W
+            t2 = time.perf_counter()
+            td += t1 - t0
+            tm += t2 - t1
+        Y.append(out)
+    return Y[1], td, tm
+
+
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        return max((i.get("num_threads") or 0) for i in threadpool_info()) or None
+    except Exception:
+        return None
 
 
 def cpu_cores():
@@ -169,29 +196,126 @@ def cpu_cores():
 
 
 def run_reference(a):
+    """--impl reference: the CPU oracle as it stands, one FULL forward per step (no sampling, no
+    extrapolation), exactly --steps timed steps after --warmup untimed ones, rank 0 only."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    tp = a.gpus
     K1, N1, N2, G = synth.SHAPES[a.shape]
     p = synth.make_named(a.shape, a.m, a.seed)
-    den = 4 if a.shape != "tiny" else 1
-    for _ in range(min(a.warmup, 1)):
-        oracle_sample_time(p, den)
-    ts = [oracle_sample_time(p, den) for _ in range(max(1, min(a.steps, 3)))]
-    us = statistics.median(ts) * 1e6
-    sample = f"Alg.3 tp=1 oracle on W1[:, :N1/{den}], W2[:N1/{den}, :] (1/{den} of the work), x{den}"
+    L1, L2, prep = oracle_prepare(p)
+    for _ in range(a.warmup):
+        oracle_forward(p.X, L1, L2)
+    ts, tds, tms = [], [], []
+    for _ in range(a.steps):
+        t0 = time.perf_counter()
+        _, td, tm = oracle_forward(p.X, L1, L2)
+        ts.append(time.perf_counter() - t0)
+        tds.append(td)
+        tms.append(tm)
+    us = statistics.mean(ts) * 1e6
+    base = {"value": us, "unit": "us", "cores": cpu_cores(), "blas_threads": blas_threads(), "kind": "oracle",
+            "sample": f"full forward per step: fp64 dequantize + matmul of both layers (M={a.m}), column blocks of 2048",
+            "phases_s": {"dequant": statistics.median(tds), "matmul": statistics.median(tms),
+                         "total": statistics.median(ts), "offline_unpack": prep["unpack_s"],
+                         "offline_alg1": prep["alg1_s"]}}
     line = {"metric": METRIC, "value": us, "unit": "us", "impl": "reference", "n_gpus": a.gpus,
-            "steps": len(ts), "warmup": min(a.warmup, 1), "ms_per_step": us / 1e3, "higher_is_better": False,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": us / 1e3, "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{a.shape}-mlp K1={K1} N1={N1} N2={N2} G={G} M={a.m} tp={tp} {a.variant}",
-                       "M": a.m, "tp": tp},
-            "cpu_baseline": {"value": us, "unit": "us", "cores": cpu_cores(), "kind": "oracle", "sample": sample},
+            "config": {"workload": f"{a.shape}-mlp K1={K1} N1={N1} N2={N2} G={G} M={a.m} tp=1 {a.variant}", "M": a.m,
+                       "tp": 1, "variant": a.variant, "implementation": "CPU oracle (oracle/, fp64 numpy), tp = 1"},
+            "cpu_baseline": base,
             "e2e": {"value": us, "unit": "us", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
 # ------------------------------------------------------------------------------------ ours
+def make_handles(tpq, p, P1, P2, tp, rank, variant, local, step_bytes, dev):
+    """R replicas of one rank's shard so that R x (bytes per forward) >= 3 x L2: consecutive
+    forwards in the timed region read cold weights (the 80-layer case)."""
+    import torch
+    l2_cache = torch.cuda.get_device_properties(dev).L2_cache_size
+    R = max(1, -(-3 * l2_cache // int(step_bytes)))
+    hs = [tpq.TpMlp(p.w1, p.w2, P1, P2, tp=tp, rank=rank, variant=variant, M_max=16, device=local) for _ in range(R)]
+    return hs, R, l2_cache
+
+
+def graph_of(torch, stream, n, launch):
+    """CUDA graph of n consecutive launches (launch(i) enqueues the i-th)."""
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=stream):
+        for i in range(n):
+            launch(i)
+    return g
+
+
+def time_graph(torch, stream, g, reps, per):
+    """Mean device time per launch of a captured graph of `per` launches, replayed `reps` times
+    between two events on `stream` (no event inside the graph)."""
+    for _ in range(3):
+        g.replay()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        s.record(stream)
+        for _ in range(reps):
+            g.replay()
+        e.record(stream)
+    e.synchronize()
+    return s.elapsed_time(e) * 1e3 / (reps * per)
+
+
+def step_latency(torch, tpq, hs, R, stream, M, sim_tp, X, Y, reps=40):
+    """Graph-timed forward latency (us) at M rows, rotating the weight replicas."""
+    per = R * max(1, 16 // R)
+    f = (lambda h: h.forward_local(X, M, Y, stream=stream)) if sim_tp else (lambda h: h.forward(X, M, Y, stream=stream))
+    with torch.cuda.stream(stream):
+        for i in range(per):
+            f(hs[i % R])
+        g = graph_of(torch, stream, per, lambda i: f(hs[i % R]))
+    return time_graph(torch, stream, g, max(1, reps * 16 // per), per)
+
+
+def kernel_times(torch, tpq, hs, R, stream, M, tp):
+    """Device time per launch (us) of each step of the forward, timed alone: a CUDA graph of many
+    launches of that step alone (rotating the cold weight replicas), events only around the
+    replays.  Layer steps include the split-tile fix-up kernel that follows each GEMV."""
+    per = R * max(1, 16 // R)
+    steps = [("gather", tpq.TPQ_STEP_GATHER), ("layer1", tpq.TPQ_STEP_LAYER1), ("layer2", tpq.TPQ_STEP_LAYER2)]
+    if tp > 1 and hs[0].info.has_comm:
+        steps.append(("allreduce", tpq.TPQ_STEP_ALLREDUCE))
+    out = {}
+    for name, st in steps:
+        with torch.cuda.stream(stream):
+            for i in range(per):
+                hs[i % R].run_step(st, M, stream=stream)
+            g = graph_of(torch, stream, per, lambda i: hs[i % R].run_step(st, M, stream=stream))
+        out[name] = time_graph(torch, stream, g, max(5, 1600 // per), per)
+    return out
+
+
+def extra_workload(torch, tpq, shape, M_list, sim_tp, seed, local, dev, stream):
+    """Graph-timed step latency of another BASELINE.json workload on this GPU (N = 1):
+    Granite-20B at TP = 1, or one rank's shard of a TP = k Llama MLP (no collective)."""
+    K1, N1, N2, G = synth.SHAPES[shape]
+    p = synth.make_named(shape, 16, seed)
+    P1, _ = tpq.gptq_reorder(p.w1.g_idx, G)
+    P2, _ = tpq.gptq_reorder(p.w2.g_idx, G)
+    tp = sim_tp or 1
+    _, _, step_b = algorithmic_bytes(K1, N1, N2, G, 16, tp)
+    hs, R, _ = make_handles(tpq, p, P1, P2, tp, 0, tpq.TPQ_TP_AWARE, local, step_b, dev)
+    X = torch.from_numpy(p.X.copy()).to(dev)
+    Y = torch.empty(16, N2, dtype=torch.float16, device=dev)
+    res = {}
+    peak, _ = peaks()
+    for M in M_list:
+        us = step_latency(torch, tpq, hs, R, stream, M, sim_tp, X, Y)
+        b = algorithmic_bytes(K1, N1, N2, G, M, tp)[2]
+        res[str(M)] = {"us": us, "hbm_frac": b / (us * 1e-6) / 1e9 / peak}
+    for h in hs:
+        h.close()
+    return res
+
+
 def main():
     a = parse()
     if a.impl == "reference":
@@ -214,17 +338,14 @@ def main():
     shard_tp = sim_tp or tp
     K1, N1, N2, G = synth.SHAPES[a.shape]
     M = a.m
+    assert 1 <= M <= 16, "bench.py times the M <= 16 path (BASELINE.json configs[1-2])"
     variant = tpq.TPQ_TP_AWARE if a.variant == "tp_aware" else tpq.TPQ_NAIVE
     p = synth.make_named(a.shape, max(M, 16), a.seed)
     P1, _ = tpq.gptq_reorder(p.w1.g_idx, G)
     P2, _ = tpq.gptq_reorder(p.w2.g_idx, G)
-
     l1_bytes, l2_bytes, step_bytes = algorithmic_bytes(K1, N1, N2, G, M, shard_tp)
-    # cold L2: rotate R weight replicas with R * bytes >= 3 x L2
-    l2_cache = torch.cuda.get_device_properties(dev).L2_cache_size
-    R = max(1, -(-3 * l2_cache // int(step_bytes)))
-    hs = [tpq.TpMlp(p.w1, p.w2, P1, P2, tp=shard_tp, rank=rank, variant=variant, M_max=16, device=local)
-          for _ in range(R)]
+    hs, R, l2_cache = make_handles(tpq, p, P1, P2, shard_tp, rank, variant, local, step_bytes, dev)
+    comm = None
     if tp > 1:
         uid = torch.zeros(128, dtype=torch.uint8, device=dev)
         if rank == 0:
@@ -244,46 +365,33 @@ def main():
             dist.barrier()
             torch.cuda.synchronize(dev)
 
-    # ---------------- warm-up
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---------------- warm-up: W eager forwards, then the graphs are captured and replayed
     with torch.cuda.stream(stream):
         for i in range(max(3, a.warmup)):
             fwd(hs[i % R])
     sync_all()
 
-    # ---------------- timed region: exactly K steps.
-    # Default: the steps are replayed from CUDA graphs of consecutive forwards (rotating the
-    # weight replicas) so host launch overhead is not measured: a graph of `per_graph` forwards
-    # replayed K // per_graph times plus a graph of the K % per_graph remaining forwards.  No
-    # timing events sit inside these graphs (an event node between kernels would break the
-    # programmatic-dependent-launch overlap); the per-kernel breakdown comes from a separate
-    # graph with the library's event hook, replayed after the timed region.
+    # ---------------- timed region: exactly K steps.  The steps are replayed from CUDA graphs of
+    # consecutive forwards (rotating the weight replicas, no event nodes inside): a graph of
+    # `per_graph` forwards replayed K // per_graph times plus a graph of the K % per_graph rest.
     # --no-graph launches every forward eagerly through the C-ABI.
     K = a.steps
-    per_graph = R * max(1, 16 // R)
+    # short runs: ONE graph of exactly K forwards (a graph replay's first forward has no PDL overlap
+    # with a preceding one; one replay per run keeps that to once); long runs: graphs of 16
+    per_graph = K if K <= 128 else R * max(1, 16 // R)
     rem = K % per_graph
-
-    def capture(n, timed_evs=None):
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, stream=stream):
-            for i in range(n):
-                h = hs[i % R]
-                if timed_evs is not None:
-                    h.set_timing(timed_evs[i])
-                fwd(h)
-                if timed_evs is not None:
-                    h.set_timing(None)
-        return g
-
-    n_ev = per_graph
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(6)] for _ in range(n_ev)]
-    for es_ in evs:  # torch creates the cudaEvent_t lazily, on first record
-        for e in es_:
-            e.record(stream)
-    sync_all()
     graph = graph_rem = None
     if not a.no_graph:
-        graph = capture(per_graph)
-        graph_rem = capture(rem) if rem else None
+        with torch.cuda.stream(stream):
+            graph = graph_of(torch, stream, per_graph, lambda i: fwd(hs[i % R]))
+            graph_rem = graph_of(torch, stream, rem, lambda i: fwd(hs[i % R])) if rem else None
         for _ in range(max(3, a.warmup // per_graph)):
             graph.replay()
         if graph_rem is not None:
@@ -307,60 +415,51 @@ def main():
         end.record(stream)
     sync_all()
     clk = clocks.stop()
-    total_ms = start.elapsed_time(end)
-    if world > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
-    ms_per_step = total_ms / K
+    ms_per_step = max_over_ranks(start.elapsed_time(end)) / K
 
-    # ---------------- per-kernel breakdown (events around each launch; not the headline)
-    with torch.cuda.stream(stream):
-        if graph is not None:
-            gev = capture(per_graph, evs)
-            for _ in range(3):
-                gev.replay()
-        else:
-            for i in range(n_ev):
-                h = hs[i % R]
-                h.set_timing(evs[i])
-                fwd(h)
-                h.set_timing(None)
-    sync_all()
-    t_l1 = statistics.mean(e[1].elapsed_time(e[2]) for e in evs) * 1e3  # us
-    t_l2 = statistics.mean(e[3].elapsed_time(e[4]) for e in evs) * 1e3
-    t_gather = statistics.mean(e[0].elapsed_time(e[1]) for e in evs) * 1e3
-    t_coll = statistics.mean(e[4].elapsed_time(e[5]) for e in evs) * 1e3
-    t_mid = statistics.mean(e[2].elapsed_time(e[3]) for e in evs) * 1e3
+    # ---------------- per-step distribution: events around each replay of the same graph
+    stats = None
+    if graph is not None:
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(61)]
+        with torch.cuda.stream(stream):
+            for i in range(61):
+                evs[i].record(stream)
+                if i < 60:
+                    graph.replay()
+        sync_all()
+        per_step = sorted(evs[i].elapsed_time(evs[i + 1]) * 1e3 / per_graph for i in range(60))
+        q = lambda f: per_step[min(59, int(f * 60))]  # noqa: E731
+        stats = {"median_us": max_over_ranks(statistics.median(per_step)), "p10_us": max_over_ranks(q(0.1)),
+                 "p90_us": max_over_ranks(q(0.9)), "samples": 60,
+                 "what": f"60 replays of the {per_graph}-forward graph after the timed region, per-step mean "
+                         "of each replay; max over ranks"}
+
+    # ---------------- each step's kernels timed alone (roofline of the dominant kernel)
+    kt = kernel_times(torch, tpq, hs, R, stream, M, tp)
+    kt = {k: max_over_ranks(v) for k, v in kt.items()}
+    peak, peak_kind = peaks()
+    gemv_us = kt["layer1"] + kt["layer2"]
+    achieved = (l1_bytes + l2_bytes) / (gemv_us * 1e-6) / 1e9
 
     # ---------------- e2e through the public host-buffer API (pinned host memory)
     # (--sim-tp has no host-buffer path: one rank's shard alone is not a complete forward)
     Xh = torch.from_numpy(p.X[:M].copy()).pin_memory()
     Yh = torch.empty(M, N2, dtype=torch.float16).pin_memory()
     Ke = max(20, min(K // 10, 2000))
-    es, ee = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2e = None
     if not sim_tp:
         for i in range(5):
             hs[i % R].forward_host(Xh.numpy(), Yh.numpy(), stream=stream)
         sync_all()
+        es, ee = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         es.record(stream)
         for i in range(Ke):
             hs[i % R].forward_host(Xh.numpy(), Yh.numpy(), stream=stream)
         ee.record(stream)
-    else:
-        es.record(stream)
-        ee.record(stream)
-    sync_all()
-    e2e_ms = es.elapsed_time(ee) / Ke if not sim_tp else float("nan")
-    if world > 1:
-        t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
+        sync_all()
+        e2e = {"value": max_over_ranks(es.elapsed_time(ee) / Ke) * 1e3, "unit": "us",
+               "h2d_bytes_per_step": 2 * M * K1, "d2h_bytes_per_step": 2 * M * N2}
 
-    # ---------------- roofline of the dominant kernel (the dequant GEMV, both launches)
-    peak, peak_kind = peaks()
-    gemv_us = t_l1 + t_l2
-    achieved = (l1_bytes + l2_bytes) / (gemv_us * 1e-6) / 1e9
     line = {
         "metric": METRIC, "value": ms_per_step * 1e3, "unit": "us", "n_gpus": world, "steps": K,
         "warmup": max(3, a.warmup), "ms_per_step": ms_per_step, "higher_is_better": False,
@@ -374,16 +473,19 @@ def main():
                       f"CUDA graphs: {per_graph} forwards x {K // per_graph} replays + {rem}",
             "parallelism": f"tp{shard_tp}",
         },
+        "step_stats": stats,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": ncu_traffic(a, shard_tp), "peak_kind": peak_kind,
-                     "kernel": "k_dqgemv (layer-1 + layer-2 launches)",
-                     "algorithmic_bytes_per_launch": (l1_bytes + l2_bytes) / 2},
-        "breakdown_us": {"gather": t_gather, "gemv_l1": t_l1, "between": t_mid, "gemv_l2": t_l2,
-                         "allreduce": t_coll},
+                     "kernel": "k_dqgemv + split-tile fix-up, layer 1 and layer 2",
+                     "algorithmic_bytes_per_launch": (l1_bytes + l2_bytes) / 2,
+                     "launch_us": {"layer1": kt["layer1"], "layer2": kt["layer2"]},
+                     "how": "each layer's GEMV (+ fix-up) alone in a CUDA graph of many launches over the cold "
+                            "replicas, CUDA events around the replays only"},
+        "kernel_us": kt,
+        "kernel_sum_us": sum(kt.values()),
         "step_roofline": {"bytes": step_bytes, "GBps": step_bytes / (ms_per_step * 1e-3) / 1e9,
                           "frac": step_bytes / (ms_per_step * 1e-3) / 1e9 / peak},
-        "e2e": None if sim_tp else {"value": e2e_ms * 1e3, "unit": "us", "h2d_bytes_per_step": 2 * M * K1,
-                                    "d2h_bytes_per_step": 2 * M * N2},
+        "e2e": e2e,
         "gpu_launches": K * launches_per_step(M, variant == tpq.TPQ_NAIVE),
         "clocks": clk,
     }
@@ -395,18 +497,35 @@ def main():
                                                  sync_all, world, dev, ms_per_step)
         except Exception as e:  # report, keep the TP-aware line
             line["naive_allgather"] = {"error": f"{type(e).__name__}: {e}"}
-    if world == 1 and a.sweep:  # (collective forwards at N > 1 would need every rank)
-        line["sweep_us_by_M"] = sweep_m(hs, p, R, stream, dev, sim_tp)
-    if rank == 0 and world == 1 and not a.no_cpu_baseline:
-        den = 4 if a.shape != "tiny" else 1
-        t = oracle_sample_time(synth.make_named(a.shape, M, a.seed), den)
-        line["cpu_baseline"] = {"value": t * 1e6, "unit": "us", "cores": cpu_cores(), "kind": "oracle",
-                                "sample": f"Alg.3 tp=1 fp64 oracle on W1[:, :N1/{den}], W2[:N1/{den}, :] "
-                                          f"(1/{den} of one forward), scaled x{den}"}
-    if rank == 0:
-        print(json.dumps(line), flush=True)
+    if world == 1 and not a.quick:
+        # the rest of the metric's grid on this GPU (graph-timed, after the timed region)
+        line["sweep_us_by_M"] = {str(m): step_latency(torch, tpq, hs, R, stream, m, sim_tp, X if m <= M else
+                                                      torch.from_numpy(p.X[:m].copy()).to(dev), Y if m <= M else
+                                                      torch.empty(m, N2, dtype=torch.float16, device=dev))
+                                 for m in (1, 4, 8, 16)}
     for h in hs:
         h.close()
+    if world == 1 and not a.quick and not sim_tp and a.shape == "llama70b":
+        line["granite20b_tp1"] = extra_workload(torch, tpq, "granite20b", (1, 16), 0, a.seed, local, dev, stream)
+        line["llama70b_tp8_shard"] = extra_workload(torch, tpq, "llama70b", (1, 16), 8, a.seed, local, dev, stream)
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        pc = synth.make_named(a.shape, M, a.seed)
+        L1, L2, prep = oracle_prepare(pc)
+        ts, tds, tms = [], [], []
+        for _ in range(2):
+            t0 = time.perf_counter()
+            _, td, tm = oracle_forward(pc.X, L1, L2)
+            ts.append(time.perf_counter() - t0)
+            tds.append(td)
+            tms.append(tm)
+        line["cpu_baseline"] = {"value": min(ts) * 1e6, "unit": "us", "cores": cpu_cores(),
+                                "blas_threads": blas_threads(), "kind": "oracle",
+                                "sample": f"one full forward (fp64 dequantize + matmul, both layers, M={M}), "
+                                          "best of 2, no extrapolation",
+                                "phases_s": {"dequant": min(tds), "matmul": min(tms), "total": min(ts),
+                                             "offline_unpack": prep["unpack_s"], "offline_alg1": prep["alg1_s"]}}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
     if tp > 1:
         comm.close()
     if world > 1:
@@ -460,36 +579,6 @@ def time_naive(a, p, P1, P2, tp, rank, local, R, comm, X, Y, stream, sync_all, w
             "speedup_tp_aware": ms / ours_ms,
             "what": "Alg. 2: layer 1, ncclAllGather(Y1), P2 gather + CHUNK, layer 2, ncclAllReduce; "
                     "same kernels, CUDA-graph timed, max over ranks"}
-
-
-def sweep_m(hs, p, R, stream, dev, sim_tp):
-    """Step latency (us) at M = 1, 4, 8, 16 on the same handles: CUDA graphs of R * k forwards
-    (rotating the cold weight replicas) replayed after warm-up, as in the main timed region."""
-    import torch
-    out = {}
-    per = R * max(1, 16 // R)
-    for M in (1, 4, 8, 16):
-        X = torch.from_numpy(p.X[:M].copy()).to(dev)
-        Y = torch.empty(M, p.N2, dtype=torch.float16, device=dev)
-        f = (lambda h: h.forward_local(X, M, Y, stream=stream)) if sim_tp else (lambda h: h.forward(X, M, Y, stream=stream))
-        with torch.cuda.stream(stream):
-            for i in range(per):
-                f(hs[i % R])
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=stream):
-                for i in range(per):
-                    f(hs[i % R])
-            for _ in range(5):
-                g.replay()
-            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            reps = max(1, 2000 // per)
-            s.record(stream)
-            for _ in range(reps):
-                g.replay()
-            e.record(stream)
-        torch.cuda.synchronize(dev)
-        out[str(M)] = s.elapsed_time(e) * 1e3 / (reps * per)
-    return out
 
 
 if __name__ == "__main__":

@@ -175,12 +175,20 @@ int tpq_layer2(tpq_mlp* h, const void* Y1in, int64_t M, void* Y2_local, void* st
 int tpq_sum_partials(const void* const* parts, int nparts, int64_t count, void* out,
                      void* stream);
 
-/* Optional timing hook (benchmarking): `events` is a HOST array of 6 cudaEvent_t (as void*)
- * created on the handle's device, or NULL to disable.  While set, each forward records on its
- * stream: [0] before the X[:,P1] gather, [1] before the layer-1 GEMV, [2] after it, [3] before
- * the layer-2 GEMV (after the naive AllGather + P2 gather; == [2] for TP-aware), [4] after the
- * layer-2 GEMV, [5] after the AllReduce.  The array is copied; events stay caller-owned. */
-int tpq_mlp_set_timing(tpq_mlp* h, void* const* events);
+/* Benchmarking export: enqueue ONE step of the M <= 16 TP-aware forward on the handle's own
+ * device buffers (contents are whatever the buffers hold; no result is defined), so that each
+ * step's kernels can be timed alone, e.g. as a CUDA graph of many launches (bench.py):
+ *   TPQ_STEP_GATHER    (0)  X[:, P1] gather (Alg. 3 L1 operand) from the host-forward staging buffer
+ *   TPQ_STEP_LAYER1    (1)  layer-1 dequant-GEMV + its split-tile fix-up      (Alg. 3 L1)
+ *   TPQ_STEP_LAYER2    (2)  layer-2 dequant-GEMV + its split-tile fix-up      (Alg. 3 L2)
+ *   TPQ_STEP_ALLREDUCE (3)  ncclAllReduce of the [M][N2] output (tp > 1 with a comm; Alg. 3 L3)
+ * TPQ_EINVAL for an unknown step or M outside [1, min(16, M_max)]; TPQ_ESTATE for a host-only
+ * handle or step 3 without a comm. */
+#define TPQ_STEP_GATHER 0
+#define TPQ_STEP_LAYER1 1
+#define TPQ_STEP_LAYER2 2
+#define TPQ_STEP_ALLREDUCE 3
+int tpq_mlp_run_step(tpq_mlp* h, int step, int64_t M, void* stream);
 
 
 /* ------------------------------- introspection / test-only exports ------------------- */

@@ -17,6 +17,7 @@ LIB_PATH = os.environ.get("TPQ_LIB_PATH") or os.path.join(_PKG, "libtpq.so")
 
 TPQ_OK, TPQ_EINVAL, TPQ_EUNSUPPORTED, TPQ_ECUDA, TPQ_ENCCL, TPQ_ENOMEM, TPQ_ESTATE = range(7)
 TPQ_NAIVE, TPQ_TP_AWARE = 0, 1
+TPQ_STEP_GATHER, TPQ_STEP_LAYER1, TPQ_STEP_LAYER2, TPQ_STEP_ALLREDUCE = 0, 1, 2, 3
 _CODES = {1: "EINVAL", 2: "EUNSUPPORTED", 3: "ECUDA", 4: "ENCCL", 5: "ENOMEM", 6: "ESTATE"}
 
 # Every symbol include/tpq.h declares (tests check the .so exports all of them).
@@ -25,7 +26,7 @@ EXPORTS = [
     "tpq_comm_unique_id", "tpq_comm_create", "tpq_comm_destroy", "tpq_mlp_set_comm",
     "tp_mlp_forward", "tp_mlp_forward_host",
     "tp_mlp_forward_local", "tpq_layer1", "tpq_naive_gather", "tpq_layer2", "tpq_sum_partials",
-    "tpq_mlp_info", "tpq_mlp_index_maps", "tpq_mlp_export_canonical", "tpq_mlp_set_timing",
+    "tpq_mlp_info", "tpq_mlp_index_maps", "tpq_mlp_export_canonical", "tpq_mlp_run_step",
 ]
 
 
@@ -82,7 +83,7 @@ def lib() -> C.CDLL:
             "tpq_mlp_info": [vp, C.POINTER(MlpInfo)],
             "tpq_mlp_index_maps": [vp, vp, vp, C.POINTER(i32), C.POINTER(i32)],
             "tpq_mlp_export_canonical": [vp, C.c_int, vp, vp, vp],
-            "tpq_mlp_set_timing": [vp, vp],
+            "tpq_mlp_run_step": [vp, C.c_int, C.c_int64, vp],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -228,13 +229,9 @@ class TpMlp:
     def layer2(self, Y1in, M: int, Y2, stream=None):
         _check(lib().tpq_layer2(self._h, _ptr(Y1in), M, _ptr(Y2), _stream(stream)))
 
-    def set_timing(self, events):
-        """events: 6 torch.cuda.Event (or None to disable); see tpq_mlp_set_timing."""
-        if events is None:
-            _check(lib().tpq_mlp_set_timing(self._h, None))
-            return
-        arr = (C.c_void_p * 6)(*[e.cuda_event for e in events])
-        _check(lib().tpq_mlp_set_timing(self._h, C.cast(arr, C.c_void_p)))
+    def run_step(self, step: int, M: int, stream=None):
+        """Benchmarking: enqueue one step (TPQ_STEP_*) on the handle's own buffers."""
+        _check(lib().tpq_mlp_run_step(self._h, int(step), M, _stream(stream)))
 
     # --- test exports
     def index_maps(self):

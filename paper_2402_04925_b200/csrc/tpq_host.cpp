@@ -221,8 +221,6 @@ struct tpq_mlp {
   int sms = 148;
   int rows = 16;                       // activation rows per pass: 16 (GEMV) or 256 (M_max > 16)
   ncclComm_t comm = nullptr;
-  cudaEvent_t ev[6] = {};
-  bool timing = false;
 };
 
 namespace {
@@ -579,19 +577,7 @@ int check_fwd(tpq_mlp* h, const void* X, int64_t M, const void* Y) {
 // Gather + layer 1 + (naive: AllGather + P2 gather) + layer 2 for one chunk of <= 16 rows.
 // Writes the rank-local partial Y2 (row-major [mc][N2] at Y).  `collective` enables the naive
 // AllGather (tp > 1); otherwise the naive path must be at tp == 1.
-// External event record: under stream capture this becomes a timed event node of the graph.
-#define TPQ_MARK(i) \
-  if (h->timing) TPQ_CUDA(mark_event(h->ev[i], st))
 
-// Under stream capture an external record becomes a timed event node of the graph; outside a
-// capture a plain record is the only legal form.
-static cudaError_t mark_event(cudaEvent_t e, cudaStream_t st) {
-  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-  cudaError_t err = cudaStreamIsCapturing(st, &cs);
-  if (err != cudaSuccess) return err;
-  return cs == cudaStreamCaptureStatusActive ? cudaEventRecordWithFlags(e, st, cudaEventRecordExternal)
-                                             : cudaEventRecord(e, st);
-}
 
 // One dequant-GEMM layer for mc rows: the GEMV (mc <= 16) or the A7 tensor-core GEMM (mc <= 256).
 cudaError_t run_layer(tpq_mlp* h, int layer, int mc, void* out, int64_t out_ld, cudaStream_t st) {
@@ -609,16 +595,13 @@ int64_t pass_rows(const tpq_mlp* h, int64_t M) { return M <= tpq::kMaxM ? tpq::k
 
 int chunk_forward(tpq_mlp* h, const uint16_t* X, int mc, void* Y, cudaStream_t st, bool collective) {
   TPQ_CUDA(tpq::launch_gather_rowmajor(X, h->K1, h->d_P1, tpq::GATHER_COLS, 0, mc, h->K1, h->d_x1, st));  // X[:,P1]
-  TPQ_MARK(1);
   if (h->variant == TPQ_TP_AWARE) {
     // Alg. 3 L1: Y1_local is already in the row order of this rank's W2[P2] block (no exchange)
     TPQ_CUDA(run_layer(h, 1, mc, h->d_y1, h->n, st));
-    TPQ_MARK(2);
   } else {
     // Alg. 2 L1 into this rank's slot of the AllGather buffer [tp][mc][n]
     uint8_t* slot = (uint8_t*)h->d_buf + (size_t)h->rank * mc * h->n * 2;
     TPQ_CUDA(run_layer(h, 1, mc, slot, h->n, st));
-    TPQ_MARK(2);
     if (h->tp > 1) {
       if (!collective) return fail(TPQ_ESTATE, "naive variant with tp > 1 needs the AllGather (use tp_mlp_forward)");
       TPQ_NCCL(ncclAllGather(slot, h->d_buf, (size_t)mc * h->n, ncclFloat16, h->comm, st));  // Alg. 2 L2
@@ -626,16 +609,13 @@ int chunk_forward(tpq_mlp* h, const uint16_t* X, int mc, void* Y, cudaStream_t s
     // Alg. 2 L3-4: Y1_global[:, P2] then CHUNK(rank), fused into one gather
     TPQ_CUDA(tpq::launch_gather_rowmajor(h->d_buf, 0, h->d_gcols, tpq::GATHER_ALLGATHER, h->n, mc, h->n, h->d_y1, st));
   }
-  TPQ_MARK(3);
   TPQ_CUDA(run_layer(h, 2, mc, Y, h->N2, st));  // L2 GEMM
-  TPQ_MARK(4);
   return TPQ_OK;
 }
 
 int forward_impl(tpq_mlp* h, const void* X, int64_t M, void* Y, cudaStream_t st, bool collective) {
   if (collective && h->tp > 1 && !h->comm) return fail(TPQ_ESTATE, "tp=%d requires tpq_mlp_set_comm", h->tp);
   TPQ_CUDA(cudaSetDevice(h->device));
-  TPQ_MARK(0);
   const int64_t R = pass_rows(h, M);
   for (int64_t m0 = 0; m0 < M; m0 += R) {
     const int mc = (int)std::min<int64_t>(R, M - m0);
@@ -645,7 +625,6 @@ int forward_impl(tpq_mlp* h, const void* X, int64_t M, void* Y, cudaStream_t st,
   }
   if (collective && h->tp > 1)  // Alg. 2 L6 / Alg. 3 L3
     TPQ_NCCL(ncclAllReduce(Y, Y, (size_t)M * h->N2, ncclFloat16, ncclSum, h->comm, st));
-  TPQ_MARK(5);
   return TPQ_OK;
 }
 
@@ -733,18 +712,30 @@ int tpq_debug_cta(unsigned long long* out) { return tpq::cta_read(out) ? TPQ_ECU
 int tpq_debug_trace(long long* out) { return tpq::trace_read(out) ? TPQ_ECUDA : TPQ_OK; }
 #endif
 
-int tpq_mlp_set_timing(tpq_mlp* h, void* const* events) {
+int tpq_mlp_run_step(tpq_mlp* h, int step, int64_t M, void* stream) {
   if (!h) return fail(TPQ_EINVAL, "NULL handle");
-  if (!events) {
-    h->timing = false;
-    return TPQ_OK;
+  if (h->device < 0) return fail(TPQ_ESTATE, "host-only handle (device=-1)");
+  if (M < 1 || M > std::min<int64_t>(tpq::kMaxM, h->M_max)) return fail(TPQ_EINVAL, "M=%lld not in [1, 16]", (long long)M);
+  cudaStream_t st = (cudaStream_t)stream;
+  TPQ_CUDA(cudaSetDevice(h->device));
+  const int mc = (int)M;
+  switch (step) {
+    case TPQ_STEP_GATHER:
+      TPQ_CUDA(tpq::launch_gather_rowmajor(h->d_xin, h->K1, h->d_P1, tpq::GATHER_COLS, 0, mc, h->K1, h->d_x1, st));
+      return TPQ_OK;
+    case TPQ_STEP_LAYER1:
+      TPQ_CUDA(run_layer(h, 1, mc, h->d_y1, h->n, st));
+      return TPQ_OK;
+    case TPQ_STEP_LAYER2:
+      TPQ_CUDA(run_layer(h, 2, mc, h->d_yout, h->N2, st));
+      return TPQ_OK;
+    case TPQ_STEP_ALLREDUCE:
+      if (!h->comm) return fail(TPQ_ESTATE, "no communicator attached");
+      TPQ_NCCL(ncclAllReduce(h->d_yout, h->d_yout, (size_t)M * h->N2, ncclFloat16, ncclSum, h->comm, st));
+      return TPQ_OK;
+    default:
+      return fail(TPQ_EINVAL, "unknown step %d", step);
   }
-  for (int i = 0; i < 6; ++i) {
-    if (!events[i]) return fail(TPQ_EINVAL, "events[%d] is NULL", i);
-    h->ev[i] = (cudaEvent_t)events[i];
-  }
-  h->timing = true;
-  return TPQ_OK;
 }
 
 
