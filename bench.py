@@ -250,18 +250,19 @@ def graph_of(torch, stream, n, launch):
 
 
 def time_graph(torch, stream, g, reps, per):
-    """Mean device time per launch of a captured graph of `per` launches, replayed `reps` times
-    between two events on `stream` (no event inside the graph)."""
+    """Device time per launch (us) of a captured graph of `per` launches: the median over `reps`
+    replays, each bracketed by events on `stream` (no event inside the graph).  The median keeps
+    the number of a short, unthrottled run even if a long sequence of replays meets the power cap."""
     for _ in range(3):
         g.replay()
-    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(reps + 1)]
     with torch.cuda.stream(stream):
-        s.record(stream)
-        for _ in range(reps):
-            g.replay()
-        e.record(stream)
-    e.synchronize()
-    return s.elapsed_time(e) * 1e3 / (reps * per)
+        for i in range(reps + 1):
+            evs[i].record(stream)
+            if i < reps:
+                g.replay()
+    evs[-1].synchronize()
+    return statistics.median(evs[i].elapsed_time(evs[i + 1]) for i in range(reps)) * 1e3 / per
 
 
 def step_latency(torch, tpq, hs, R, stream, M, sim_tp, X, Y, reps=40):
@@ -272,7 +273,7 @@ def step_latency(torch, tpq, hs, R, stream, M, sim_tp, X, Y, reps=40):
         for i in range(per):
             f(hs[i % R])
         g = graph_of(torch, stream, per, lambda i: f(hs[i % R]))
-    return time_graph(torch, stream, g, max(1, reps * 16 // per), per)
+    return time_graph(torch, stream, g, reps, per)
 
 
 def kernel_times(torch, tpq, hs, R, stream, M, tp):
@@ -289,7 +290,7 @@ def kernel_times(torch, tpq, hs, R, stream, M, tp):
             for i in range(per):
                 hs[i % R].run_step(st, M, stream=stream)
             g = graph_of(torch, stream, per, lambda i: hs[i % R].run_step(st, M, stream=stream))
-        out[name] = time_graph(torch, stream, g, max(5, 1600 // per), per)
+        out[name] = time_graph(torch, stream, g, 40, per)
     return out
 
 
@@ -314,6 +315,26 @@ def extra_workload(torch, tpq, shape, M_list, sim_tp, seed, local, dev, stream):
     for h in hs:
         h.close()
     return res
+
+
+def unordered_line(torch, tpq, p, shape, local, dev, stream, kt_ordered, M):
+    """the same MLP WITHOUT Alg. 1 (TPQ_UNORDERED: rows in checkpoint order,
+    per-row group metadata looked up, the Fig. 1 formulation of PAPER.md:L36), same pipeline and
+    launch structure, timed like the main line: the paper's locality claim
+    measured on B200 as the per-layer kernel-time ratio."""
+    K1, N1, N2, G = synth.SHAPES[shape]
+    _, _, step_b = algorithmic_bytes(K1, N1, N2, G, M, 1)
+    hs, R, _ = make_handles(tpq, p, None, None, 1, 0, tpq.TPQ_UNORDERED, local, step_b, dev)
+    X = torch.from_numpy(p.X[:M].copy()).to(dev)
+    Y = torch.empty(M, N2, dtype=torch.float16, device=dev)
+    us = step_latency(torch, tpq, hs, R, stream, M, 0, X, Y)
+    kt = kernel_times(torch, tpq, hs, R, stream, M, 1)
+    for h in hs:
+        h.close()
+    return {"M": M, "step_us": us, "kernel_us": kt,
+            "layer_time_ratio_vs_ordered": {k: kt[k] / kt_ordered[k] for k in ("layer1", "layer2")},
+            "what": "no reorder; each 128-row block re-reads {s', -z s'} per row from an L2-resident "
+                    "[ng][N] table (64 KB per 128 x 128 block vs the 320 B header of an ordered record)"}
 
 
 def main():
@@ -497,6 +518,8 @@ def main():
                                                  sync_all, world, dev, ms_per_step)
         except Exception as e:  # report, keep the TP-aware line
             line["naive_allgather"] = {"error": f"{type(e).__name__}: {e}"}
+    clocks_x = ClockSampler(local)
+    clocks_x.start()
     if world == 1 and not a.quick:
         # the rest of the metric's grid on this GPU (graph-timed, after the timed region)
         line["sweep_us_by_M"] = {str(m): step_latency(torch, tpq, hs, R, stream, m, sim_tp, X if m <= M else
@@ -508,6 +531,9 @@ def main():
     if world == 1 and not a.quick and not sim_tp and a.shape == "llama70b":
         line["granite20b_tp1"] = extra_workload(torch, tpq, "granite20b", (1, 16), 0, a.seed, local, dev, stream)
         line["llama70b_tp8_shard"] = extra_workload(torch, tpq, "llama70b", (1, 16), 8, a.seed, local, dev, stream)
+    if world == 1 and not a.quick and not sim_tp and a.variant == "tp_aware":
+        line["unordered_tp1"] = unordered_line(torch, tpq, p, a.shape, local, dev, stream, kt, M)
+    line["clocks_extra_lines"] = clocks_x.stop()
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         pc = synth.make_named(a.shape, M, a.seed)
         L1, L2, prep = oracle_prepare(pc)

@@ -41,6 +41,7 @@ extern "C" {
 
 #define TPQ_NAIVE 0         /* Alg. 2: W1[P1] + AllGather + Y1[:,P2] + CHUNK */
 #define TPQ_TP_AWARE 1      /* Alg. 3: W1[P1,P2], no AllGather               */
+#define TPQ_UNORDERED 2     /* locality baseline (Fig. 1): no reorder, per-row g_idx */
 
 const char* tpq_last_error(void);
 int tpq_version(void); /* returns (major << 16) | minor; never fails */
@@ -90,6 +91,11 @@ typedef struct tpq_mlp tpq_mlp; /* opaque: one rank's shard of the two-layer MLP
  *   variant   TPQ_TP_AWARE: rank keeps W1[P1,P2] columns [r*n, (r+1)*n) (= original
  *             columns P2[r*n..]) and W2[P2] rows [r*n, (r+1)*n);  TPQ_NAIVE: rank keeps W1[P1]
  *             columns [r*n, (r+1)*n) and the same W2 rows.  n = N1 / tp.
+ *             TPQ_UNORDERED: the locality baseline of SURVEY.md §8(f) f3 -- NO reordering: rows
+ *             stay in checkpoint order with their Eq.-3 g_idx and the kernel looks each row's
+ *             group metadata up (the Fig. 1 formulation).  tp must be 1
+ *             (TPQ_EINVAL), M_max <= 16 and K/G <= 256 per layer (TPQ_EUNSUPPORTED); P1 and P2
+ *             are ignored (may be NULL); g_idx values must lie in [0, K/G).
  *   M_max     largest batch (rows of X) later passed to the forward; 1 <= M_max <= 512.
  *   device    CUDA device ordinal that will own the shard, or -1 for a HOST-ONLY handle
  *             (packing + index maps + export only; no CUDA call is made; forward = ESTATE).

@@ -16,7 +16,7 @@ _PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("TPQ_LIB_PATH") or os.path.join(_PKG, "libtpq.so")
 
 TPQ_OK, TPQ_EINVAL, TPQ_EUNSUPPORTED, TPQ_ECUDA, TPQ_ENCCL, TPQ_ENOMEM, TPQ_ESTATE = range(7)
-TPQ_NAIVE, TPQ_TP_AWARE = 0, 1
+TPQ_NAIVE, TPQ_TP_AWARE, TPQ_UNORDERED = 0, 1, 2
 TPQ_STEP_GATHER, TPQ_STEP_LAYER1, TPQ_STEP_LAYER2, TPQ_STEP_ALLREDUCE = 0, 1, 2, 3
 _CODES = {1: "EINVAL", 2: "EUNSUPPORTED", 3: "ECUDA", 4: "ENCCL", 5: "ENOMEM", 6: "ESTATE"}
 
@@ -182,8 +182,9 @@ class TpMlp:
                  M_max: int = 16, device: int = 0):
         s1, k1 = _layer_struct(w1)
         s2, k2 = _layer_struct(w2)
-        P1 = np.ascontiguousarray(P1, dtype=np.int32)
-        P2 = np.ascontiguousarray(P2, dtype=np.int32)
+        # TPQ_UNORDERED ignores the permutations (NULL pointers)
+        P1 = None if P1 is None else np.ascontiguousarray(P1, dtype=np.int32)
+        P2 = None if P2 is None else np.ascontiguousarray(P2, dtype=np.int32)
         h = C.c_void_p()
         _check(lib().tp_shard_mlp(C.byref(s1), C.byref(s2), _ptr(P1), _ptr(P2), tp, rank, variant,
                                   M_max, device, C.byref(h)))

@@ -53,6 +53,8 @@ struct LayerDev {
   float* ws_mm = nullptr;  // [grid_mm][2 slots][256][128] fp32 stream-K partials (A7 GEMM)
   float* ws_ss = nullptr;  // [items][128][128] fp32 k-split partials (A7 SS GEMM, M >= 128)
   const float* colf = nullptr;  // [N] 2^(24 - E_n): records hold s' = s 2^E_n (tpq_host.cpp column_exponents)
+  const uint32_t* meta = nullptr;  // unordered layer (TPQ_UNORDERED): [ng][N] {fp16 s', fp16 -z s' 2^-24}
+  int unord = 0;                   // 1: records in checkpoint row order with per-row group ids (k_dqgemv<0>)
 };
 
 enum GatherMode { GATHER_COLS = 0, GATHER_ALLGATHER = 1 };

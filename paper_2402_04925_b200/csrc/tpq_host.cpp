@@ -153,6 +153,55 @@ std::vector<uint8_t> pack_layer(const Canon& c, const std::vector<int>& E) {
   return out;
 }
 
+// Unordered-g_idx layer (TPQ_UNORDERED, the Fig. 1 formulation): records of the codes in checkpoint
+// row order (same code layout as pack_layer) followed by the 128 rows' group ids (uint8), and the
+// [ng][N] table {lo: fp16 s' = s 2^E_n, hi: fp16(-z s' 2^-24)} the kernel reads per row.
+struct Unord {
+  std::vector<uint8_t> rec;
+  std::vector<uint32_t> table;
+};
+uint16_t half_rn(float f) {  // round-to-nearest-even, subnormals included (host _Float16)
+  const _Float16 h = (_Float16)f;
+  uint16_t b;
+  memcpy(&b, &h, 2);
+  return b;
+}
+float half_to_float(uint16_t b) {
+  _Float16 h;
+  memcpy(&h, &b, 2);
+  return (float)h;
+}
+Unord pack_layer_unordered(const Canon& c, const std::vector<int>& E, const std::vector<int32_t>& gk) {
+  const int64_t NT = c.N / tpq::kTileCols, NKB = c.K / tpq::kUnitK, ng = c.K / c.G;
+  constexpr int64_t kCodes = tpq::kUnitK * tpq::kTileCols / 2, UB = kCodes + tpq::kUnitK;
+  Unord u;
+  u.rec.assign((size_t)(NT * NKB * UB), 0);
+  parallel_for(NT * NKB, [&](int64_t un) {
+    const int64_t t = un / NKB, kb = un % NKB;
+    uint8_t* rec = u.rec.data() + un * UB;
+    uint32_t* words = reinterpret_cast<uint32_t*>(rec);
+    for (int j = 0; j < tpq::kTileCols; ++j) {
+      const int64_t n = t * tpq::kTileCols + j;
+      for (int ch = 0; ch < tpq::kUnitK / 32; ++ch)
+        for (int w = 0; w < 4; ++w) {
+          const int64_t k0 = kb * tpq::kUnitK + 32 * ch + 8 * w;
+          uint32_t word = 0;
+          for (int i = 0; i < 8; ++i) word |= (uint32_t)c.q[(size_t)((k0 + i) * c.N + n)] << (4 * kNibbleOfK[i]);
+          words[tpq::code_block(ch, j) * 4 + w] = word;
+        }
+    }
+    for (int r = 0; r < tpq::kUnitK; ++r) rec[kCodes + r] = (uint8_t)gk[(size_t)(kb * tpq::kUnitK + r)];
+  });
+  u.table.resize((size_t)(ng * c.N));
+  for (int64_t g = 0; g < ng; ++g)
+    for (int64_t n = 0; n < c.N; ++n) {
+      const uint16_t sp = half_scale_up(c.s[(size_t)(g * c.N + n)], E[(size_t)n]);
+      const uint16_t cc = half_rn(-(float)c.z[(size_t)(g * c.N + n)] * half_to_float(sp) * 5.9604644775390625e-8f);
+      u.table[(size_t)(g * c.N + n)] = (uint32_t)sp | ((uint32_t)cc << 16);
+    }
+  return u;
+}
+
 // Inverse of pack_layer (test export).
 void unpack_layer(const std::vector<uint8_t>& pk, const std::vector<int>& E, int64_t K, int64_t N, int G, uint8_t* q,
                   uint16_t* s, uint8_t* z) {
@@ -201,6 +250,10 @@ struct tpq_mlp {
   std::vector<int32_t> P1, P2, w1_cols, w2_rows, gather_cols;
   int32_t w2_group_lo = 0, w2_group_hi = 0;
   std::vector<uint8_t> pk1, pk2;  // packed host copies
+  std::vector<uint32_t> tab1, tab2;  // unordered layers: [ng][N] {s', C} tables (TPQ_UNORDERED)
+  std::vector<uint8_t> z1u, z2u;      // unordered layers: zeros [ng][N] (export only)
+  std::vector<int32_t> g1u, g2u;      // unordered layers: per-row group (export only)
+  void* d_tab = nullptr;
   std::vector<int> E1, E2;        // per-column scale exponents of the records (column_exponents)
   tpq::LayerDev L1, L2;
   // device buffers
@@ -255,7 +308,7 @@ int validate_perm(const int32_t* P, const gptq_layer* w, const char* name) {
 void free_dev(tpq_mlp* h) {
   if (h->device < 0) return;
   cudaSetDevice(h->device);
-  void* ptrs[] = {h->d_w1, h->d_w2, h->d_P1, h->d_gcols, h->d_x1, h->d_y1, h->d_buf, h->d_xin, h->d_yout, h->d_ws, h->d_colf};
+  void* ptrs[] = {h->d_w1, h->d_w2, h->d_P1, h->d_gcols, h->d_x1, h->d_y1, h->d_buf, h->d_xin, h->d_yout, h->d_ws, h->d_colf, h->d_tab};
   for (void* p : ptrs)
     if (p) cudaFree(p);
 }
@@ -346,7 +399,11 @@ int tp_shard_mlp(const gptq_layer* w1, const gptq_layer* w2, const int32_t* P1, 
     return fail(TPQ_EINVAL, "w1->N=%lld != w2->K=%lld", (long long)w1->N, (long long)w2->K);
   if (tp != 1 && tp != 2 && tp != 4 && tp != 8) return fail(TPQ_EINVAL, "tp=%d not in {1,2,4,8}", tp);
   if (rank < 0 || rank >= tp) return fail(TPQ_EINVAL, "rank=%d not in [0,%d)", rank, tp);
-  if (variant != TPQ_NAIVE && variant != TPQ_TP_AWARE) return fail(TPQ_EINVAL, "variant=%d", variant);
+  if (variant != TPQ_NAIVE && variant != TPQ_TP_AWARE && variant != TPQ_UNORDERED)
+    return fail(TPQ_EINVAL, "variant=%d", variant);
+  const bool unord = variant == TPQ_UNORDERED;
+  if (unord && tp != 1) return fail(TPQ_EINVAL, "TPQ_UNORDERED is the single-rank locality baseline: tp=%d", tp);
+  if (unord && M_max > 16) return fail(TPQ_EUNSUPPORTED, "TPQ_UNORDERED runs the M <= 16 GEMV only (M_max=%lld)", (long long)M_max);
   if (M_max < 1 || M_max > 512) return fail(TPQ_EINVAL, "M_max=%lld not in [1,512]", (long long)M_max);
   if (device < -1) return fail(TPQ_EINVAL, "device=%d", device);
   const int64_t K1 = w1->K, N1 = w1->N, N2 = w2->N;
@@ -361,16 +418,33 @@ int tp_shard_mlp(const gptq_layer* w1, const gptq_layer* w2, const int32_t* P1, 
     return fail(TPQ_EINVAL, "n=N1/tp=%lld and N2=%lld must be multiples of 128 (device tiles)", (long long)n,
                 (long long)N2);
   if (n % w2->G) return fail(TPQ_EINVAL, "n=%lld not a multiple of G2=%d: W2 shard would split a group (c12)", (long long)n, w2->G);
-  if ((rc = validate_perm(P1, w1, "P1"))) return rc;
-  if ((rc = validate_perm(P2, w2, "P2"))) return rc;
+  if (unord) {
+    for (const gptq_layer* w : {w1, w2}) {
+      if (w->K / w->G > 256) return fail(TPQ_EUNSUPPORTED, "TPQ_UNORDERED: %lld groups > 256 (uint8 group ids)", (long long)(w->K / w->G));
+      for (int64_t k = 0; k < w->K; ++k)
+        if (w->g_idx[k] < 0 || w->g_idx[k] >= w->K / w->G) return fail(TPQ_EINVAL, "g_idx[%lld]=%d out of range", (long long)k, w->g_idx[k]);
+    }
+  } else {
+    if ((rc = validate_perm(P1, w1, "P1"))) return rc;
+    if ((rc = validate_perm(P2, w2, "P2"))) return rc;
+  }
 
   tpq_mlp* h = nullptr;
   try {
     h = new tpq_mlp();
     h->K1 = K1; h->N1 = N1; h->N2 = N2; h->n = n; h->M_max = M_max;
     h->G1 = w1->G; h->G2 = w2->G; h->tp = tp; h->rank = rank; h->variant = variant; h->device = device;
-    h->P1.assign(P1, P1 + K1);
-    h->P2.assign(P2, P2 + N1);
+    if (unord) {  // no reordering: identity maps (checkpoint order)
+      h->P1.resize(K1);
+      h->P2.resize(N1);
+      for (int64_t k = 0; k < K1; ++k) h->P1[k] = (int32_t)k;
+      for (int64_t k = 0; k < N1; ++k) h->P2[k] = (int32_t)k;
+      P1 = h->P1.data();
+      P2 = h->P2.data();
+    } else {
+      h->P1.assign(P1, P1 + K1);
+      h->P2.assign(P2, P2 + N1);
+    }
     h->w1_cols.resize(n);
     h->w2_rows.resize(n);
     for (int64_t j = 0; j < n; ++j) {
@@ -418,8 +492,21 @@ int tp_shard_mlp(const gptq_layer* w1, const gptq_layer* w2, const int32_t* P1, 
     }
     h->E1 = column_exponents(c1);
     h->E2 = column_exponents(c2);
-    h->pk1 = pack_layer(c1, h->E1);
-    h->pk2 = pack_layer(c2, h->E2);
+    if (unord) {
+      h->g1u.assign(w1->g_idx, w1->g_idx + K1);
+      h->g2u.assign(w2->g_idx, w2->g_idx + N1);
+      Unord u1 = pack_layer_unordered(c1, h->E1, h->g1u), u2 = pack_layer_unordered(c2, h->E2, h->g2u);
+      h->pk1 = std::move(u1.rec);
+      h->pk2 = std::move(u2.rec);
+      h->tab1 = std::move(u1.table);
+      h->tab2 = std::move(u2.table);
+      h->z1u = c1.z;
+      h->z2u = c2.z;
+      h->L1.unord = h->L2.unord = 1;
+    } else {
+      h->pk1 = pack_layer(c1, h->E1);
+      h->pk2 = pack_layer(c2, h->E2);
+    }
     plan_layer(h->L1, K1, n, w1->G, device);
     plan_layer(h->L2, n, N2, w2->G, device);
 
@@ -456,7 +543,8 @@ int tp_shard_mlp(const gptq_layer* w1, const gptq_layer* w2, const int32_t* P1, 
             (r = A(&h->d_y1, (size_t)h->rows * n * 2)) || (r = A(&h->d_buf, (size_t)tp * h->rows * n * 2)) ||
             (r = A(&h->d_xin, (size_t)M_max * K1 * 2)) || (r = A(&h->d_yout, (size_t)M_max * N2 * 2)) ||
             (r = A((void**)&h->d_ws, (ws1 + ws2 + wm1 + wm2 + ws1s + ws2s) * 4)) ||
-            (r = A((void**)&h->d_colf, (size_t)(n + N2) * 4)))
+            (r = A((void**)&h->d_colf, (size_t)(n + N2) * 4)) ||
+            (r = A(&h->d_tab, (h->tab1.size() + h->tab2.size()) * 4)))
           return r;
         TPQ_CUDA(cudaMemcpy(h->d_w1, h->pk1.data(), h->pk1.size(), cudaMemcpyHostToDevice));
         TPQ_CUDA(cudaMemcpy(h->d_w2, h->pk2.data(), h->pk2.size(), cudaMemcpyHostToDevice));
@@ -476,6 +564,13 @@ int tp_shard_mlp(const gptq_layer* w1, const gptq_layer* w2, const int32_t* P1, 
                 tpq::make_xmap(&h->ss2, h->d_y1, n, kGemmRows, 128);
         }
         if (!mok) return fail(TPQ_ECUDA, "cuTensorMapEncodeTiled failed for the activation buffers");
+        if (unord) {
+          TPQ_CUDA(cudaMemcpy(h->d_tab, h->tab1.data(), h->tab1.size() * 4, cudaMemcpyHostToDevice));
+          TPQ_CUDA(cudaMemcpy((uint32_t*)h->d_tab + h->tab1.size(), h->tab2.data(), h->tab2.size() * 4,
+                              cudaMemcpyHostToDevice));
+          h->L1.meta = (const uint32_t*)h->d_tab;
+          h->L2.meta = (const uint32_t*)h->d_tab + h->tab1.size();
+        }
         h->L1.colf = h->d_colf;
         h->L2.colf = h->d_colf + n;
         h->L1.packed = (const uint8_t*)h->d_w1;
@@ -595,8 +690,8 @@ int64_t pass_rows(const tpq_mlp* h, int64_t M) { return M <= tpq::kMaxM ? tpq::k
 
 int chunk_forward(tpq_mlp* h, const uint16_t* X, int mc, void* Y, cudaStream_t st, bool collective) {
   TPQ_CUDA(tpq::launch_gather_rowmajor(X, h->K1, h->d_P1, tpq::GATHER_COLS, 0, mc, h->K1, h->d_x1, st));  // X[:,P1]
-  if (h->variant == TPQ_TP_AWARE) {
-    // Alg. 3 L1: Y1_local is already in the row order of this rank's W2[P2] block (no exchange)
+  if (h->variant != TPQ_NAIVE) {
+    // Alg. 3 L1 (TPQ_UNORDERED: P1 = identity, checkpoint order): Y1_local is already in the row order of this rank's W2[P2] block (no exchange)
     TPQ_CUDA(run_layer(h, 1, mc, h->d_y1, h->n, st));
   } else {
     // Alg. 2 L1 into this rank's slot of the AllGather buffer [tp][mc][n]
@@ -764,6 +859,32 @@ int tpq_mlp_index_maps(const tpq_mlp* h, int32_t* w1_cols, int32_t* w2_rows, int
 
 int tpq_mlp_export_canonical(const tpq_mlp* h, int layer, uint8_t* q, uint16_t* s, uint8_t* z) {
   if (!h || !q || !s || !z) return fail(TPQ_EINVAL, "NULL");
+  if (h->variant == TPQ_UNORDERED) {
+    // codes from the records (checkpoint row order), scales from the table, zeros as packed
+    const std::vector<uint8_t>& pk = layer == 1 ? h->pk1 : h->pk2;
+    const std::vector<uint32_t>& tab = layer == 1 ? h->tab1 : h->tab2;
+    const std::vector<int>& E = layer == 1 ? h->E1 : h->E2;
+    const int64_t K = layer == 1 ? h->K1 : h->n, N = layer == 1 ? h->n : h->N2, G = layer == 1 ? h->G1 : h->G2;
+    if (layer != 1 && layer != 2) return fail(TPQ_EINVAL, "layer=%d", layer);
+    const int64_t NKB = K / tpq::kUnitK, UB = tpq::kUnitK * tpq::kTileCols / 2 + tpq::kUnitK;
+    for (int64_t un = 0; un < (N / tpq::kTileCols) * NKB; ++un) {
+      const int64_t t = un / NKB, kb = un % NKB;
+      const uint32_t* words = reinterpret_cast<const uint32_t*>(pk.data() + un * UB);
+      for (int j = 0; j < tpq::kTileCols; ++j)
+        for (int ch = 0; ch < tpq::kUnitK / 32; ++ch)
+          for (int w = 0; w < 4; ++w) {
+            const uint32_t word = words[tpq::code_block(ch, j) * 4 + w];
+            const int64_t k0 = kb * tpq::kUnitK + 32 * ch + 8 * w;
+            for (int i = 0; i < 8; ++i) q[(k0 + i) * N + t * tpq::kTileCols + j] = (word >> (4 * kNibbleOfK[i])) & 0xF;
+          }
+    }
+    for (int64_t g = 0; g < K / G; ++g)
+      for (int64_t c = 0; c < N; ++c) {
+        s[g * N + c] = half_scale_down((uint16_t)(tab[(size_t)(g * N + c)] & 0xFFFF), E[(size_t)c]);
+        z[g * N + c] = (layer == 1 ? h->z1u : h->z2u)[(size_t)(g * N + c)];
+      }
+    return TPQ_OK;
+  }
   if (layer == 1) unpack_layer(h->pk1, h->E1, h->K1, h->n, h->G1, q, s, z);
   else if (layer == 2) unpack_layer(h->pk2, h->E2, h->n, h->N2, h->G2, q, s, z);
   else return fail(TPQ_EINVAL, "layer=%d", layer);

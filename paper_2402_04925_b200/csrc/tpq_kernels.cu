@@ -258,6 +258,8 @@ struct GemvArgs {
   int64_t out_ld;
   float* ws;        // [grid][2 slots][16][128] fp32 split-tile partials (slot 0 = first segment, 1 = last)
   const float* colf;  // [N] 2^(24 - E_n): the records hold s' = s 2^E_n per column n
+  const uint32_t* meta;  // unordered layers: [ng][ldm] {lo: fp16 s', hi: fp16 C = -z s' 2^-24}
+  int64_t ldm;
 };
 
 // ------------------------------------------------------------------ GEMV (M <= 16)
@@ -274,10 +276,14 @@ struct GemvArgs {
 constexpr int kSets = 3, kDeq0 = 4, kProdWarp = 16, kStageWarp = 17, kMmaWarp = 18;
 constexpr int kGemvThreads = 20 * 32;
 
+// G = 0: the unordered-g_idx layer (TPQ_UNORDERED, the Fig. 1 formulation): a record
+// holds the 128 rows' codes in checkpoint order plus their group ids (uint8), and the dequant warps
+// look each row's {s', C} up in an L2-resident [ng][N] table instead of a per-block record header.
 template <int G>
 struct TC {
-  static constexpr int KG = kUnitK / G;
-  static constexpr int UB = (int)unit_bytes_c(G);
+  static constexpr bool UN = G == 0;
+  static constexpr int KG = UN ? 1 : kUnitK / G;
+  static constexpr int UB = UN ? kUnitK * kTileCols / 2 + kUnitK : (int)unit_bytes_c(G == 0 ? 128 : G);
   static constexpr int STAGE = (UB + 127) / 128 * 128;
   static constexpr int NS = 18;                   // weight ring stages (units)
   static constexpr int XU = kNPad * kUnitK * 2;   // activation bytes per unit
@@ -372,40 +378,91 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_dqgemv(const GemvArgs a, co
         mbar_wait(full + sh_, phh);
         if (h == 0) { TPQ_EV(1, p) }
         const uint8_t* sp = smem + C::WRING + sh_ * C::STAGE;
-        __half2 sl[C::KG], shh[C::KG], zc[C::KG];
+        if constexpr (C::UN) {
+          // Fig. 1 formulation: every row k has its own group g(k); the pair (k, k+1) of a half2 gets
+          // S2 = (s'_g(k), s'_g(k+1)) and C2 = (C_g(k), C_g(k+1)) from the table, 4 bytes per (row,
+          // column) read from L2 (coalesced across the warp's 32 columns): 64 KB per 128 x 128 block
+          // against the 320 B header an ordered record carries ("frequently reload").
+          const uint32_t* gw = reinterpret_cast<const uint32_t*>(sp + kUnitK * kTileCols / 2);
+          const uint32_t* tab = a.meta + ((u0 + i) / a.NKB) * kTileCols + col;
+          uint4 cw[4];
 #pragma unroll
-        for (int g = 0; g < C::KG; ++g) {
-          const float z = (float)((sp[zbyte + g * 64] >> zsh) & 0xFu);
-          const float sf = __half2float(*reinterpret_cast<const __half*>(sp + sbyte + g * 256));
-          sl[g] = __float2half2_rn(sf);
-          shh[g] = __float2half2_rn(sf * 0.0625f);
-          zc[g] = __float2half2_rn(-z * sf * 5.9604644775390625e-8f);
-        }
-        uint4 cw[4];
+          for (int c = 0; c < 4; ++c) cw[c] = *reinterpret_cast<const uint4*>(sp + code_block(c, col) * 16);
+          const __half2 k16 = __float2half2_rn(0.0625f);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) cw[c] = *reinterpret_cast<const uint4*>(sp + code_block(c, col) * 16);
+          for (int kh = 0; kh < 2; ++kh) {
+            uint32_t r[32];
 #pragma unroll
-        for (int kh = 0; kh < 2; ++kh) {
-          uint32_t r[32];
+            for (int hb = 0; hb < 2; ++hb) {  // 4 words (32 rows) per batch: 32 table loads in flight
+              uint32_t t[32];
 #pragma unroll
-          for (int w = 0; w < 8; ++w) {
-            const int j = (64 * kh + 8 * w) / G;
-            const uint4 c4 = cw[2 * kh + w / 4];
-            const uint32_t x = (w & 3) == 0 ? c4.x : (w & 3) == 1 ? c4.y : (w & 3) == 2 ? c4.z : c4.w;
-            const uint32_t x8 = x >> 8;
-            r[4 * w + 0] = h2u(__hfma2(u2h(x & 0x000F000Fu), sl[j], zc[j]));
-            r[4 * w + 1] = h2u(__hfma2(u2h(x & 0x00F000F0u), shh[j], zc[j]));
-            r[4 * w + 2] = h2u(__hfma2(u2h(x8 & 0x000F000Fu), sl[j], zc[j]));
-            r[4 * w + 3] = h2u(__hfma2(u2h(x8 & 0x00F000F0u), shh[j], zc[j]));
+              for (int w = 0; w < 4; ++w) {
+                const int k0 = 64 * kh + 32 * hb + 8 * w;
+                const uint32_t ga = gw[k0 / 4], gb = gw[k0 / 4 + 1];
+#pragma unroll
+                for (int e = 0; e < 8; ++e)
+                  t[8 * w + e] = __ldg(tab + (int64_t)(((e < 4 ? ga : gb) >> (8 * (e & 3))) & 0xFFu) * a.ldm);
+              }
+#pragma unroll
+              for (int w = 0; w < 4; ++w) {
+                const int ww = 4 * hb + w;
+                const uint4 c4 = cw[2 * kh + ww / 4];
+                const uint32_t x = (ww & 3) == 0 ? c4.x : (ww & 3) == 1 ? c4.y : (ww & 3) == 2 ? c4.z : c4.w;
+                const uint32_t x8 = x >> 8;
+                const uint32_t* tt = t + 8 * w;
+                const __half2 s0 = u2h(__byte_perm(tt[0], tt[1], 0x5410)), c0 = u2h(__byte_perm(tt[0], tt[1], 0x7632));
+                const __half2 s1 = __hmul2(u2h(__byte_perm(tt[2], tt[3], 0x5410)), k16), c1 = u2h(__byte_perm(tt[2], tt[3], 0x7632));
+                const __half2 s2 = u2h(__byte_perm(tt[4], tt[5], 0x5410)), c2 = u2h(__byte_perm(tt[4], tt[5], 0x7632));
+                const __half2 s3 = __hmul2(u2h(__byte_perm(tt[6], tt[7], 0x5410)), k16), c3 = u2h(__byte_perm(tt[6], tt[7], 0x7632));
+                r[4 * ww + 0] = h2u(__hfma2(u2h(x & 0x000F000Fu), s0, c0));
+                r[4 * ww + 1] = h2u(__hfma2(u2h(x & 0x00F000F0u), s1, c1));
+                r[4 * ww + 2] = h2u(__hfma2(u2h(x8 & 0x000F000Fu), s2, c2));
+                r[4 * ww + 3] = h2u(__hfma2(u2h(x8 & 0x00F000F0u), s3, c3));
+              }
+            }
+            if (h == 0 && kh == 0 && p >= kSets) {
+              const int q = p - kSets;
+              mbar_wait_backoff(done + q % C::RD, (uint32_t)((q / C::RD) & 1), 0);
+              tc_fence_after();
+            }
+            tmem_st32(a_buf + h * C::AU + kh * 32, r);
           }
-          if (h == 0 && kh == 0 && p >= kSets) {
-            // own buffer free: pair p - 3's MMAs completed
-            const int q = p - kSets;
-            mbar_wait_backoff(done + q % C::RD, (uint32_t)((q / C::RD) & 1), 0);
-            TPQ_EV(2, p)
-            tc_fence_after();
+        } else {
+          __half2 sl[C::KG], shh[C::KG], zc[C::KG];
+  #pragma unroll
+          for (int g = 0; g < C::KG; ++g) {
+            const float z = (float)((sp[zbyte + g * 64] >> zsh) & 0xFu);
+            const float sf = __half2float(*reinterpret_cast<const __half*>(sp + sbyte + g * 256));
+            sl[g] = __float2half2_rn(sf);
+            shh[g] = __float2half2_rn(sf * 0.0625f);
+            zc[g] = __float2half2_rn(-z * sf * 5.9604644775390625e-8f);
           }
-          tmem_st32(a_buf + h * C::AU + kh * 32, r);
+          uint4 cw[4];
+  #pragma unroll
+          for (int c = 0; c < 4; ++c) cw[c] = *reinterpret_cast<const uint4*>(sp + code_block(c, col) * 16);
+  #pragma unroll
+          for (int kh = 0; kh < 2; ++kh) {
+            uint32_t r[32];
+  #pragma unroll
+            for (int w = 0; w < 8; ++w) {
+              const int j = (64 * kh + 8 * w) / G;
+              const uint4 c4 = cw[2 * kh + w / 4];
+              const uint32_t x = (w & 3) == 0 ? c4.x : (w & 3) == 1 ? c4.y : (w & 3) == 2 ? c4.z : c4.w;
+              const uint32_t x8 = x >> 8;
+              r[4 * w + 0] = h2u(__hfma2(u2h(x & 0x000F000Fu), sl[j], zc[j]));
+              r[4 * w + 1] = h2u(__hfma2(u2h(x & 0x00F000F0u), shh[j], zc[j]));
+              r[4 * w + 2] = h2u(__hfma2(u2h(x8 & 0x000F000Fu), sl[j], zc[j]));
+              r[4 * w + 3] = h2u(__hfma2(u2h(x8 & 0x00F000F0u), shh[j], zc[j]));
+            }
+            if (h == 0 && kh == 0 && p >= kSets) {
+              // own buffer free: pair p - 3's MMAs completed
+              const int q = p - kSets;
+              mbar_wait_backoff(done + q % C::RD, (uint32_t)((q / C::RD) & 1), 0);
+              TPQ_EV(2, p)
+              tc_fence_after();
+            }
+            tmem_st32(a_buf + h * C::AU + kh * 32, r);
+          }
         }
         // every register loaded from the stage fed the tcgen05.st just issued (in-order issue)
         __syncwarp();
@@ -1376,8 +1433,9 @@ bool prepare_gemv() {
 
 bool gemv_prepare(int G) {
   if (!(max_carveout(k_gather_rm) && max_carveout(k_gather_rows) && max_carveout(k_mm_fixup) && max_carveout(k_gemv_fixup) &&
-        max_carveout(k_ss_fixup) && max_carveout(k_sum_partials)))
+        max_carveout(k_ss_fixup) && max_carveout(k_sum_partials) && max_carveout(k_dqgemv<0>)))
     return false;
+  if (!prepare_gemv<0>()) return false;  // unordered-g_idx layers (any G)
   if (!(G == 128 ? carveout_g<128>() : G == 64 ? carveout_g<64>() : G == 32 ? carveout_g<32>() : false)) return false;
   if (G == 128) return prepare_gemv<128>() && prepare_mm_g<128>();
   if (G == 64) return prepare_gemv<64>() && prepare_mm_g<64>();
@@ -1398,7 +1456,10 @@ cudaError_t launch_gemv(const LayerDev& L, const CUtensorMap& xmap, int M, void*
   a.out_ld = out_ld;
   a.ws = L.ws;
   a.colf = L.colf;
-  cudaError_t e = L.G == 128 ? launch_pdl(k_dqgemv<128>, dim3(a.grid), dim3(kGemvThreads), TC<128>::SMEM, st, a, xmap)
+  a.meta = L.meta;
+  a.ldm = L.N;
+  cudaError_t e = L.unord ? launch_pdl(k_dqgemv<0>, dim3(a.grid), dim3(kGemvThreads), TC<0>::SMEM, st, a, xmap)
+                  : L.G == 128 ? launch_pdl(k_dqgemv<128>, dim3(a.grid), dim3(kGemvThreads), TC<128>::SMEM, st, a, xmap)
                   : L.G == 64 ? launch_pdl(k_dqgemv<64>, dim3(a.grid), dim3(kGemvThreads), TC<64>::SMEM, st, a, xmap)
                   : L.G == 32 ? launch_pdl(k_dqgemv<32>, dim3(a.grid), dim3(kGemvThreads), TC<32>::SMEM, st, a, xmap)
                               : cudaErrorInvalidValue;

@@ -191,3 +191,23 @@ def test_export_exact_over_wide_and_extreme_scales():
         assert (s_1 == want1).all()
         assert (s_2 == np.asarray(p.w2.scales_bits)[ref["w2_group_lo"]:ref["w2_group_hi"]]).all()
         h.close()
+
+
+def test_unordered_variant_host_export_and_checks():
+    """TPQ_UNORDERED: rows stay in checkpoint order, so the exported shard is
+    the checkpoint itself (codes, scales bit-exact through the per-column exponent, zeros); tp > 1
+    and M_max > 16 are rejected."""
+    p = synth.make_problem(256, 1024, 256, 32, 1, seed=12, wide_scales=True)
+    L1, L2 = _olayers(p)
+    h = tpq.TpMlp(p.w1, p.w2, None, None, tp=1, rank=0, variant=tpq.TPQ_UNORDERED, M_max=16, device=-1)
+    q1, s1, z1 = h.export_canonical(1)
+    q2, s2, z2 = h.export_canonical(2)
+    assert (q1 == L1.q).all() and (z1 == L1.z).all() and (s1 == np.asarray(p.w1.scales_bits)).all()
+    assert (q2 == L2.q).all() and (z2 == L2.z).all() and (s2 == np.asarray(p.w2.scales_bits)).all()
+    h.close()
+    with pytest.raises(tpq.TPQError) as e:
+        tpq.TpMlp(p.w1, p.w2, None, None, tp=2, rank=0, variant=tpq.TPQ_UNORDERED, M_max=16, device=-1)
+    assert e.value.code == 1
+    with pytest.raises(tpq.TPQError) as e:
+        tpq.TpMlp(p.w1, p.w2, None, None, tp=1, rank=0, variant=tpq.TPQ_UNORDERED, M_max=17, device=-1)
+    assert e.value.code == 2

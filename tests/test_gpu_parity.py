@@ -424,3 +424,35 @@ def test_full_size_tp_shards(tp, M):
         _assert_close(_np(Y1), Y1r, f"tp={tp} rank {r} Y1_local")
         _assert_close(_np(Y2)[:, cols], Y2r, f"tp={tp} rank {r} Y2_local sampled")
         h.close()
+
+
+@pytest.mark.parametrize("G,M", [(32, 1), (64, 5), (128, 16)])
+def test_unordered_locality_baseline(G, M):
+    """TPQ_UNORDERED (f3, the Fig. 1 formulation): no reordering, per-row group metadata looked up
+    from the table; Y1 (checkpoint column order) and Y2 against the oracle's plain definition with
+    the unordered g_idx (exactly what oracle.dequantize computes)."""
+    p = synth.make_problem(1024, 1408, 640, G, M, seed=31)
+    L1, L2 = _olayers(p)
+    h = tpq.TpMlp(p.w1, p.w2, None, None, variant=tpq.TPQ_UNORDERED, M_max=16)
+    X = _dev(p.X)
+    Y1 = _empty(M, p.N1)
+    h.layer1(X, M, Y1)
+    Y = _empty(M, p.N2)
+    h.forward(X, M, Y)
+    Y1r, Y2r = O.dense_mlp(p.X, O.dequantize(L1), O.dequantize(L2))
+    _assert_close(_np(Y1), Y1r, "Y1 unordered")
+    _assert_close(_np(Y), Y2r, "Y2 unordered")
+    h.close()
+
+
+@pytest.mark.parametrize("M", [1, 16])
+def test_unordered_full_size_llama(M):
+    p = synth.make_named("llama70b", M, seed=0)
+    L1, L2 = _olayers(p)
+    cols = np.sort(np.random.default_rng(3).choice(p.N2, 256, replace=False))
+    h = tpq.TpMlp(p.w1, p.w2, None, None, variant=tpq.TPQ_UNORDERED, M_max=16)
+    Y = _empty(M, p.N2)
+    h.forward(_dev(p.X), M, Y)
+    _, Y2r = O.dense_mlp_columns(p.X, L1, L2, cols2=cols)
+    _assert_close(_np(Y)[:, cols], Y2r, "Y2 unordered, full size")
+    h.close()
