@@ -23,7 +23,7 @@ __all__ = [
     "unpack_qweight", "unpack_qzeros", "fp16_bits_to_f64", "OLayer", "layer_from_checkpoint",
     "dequantize", "metadata_loads", "dense_mlp", "permute_rows", "permute_cols",
     "alg2_naive", "alg3_tp_aware", "shard_maps", "canonical_shard", "check_rows_close",
-    "dense_mlp_columns",
+    "dense_mlp_columns", "silu", "gated_mlp", "alg3_tp_aware_gated", "alg2_naive_gated",
 ]
 
 
@@ -273,6 +273,73 @@ def alg3_tp_aware(X, L1: OLayer, L2: OLayer, tp: int):
         y2_local.append(y1 @ dequantize(W2_local))                             # L2
     Y2 = _all_reduce_sum(y2_local)                                             # L3
     return {"Y2": Y2, "Y1_local": y1_local, "Y2_local": y2_local, "P1": P1, "P2": P2}
+
+
+# ----------------------------------------------------------------------------- gate_proj (f2)
+def silu(x):
+    """SiLU(x) = x * sigmoid(x) = x / (1 + exp(-x)), the gate activation of the Llama MLP (reading
+    c23: PAPER.md:L151 only says the method "can be generalized to the implementation in practice
+    where a gate_proj layer is also present")."""
+    x = np.asarray(x, dtype=np.float64)
+    return x / (1.0 + np.exp(-x))
+
+
+def gated_mlp(X, Wg, Wu, Wd):
+    """Y1 = SiLU(X . Wg) * (X . Wu) (elementwise), Y2 = Y1 . Wd in fp64 (reading c23)."""
+    X = np.asarray(X, dtype=np.float64)
+    Y1 = silu(X @ Wg) * (X @ Wu)
+    return Y1, Y1 @ Wd
+
+
+def alg3_tp_aware_gated(X, Lg: OLayer, Lu: OLayer, Ld: OLayer, tp: int):
+    """Alg. 3 generalized to a gate_proj layer (reading c24): P1g, P1u, P2 from
+    Alg. 1 on each layer's own g_idx; Wg and Wu stored as Wg[P1g, P2] and Wu[P1u, P2] -- the SAME
+    column permutation P2 on both, so their elementwise product lands in Wd[P2]'s row order
+    (an elementwise op commutes with a common column permutation); Wd stored as Wd[P2].
+      L1: Y1_local = SiLU(X[:, P1g] @ Wg_local) * (X[:, P1u] @ Wu_local)
+      L2: Y2_local = Y1_local @ Wd_local
+      L3: Y2_global = AllReduce(Y2_local, op=SUM)"""
+    X = np.asarray(X, dtype=np.float64)
+    N1 = Lg.N
+    _check_tp(N1, tp)
+    n = N1 // tp
+    P1g, _ = alg1_reorder(Lg.g)
+    P1u, _ = alg1_reorder(Lu.g)
+    P2, _ = alg1_reorder(Ld.g)
+    Wga = permute_cols(permute_rows(Lg, P1g), P2)
+    Wua = permute_cols(permute_rows(Lu, P1u), P2)
+    Wdr = permute_rows(Ld, P2)
+    y1_local, y2_local = [], []
+    for r in range(tp):
+        g = X[:, P1g] @ dequantize(_col_block(Wga, r * n, (r + 1) * n))
+        u = X[:, P1u] @ dequantize(_col_block(Wua, r * n, (r + 1) * n))
+        y1 = silu(g) * u                                                       # L1
+        y1_local.append(y1)
+        y2_local.append(y1 @ dequantize(_row_block(Wdr, r * n, (r + 1) * n)))  # L2
+    return {"Y2": _all_reduce_sum(y2_local), "Y1_local": y1_local, "Y2_local": y2_local,
+            "P1g": P1g, "P1u": P1u, "P2": P2}
+
+
+def alg2_naive_gated(X, Lg: OLayer, Lu: OLayer, Ld: OLayer, tp: int):
+    """Alg. 2 with a gate_proj layer: Wg[P1g], Wu[P1u] column blocks (original
+    column order), Y1_local = SiLU(gate) * up, then AllGather, Y1[:, P2], CHUNK, Wd[P2] rows."""
+    X = np.asarray(X, dtype=np.float64)
+    N1 = Lg.N
+    _check_tp(N1, tp)
+    n = N1 // tp
+    P1g, _ = alg1_reorder(Lg.g)
+    P1u, _ = alg1_reorder(Lu.g)
+    P2, _ = alg1_reorder(Ld.g)
+    Wgr, Wur, Wdr = permute_rows(Lg, P1g), permute_rows(Lu, P1u), permute_rows(Ld, P2)
+    y1_local = []
+    for r in range(tp):
+        g = X[:, P1g] @ dequantize(_col_block(Wgr, r * n, (r + 1) * n))
+        u = X[:, P1u] @ dequantize(_col_block(Wur, r * n, (r + 1) * n))
+        y1_local.append(silu(g) * u)                                           # L1
+    y1_perm = np.concatenate(y1_local, axis=1)[:, P2]                         # L2-L3
+    y2_local = [y1_perm[:, r * n:(r + 1) * n] @ dequantize(_row_block(Wdr, r * n, (r + 1) * n))
+                for r in range(tp)]                                            # L4-L5
+    return {"Y2": _all_reduce_sum(y2_local), "Y1_local": y1_local, "Y2_local": y2_local}
 
 
 # ----------------------------------------------------------------------------- shard maps

@@ -429,3 +429,62 @@ def test_canonical_shard_hand_example():
     n0 = O.canonical_shard(L1, L2, 2, 0, "naive")
     assert n0["w1_cols"].tolist() == [0, 1] and n0["w1_q"].tolist() == [[4, 5], [8, 9], [0, 1], [12, 13]]
     assert n0["w2_q"].tolist() == a0["w2_q"].tolist()
+
+
+# ----------------------------------------------------------------------------- gate_proj (f2)
+def test_silu_closed_forms():
+    """SiLU(x) = x sigmoid(x): sigmoid(ln 3) = 3/4 and sigmoid(-ln 3) = 1/4 exactly, SiLU(0) = 0,
+    and SiLU(x) - SiLU(-x) = x (sigmoid(x) + sigmoid(-x) = 1) for any x."""
+    ln3 = math.log(3.0)
+    v = O.silu(np.array([0.0, ln3, -ln3, 2 * ln3]))
+    assert v[0] == 0.0
+    assert abs(v[1] - 0.75 * ln3) < 1e-15 and abs(v[2] + 0.25 * ln3) < 1e-15
+    assert abs(v[3] - 2 * ln3 * 0.9) < 1e-15   # sigmoid(ln 9) = 9/10
+    x = np.linspace(-20, 20, 81)
+    assert np.max(np.abs(O.silu(x) - O.silu(-x) - x)) < 1e-12
+
+
+def _gated_problem(K1, N1, N2, G, M, seed):
+    p = synth.make_problem(K1, N1, N2, G, M, seed=seed)
+    q = synth.make_problem(K1, N1, N2, G, M, seed=seed + 1000)  # an independent up_proj layer
+    return p, p.w1, q.w1, p.w2
+
+
+def _ol(w, K, N):
+    return O.layer_from_checkpoint(w.qweight, w.scales_bits, w.qzeros, w.g_idx, K, N, w.G)
+
+
+def test_gated_bruteforce_tiny():
+    """gated_mlp against a pure-Python triple loop with the SiLU written out (math.exp)."""
+    p, wg, wu, wd = _gated_problem(16, 16, 8, 4, 2, seed=3)
+    Lg, Lu, Ld = _ol(wg, 16, 16), _ol(wu, 16, 16), _ol(wd, 16, 8)
+    Wg, Wu, Wd = O.dequantize(Lg), O.dequantize(Lu), O.dequantize(Ld)
+    X = p.X.astype(np.float64)
+    _, Y2 = O.gated_mlp(X, Wg, Wu, Wd)
+    for m in range(2):
+        y1 = []
+        for j in range(16):
+            g = sum(X[m, k] * Lg.s[Lg.g[k], j] * (Lg.q[k, j] - Lg.z[Lg.g[k], j]) for k in range(16))
+            u = sum(X[m, k] * Lu.s[Lu.g[k], j] * (Lu.q[k, j] - Lu.z[Lu.g[k], j]) for k in range(16))
+            y1.append(g / (1.0 + math.exp(-g)) * u)
+        for c in range(8):
+            y2 = sum(y1[j] * Ld.s[Ld.g[j], c] * (Ld.q[j, c] - Ld.z[Ld.g[j], c]) for j in range(16))
+            assert abs(y2 - Y2[m, c]) <= 1e-12 * max(1.0, abs(y2))
+
+
+@pytest.mark.parametrize("tp", [1, 2, 4])
+def test_gated_tp_variants_equal_dense(tp):
+    """Both gated TP algorithms equal the dense definition (permutations and the AllReduce sum are
+    exact up to fp64 rounding), and each rank's TP-aware Y1_local is the dense Y1 at columns
+    P2[r n:(r+1) n] (the gate/up elementwise product commutes with the common column permutation)."""
+    p, wg, wu, wd = _gated_problem(64, 128, 48, 16, 3, seed=7)
+    Lg, Lu, Ld = _ol(wg, 64, 128), _ol(wu, 64, 128), _ol(wd, 128, 48)
+    Y1d, Y2d = O.gated_mlp(p.X, O.dequantize(Lg), O.dequantize(Lu), O.dequantize(Ld))
+    a = O.alg3_tp_aware_gated(p.X, Lg, Lu, Ld, tp)
+    b = O.alg2_naive_gated(p.X, Lg, Lu, Ld, tp)
+    scale = np.max(np.abs(Y2d))
+    assert np.max(np.abs(a["Y2"] - Y2d)) <= 1e-12 * scale and np.max(np.abs(b["Y2"] - Y2d)) <= 1e-12 * scale
+    n = 128 // tp
+    for r in range(tp):
+        assert np.max(np.abs(a["Y1_local"][r] - Y1d[:, a["P2"][r * n:(r + 1) * n]])) <= 1e-12 * np.max(np.abs(Y1d))
+    assert not np.array_equal(a["P1g"], a["P1u"])  # the two layers carry their own act_order
