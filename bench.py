@@ -337,6 +337,35 @@ def unordered_line(torch, tpq, p, shape, local, dev, stream, kt_ordered, M):
                     "[ng][N] table (64 KB per 128 x 128 block vs the 320 B header of an ordered record)"}
 
 
+def gated_line(torch, tpq, shape, seed, local, dev, stream):
+    """the gate_proj variant Y = (SiLU(X.Wg) * (X.Wu)).Wd at TP = 1 (the real
+    Llama MLP: up layer drawn from the next seed's layer-1 recipe), graph-timed like the main line."""
+    K1, N1, N2, G = synth.SHAPES[shape]
+    p = synth.make_named(shape, 16, seed)
+    q = synth.make_named(shape, 16, seed + 1000)
+    ws = (p.w1, q.w1, p.w2)
+    Ps = [tpq.gptq_reorder(w.g_idx, G)[0] for w in ws]
+    l1, l2, _ = algorithmic_bytes(K1, N1, N2, G, 16, 1)
+    step_b = 2 * l1 + l2
+    l2_cache = torch.cuda.get_device_properties(dev).L2_cache_size
+    R = max(1, -(-3 * l2_cache // int(step_b)))
+    hs = [tpq.TpMlp.gated(*ws, *Ps, M_max=16, device=local) for _ in range(R)]
+    X = torch.from_numpy(p.X.copy()).to(dev)
+    Y = torch.empty(16, N2, dtype=torch.float16, device=dev)
+    peak, _ = peaks()
+    out = {}
+    for M in (1, 16):
+        us = step_latency(torch, tpq, hs, R, stream, M, 0, X, Y)
+        l1m, l2m, _ = algorithmic_bytes(K1, N1, N2, G, M, 1)
+        b = 2 * l1m + l2m
+        out[str(M)] = {"us": us, "hbm_frac": b / (us * 1e-6) / 1e9 / peak, "bytes": b}
+    kt = kernel_times(torch, tpq, hs, R, stream, 16, 1)
+    for h in hs:
+        h.close()
+    out["kernel_us_M16"] = kt
+    return out
+
+
 def main():
     a = parse()
     if a.impl == "reference":
@@ -533,6 +562,7 @@ def main():
         line["llama70b_tp8_shard"] = extra_workload(torch, tpq, "llama70b", (1, 16), 8, a.seed, local, dev, stream)
     if world == 1 and not a.quick and not sim_tp and a.variant == "tp_aware":
         line["unordered_tp1"] = unordered_line(torch, tpq, p, a.shape, local, dev, stream, kt, M)
+        line["gated_tp1"] = gated_line(torch, tpq, a.shape, a.seed, local, dev, stream)
     line["clocks_extra_lines"] = clocks_x.stop()
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         pc = synth.make_named(a.shape, M, a.seed)

@@ -112,6 +112,24 @@ typedef struct tpq_mlp tpq_mlp; /* opaque: one rank's shard of the two-layer MLP
 int tp_shard_mlp(const gptq_layer* w1, const gptq_layer* w2, const int32_t* P1,
                  const int32_t* P2, int tp, int rank, int variant, int64_t M_max, int device,
                  tpq_mlp** out);
+
+/* tp_shard_gated_mlp -- the gate_proj variant ("can be
+ * generalized to the implementation in practice where a gate_proj layer is also present"):
+ * Y = (SiLU(X.Wg) * (X.Wu)).Wd, the Llama MLP (readings c23-c25).
+ *   wg, wu    gate and up layers, K1 x N1 each with their own act_order g_idx and equal G;
+ *   wd        down layer, N1 x N2;  P1g, P1u, P2 = Alg. 1 permutations of wg, wu, wd g_idx.
+ * TPQ_TP_AWARE: the rank keeps Wg[P1g, P2] and Wu[P1u, P2] columns [r n, (r+1) n) -- the SAME
+ * column permutation P2 on both, so SiLU(gate) * up lands in Wd[P2]'s row order with no exchange
+ * (the elementwise product commutes with a common column permutation) -- and Wd[P2] rows
+ * [r n, (r+1) n); TPQ_NAIVE: Wg[P1g], Wu[P1u] column blocks, AllGather + P2 gather before Wd.
+ * The forward entry points are those of tp_shard_mlp; layer 1 is one GEMV over interleaved gate/up
+ * records whose epilogue writes fp16(SiLU(gate) * up) from fp32 accumulators.  Same requirements
+ * and errors as tp_shard_mlp, plus: wu matching wg in K, N and G (TPQ_EINVAL); M_max <= 16
+ * (TPQ_EUNSUPPORTED: no tensor-core A7 path for the gated layer); TPQ_UNORDERED is rejected.
+ * tpq_mlp_export_canonical: layer 1 = gate, 3 = up, 2 = down. */
+int tp_shard_gated_mlp(const gptq_layer* wg, const gptq_layer* wu, const gptq_layer* wd, const int32_t* P1g,
+                       const int32_t* P1u, const int32_t* P2, int tp, int rank, int variant, int64_t M_max,
+                       int device, tpq_mlp** out);
 int tpq_mlp_destroy(tpq_mlp* h); /* NULL is a no-op; frees device memory and the NCCL comm */
 
 /* ---------------------------------------------------------------------------------------

@@ -22,7 +22,7 @@ _CODES = {1: "EINVAL", 2: "EUNSUPPORTED", 3: "ECUDA", 4: "ENCCL", 5: "ENOMEM", 6
 
 # Every symbol include/tpq.h declares (tests check the .so exports all of them).
 EXPORTS = [
-    "tpq_last_error", "tpq_version", "gptq_reorder", "tp_shard_mlp", "tpq_mlp_destroy",
+    "tpq_last_error", "tpq_version", "gptq_reorder", "tp_shard_mlp", "tp_shard_gated_mlp", "tpq_mlp_destroy",
     "tpq_comm_unique_id", "tpq_comm_create", "tpq_comm_destroy", "tpq_mlp_set_comm",
     "tp_mlp_forward", "tp_mlp_forward_host",
     "tp_mlp_forward_local", "tpq_layer1", "tpq_naive_gather", "tpq_layer2", "tpq_sum_partials",
@@ -68,6 +68,8 @@ def lib() -> C.CDLL:
             "gptq_reorder": [vp, i64, i32, vp, vp],
             "tp_shard_mlp": [C.POINTER(GptqLayer), C.POINTER(GptqLayer), vp, vp, C.c_int, C.c_int,
                              C.c_int, i64, C.c_int, C.POINTER(vp)],
+            "tp_shard_gated_mlp": [C.POINTER(GptqLayer), C.POINTER(GptqLayer), C.POINTER(GptqLayer), vp, vp, vp,
+                                   C.c_int, C.c_int, C.c_int, C.c_int64, C.c_int, C.POINTER(vp)],
             "tpq_mlp_destroy": [vp],
             "tpq_comm_unique_id": [vp],
             "tpq_comm_create": [vp, C.c_int, C.c_int, C.c_int, C.POINTER(vp)],
@@ -192,6 +194,23 @@ class TpMlp:
         self.info = MlpInfo()
         _check(lib().tpq_mlp_info(self._h, C.byref(self.info)))
 
+    @classmethod
+    def gated(cls, wg, wu, wd, P1g, P1u, P2, tp: int = 1, rank: int = 0, variant: int = TPQ_TP_AWARE,
+              M_max: int = 16, device: int = 0) -> "TpMlp":
+        """gate_proj variant (tp_shard_gated_mlp): Y = (SiLU(X.Wg) * (X.Wu)).Wd."""
+        self = cls.__new__(cls)
+        sg, kg = _layer_struct(wg)
+        su, ku = _layer_struct(wu)
+        sd, kd = _layer_struct(wd)
+        Ps = [np.ascontiguousarray(P, dtype=np.int32) for P in (P1g, P1u, P2)]
+        h = C.c_void_p()
+        _check(lib().tp_shard_gated_mlp(C.byref(sg), C.byref(su), C.byref(sd), *[_ptr(P) for P in Ps], tp, rank,
+                                        variant, M_max, device, C.byref(h)))
+        self._h = h
+        self.info = MlpInfo()
+        _check(lib().tpq_mlp_info(self._h, C.byref(self.info)))
+        return self
+
     def close(self):
         if getattr(self, "_h", None):
             lib().tpq_mlp_destroy(self._h)
@@ -245,7 +264,7 @@ class TpMlp:
 
     def export_canonical(self, layer: int):
         i = self.info
-        K, N, G = (i.K1, i.n, i.G1) if layer == 1 else (i.n, i.N2, i.G2)
+        K, N, G = (i.K1, i.n, i.G1) if layer in (1, 3) else (i.n, i.N2, i.G2)  # 3: up layer of a gated shard
         q = np.empty((K, N), np.uint8)
         s = np.empty((K // G, N), np.uint16)
         z = np.empty((K // G, N), np.uint8)

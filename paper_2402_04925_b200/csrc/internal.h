@@ -55,6 +55,7 @@ struct LayerDev {
   const float* colf = nullptr;  // [N] 2^(24 - E_n): records hold s' = s 2^E_n (tpq_host.cpp column_exponents)
   const uint32_t* meta = nullptr;  // unordered layer (TPQ_UNORDERED): [ng][N] {fp16 s', fp16 -z s' 2^-24}
   int unord = 0;                   // 1: records in checkpoint row order with per-row group ids (k_dqgemv<0>)
+  int gated = 0;                   // 1: gate_proj layer 1: gate(t, kb), up(t, kb) record pairs; U counts the pairs
 };
 
 enum GatherMode { GATHER_COLS = 0, GATHER_ALLGATHER = 1 };
@@ -65,7 +66,10 @@ bool gemv_prepare(int G);
 // out[m][n] = sum_k x[m][k] deq(W)[k][n] for M <= 16 rows (k_dqgemv + its split-tile fix-up); x is
 // a [16][K] fp16 row-major buffer described by `xmap` (make_xmap, 16-row boxes), out is [M][out_ld]
 // fp16 row-major.
-cudaError_t launch_gemv(const LayerDev& L, const CUtensorMap& xmap, int M, void* out, int64_t out_ld, cudaStream_t st);
+// Gated layer (L.gated): xmap = X[:, P1g] (gate records), xmapu = X[:, P1u] (up records), out =
+// fp16(SiLU(gate) * up); otherwise xmapu may be NULL.
+cudaError_t launch_gemv(const LayerDev& L, const CUtensorMap& xmap, const CUtensorMap* xmapu, int M, void* out,
+                        int64_t out_ld, cudaStream_t st);
 
 // A7 (M > 16): out[m][n] = sum_k x[m][k] deq(W)[k][n] for M <= nb rows (nb in {64, 128, 256}), x a
 // [nb][K] fp16 row-major buffer described by xmap (make_xmap with rows = nb), out [M][out_ld].

@@ -269,6 +269,12 @@ struct tpq_mlp {
   float* d_ws = nullptr;
   float* d_colf = nullptr;     // per-column 2^(24 - E) of layer 1 [n] then layer 2 [N2]
   CUtensorMap xmap1 = {}, xmap2 = {};  // TMA views of d_x1 / d_y1 (GEMV activation operand, 16 rows)
+  // gate_proj variant (f2): layer 1 = gate + up; the up layer's own P1u and gathered X[:, P1u]
+  bool gated = false;
+  std::vector<int32_t> P1u;
+  int32_t* d_P1u = nullptr;
+  void* d_x1u = nullptr;
+  CUtensorMap xmap1u = {};
   CUtensorMap mm1[3] = {}, mm2[3] = {};  // A7 views of d_x1 / d_y1 with 64 / 128 / 256 rows
   CUtensorMap ss1 = {}, ss2 = {};        // A7 SS views: 256-row buffers, 128-row boxes
   int sms = 148;
@@ -308,7 +314,7 @@ int validate_perm(const int32_t* P, const gptq_layer* w, const char* name) {
 void free_dev(tpq_mlp* h) {
   if (h->device < 0) return;
   cudaSetDevice(h->device);
-  void* ptrs[] = {h->d_w1, h->d_w2, h->d_P1, h->d_gcols, h->d_x1, h->d_y1, h->d_buf, h->d_xin, h->d_yout, h->d_ws, h->d_colf, h->d_tab};
+  void* ptrs[] = {h->d_w1, h->d_w2, h->d_P1, h->d_gcols, h->d_x1, h->d_y1, h->d_buf, h->d_xin, h->d_yout, h->d_ws, h->d_colf, h->d_tab, h->d_P1u, h->d_x1u};
   for (void* p : ptrs)
     if (p) cudaFree(p);
 }
@@ -388,13 +394,27 @@ int gptq_reorder(const int32_t* g_idx, int64_t K, int32_t G, int32_t* perm_out, 
   }
 }
 
-int tp_shard_mlp(const gptq_layer* w1, const gptq_layer* w2, const int32_t* P1, const int32_t* P2, int tp, int rank,
-                 int variant, int64_t M_max, int device, tpq_mlp** out) {
+}  // extern "C"
+
+namespace {
+
+// Shared body of tp_shard_mlp and tp_shard_gated_mlp (wu, P1u non-NULL: gate_proj variant, w1 = gate).
+int shard_impl(const gptq_layer* w1, const gptq_layer* wu, const gptq_layer* w2, const int32_t* P1, const int32_t* P1u,
+               const int32_t* P2, int tp, int rank, int variant, int64_t M_max, int device, tpq_mlp** out) {
   if (!out) return fail(TPQ_EINVAL, "tp_shard_mlp: out is NULL");
   *out = nullptr;
   int rc;
-  if ((rc = validate_layer(w1, "w1"))) return rc;
-  if ((rc = validate_layer(w2, "w2"))) return rc;
+  const bool gated = wu != nullptr;
+  if ((rc = validate_layer(w1, gated ? "wg" : "w1"))) return rc;
+  if ((rc = validate_layer(w2, gated ? "wd" : "w2"))) return rc;
+  if (gated) {
+    if ((rc = validate_layer(wu, "wu"))) return rc;
+    if (wu->K != w1->K || wu->N != w1->N || wu->G != w1->G)
+      return fail(TPQ_EINVAL, "wu (K=%lld N=%lld G=%d) must match wg (K=%lld N=%lld G=%d)", (long long)wu->K,
+                  (long long)wu->N, wu->G, (long long)w1->K, (long long)w1->N, w1->G);
+    if (variant == TPQ_UNORDERED) return fail(TPQ_EINVAL, "the gate_proj variant has no TPQ_UNORDERED baseline");
+    if (M_max > 16) return fail(TPQ_EUNSUPPORTED, "the gate_proj variant runs the M <= 16 GEMV only (M_max=%lld)", (long long)M_max);
+  }
   if (w1->N != w2->K)
     return fail(TPQ_EINVAL, "w1->N=%lld != w2->K=%lld", (long long)w1->N, (long long)w2->K);
   if (tp != 1 && tp != 2 && tp != 4 && tp != 8) return fail(TPQ_EINVAL, "tp=%d not in {1,2,4,8}", tp);
@@ -425,8 +445,9 @@ int tp_shard_mlp(const gptq_layer* w1, const gptq_layer* w2, const int32_t* P1, 
         if (w->g_idx[k] < 0 || w->g_idx[k] >= w->K / w->G) return fail(TPQ_EINVAL, "g_idx[%lld]=%d out of range", (long long)k, w->g_idx[k]);
     }
   } else {
-    if ((rc = validate_perm(P1, w1, "P1"))) return rc;
+    if ((rc = validate_perm(P1, w1, gated ? "P1g" : "P1"))) return rc;
     if ((rc = validate_perm(P2, w2, "P2"))) return rc;
+    if (gated && (rc = validate_perm(P1u, wu, "P1u"))) return rc;
   }
 
   tpq_mlp* h = nullptr;
@@ -456,23 +477,32 @@ int tp_shard_mlp(const gptq_layer* w1, const gptq_layer* w2, const int32_t* P1, 
     h->w2_group_hi = (int32_t)((rank + 1) * n / w2->G);
 
     // ---- canonical shards ----
-    Canon c1, c2;
-    c1.K = K1; c1.N = n; c1.G = w1->G;
-    c1.q.resize((size_t)(K1 * n));
-    parallel_for(K1, [&](int64_t k) {  // row k of W1[P1] = original row P1[k]
-      const int32_t src = P1[k];
-      const uint32_t* row = w1->qweight + (size_t)(src / 8) * N1;
-      for (int64_t j = 0; j < n; ++j) c1.q[(size_t)(k * n + j)] = (uint8_t)nib(row[h->w1_cols[j]], src % 8);
-    });
-    const int64_t ng1 = K1 / w1->G;
-    c1.s.resize((size_t)(ng1 * n));
-    c1.z.resize((size_t)(ng1 * n));
-    for (int64_t g = 0; g < ng1; ++g)
-      for (int64_t j = 0; j < n; ++j) {
-        const int32_t col = h->w1_cols[j];
-        c1.s[(size_t)(g * n + j)] = w1->scales[(size_t)(g * N1 + col)];
-        c1.z[(size_t)(g * n + j)] = (uint8_t)nib(w1->qzeros[(size_t)(g * (N1 / 8) + col / 8)], col % 8);
-      }
+    auto build_c1 = [&](const gptq_layer* w, const int32_t* P) {  // W[P][:, w1_cols] (rows by P, cols by P2 or identity)
+      Canon c;
+      c.K = K1; c.N = n; c.G = w->G;
+      c.q.resize((size_t)(K1 * n));
+      parallel_for(K1, [&](int64_t k) {  // row k of W[P] = original row P[k]
+        const int32_t src = P[k];
+        const uint32_t* row = w->qweight + (size_t)(src / 8) * N1;
+        for (int64_t j = 0; j < n; ++j) c.q[(size_t)(k * n + j)] = (uint8_t)nib(row[h->w1_cols[j]], src % 8);
+      });
+      const int64_t ng1 = K1 / w->G;
+      c.s.resize((size_t)(ng1 * n));
+      c.z.resize((size_t)(ng1 * n));
+      for (int64_t g = 0; g < ng1; ++g)
+        for (int64_t j = 0; j < n; ++j) {
+          const int32_t col = h->w1_cols[j];
+          c.s[(size_t)(g * n + j)] = w->scales[(size_t)(g * N1 + col)];
+          c.z[(size_t)(g * n + j)] = (uint8_t)nib(w->qzeros[(size_t)(g * (N1 / 8) + col / 8)], col % 8);
+        }
+      return c;
+    };
+    Canon c1 = build_c1(w1, P1), c2, c1u;
+    if (gated) {
+      h->gated = true;
+      h->P1u.assign(P1u, P1u + K1);
+      c1u = build_c1(wu, P1u);  // Wu[P1u, P2]: the SAME column permutation as Wg (reading c24)
+    }
     c2.K = n; c2.N = N2; c2.G = w2->G;
     c2.q.resize((size_t)(n * N2));
     parallel_for(n, [&](int64_t i) {  // local row i of W2[P2] block r = original row P2[r n + i]
@@ -492,6 +522,10 @@ int tp_shard_mlp(const gptq_layer* w1, const gptq_layer* w2, const int32_t* P1, 
     }
     h->E1 = column_exponents(c1);
     h->E2 = column_exponents(c2);
+    if (gated) {  // one exponent per column for gate and up: the smaller one keeps both exact
+      const std::vector<int> Eu = column_exponents(c1u);
+      for (size_t j = 0; j < h->E1.size(); ++j) h->E1[j] = std::min(h->E1[j], Eu[j]);
+    }
     if (unord) {
       h->g1u.assign(w1->g_idx, w1->g_idx + K1);
       h->g2u.assign(w2->g_idx, w2->g_idx + N1);
@@ -503,11 +537,22 @@ int tp_shard_mlp(const gptq_layer* w1, const gptq_layer* w2, const int32_t* P1, 
       h->z1u = c1.z;
       h->z2u = c2.z;
       h->L1.unord = h->L2.unord = 1;
+    } else if (gated) {
+      // records of (tile, k-block) u as the pair gate(u), up(u) (k_dqgemv<G, true>)
+      const std::vector<uint8_t> pg = pack_layer(c1, h->E1), pu = pack_layer(c1u, h->E1);
+      const size_t UB = (size_t)tpq::unit_bytes(w1->G), nun = pg.size() / UB;
+      h->pk1.resize(2 * pg.size());
+      for (size_t u = 0; u < nun; ++u) {
+        memcpy(h->pk1.data() + (2 * u) * UB, pg.data() + u * UB, UB);
+        memcpy(h->pk1.data() + (2 * u + 1) * UB, pu.data() + u * UB, UB);
+      }
+      h->pk2 = pack_layer(c2, h->E2);
     } else {
       h->pk1 = pack_layer(c1, h->E1);
       h->pk2 = pack_layer(c2, h->E2);
     }
     plan_layer(h->L1, K1, n, w1->G, device);
+    h->L1.gated = gated ? 1 : 0;
     plan_layer(h->L2, n, N2, w2->G, device);
 
     if (device >= 0) {
@@ -521,7 +566,7 @@ int tp_shard_mlp(const gptq_layer* w1, const gptq_layer* w2, const int32_t* P1, 
           }
         int r;
         auto A = [&](void** p, size_t b) { return dev_alloc(p, b); };
-        const size_t ws1 = (size_t)h->L1.grid * 2 * tpq::kNPad * tpq::kTileCols;  // [grid][2 slots][16][128]
+        const size_t ws1 = (size_t)h->L1.grid * 2 * tpq::kNPad * tpq::kTileCols * (gated ? 2 : 1);  // [grid][2 slots][gate, up][16][128]
         const size_t ws2 = (size_t)h->L2.grid * 2 * tpq::kNPad * tpq::kTileCols;
         h->rows = M_max > tpq::kMaxM ? kGemmRows : tpq::kMaxM;
         const size_t wm1 = M_max > tpq::kMaxM ? (size_t)h->L1.grid_mm * 2 * kGemmRows * tpq::kTileCols : 0;
@@ -544,8 +589,14 @@ int tp_shard_mlp(const gptq_layer* w1, const gptq_layer* w2, const int32_t* P1, 
             (r = A(&h->d_xin, (size_t)M_max * K1 * 2)) || (r = A(&h->d_yout, (size_t)M_max * N2 * 2)) ||
             (r = A((void**)&h->d_ws, (ws1 + ws2 + wm1 + wm2 + ws1s + ws2s) * 4)) ||
             (r = A((void**)&h->d_colf, (size_t)(n + N2) * 4)) ||
-            (r = A(&h->d_tab, (h->tab1.size() + h->tab2.size()) * 4)))
+            (r = A(&h->d_tab, (h->tab1.size() + h->tab2.size()) * 4)) ||
+            (gated && (r = A((void**)&h->d_P1u, K1 * 4))) || (gated && (r = A(&h->d_x1u, (size_t)h->rows * K1 * 2))))
           return r;
+        if (gated) {
+          TPQ_CUDA(cudaMemcpy(h->d_P1u, P1u, K1 * 4, cudaMemcpyHostToDevice));
+          if (!tpq::make_xmap(&h->xmap1u, h->d_x1u, K1, tpq::kNPad))
+            return fail(TPQ_ECUDA, "cuTensorMapEncodeTiled failed for the up_proj activation buffer");
+        }
         TPQ_CUDA(cudaMemcpy(h->d_w1, h->pk1.data(), h->pk1.size(), cudaMemcpyHostToDevice));
         TPQ_CUDA(cudaMemcpy(h->d_w2, h->pk2.data(), h->pk2.size(), cudaMemcpyHostToDevice));
         TPQ_CUDA(cudaMemcpy(h->d_P1, P1, K1 * 4, cudaMemcpyHostToDevice));
@@ -599,6 +650,22 @@ int tp_shard_mlp(const gptq_layer* w1, const gptq_layer* w2, const int32_t* P1, 
     if (h) { free_dev(h); delete h; }
     return fail(TPQ_EINVAL, "tp_shard_mlp: unexpected exception");
   }
+}
+
+}  // namespace
+
+extern "C" {
+
+int tp_shard_mlp(const gptq_layer* w1, const gptq_layer* w2, const int32_t* P1, const int32_t* P2, int tp, int rank,
+                 int variant, int64_t M_max, int device, tpq_mlp** out) {
+  return shard_impl(w1, nullptr, w2, P1, nullptr, P2, tp, rank, variant, M_max, device, out);
+}
+
+int tp_shard_gated_mlp(const gptq_layer* wg, const gptq_layer* wu, const gptq_layer* wd, const int32_t* P1g,
+                       const int32_t* P1u, const int32_t* P2, int tp, int rank, int variant, int64_t M_max, int device,
+                       tpq_mlp** out) {
+  if (!wu) return fail(TPQ_EINVAL, "tp_shard_gated_mlp: wu is NULL");
+  return shard_impl(wg, wu, wd, P1g, P1u, P2, tp, rank, variant, M_max, device, out);
 }
 
 int tpq_mlp_destroy(tpq_mlp* h) {
@@ -678,7 +745,8 @@ int check_fwd(tpq_mlp* h, const void* X, int64_t M, const void* Y) {
 cudaError_t run_layer(tpq_mlp* h, int layer, int mc, void* out, int64_t out_ld, cudaStream_t st) {
   const tpq::LayerDev& L = layer == 1 ? h->L1 : h->L2;
   if (mc <= tpq::kMaxM)
-    return tpq::launch_gemv(L, layer == 1 ? h->xmap1 : h->xmap2, mc, out, out_ld, st);
+    return tpq::launch_gemv(L, layer == 1 ? h->xmap1 : h->xmap2, layer == 1 && L.gated ? &h->xmap1u : nullptr, mc, out,
+                            out_ld, st);
   if (mc >= 128 && !getenv("TPQ_NO_SS"))  // compute-bound: activations as the reused A operand
     return tpq::launch_gemm_ss(L, layer == 1 ? h->ss1 : h->ss2, mc, h->sms, out, out_ld, st);
   const int v = mc <= 64 ? 0 : mc <= 128 ? 1 : 2;
@@ -690,6 +758,8 @@ int64_t pass_rows(const tpq_mlp* h, int64_t M) { return M <= tpq::kMaxM ? tpq::k
 
 int chunk_forward(tpq_mlp* h, const uint16_t* X, int mc, void* Y, cudaStream_t st, bool collective) {
   TPQ_CUDA(tpq::launch_gather_rowmajor(X, h->K1, h->d_P1, tpq::GATHER_COLS, 0, mc, h->K1, h->d_x1, st));  // X[:,P1]
+  if (h->gated)  // gate_proj variant: the up layer's own act_order, X[:, P1u]
+    TPQ_CUDA(tpq::launch_gather_rowmajor(X, h->K1, h->d_P1u, tpq::GATHER_COLS, 0, mc, h->K1, h->d_x1u, st));
   if (h->variant != TPQ_NAIVE) {
     // Alg. 3 L1 (TPQ_UNORDERED: P1 = identity, checkpoint order): Y1_local is already in the row order of this rank's W2[P2] block (no exchange)
     TPQ_CUDA(run_layer(h, 1, mc, h->d_y1, h->n, st));
@@ -761,6 +831,9 @@ int tpq_layer1(tpq_mlp* h, const void* X, int64_t M, void* Y1_local, void* strea
     const int mc = (int)std::min<int64_t>(R, M - m0);
     TPQ_CUDA(tpq::launch_gather_rowmajor((const uint16_t*)X + m0 * h->K1, h->K1, h->d_P1, tpq::GATHER_COLS, 0, mc,
                                          h->K1, h->d_x1, st));
+    if (h->gated)
+      TPQ_CUDA(tpq::launch_gather_rowmajor((const uint16_t*)X + m0 * h->K1, h->K1, h->d_P1u, tpq::GATHER_COLS, 0, mc,
+                                           h->K1, h->d_x1u, st));
     TPQ_CUDA(run_layer(h, 1, mc, (uint8_t*)Y1_local + (size_t)m0 * h->n * 2, h->n, st));
   }
   return TPQ_OK;
@@ -817,6 +890,8 @@ int tpq_mlp_run_step(tpq_mlp* h, int step, int64_t M, void* stream) {
   switch (step) {
     case TPQ_STEP_GATHER:
       TPQ_CUDA(tpq::launch_gather_rowmajor(h->d_xin, h->K1, h->d_P1, tpq::GATHER_COLS, 0, mc, h->K1, h->d_x1, st));
+      if (h->gated)
+        TPQ_CUDA(tpq::launch_gather_rowmajor(h->d_xin, h->K1, h->d_P1u, tpq::GATHER_COLS, 0, mc, h->K1, h->d_x1u, st));
       return TPQ_OK;
     case TPQ_STEP_LAYER1:
       TPQ_CUDA(run_layer(h, 1, mc, h->d_y1, h->n, st));
@@ -883,6 +958,13 @@ int tpq_mlp_export_canonical(const tpq_mlp* h, int layer, uint8_t* q, uint16_t* 
         s[g * N + c] = half_scale_down((uint16_t)(tab[(size_t)(g * N + c)] & 0xFFFF), E[(size_t)c]);
         z[g * N + c] = (layer == 1 ? h->z1u : h->z2u)[(size_t)(g * N + c)];
       }
+    return TPQ_OK;
+  }
+  if (h->gated && (layer == 1 || layer == 3)) {  // gate (1) / up (3) records of the interleaved layer 1
+    const size_t UB = (size_t)tpq::unit_bytes(h->G1), nun = h->pk1.size() / (2 * UB);
+    std::vector<uint8_t> part(nun * UB);
+    for (size_t u = 0; u < nun; ++u) memcpy(part.data() + u * UB, h->pk1.data() + (2 * u + (layer == 3)) * UB, UB);
+    unpack_layer(part, h->E1, h->K1, h->n, h->G1, q, s, z);
     return TPQ_OK;
   }
   if (layer == 1) unpack_layer(h->pk1, h->E1, h->K1, h->n, h->G1, q, s, z);

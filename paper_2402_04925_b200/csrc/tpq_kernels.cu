@@ -245,6 +245,8 @@ __device__ __forceinline__ int cta_of_unit(int64_t u, int64_t U, int grid) {
 }
 
 __device__ __forceinline__ uint32_t h2u(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
+// SiLU(x) = x / (1 + exp(-x)) in fp32 (the gate activation of the gate_proj variant, reading c23)
+__device__ __forceinline__ float silu_f(float x) { return x / (1.f + expf(-x)); }
 __device__ __forceinline__ __half2 u2h(uint32_t u) { return *reinterpret_cast<__half2*>(&u); }
 
 
@@ -279,9 +281,13 @@ constexpr int kGemvThreads = 20 * 32;
 // G = 0: the unordered-g_idx layer (TPQ_UNORDERED, the Fig. 1 formulation): a record
 // holds the 128 rows' codes in checkpoint order plus their group ids (uint8), and the dequant warps
 // look each row's {s', C} up in an L2-resident [ng][N] table instead of a per-block record header.
-template <int G>
+// GT: the gated layer 1 of the gate_proj variant (f2, readings c23-c25): records stream as gate(t, kb),
+// up(t, kb) pairs, so a dequant pair IS one (tile, k-block) of both layers; gate and up accumulate in
+// separate TMEM accumulators and the epilogue writes fp16(SiLU(gate) * up).
+template <int G, bool GT = false>
 struct TC {
   static constexpr bool UN = G == 0;
+  static_assert(!(UN && GT), "the unordered baseline has no gated variant");
   static constexpr int KG = UN ? 1 : kUnitK / G;
   static constexpr int UB = UN ? kUnitK * kTileCols / 2 + kUnitK : (int)unit_bytes_c(G == 0 ? 128 : G);
   static constexpr int STAGE = (UB + 127) / 128 * 128;
@@ -299,7 +305,7 @@ struct TC {
   // done(p - NX) before reusing slot p % NX: the next one, p - NX + RD >= p, needs its own later load.
   static_assert(RD % kSets == 0 && RD >= NX, "done ring aliasing");
   static constexpr int TCOLS = 512;
-  static constexpr int DC = 4 * kNPad;            // [2 segment buffers][2 issuers] x 16 columns
+  static constexpr int DC = (GT ? 8 : 4) * kNPad;  // [2 segment buffers][2 issuers][gate, up if GT] x 16 columns
   static_assert(DC + kSets * 2 * AU <= TCOLS, "TMEM budget");
   static constexpr int XRING = 0;
   static constexpr int WRING = NX * 2 * XU;
@@ -307,9 +313,10 @@ struct TC {
   static constexpr int SMEM = BARS + 8 * (2 * NS + NX + NAF + RD + 4);
 };
 
-template <int G>
-__global__ void __launch_bounds__(kGemvThreads, 1) k_dqgemv(const GemvArgs a, const __grid_constant__ CUtensorMap xmap) {
-  using C = TC<G>;
+template <int G, bool GT>
+__global__ void __launch_bounds__(kGemvThreads, 1)
+    k_dqgemv(const GemvArgs a, const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap xmapu) {
+  using C = TC<G, GT>;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BARS);
   uint64_t* full = bars;                // [NS] weight record landed
@@ -321,8 +328,11 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_dqgemv(const GemvArgs a, co
   uint64_t* d_empty = d_full + 2;       // [2] epilogue read them (4 warps)
   __shared__ uint32_t s_tmem;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t u0 = cta_start(blockIdx.x, a.U, a.grid);
-  const int nu = (int)(cta_start(blockIdx.x + 1, a.U, a.grid) - u0);
+  // stream-K over a.U units; gated (GT): over a.U (tile, k-block) pairs of gate + up records
+  const int64_t v0 = cta_start(blockIdx.x, a.U, a.grid);
+  const int nv = (int)(cta_start(blockIdx.x + 1, a.U, a.grid) - v0);
+  const int64_t u0 = GT ? 2 * v0 : v0;  // first record of the CTA
+  const int nu = GT ? 2 * nv : nv;      // records of the CTA
   const int np = (nu + 1) / 2;
 
   if (threadIdx.x == 0) {
@@ -485,45 +495,93 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_dqgemv(const GemvArgs a, co
     const int qw = warp, col = qw * 32 + lane;
     const uint32_t lane_base = (uint32_t)(qw * 32) << 16;
     pdl_wait();
-    int tile = (int)(u0 / a.NKB);
-    int64_t seg_start = u0;
-    const int64_t uend = u0 + nu;
-    for (int seg = 0; seg_start < uend; ++seg, ++tile) {
-      const int64_t tile_end = (int64_t)(tile + 1) * a.NKB;
-      const int64_t seg_end = tile_end < uend ? tile_end : uend;  // exclusive
-      const int lo = (int)(seg_start - u0), hi = (int)(seg_end - 1 - u0);
-      const int d = seg & 1;
-      const float up = __ldg(a.colf + (int64_t)tile * kTileCols + col);  // 2^(24 - E) of this column
-      mbar_wait_backoff(d_full + d, (uint32_t)((seg >> 1) & 1), 256);
-      tc_fence_after();
-      const bool w0 = hi - lo >= 3 || ((lo >> 1) & 1) == 0 || ((hi >> 1) & 1) == 0;
-      const bool w1 = hi - lo >= 3 || ((lo >> 1) & 1) == 1 || ((hi >> 1) & 1) == 1;
-      uint32_t v[kNPad], v1[kNPad];
-      const uint32_t dcol = tmem + lane_base + 2 * d * kNPad;
-      if (w0) tmem_ld16(dcol, v);
-      if (w1) tmem_ld16(dcol + kNPad, v1);
-      tmem_wait_ld();
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(d_empty + d);
+    if constexpr (GT) {
+      // segments over (tile, k-block) pairs; issuer w owns the pairs p % 2 == w of a segment
+      int tile = (int)(v0 / a.NKB);
+      int64_t seg_start = v0;
+      const int64_t vend = v0 + nv;
+      for (int seg = 0; seg_start < vend; ++seg, ++tile) {
+        const int64_t tile_end = (int64_t)(tile + 1) * a.NKB;
+        const int64_t seg_end = tile_end < vend ? tile_end : vend;
+        const int lo = (int)(seg_start - v0), hi = (int)(seg_end - 1 - v0);
+        const int d = seg & 1;
+        const float up = __ldg(a.colf + (int64_t)tile * kTileCols + col);
+        mbar_wait_backoff(d_full + d, (uint32_t)((seg >> 1) & 1), 256);
+        tc_fence_after();
+        const bool w0 = hi > lo || (lo & 1) == 0, w1 = hi > lo || (lo & 1) == 1;
+        float gu[2][kNPad];
 #pragma unroll
-      for (int m = 0; m < kNPad; ++m)
-        v[m] = __float_as_uint(up * (w0 ? (w1 ? __uint_as_float(v[m]) + __uint_as_float(v1[m]) : __uint_as_float(v[m]))
-                                        : __uint_as_float(v1[m])));
-      const int64_t n = (int64_t)tile * kTileCols + col;
-      if (seg_start == (int64_t)tile * a.NKB && seg_end == tile_end) {
+        for (int kind = 0; kind < 2; ++kind) {  // 0 gate, 1 up: accumulator ((2 d + w) 2 + kind) x 16
+          uint32_t v[kNPad], v1[kNPad];
+          const uint32_t base = tmem + lane_base + (4 * d + kind) * kNPad;
+          if (w0) tmem_ld16(base, v);
+          if (w1) tmem_ld16(base + 2 * kNPad, v1);
+          tmem_wait_ld();
 #pragma unroll
-        for (int m = 0; m < kNPad; ++m)
-          if (m < a.M) a.out[m * a.out_ld + n] = __float2half_rn(__uint_as_float(v[m]));
-      } else {
-        // split tile: partial into this CTA's slot (0 = its first segment, 1 = its last), summed by
-        // the fix-up kernel in CTA order after this kernel
-        float* mine = a.ws + ((size_t)blockIdx.x * 2 + (seg_start == u0 ? 0 : 1)) * (kNPad * kTileCols);
+          for (int m = 0; m < kNPad; ++m)
+            gu[kind][m] = up * (w0 ? (w1 ? __uint_as_float(v[m]) + __uint_as_float(v1[m]) : __uint_as_float(v[m]))
+                                   : __uint_as_float(v1[m]));
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(d_empty + d);
+        const int64_t n = (int64_t)tile * kTileCols + col;
+        if (seg_start == (int64_t)tile * a.NKB && seg_end == tile_end) {
 #pragma unroll
-        for (int m = 0; m < kNPad; ++m)
-          if (m < a.M) __stcg(mine + m * kTileCols + col, __uint_as_float(v[m]));
+          for (int m = 0; m < kNPad; ++m)
+            if (m < a.M) a.out[m * a.out_ld + n] = __float2half_rn(silu_f(gu[0][m]) * gu[1][m]);
+        } else {
+          // split tile: gate and up partials into this CTA's slot; k_mm_fixup (gated) finishes them
+          float* mine = a.ws + ((size_t)blockIdx.x * 2 + (seg_start == v0 ? 0 : 1)) * (2 * kNPad * kTileCols);
+#pragma unroll
+          for (int kind = 0; kind < 2; ++kind)
+#pragma unroll
+            for (int m = 0; m < kNPad; ++m)
+              if (m < a.M) __stcg(mine + (kind * kNPad + m) * kTileCols + col, gu[kind][m]);
+        }
+        seg_start = seg_end;
       }
-      seg_start = seg_end;
+    } else {
+      int tile = (int)(u0 / a.NKB);
+      int64_t seg_start = u0;
+      const int64_t uend = u0 + nu;
+      for (int seg = 0; seg_start < uend; ++seg, ++tile) {
+        const int64_t tile_end = (int64_t)(tile + 1) * a.NKB;
+        const int64_t seg_end = tile_end < uend ? tile_end : uend;  // exclusive
+        const int lo = (int)(seg_start - u0), hi = (int)(seg_end - 1 - u0);
+        const int d = seg & 1;
+        const float up = __ldg(a.colf + (int64_t)tile * kTileCols + col);  // 2^(24 - E) of this column
+        mbar_wait_backoff(d_full + d, (uint32_t)((seg >> 1) & 1), 256);
+        tc_fence_after();
+        const bool w0 = hi - lo >= 3 || ((lo >> 1) & 1) == 0 || ((hi >> 1) & 1) == 0;
+        const bool w1 = hi - lo >= 3 || ((lo >> 1) & 1) == 1 || ((hi >> 1) & 1) == 1;
+        uint32_t v[kNPad], v1[kNPad];
+        const uint32_t dcol = tmem + lane_base + 2 * d * kNPad;
+        if (w0) tmem_ld16(dcol, v);
+        if (w1) tmem_ld16(dcol + kNPad, v1);
+        tmem_wait_ld();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(d_empty + d);
+  #pragma unroll
+        for (int m = 0; m < kNPad; ++m)
+          v[m] = __float_as_uint(up * (w0 ? (w1 ? __uint_as_float(v[m]) + __uint_as_float(v1[m]) : __uint_as_float(v[m]))
+                                          : __uint_as_float(v1[m])));
+        const int64_t n = (int64_t)tile * kTileCols + col;
+        if (seg_start == (int64_t)tile * a.NKB && seg_end == tile_end) {
+  #pragma unroll
+          for (int m = 0; m < kNPad; ++m)
+            if (m < a.M) a.out[m * a.out_ld + n] = __float2half_rn(__uint_as_float(v[m]));
+        } else {
+          // split tile: partial into this CTA's slot (0 = its first segment, 1 = its last), summed by
+          // the fix-up kernel in CTA order after this kernel
+          float* mine = a.ws + ((size_t)blockIdx.x * 2 + (seg_start == u0 ? 0 : 1)) * (kNPad * kTileCols);
+  #pragma unroll
+          for (int m = 0; m < kNPad; ++m)
+            if (m < a.M) __stcg(mine + m * kTileCols + col, __uint_as_float(v[m]));
+        }
+        seg_start = seg_end;
+      }
     }
   } else if (warp == kProdWarp) {
     // ===================== TMA producer =====================
@@ -555,18 +613,36 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_dqgemv(const GemvArgs a, co
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&xmap)) : "memory");
     pdl_wait();
     if (lane == 0) { TPQ_CTA(1, gtime()) }
-    int kb = (int)(u0 % a.NKB);
-    for (int p = 0; p < np; ++p) {
-      const int x = p % C::NX, nh = (2 * p + 1 < nu) ? 2 : 1;
-      const int kb1 = kb + 1 == a.NKB ? 0 : kb + 1;
-      if (p >= C::NX) mbar_wait_sleep(done + (p - C::NX) % C::RD, (uint32_t)(((p - C::NX) / C::RD) & 1));
-      if (elect_one()) {
-        mbar_arrive_expect_tx(xfull + x, nh * C::XU);
-        tma_load_3d(smem + C::XRING + 2 * x * C::XU, &xmap, 0, 0, 2 * kb, xfull + x);
-        if (nh == 2) tma_load_3d(smem + C::XRING + (2 * x + 1) * C::XU, &xmap, 0, 0, 2 * kb1, xfull + x);
+    if constexpr (GT) {
+      // pair p = (tile, k-block) v0 + p: the gate record's slice from X[:, P1g] (xmap), the up
+      // record's from X[:, P1u] (xmapu), both at k-block kb
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&xmapu)) : "memory");
+      int kb = (int)(v0 % a.NKB);
+      for (int p = 0; p < np; ++p) {
+        const int x = p % C::NX;
+        if (p >= C::NX) mbar_wait_sleep(done + (p - C::NX) % C::RD, (uint32_t)(((p - C::NX) / C::RD) & 1));
+        if (elect_one()) {
+          mbar_arrive_expect_tx(xfull + x, 2 * C::XU);
+          tma_load_3d(smem + C::XRING + 2 * x * C::XU, &xmap, 0, 0, 2 * kb, xfull + x);
+          tma_load_3d(smem + C::XRING + (2 * x + 1) * C::XU, &xmapu, 0, 0, 2 * kb, xfull + x);
+        }
+        __syncwarp();
+        kb = kb + 1 == a.NKB ? 0 : kb + 1;
       }
-      __syncwarp();
-      kb = nh == 2 ? (kb1 + 1 == a.NKB ? 0 : kb1 + 1) : kb1;
+    } else {
+      int kb = (int)(u0 % a.NKB);
+      for (int p = 0; p < np; ++p) {
+        const int x = p % C::NX, nh = (2 * p + 1 < nu) ? 2 : 1;
+        const int kb1 = kb + 1 == a.NKB ? 0 : kb + 1;
+        if (p >= C::NX) mbar_wait_sleep(done + (p - C::NX) % C::RD, (uint32_t)(((p - C::NX) / C::RD) & 1));
+        if (elect_one()) {
+          mbar_arrive_expect_tx(xfull + x, nh * C::XU);
+          tma_load_3d(smem + C::XRING + 2 * x * C::XU, &xmap, 0, 0, 2 * kb, xfull + x);
+          if (nh == 2) tma_load_3d(smem + C::XRING + (2 * x + 1) * C::XU, &xmap, 0, 0, 2 * kb1, xfull + x);
+        }
+        __syncwarp();
+        kb = nh == 2 ? (kb1 + 1 == a.NKB ? 0 : kb1 + 1) : kb1;
+      }
     }
   } else {
     // ===================== MMA issuers: warp kMmaWarp + w takes the pairs p % 2 == w ===============
@@ -582,6 +658,37 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_dqgemv(const GemvArgs a, co
       ++sw;
     };
     static_assert(C::XU == 4096 && C::AU == 64, "umma_unit16 offsets");
+    if constexpr (GT) {
+      // one pair = one (tile, k-block): gate record -> gate accumulator, up record -> up accumulator
+      const int kbv = (int)(v0 % a.NKB);
+      const int nsegv = nv > 0 ? (kbv + nv - 1) / a.NKB + 1 : 0;
+      for (int p = w; p < np; p += 2) {
+        const int sg = (kbv + p) / a.NKB;
+        while (sw < sg) skip_seg();
+        const int lo = sg * a.NKB - kbv > 0 ? sg * a.NKB - kbv : 0;
+        const int hi = (sg + 1) * a.NKB - kbv - 1 < nv - 1 ? (sg + 1) * a.NKB - kbv - 1 : nv - 1;
+        const bool first = p - 2 < lo, last = p + 2 > hi;
+        const int x = p % C::NX, b = p % kSets, d = sg & 1;
+        const uint64_t bd0 = bdesc_sw128(xring + 2 * x * C::XU);
+        const uint32_t at = tmem + kA0 + b * 2 * C::AU;
+        mbar_wait_backoff(a_full + p % C::NAF, (uint32_t)((p / C::NAF) & 1), 0);
+        tc_fence_after();
+        if (first) {
+          mbar_wait(d_empty + d, (uint32_t)(((sg >> 1) & 1) ^ 1));
+          tc_fence_after();
+        }
+        const uint32_t dg = tmem + (4 * d + 2 * w) * kNPad;  // gate; up at + kNPad
+        if (elect_one()) {
+          umma_unit16(dg, at, bd0, kIdesc, first ? 0u : 1u);
+          umma_unit16(dg + kNPad, at + C::AU, bd0 + (C::XU >> 4), kIdesc, first ? 0u : 1u);
+          if (last) umma_commit1(d_full + d);
+          umma_commit1(done + p % C::RD);
+        }
+        __syncwarp();
+        if (last) ++sw;
+      }
+      while (sw < nsegv) skip_seg();
+    } else {
     for (int p = w; p < np; p += 2) {
       const int x = p % C::NX, b = p % kSets;
       const uint64_t bd0 = bdesc_sw128(xring + 2 * x * C::XU);
@@ -632,6 +739,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1) k_dqgemv(const GemvArgs a, co
       TPQ_EV(3, p)
     }
     while (sw < nseg) skip_seg();
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -1197,7 +1305,7 @@ __global__ void k_gather_rm(const __half* __restrict__ src, int64_t ld, const in
 // out[m][t*128 + j] = sum over c of the partial of CTA c (its slot for tile t), in CTA order.
 // Block (t, mb): rows 4 mb + warp, thread j: columns 4 lane .. +3 (float4 loads, 8-byte stores).
 __global__ void k_mm_fixup(const float* __restrict__ ws, int nb, int M, int NKB, int64_t U, int grid,
-                           __half* __restrict__ out, int64_t out_ld) {
+                           __half* __restrict__ out, int64_t out_ld, int gated) {
   pdl_launch_dependents();
   pdl_wait();  // the partials come from the GEMM just before
   const int t = blockIdx.x;
@@ -1205,27 +1313,40 @@ __global__ void k_mm_fixup(const float* __restrict__ ws, int nb, int M, int NKB,
   if (c_first == c_last) return;  // the tile lies inside one CTA's range: written by the GEMM
   const int m = blockIdx.y * 4 + (threadIdx.x >> 5), j = (threadIdx.x & 31) * 4;
   if (m >= M) return;
-  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  const int s_first = cta_start(c_first, U, grid) == (int64_t)t * NKB ? 0 : 1;  // see k_gemv_fixup
-  // contributors in CTA order, eight loads in flight per batch (one L2 round trip per batch)
-  for (int c0 = c_first; c0 <= c_last; c0 += 8) {
-    float4 v[8];
+  // contributor c's slot: every CTA after c_first starts inside tile t (slot 0, its first segment);
+  // c_first's slot is 0 only if its range starts exactly at the tile.  Gated (gate_proj layer 1):
+  // each slot holds the gate partials then the up partials, and the output is SiLU(gate) * up.
+  const int s_first = cta_start(c_first, U, grid) == (int64_t)t * NKB ? 0 : 1;
+  const int kinds = gated ? 2 : 1;
+  float4 acc[2] = {make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f)};
+  for (int kind = 0; kind < kinds; ++kind) {
+    // contributors in CTA order, eight loads in flight per batch (one L2 round trip per batch)
+    for (int c0 = c_first; c0 <= c_last; c0 += 8) {
+      float4 v[8];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int c = c0 + q <= c_last ? c0 + q : c_last;
-      const int slot = c > c_first ? 0 : s_first;
-      v[q] = __ldcg(reinterpret_cast<const float4*>(ws + (((size_t)c * 2 + slot) * nb + m) * kTileCols + j));
-    }
-#pragma unroll
-    for (int q = 0; q < 8; ++q)
-      if (c0 + q <= c_last) {
-        acc.x += v[q].x;
-        acc.y += v[q].y;
-        acc.z += v[q].z;
-        acc.w += v[q].w;
+      for (int q = 0; q < 8; ++q) {
+        const int c = c0 + q <= c_last ? c0 + q : c_last;
+        const int slot = c > c_first ? 0 : s_first;
+        v[q] = __ldcg(reinterpret_cast<const float4*>(ws + (((size_t)c * 2 + slot) * kinds * nb + kind * nb + m) * kTileCols + j));
       }
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (c0 + q <= c_last) {
+          acc[kind].x += v[q].x;
+          acc[kind].y += v[q].y;
+          acc[kind].z += v[q].z;
+          acc[kind].w += v[q].w;
+        }
+    }
   }
-  const __half2 lo = __floats2half2_rn(acc.x, acc.y), hi = __floats2half2_rn(acc.z, acc.w);
+  float4 y = acc[0];
+  if (gated) {
+    y.x = silu_f(acc[0].x) * acc[1].x;
+    y.y = silu_f(acc[0].y) * acc[1].y;
+    y.z = silu_f(acc[0].z) * acc[1].z;
+    y.w = silu_f(acc[0].w) * acc[1].w;
+  }
+  const __half2 lo = __floats2half2_rn(y.x, y.y), hi = __floats2half2_rn(y.z, y.w);
   uint2 pk;
   pk.x = *reinterpret_cast<const uint32_t*>(&lo);
   pk.y = *reinterpret_cast<const uint32_t*>(&hi);
@@ -1414,43 +1535,51 @@ bool max_carveout(Kern k) {
 }
 template <int G>
 bool carveout_g() {
-  return max_carveout(k_dqgemv<G>) && max_carveout(k_dqgemm<G, 64>) && max_carveout(k_dqgemm<G, 128>) &&
+  return max_carveout(k_dqgemv<G, false>) && max_carveout(k_dqgemv<G, true>) && max_carveout(k_dqgemm<G, 64>) && max_carveout(k_dqgemm<G, 128>) &&
          max_carveout(k_dqgemm<G, 256>) && max_carveout(k_dqgemm_ss<G, 128>);
 }
 
-template <int G>
+template <int G, bool GT>
 bool prepare_gemv() {
-  static_assert(TC<G>::SMEM <= 227 * 1024 && 2 * TC<G>::SMEM > 228 * 1024, "GEMV: one CTA per SM (TMEM 512 columns)");
-  if (cudaFuncSetAttribute(k_dqgemv<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, TC<G>::SMEM) != cudaSuccess)
+  using C = TC<G, GT>;
+  static_assert(C::SMEM <= 227 * 1024 && 2 * C::SMEM > 228 * 1024, "GEMV: one CTA per SM (TMEM 512 columns)");
+  if (cudaFuncSetAttribute(k_dqgemv<G, GT>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM) != cudaSuccess)
     return false;
   if (getenv("TPQ_VERBOSE")) {
     cudaFuncAttributes fa;
-    cudaFuncGetAttributes(&fa, k_dqgemv<G>);
-    fprintf(stderr, "[tpq] k_dqgemv<%d>: regs %d, local %zu, smem dyn %d\n", G, fa.numRegs, fa.localSizeBytes, TC<G>::SMEM);
+    cudaFuncGetAttributes(&fa, k_dqgemv<G, GT>);
+    fprintf(stderr, "[tpq] k_dqgemv<%d,%d>: regs %d, local %zu, smem dyn %d\n", G, (int)GT, fa.numRegs, fa.localSizeBytes,
+            C::SMEM);
   }
   return true;
 }
 
 bool gemv_prepare(int G) {
   if (!(max_carveout(k_gather_rm) && max_carveout(k_gather_rows) && max_carveout(k_mm_fixup) && max_carveout(k_gemv_fixup) &&
-        max_carveout(k_ss_fixup) && max_carveout(k_sum_partials) && max_carveout(k_dqgemv<0>)))
+        max_carveout(k_ss_fixup) && max_carveout(k_sum_partials) && max_carveout(k_dqgemv<0, false>)))
     return false;
-  if (!prepare_gemv<0>()) return false;  // unordered-g_idx layers (any G)
+  if (!prepare_gemv<0, false>()) return false;  // unordered-g_idx layers (any G)
   if (!(G == 128 ? carveout_g<128>() : G == 64 ? carveout_g<64>() : G == 32 ? carveout_g<32>() : false)) return false;
-  if (G == 128) return prepare_gemv<128>() && prepare_mm_g<128>();
-  if (G == 64) return prepare_gemv<64>() && prepare_mm_g<64>();
-  if (G == 32) return prepare_gemv<32>() && prepare_mm_g<32>();
+  if (G == 128) return prepare_gemv<128, false>() && prepare_gemv<128, true>() && prepare_mm_g<128>();
+  if (G == 64) return prepare_gemv<64, false>() && prepare_gemv<64, true>() && prepare_mm_g<64>();
+  if (G == 32) return prepare_gemv<32, false>() && prepare_gemv<32, true>() && prepare_mm_g<32>();
   return false;
 }
 
-cudaError_t launch_gemv(const LayerDev& L, const CUtensorMap& xmap, int M, void* out, int64_t out_ld, cudaStream_t st) {
-  if (M < 1 || M > kMaxM) return cudaErrorInvalidValue;
+template <int G, bool GT>
+cudaError_t launch_gemv_t(const GemvArgs& a, const CUtensorMap& xmap, const CUtensorMap& xmapu, cudaStream_t st) {
+  return launch_pdl(k_dqgemv<G, GT>, dim3(a.grid), dim3(kGemvThreads), TC<G, GT>::SMEM, st, a, xmap, xmapu);
+}
+
+cudaError_t launch_gemv(const LayerDev& L, const CUtensorMap& xmap, const CUtensorMap* xmapu, int M, void* out,
+                        int64_t out_ld, cudaStream_t st) {
+  if (M < 1 || M > kMaxM || (L.gated && !xmapu)) return cudaErrorInvalidValue;
   GemvArgs a;
   a.packed = L.packed;
   a.M = M;
   a.NT = L.NT;
   a.NKB = L.NKB;
-  a.U = L.U;
+  a.U = L.U;  // gated: (tile, k-block) pairs of gate + up records
   a.grid = L.grid;
   a.out = reinterpret_cast<__half*>(out);
   a.out_ld = out_ld;
@@ -1458,21 +1587,25 @@ cudaError_t launch_gemv(const LayerDev& L, const CUtensorMap& xmap, int M, void*
   a.colf = L.colf;
   a.meta = L.meta;
   a.ldm = L.N;
-  cudaError_t e = L.unord ? launch_pdl(k_dqgemv<0>, dim3(a.grid), dim3(kGemvThreads), TC<0>::SMEM, st, a, xmap)
-                  : L.G == 128 ? launch_pdl(k_dqgemv<128>, dim3(a.grid), dim3(kGemvThreads), TC<128>::SMEM, st, a, xmap)
-                  : L.G == 64 ? launch_pdl(k_dqgemv<64>, dim3(a.grid), dim3(kGemvThreads), TC<64>::SMEM, st, a, xmap)
-                  : L.G == 32 ? launch_pdl(k_dqgemv<32>, dim3(a.grid), dim3(kGemvThreads), TC<32>::SMEM, st, a, xmap)
-                              : cudaErrorInvalidValue;
+  const CUtensorMap& xu = xmapu ? *xmapu : xmap;
+  cudaError_t e = cudaErrorInvalidValue;
+  if (L.unord) e = launch_gemv_t<0, false>(a, xmap, xu, st);
+  else if (L.gated) e = L.G == 128 ? launch_gemv_t<128, true>(a, xmap, xu, st)
+                      : L.G == 64 ? launch_gemv_t<64, true>(a, xmap, xu, st)
+                      : L.G == 32 ? launch_gemv_t<32, true>(a, xmap, xu, st) : cudaErrorInvalidValue;
+  else e = L.G == 128 ? launch_gemv_t<128, false>(a, xmap, xu, st)
+           : L.G == 64 ? launch_gemv_t<64, false>(a, xmap, xu, st)
+           : L.G == 32 ? launch_gemv_t<32, false>(a, xmap, xu, st) : cudaErrorInvalidValue;
   if (e != cudaSuccess) return e;
   // split tiles, summed in CTA order after the GEMV: M <= 4 one thread per column with every
-  // contributor's rows in flight (k_gemv_fixup); M > 4 one warp per row, float4 per lane (k_mm_fixup),
-  // measured faster there.  Separate kernels ordered by griddepcontrol.wait beat an in-kernel
+  // contributor's rows in flight (k_gemv_fixup); M > 4 (and the gated layer) one warp per row,
+  // float4 per lane (k_mm_fixup).  Separate kernels ordered by griddepcontrol.wait beat an in-kernel
   // last-arriver reduction (branch exp-fused-forward, profiles/r02_summary.md).
-  if (M <= 4)
+  if (M <= 4 && !L.gated)
     return launch_pdl(k_gemv_fixup, dim3((unsigned)L.NT), dim3(128), 0, st, (const float*)L.ws, M, L.NKB, L.U, L.grid,
                       reinterpret_cast<__half*>(out), out_ld);
   return launch_pdl(k_mm_fixup, dim3((unsigned)L.NT, (unsigned)((M + 3) / 4)), dim3(128), 0, st, (const float*)L.ws, kNPad,
-                    M, L.NKB, L.U, L.grid, reinterpret_cast<__half*>(out), out_ld);
+                    M, L.NKB, L.U, L.grid, reinterpret_cast<__half*>(out), out_ld, L.gated);
 }
 
 template <int G>
@@ -1503,7 +1636,7 @@ cudaError_t launch_gemm(const LayerDev& L, const CUtensorMap& xmap, int nb, int 
                               : cudaErrorInvalidValue;
   if (e != cudaSuccess) return e;
   return launch_pdl(k_mm_fixup, dim3((unsigned)L.NT, (unsigned)((M + 3) / 4)), dim3(128), 0, st, (const float*)L.ws_mm,
-                    nb, M, L.NKB, L.U, L.grid_mm, reinterpret_cast<__half*>(out), out_ld);
+                    nb, M, L.NKB, L.U, L.grid_mm, reinterpret_cast<__half*>(out), out_ld, 0);
 }
 
 template <int G, int BN>

@@ -211,3 +211,28 @@ def test_unordered_variant_host_export_and_checks():
     with pytest.raises(tpq.TPQError) as e:
         tpq.TpMlp(p.w1, p.w2, None, None, tp=1, rank=0, variant=tpq.TPQ_UNORDERED, M_max=17, device=-1)
     assert e.value.code == 2
+
+
+@pytest.mark.parametrize("tp", [1, 4])
+def test_gated_shard_export(tp):
+    """gate_proj variant (f2): the gate shard is Wg[P1g][:, P2 block] and the up shard Wu[P1u][:, P2
+    block] -- the same columns for both (reading c24) -- with Wd[P2] rows, bit-exactly."""
+    p = synth.make_problem(256, 1024, 256, 32, 1, seed=14)
+    q = synth.make_problem(256, 1024, 256, 32, 1, seed=15)
+    wg, wu, wd = p.w1, q.w1, p.w2
+    Lg, Ld = _olayers(p)
+    Lu = O.layer_from_checkpoint(wu.qweight, wu.scales_bits, wu.qzeros, wu.g_idx, 256, 1024, 32)
+    Ps = [tpq.gptq_reorder(w.g_idx, 32)[0] for w in (wg, wu, wd)]
+    for r in range(tp):
+        h = tpq.TpMlp.gated(wg, wu, wd, *Ps, tp=tp, rank=r, M_max=16, device=-1)
+        rg = O.canonical_shard(Lg, Ld, tp, r, "tp_aware")
+        ru = O.canonical_shard(Lu, Ld, tp, r, "tp_aware")
+        qg, sg, zg = h.export_canonical(1)
+        qu, su, zu = h.export_canonical(3)
+        qd, sd, zd = h.export_canonical(2)
+        assert (qg == rg["w1_q"]).all() and (zg == rg["w1_z"]).all() and (sg.view(np.float16).astype(np.float64) == rg["w1_s"]).all()
+        assert (qu == ru["w1_q"]).all() and (zu == ru["w1_z"]).all() and (su.view(np.float16).astype(np.float64) == ru["w1_s"]).all()
+        assert (qd == rg["w2_q"]).all() and (zd == rg["w2_z"]).all()
+        h.close()
+    with pytest.raises(tpq.TPQError):
+        tpq.TpMlp.gated(wg, wu, wd, *Ps, M_max=64, device=-1)

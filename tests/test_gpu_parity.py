@@ -456,3 +456,95 @@ def test_unordered_full_size_llama(M):
     _, Y2r = O.dense_mlp_columns(p.X, L1, L2, cols2=cols)
     _assert_close(_np(Y)[:, cols], Y2r, "Y2 unordered, full size")
     h.close()
+
+
+def _gated(K1, N1, N2, G, M, seed):
+    """gate (p.w1), up (an independent layer from another seed's w1), down (p.w2)."""
+    p = synth.make_problem(K1, N1, N2, G, M, seed=seed)
+    q = synth.make_problem(K1, N1, N2, G, M, seed=seed + 1000)
+    wg, wu, wd = p.w1, q.w1, p.w2
+    Lg = O.layer_from_checkpoint(wg.qweight, wg.scales_bits, wg.qzeros, wg.g_idx, K1, N1, G)
+    Lu = O.layer_from_checkpoint(wu.qweight, wu.scales_bits, wu.qzeros, wu.g_idx, K1, N1, G)
+    Ld = O.layer_from_checkpoint(wd.qweight, wd.scales_bits, wd.qzeros, wd.g_idx, N1, N2, G)
+    Ps = [tpq.gptq_reorder(w.g_idx, G)[0] for w in (wg, wu, wd)]
+    return p, (wg, wu, wd), (Lg, Lu, Ld), Ps
+
+
+@pytest.mark.parametrize("G,M", [(32, 1), (64, 5), (128, 16)])
+def test_gated_tp_aware_vs_oracle(G, M):
+    """f2: Y = (SiLU(X.Wg) * (X.Wu)).Wd, one GEMV over interleaved gate/up records with the SiLU
+    product in its epilogue (and in the split-tile fix-up), vs the oracle's Alg. 3 generalization."""
+    p, ws, Ls, Ps = _gated(1024, 1408, 640, G, M, seed=50 + G)
+    ref = O.alg3_tp_aware_gated(p.X, *Ls, 1)
+    h = tpq.TpMlp.gated(*ws, *Ps, M_max=16)
+    X = _dev(p.X)
+    Y1 = _empty(M, p.N1)
+    h.layer1(X, M, Y1)
+    Y = _empty(M, p.N2)
+    h.forward(X, M, Y)
+    _assert_close(_np(Y1), ref["Y1_local"][0], "gated Y1 (P2 order)")
+    _assert_close(_np(Y), ref["Y2"], "gated Y2")
+    h.close()
+
+
+@pytest.mark.parametrize("tp", [2, 4, 8])
+def test_gated_tp_shards_and_naive(tp):
+    """Every rank's gated shard on cuda:0 (partials summed in rank order) vs the gated Alg. 3, and
+    the gated Alg. 2 step by step (layer 1 -> AllGather buffer -> P2 gather + CHUNK -> layer 2)."""
+    M = 4
+    p, ws, Ls, Ps = _gated(512, 2048, 512, 128, M, seed=60 + tp)
+    X = _dev(p.X)
+    ref = O.alg3_tp_aware_gated(p.X, *Ls, tp)
+    parts = []
+    for r in range(tp):
+        h = tpq.TpMlp.gated(*ws, *Ps, tp=tp, rank=r, M_max=16)
+        y1 = _empty(M, p.N1 // tp)
+        h.layer1(X, M, y1)
+        _assert_close(_np(y1), ref["Y1_local"][r], f"gated Y1 rank {r}")
+        y2 = _empty(M, p.N2)
+        h.forward_local(X, M, y2)
+        parts.append(y2)
+        h.close()
+    Y = _empty(M, p.N2)
+    tpq.sum_partials(parts, Y)
+    _assert_close(_np(Y), ref["Y2"], "gated Y2 TP-aware")
+    refn = O.alg2_naive_gated(p.X, *Ls, tp)
+    n = p.N1 // tp
+    hs = [tpq.TpMlp.gated(*ws, *Ps, tp=tp, rank=r, variant=tpq.TPQ_NAIVE, M_max=16) for r in range(tp)]
+    buf = torch.empty(tp, M, n, dtype=torch.float16, device=DEV)
+    for r, h in enumerate(hs):
+        h.layer1(X, M, buf[r])
+        _assert_close(_np(buf[r]), refn["Y1_local"][r], f"gated naive Y1 rank {r}")
+    parts = []
+    for h in hs:
+        y1in = _empty(M, n)
+        h.naive_gather(buf, M, y1in)
+        y2 = _empty(M, p.N2)
+        h.layer2(y1in, M, y2)
+        parts.append(y2)
+        h.close()
+    tpq.sum_partials(parts, Y)
+    _assert_close(_np(Y), refn["Y2"], "gated Y2 naive")
+
+
+@pytest.mark.parametrize("M", [1, 16])
+def test_gated_full_size_llama(M):
+    """Llama-70B with a gate_proj layer (K1=8192, N1=28672 for gate and up): all of Y1 and 256
+    sampled columns of Y2 against the oracle's definition."""
+    p, ws, Ls, Ps = _gated(8192, 28672, 8192, 128, M, seed=70)
+    Lg, Lu, Ld = Ls
+    h = tpq.TpMlp.gated(*ws, *Ps, M_max=16)
+    X = _dev(p.X)
+    Y1 = _empty(M, p.N1)
+    h.layer1(X, M, Y1)
+    Y = _empty(M, p.N2)
+    h.forward(X, M, Y)
+    Xf = p.X.astype(np.float64)
+    g = np.concatenate([Xf @ O.dequantize(O.permute_cols(Lg, np.arange(lo, lo + 2048))) for lo in range(0, p.N1, 2048)], 1)
+    u = np.concatenate([Xf @ O.dequantize(O.permute_cols(Lu, np.arange(lo, lo + 2048))) for lo in range(0, p.N1, 2048)], 1)
+    Y1r = O.silu(g) * u
+    cols = np.sort(np.random.default_rng(4).choice(p.N2, 256, replace=False))
+    Y2r = Y1r @ O.dequantize(O.permute_cols(Ld, cols))
+    _assert_close(_np(Y1), Y1r[:, Ps[2]], "gated Y1 full size (P2 order)")
+    _assert_close(_np(Y)[:, cols], Y2r, "gated Y2 full size, sampled")
+    h.close()
