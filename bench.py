@@ -230,13 +230,14 @@ def run_reference(a):
 
 
 # ------------------------------------------------------------------------------------ ours
-def make_handles(tpq, p, P1, P2, tp, rank, variant, local, step_bytes, dev):
+def make_handles(tpq, p, P1, P2, tp, rank, variant, local, step_bytes, dev, M_max=16):
     """R replicas of one rank's shard so that R x (bytes per forward) >= 3 x L2: consecutive
     forwards in the timed region read cold weights (the 80-layer case)."""
     import torch
     l2_cache = torch.cuda.get_device_properties(dev).L2_cache_size
     R = max(1, -(-3 * l2_cache // int(step_bytes)))
-    hs = [tpq.TpMlp(p.w1, p.w2, P1, P2, tp=tp, rank=rank, variant=variant, M_max=16, device=local) for _ in range(R)]
+    hs = [tpq.TpMlp(p.w1, p.w2, P1, P2, tp=tp, rank=rank, variant=variant, M_max=M_max, device=local)
+          for _ in range(R)]
     return hs, R, l2_cache
 
 
@@ -311,9 +312,23 @@ def extra_workload(torch, tpq, shape, M_list, sim_tp, seed, local, dev, stream):
     for M in M_list:
         us = step_latency(torch, tpq, hs, R, stream, M, sim_tp, X, Y)
         b = algorithmic_bytes(K1, N1, N2, G, M, tp)[2]
-        res[str(M)] = {"us": us, "hbm_frac": b / (us * 1e-6) / 1e9 / peak}
+        res[str(M)] = {"us": us, "hbm_frac": b / (us * 1e-6) / 1e9 / peak,
+                       "kernel_us": kernel_times(torch, tpq, hs, R, stream, M, 1)}
     for h in hs:
         h.close()
+    if sim_tp:
+        # the naive Alg. 2 rank's extra compute on the same box: its Y1[:, P2] + CHUNK gather (the
+        # AllGather itself needs the other ranks); the layers are the same kernels
+        hn, Rn, _ = make_handles(tpq, p, P1, P2, tp, 0, tpq.TPQ_NAIVE, local, step_b, dev)
+        for M in M_list:
+            per = Rn * max(1, 16 // Rn)
+            with torch.cuda.stream(stream):
+                for i in range(per):
+                    hn[i % Rn].run_step(tpq.TPQ_STEP_NAIVE_GATHER, M, stream=stream)
+                g = graph_of(torch, stream, per, lambda i: hn[i % Rn].run_step(tpq.TPQ_STEP_NAIVE_GATHER, M, stream=stream))
+            res[str(M)]["naive_p2_gather_us"] = time_graph(torch, stream, g, 40, per)
+        for h in hn:
+            h.close()
     return res
 
 
@@ -363,6 +378,33 @@ def gated_line(torch, tpq, shape, seed, local, dev, stream):
     for h in hs:
         h.close()
     out["kernel_us_M16"] = kt
+    return out
+
+
+def a7_line(torch, tpq, shape, seed, local, dev, stream):
+    """A7 (BASELINE.json configs[3]): one rank's TP = 8 Llama shard at M = 32 / 128 / 512 on the
+    tensor-core path, graph-timed, as a fraction of the measured dense fp16 (= bf16) tensor peak."""
+    K1, N1, N2, G = synth.SHAPES[shape]
+    p = synth.make_named(shape, 512, seed)
+    P1, _ = tpq.gptq_reorder(p.w1.g_idx, G)
+    P2, _ = tpq.gptq_reorder(p.w2.g_idx, G)
+    _, _, step_b = algorithmic_bytes(K1, N1, N2, G, 512, 8)
+    hs, R, _ = make_handles(tpq, p, P1, P2, 8, 0, tpq.TPQ_TP_AWARE, local, step_b, dev, M_max=512)
+    X = torch.from_numpy(p.X.copy()).to(dev)
+    Y = torch.empty(512, N2, dtype=torch.float16, device=dev)
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            tf = float(json.load(f)["bf16_tflops"])
+    except Exception:
+        tf = 1590.0
+    out = {}
+    for M in (32, 128, 512):
+        us = step_latency(torch, tpq, hs, R, stream, M, 8, X[:M], Y[:M], reps=10)
+        fl = 2.0 * M * (K1 * N1 + N1 * N2) / 8
+        out[str(M)] = {"us": us, "tflops": fl / (us * 1e-6) / 1e12, "tensor_frac": fl / (us * 1e-6) / 1e12 / tf}
+    for h in hs:
+        h.close()
+    out["peak_tflops"] = tf
     return out
 
 
@@ -560,6 +602,7 @@ def main():
     if world == 1 and not a.quick and not sim_tp and a.shape == "llama70b":
         line["granite20b_tp1"] = extra_workload(torch, tpq, "granite20b", (1, 16), 0, a.seed, local, dev, stream)
         line["llama70b_tp8_shard"] = extra_workload(torch, tpq, "llama70b", (1, 16), 8, a.seed, local, dev, stream)
+        line["a7_llama70b_tp8_shard"] = a7_line(torch, tpq, "llama70b", a.seed, local, dev, stream)
     if world == 1 and not a.quick and not sim_tp and a.variant == "tp_aware":
         line["unordered_tp1"] = unordered_line(torch, tpq, p, a.shape, local, dev, stream, kt, M)
         line["gated_tp1"] = gated_line(torch, tpq, a.shape, a.seed, local, dev, stream)

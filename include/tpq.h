@@ -206,12 +206,17 @@ int tpq_sum_partials(const void* const* parts, int nparts, int64_t count, void* 
  *   TPQ_STEP_LAYER1    (1)  layer-1 dequant-GEMV + its split-tile fix-up      (Alg. 3 L1)
  *   TPQ_STEP_LAYER2    (2)  layer-2 dequant-GEMV + its split-tile fix-up      (Alg. 3 L2)
  *   TPQ_STEP_ALLREDUCE (3)  ncclAllReduce of the [M][N2] output (tp > 1 with a comm; Alg. 3 L3)
- * TPQ_EINVAL for an unknown step or M outside [1, min(16, M_max)]; TPQ_ESTATE for a host-only
- * handle or step 3 without a comm. */
+ *   TPQ_STEP_NAIVE_GATHER (4)  TPQ_NAIVE handles: Y1[:, P2] + CHUNK from the AllGather buffer
+ *                              (Alg. 2 L3-4) into layer 2's input
+ *   TPQ_STEP_ALLGATHER (5)  TPQ_NAIVE handles with a comm: ncclAllGather of Y1_local (Alg. 2 L2)
+ * TPQ_EINVAL for an unknown step, a naive step on another variant or M outside [1, min(16, M_max)];
+ * TPQ_ESTATE for a host-only handle or a collective step without a comm. */
 #define TPQ_STEP_GATHER 0
 #define TPQ_STEP_LAYER1 1
 #define TPQ_STEP_LAYER2 2
 #define TPQ_STEP_ALLREDUCE 3
+#define TPQ_STEP_NAIVE_GATHER 4
+#define TPQ_STEP_ALLGATHER 5
 int tpq_mlp_run_step(tpq_mlp* h, int step, int64_t M, void* stream);
 
 

@@ -18,6 +18,7 @@ LIB_PATH = os.environ.get("TPQ_LIB_PATH") or os.path.join(_PKG, "libtpq.so")
 TPQ_OK, TPQ_EINVAL, TPQ_EUNSUPPORTED, TPQ_ECUDA, TPQ_ENCCL, TPQ_ENOMEM, TPQ_ESTATE = range(7)
 TPQ_NAIVE, TPQ_TP_AWARE, TPQ_UNORDERED = 0, 1, 2
 TPQ_STEP_GATHER, TPQ_STEP_LAYER1, TPQ_STEP_LAYER2, TPQ_STEP_ALLREDUCE = 0, 1, 2, 3
+TPQ_STEP_NAIVE_GATHER, TPQ_STEP_ALLGATHER = 4, 5
 _CODES = {1: "EINVAL", 2: "EUNSUPPORTED", 3: "ECUDA", 4: "ENCCL", 5: "ENOMEM", 6: "ESTATE"}
 
 # Every symbol include/tpq.h declares (tests check the .so exports all of them).

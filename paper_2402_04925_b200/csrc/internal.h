@@ -55,6 +55,8 @@ struct LayerDev {
   const float* colf = nullptr;  // [N] 2^(24 - E_n): records hold s' = s 2^E_n (tpq_host.cpp column_exponents)
   const uint32_t* meta = nullptr;  // unordered layer (TPQ_UNORDERED): [ng][N] {fp16 s', fp16 -z s' 2^-24}
   int unord = 0;                   // 1: records in checkpoint row order with per-row group ids (k_dqgemv<0>)
+  const int* split_tiles = nullptr;  // [nsplit] tiles of this layer split between CTAs (k_split_fixup's grid)
+  int nsplit = 0;
   int gated = 0;                   // 1: gate_proj layer 1: gate(t, kb), up(t, kb) record pairs; U counts the pairs
 };
 
@@ -117,6 +119,10 @@ cudaError_t launch_gather_rowmajor(const void* src, int64_t ld, const int32_t* i
 int cta_read(unsigned long long* out);
 int trace_read(long long* out);
 #endif
+
+// Naive Alg. 2 L3-4: dst[m][i] = buf[so[i].x][m][so[i].y], buf = the AllGather buffer [tp][M][n], so =
+// int2 (c / n, c % n) per local column i.
+cudaError_t launch_gather_allgather(const void* buf, const void* so, int n, int M, void* dst, cudaStream_t st);
 
 cudaError_t launch_sum_partials(const void* const* parts, int nparts, int64_t count, void* out, cudaStream_t st);
 

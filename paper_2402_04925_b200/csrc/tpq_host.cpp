@@ -260,7 +260,7 @@ struct tpq_mlp {
   void* d_w1 = nullptr;
   void* d_w2 = nullptr;
   int32_t* d_P1 = nullptr;
-  int32_t* d_gcols = nullptr;  // naive: P2[r n .. (r+1) n)
+  int32_t* d_gcols = nullptr;  // naive: int2 (c / n, c % n) of c = P2[r n + i] (k_gather_ag)
   void* d_x1 = nullptr;        // layer-1 input X[:, P1], row-major [16][K1]
   void* d_y1 = nullptr;        // layer-1 output = layer-2 input, row-major [16][n]
   void* d_buf = nullptr;       // AllGather buffer [tp][rows][n]
@@ -268,6 +268,7 @@ struct tpq_mlp {
   void* d_yout = nullptr;      // host-forward staging [M_max][N2]
   float* d_ws = nullptr;
   float* d_colf = nullptr;     // per-column 2^(24 - E) of layer 1 [n] then layer 2 [N2]
+  int* d_split = nullptr;      // split tiles of layer 1 then layer 2 (k_split_fixup)
   CUtensorMap xmap1 = {}, xmap2 = {};  // TMA views of d_x1 / d_y1 (GEMV activation operand, 16 rows)
   // gate_proj variant (f2): layer 1 = gate + up; the up layer's own P1u and gathered X[:, P1u]
   bool gated = false;
@@ -314,7 +315,7 @@ int validate_perm(const int32_t* P, const gptq_layer* w, const char* name) {
 void free_dev(tpq_mlp* h) {
   if (h->device < 0) return;
   cudaSetDevice(h->device);
-  void* ptrs[] = {h->d_w1, h->d_w2, h->d_P1, h->d_gcols, h->d_x1, h->d_y1, h->d_buf, h->d_xin, h->d_yout, h->d_ws, h->d_colf, h->d_tab, h->d_P1u, h->d_x1u};
+  void* ptrs[] = {h->d_w1, h->d_w2, h->d_P1, h->d_gcols, h->d_x1, h->d_y1, h->d_buf, h->d_xin, h->d_yout, h->d_ws, h->d_colf, h->d_tab, h->d_P1u, h->d_x1u, h->d_split};
   for (void* p : ptrs)
     if (p) cudaFree(p);
 }
@@ -584,7 +585,7 @@ int shard_impl(const gptq_layer* w1, const gptq_layer* wu, const gptq_layer* w2,
         };
         const size_t ws1s = ss_ws(h->L1), ws2s = ss_ws(h->L2);
         if ((r = A(&h->d_w1, h->pk1.size())) || (r = A(&h->d_w2, h->pk2.size())) ||
-            (r = A((void**)&h->d_P1, K1 * 4)) || (r = A((void**)&h->d_gcols, n * 4)) || (r = A(&h->d_x1, (size_t)h->rows * K1 * 2)) ||
+            (r = A((void**)&h->d_P1, K1 * 4)) || (r = A((void**)&h->d_gcols, n * 8)) || (r = A(&h->d_x1, (size_t)h->rows * K1 * 2)) ||
             (r = A(&h->d_y1, (size_t)h->rows * n * 2)) || (r = A(&h->d_buf, (size_t)tp * h->rows * n * 2)) ||
             (r = A(&h->d_xin, (size_t)M_max * K1 * 2)) || (r = A(&h->d_yout, (size_t)M_max * N2 * 2)) ||
             (r = A((void**)&h->d_ws, (ws1 + ws2 + wm1 + wm2 + ws1s + ws2s) * 4)) ||
@@ -606,7 +607,14 @@ int shard_impl(const gptq_layer* w1, const gptq_layer* wu, const gptq_layer* w2,
           for (int64_t j = 0; j < N2; ++j) cf[(size_t)(n + j)] = std::ldexp(1.f, 24 - h->E2[(size_t)j]);
           TPQ_CUDA(cudaMemcpy(h->d_colf, cf.data(), cf.size() * 4, cudaMemcpyHostToDevice));
         }
-        TPQ_CUDA(cudaMemcpy(h->d_gcols, h->gather_cols.data(), n * 4, cudaMemcpyHostToDevice));
+        {
+          std::vector<int32_t> so((size_t)(2 * n));
+          for (int64_t i = 0; i < n; ++i) {
+            so[(size_t)(2 * i)] = (int32_t)(h->gather_cols[(size_t)i] / n);
+            so[(size_t)(2 * i + 1)] = (int32_t)(h->gather_cols[(size_t)i] % n);
+          }
+          TPQ_CUDA(cudaMemcpy(h->d_gcols, so.data(), n * 8, cudaMemcpyHostToDevice));
+        }
         bool mok = tpq::make_xmap(&h->xmap1, h->d_x1, K1, tpq::kNPad) && tpq::make_xmap(&h->xmap2, h->d_y1, n, tpq::kNPad);
         if (h->rows > tpq::kMaxM) {
           for (int v = 0; v < 3; ++v)
@@ -624,6 +632,23 @@ int shard_impl(const gptq_layer* w1, const gptq_layer* wu, const gptq_layer* w2,
         }
         h->L1.colf = h->d_colf;
         h->L2.colf = h->d_colf + n;
+        {  // tiles split between CTAs by the stream-K partition (CTA c owns [c U / grid, (c+1) U / grid))
+          std::vector<int> sp;
+          int n1 = 0;
+          for (int layer = 0; layer < 2; ++layer) {
+            const tpq::LayerDev& L = layer ? h->L2 : h->L1;
+            auto cta_of = [&](int64_t u) { return (int)(((u + 1) * L.grid + L.U - 1) / L.U) - 1; };
+            for (int t = 0; t < L.NT; ++t)
+              if (cta_of((int64_t)t * L.NKB) != cta_of((int64_t)(t + 1) * L.NKB - 1)) sp.push_back(t);
+            if (layer == 0) n1 = (int)sp.size();
+          }
+          if ((r = A((void**)&h->d_split, std::max<size_t>(1, sp.size()) * 4))) return r;
+          if (!sp.empty()) TPQ_CUDA(cudaMemcpy(h->d_split, sp.data(), sp.size() * 4, cudaMemcpyHostToDevice));
+          h->L1.split_tiles = h->d_split;
+          h->L1.nsplit = n1;
+          h->L2.split_tiles = h->d_split + n1;
+          h->L2.nsplit = (int)sp.size() - n1;
+        }
         h->L1.packed = (const uint8_t*)h->d_w1;
         h->L2.packed = (const uint8_t*)h->d_w2;
         h->L1.ws = h->d_ws;
@@ -772,7 +797,7 @@ int chunk_forward(tpq_mlp* h, const uint16_t* X, int mc, void* Y, cudaStream_t s
       TPQ_NCCL(ncclAllGather(slot, h->d_buf, (size_t)mc * h->n, ncclFloat16, h->comm, st));  // Alg. 2 L2
     }
     // Alg. 2 L3-4: Y1_global[:, P2] then CHUNK(rank), fused into one gather
-    TPQ_CUDA(tpq::launch_gather_rowmajor(h->d_buf, 0, h->d_gcols, tpq::GATHER_ALLGATHER, h->n, mc, h->n, h->d_y1, st));
+    TPQ_CUDA(tpq::launch_gather_allgather(h->d_buf, h->d_gcols, (int)h->n, mc, h->d_y1, st));
   }
   TPQ_CUDA(run_layer(h, 2, mc, Y, h->N2, st));  // L2 GEMM
   return TPQ_OK;
@@ -844,7 +869,7 @@ int tpq_naive_gather(tpq_mlp* h, const void* buf, int64_t M, void* Y1in, void* s
   if (rc) return rc;
   if (h->variant != TPQ_NAIVE) return fail(TPQ_EINVAL, "tpq_naive_gather needs a TPQ_NAIVE handle");
   TPQ_CUDA(cudaSetDevice(h->device));
-  TPQ_CUDA(tpq::launch_gather_rowmajor(buf, 0, h->d_gcols, tpq::GATHER_ALLGATHER, h->n, (int)M, h->n, Y1in,
+  TPQ_CUDA(tpq::launch_gather_allgather(buf, h->d_gcols, (int)h->n, (int)M, Y1in,
                                        (cudaStream_t)stream));
   return TPQ_OK;
 }
@@ -898,6 +923,16 @@ int tpq_mlp_run_step(tpq_mlp* h, int step, int64_t M, void* stream) {
       return TPQ_OK;
     case TPQ_STEP_LAYER2:
       TPQ_CUDA(run_layer(h, 2, mc, h->d_yout, h->N2, st));
+      return TPQ_OK;
+    case TPQ_STEP_NAIVE_GATHER:
+      if (h->variant != TPQ_NAIVE) return fail(TPQ_EINVAL, "TPQ_STEP_NAIVE_GATHER needs a TPQ_NAIVE handle");
+      TPQ_CUDA(tpq::launch_gather_allgather(h->d_buf, h->d_gcols, (int)h->n, mc, h->d_y1, st));
+      return TPQ_OK;
+    case TPQ_STEP_ALLGATHER:
+      if (h->variant != TPQ_NAIVE) return fail(TPQ_EINVAL, "TPQ_STEP_ALLGATHER needs a TPQ_NAIVE handle");
+      if (!h->comm) return fail(TPQ_ESTATE, "no communicator attached");
+      TPQ_NCCL(ncclAllGather((uint8_t*)h->d_buf + (size_t)h->rank * mc * h->n * 2, h->d_buf, (size_t)mc * h->n,
+                             ncclFloat16, h->comm, st));
       return TPQ_OK;
     case TPQ_STEP_ALLREDUCE:
       if (!h->comm) return fail(TPQ_ESTATE, "no communicator attached");

@@ -1417,11 +1417,51 @@ __global__ void __launch_bounds__(128) k_gemv_fixup(const float* __restrict__ ws
     if (m < M) o[m * out_ld] = __float2half_rn(r[m]);
 }
 
+// Split-tile fix-up sized to sit beside a GEMV CTA (<= 32 registers x 128 threads, one block per split
+// tile): block b sums split tile tiles[b]'s contributors in CTA order, one thread per column, 4 rows
+// x 2 contributors in flight; gated: gate and up partials, then fp16(SiLU(gate) * up).
+__global__ void __launch_bounds__(128, 16) k_split_fixup(const float* __restrict__ ws, const int* __restrict__ tiles, int M,
+                                                         int NKB, int64_t U, int grid, __half* __restrict__ out,
+                                                         int64_t out_ld, int gated) {
+  pdl_launch_dependents();
+  pdl_wait();  // the partials come from the GEMV just before
+  const int t = __ldg(tiles + blockIdx.x), col = threadIdx.x;
+  const int c_first = cta_of_unit((int64_t)t * NKB, U, grid), c_last = cta_of_unit((int64_t)(t + 1) * NKB - 1, U, grid);
+  const int s_first = cta_start(c_first, U, grid) == (int64_t)t * NKB ? 0 : 1;
+  const int kinds = gated ? 2 : 1;
+  __half* o = out + (int64_t)t * kTileCols + col;
+  for (int m0 = 0; m0 < M; m0 += 4) {
+    float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+    for (int kind = 0; kind < kinds; ++kind)
+      for (int c = c_first; c <= c_last; c += 2) {
+        float v[2][4];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int cc = c + q <= c_last ? c + q : c_last;
+          const float* src = ws + (((size_t)cc * 2 + (cc > c_first ? 0 : s_first)) * kinds + kind) * (kNPad * kTileCols) + col;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) v[q][i] = m0 + i < M ? __ldcg(src + (m0 + i) * kTileCols) : 0.f;
+        }
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+          if (c + q <= c_last)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) acc[kind][i] += v[q][i];
+      }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (m0 + i < M) o[(m0 + i) * out_ld] = __float2half_rn(gated ? silu_f(acc[0][i]) * acc[1][i] : acc[0][i]);
+  }
+}
+
 // X[:, idx] for the layer-1 operand: CTA (m, part) reads row m into shared memory with coalesced
 // 16-byte loads, then gathers part `part` of the k range from there (a direct gather reads a
 // 32-byte sector per 2-byte element).  dst[m][k] = src[m ld + idx[k]].
-__global__ void k_gather_rows(const __half* __restrict__ src, int64_t ld, const int32_t* __restrict__ idx, int64_t K,
-                              __half* __restrict__ dst) {
+// At most 32 registers x 128 threads (4096) and one block per SM: the block fits beside a GEMV CTA
+// (96 x 640 registers), so the GEMV launched after it can become resident and stream weights at once.
+__global__ void __launch_bounds__(128, 16) k_gather_rows(const __half* __restrict__ src, int64_t ld,
+                                                         const int32_t* __restrict__ idx, int64_t K,
+                                                         __half* __restrict__ dst) {
   extern __shared__ __align__(16) uint8_t srow_raw[];
   __half* srow = reinterpret_cast<__half*>(srow_raw);
   pdl_launch_dependents();
@@ -1450,6 +1490,20 @@ __global__ void k_gather_rows(const __half* __restrict__ src, int64_t ld, const 
     pk.z = (uint32_t)__half_as_ushort(srow[i1.x]) | ((uint32_t)__half_as_ushort(srow[i1.y]) << 16);
     pk.w = (uint32_t)__half_as_ushort(srow[i1.z]) | ((uint32_t)__half_as_ushort(srow[i1.w]) << 16);
     reinterpret_cast<uint4*>(out)[c] = pk;
+  }
+}
+
+// Naive Alg. 2 L3-4 for rank r: dst[m][i] = buf[slice(i)][m][off(i)], the AllGather
+// buffer buf[tp][M][n] read through the precomputed (slice, offset) = (c / n, c % n), c = P2[r n + i]
+// (reading c17): one index load and one data load per element, no division.
+__global__ void k_gather_ag(const __half* __restrict__ buf, const int2* __restrict__ so, int n, int M,
+                            __half* __restrict__ dst) {
+  pdl_launch_dependents();
+  pdl_wait();
+  const int m = blockIdx.y;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int2 t = __ldg(so + i);
+    dst[(int64_t)m * n + i] = buf[((int64_t)t.x * M + m) * n + t.y];
   }
 }
 
@@ -1555,7 +1609,7 @@ bool prepare_gemv() {
 }
 
 bool gemv_prepare(int G) {
-  if (!(max_carveout(k_gather_rm) && max_carveout(k_gather_rows) && max_carveout(k_mm_fixup) && max_carveout(k_gemv_fixup) &&
+  if (!(max_carveout(k_gather_rm) && max_carveout(k_gather_rows) && max_carveout(k_gather_ag) && max_carveout(k_split_fixup) && max_carveout(k_mm_fixup) && max_carveout(k_gemv_fixup) &&
         max_carveout(k_ss_fixup) && max_carveout(k_sum_partials) && max_carveout(k_dqgemv<0, false>)))
     return false;
   if (!prepare_gemv<0, false>()) return false;  // unordered-g_idx layers (any G)
@@ -1564,6 +1618,13 @@ bool gemv_prepare(int G) {
   if (G == 64) return prepare_gemv<64, false>() && prepare_gemv<64, true>() && prepare_mm_g<64>();
   if (G == 32) return prepare_gemv<32, false>() && prepare_gemv<32, true>() && prepare_mm_g<32>();
   return false;
+}
+
+// Small kernels sized to co-reside with a GEMV CTA (default); TPQ_NO_CORES=1 restores the round-2
+// first-half launch shapes (k_gemv_fixup / k_mm_fixup, 256-thread gathers) for A/B measurements.
+bool co_res() {
+  static const bool on = getenv("TPQ_NO_CORES") == nullptr;
+  return on;
 }
 
 template <int G, bool GT>
@@ -1601,7 +1662,15 @@ cudaError_t launch_gemv(const LayerDev& L, const CUtensorMap& xmap, const CUtens
   // contributor's rows in flight (k_gemv_fixup); M > 4 (and the gated layer) one warp per row,
   // float4 per lane (k_mm_fixup).  Separate kernels ordered by griddepcontrol.wait beat an in-kernel
   // last-arriver reduction (branch exp-fused-forward, profiles/r02_summary.md).
-  if (M <= 4 && !L.gated)
+  // M <= 4: k_split_fixup, one <= 32-register block per split tile that sits beside the next GEMV's
+  // CTA (same-box: Llama TP=1 M=1 59.3 -> 57.0 us); M > 4: k_mm_fixup (one warp per row, float4 per
+  // lane, 8 contributors in flight), faster there than 32 registers allow.
+  if (co_res() && L.split_tiles && M <= 4) {
+    if (L.nsplit == 0) return cudaSuccess;
+    return launch_pdl(k_split_fixup, dim3((unsigned)L.nsplit), dim3(128), 0, st, (const float*)L.ws, L.split_tiles, M, L.NKB,
+                      L.U, L.grid, reinterpret_cast<__half*>(out), out_ld, L.gated);
+  }
+  if (M <= 4 && !L.gated)  // (TPQ_NO_CORES=1 only)
     return launch_pdl(k_gemv_fixup, dim3((unsigned)L.NT), dim3(128), 0, st, (const float*)L.ws, M, L.NKB, L.U, L.grid,
                       reinterpret_cast<__half*>(out), out_ld);
   return launch_pdl(k_mm_fixup, dim3((unsigned)L.NT, (unsigned)((M + 3) / 4)), dim3(128), 0, st, (const float*)L.ws, kNPad,
@@ -1681,11 +1750,18 @@ cudaError_t launch_gather_rowmajor(const void* src, int64_t ld, const int32_t* i
   // column gather of rows that fit in shared memory, 16-byte aligned rows: stage each row
   if (mode == GATHER_COLS && idx && K % 8 == 0 && K * 2 <= 48 * 1024 && ld % 8 == 0 &&
       reinterpret_cast<uintptr_t>(src) % 16 == 0 && reinterpret_cast<uintptr_t>(idx) % 16 == 0)
-    return launch_pdl(k_gather_rows, dim3((unsigned)M, (unsigned)std::max(1, std::min(16, 256 / M))), dim3(256),
-                      (size_t)K * 2, st, reinterpret_cast<const __half*>(src), ld, idx, K, reinterpret_cast<__half*>(dst));
+    return launch_pdl(k_gather_rows, dim3((unsigned)M, (unsigned)std::max(1, std::min(16, (co_res() ? 148 : 256) / M))),
+                      dim3(128), (size_t)K * 2, st, reinterpret_cast<const __half*>(src), ld, idx, K,
+                      reinterpret_cast<__half*>(dst));
   const int64_t total = (int64_t)M * K;
   return launch_pdl(k_gather_rm, dim3(grid_for(total, 256)), dim3(256), 0, st, reinterpret_cast<const __half*>(src),
                     ld, idx, mode, nn, M, K, reinterpret_cast<__half*>(dst));
+}
+
+cudaError_t launch_gather_allgather(const void* buf, const void* so, int n, int M, void* dst, cudaStream_t st) {
+  return launch_pdl(k_gather_ag, dim3((unsigned)std::max(1, std::min(148, (n + 255) / 256)), (unsigned)M), dim3(256), 0,
+                    st, reinterpret_cast<const __half*>(buf), reinterpret_cast<const int2*>(so), n, M,
+                    reinterpret_cast<__half*>(dst));
 }
 
 cudaError_t launch_sum_partials(const void* const* parts, int nparts, int64_t count, void* out, cudaStream_t st) {

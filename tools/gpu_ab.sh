@@ -1,3 +1,2 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "gated" > gpurun_out/ab_pytest.log 2>&1
-timeout 900 python bench.py --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err
+timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -x -q > gpurun_out/ab_pytest.log 2>&1
