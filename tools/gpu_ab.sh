@@ -1,2 +1,6 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -x -q > gpurun_out/ab_pytest.log 2>&1
+python -c "import torch; torch.zeros(1).cuda()"
+for tool in memcheck synccheck racecheck; do
+  timeout 1200 compute-sanitizer --tool $tool --print-limit 20 python tools/sanitize_fwd.py > gpurun_out/sanitize_$tool.log 2>&1
+  echo "$tool rc=$?" >> gpurun_out/sanitize_rc.log
+done
