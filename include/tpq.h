@@ -209,7 +209,8 @@ int tpq_sum_partials(const void* const* parts, int nparts, int64_t count, void* 
  *   TPQ_STEP_NAIVE_GATHER (4)  TPQ_NAIVE handles: Y1[:, P2] + CHUNK from the AllGather buffer
  *                              (Alg. 2 L3-4) into layer 2's input
  *   TPQ_STEP_ALLGATHER (5)  TPQ_NAIVE handles with a comm: ncclAllGather of Y1_local (Alg. 2 L2)
- * TPQ_EINVAL for an unknown step, a naive step on another variant or M outside [1, min(16, M_max)];
+ * TPQ_EINVAL for an unknown step, a naive step on another variant or M outside one pass, [1, min(P, M_max)]
+ * with P = 16 for handles with M_max <= 16, else 256 (the A7 pass);
  * TPQ_ESTATE for a host-only handle or a collective step without a comm. */
 #define TPQ_STEP_GATHER 0
 #define TPQ_STEP_LAYER1 1

@@ -94,6 +94,16 @@ inline int ss_bn(int NT, int G) {
   return wide && NT % 2 == 0 && G == 128 ? 256 : 128;
 }
 
+// The CTA-pair SS GEMM (k_dqgemm_ss2, cta_group::2: 256 batch rows x 256 weight columns per pair)
+// for passes of more than 128 rows over an even tile count.  TPQ_SS2=0 selects the 1-CTA kernel.
+inline bool ss_pair(int NT, int M) {
+  static const bool off = [] {
+    const char* e = getenv("TPQ_SS2");
+    return e && e[0] == '0';
+  }();
+  return !off && NT % 2 == 0 && M > 128;
+}
+
 // k-splits of the SS GEMM for `mb` 128-row blocks and NG column groups: as many as keep the work items within one wave
 // of `sms` CTAs, at least 4 k-blocks per split, at most 16 splits.
 inline int ss_splits(int NG, int NKB, int mb, int sms) {
@@ -104,7 +114,7 @@ inline int ss_splits(int NG, int NKB, int mb, int sms) {
   return S < 1 ? 1 : S;
 }
 
-// A7 for M >= 128 (<= 256 rows per pass): mixed-input SS GEMM, xmap = the [256][K] buffer with
+// A7 for M >= 128 (<= 512 rows per pass): mixed-input SS GEMM, xmap = the [512][K] buffer with
 // 128-row boxes; k-splits chosen to cover `sms` SMs (partials in L.ws_ss, k_ss_fixup).
 cudaError_t launch_gemm_ss(const LayerDev& L, const CUtensorMap& xmap, int M, int sms, void* out, int64_t out_ld,
                            cudaStream_t st);

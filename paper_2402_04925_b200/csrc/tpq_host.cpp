@@ -237,7 +237,8 @@ inline uint32_t nib(uint32_t w, int i) { return (w >> (4 * i)) & 0xFu; }
 
 }  // namespace
 
-constexpr int kGemmRows = 256;  // A7: activation rows per GEMM pass
+constexpr int kGemmRows = 512;  // A7: activation rows per GEMM pass (the SS GEMMs take up to 512)
+constexpr int kMmRows = 256;    // A7 below 128 rows: k_dqgemm's largest N
 
 struct tpq_comm {
   ncclComm_t comm;
@@ -570,18 +571,24 @@ int shard_impl(const gptq_layer* w1, const gptq_layer* wu, const gptq_layer* w2,
         const size_t ws1 = (size_t)h->L1.grid * 2 * tpq::kNPad * tpq::kTileCols * (gated ? 2 : 1);  // [grid][2 slots][gate, up][16][128]
         const size_t ws2 = (size_t)h->L2.grid * 2 * tpq::kNPad * tpq::kTileCols;
         h->rows = M_max > tpq::kMaxM ? kGemmRows : tpq::kMaxM;
-        const size_t wm1 = M_max > tpq::kMaxM ? (size_t)h->L1.grid_mm * 2 * kGemmRows * tpq::kTileCols : 0;
-        const size_t wm2 = M_max > tpq::kMaxM ? (size_t)h->L2.grid_mm * 2 * kGemmRows * tpq::kTileCols : 0;
+        const size_t wm1 = M_max > tpq::kMaxM ? (size_t)h->L1.grid_mm * 2 * kMmRows * tpq::kTileCols : 0;
+        const size_t wm2 = M_max > tpq::kMaxM ? (size_t)h->L2.grid_mm * 2 * kMmRows * tpq::kTileCols : 0;
         cudaDeviceGetAttribute(&h->sms, cudaDevAttrMultiProcessorCount, device);
         auto ss_ws = [&](const tpq::LayerDev& L) -> size_t {  // largest k-split partial set (M >= 128 passes)
           if (M_max < 128) return 0;
           size_t items = 0;
           const int bn = tpq::ss_bn(L.NT, L.G), NG = L.NT * tpq::kTileCols / bn;
-          for (int mb = 1; mb <= 2; ++mb) {
+          for (int mb = 1; mb <= kGemmRows / 128; ++mb) {
             const int S = tpq::ss_splits(NG, L.NKB, mb, h->sms);
             if (S > 1) items = std::max(items, (size_t)mb * NG * S);
           }
-          return items * 128 * bn;
+          size_t fl = items * 128 * bn;
+          if (L.NT % 2 == 0)  // CTA-pair kernel: (NT / 2 groups x 2 MB row blocks x S) x 128 x 256
+            for (int mb = 1; mb <= kGemmRows / 256; ++mb) {
+              const int S2 = tpq::ss_splits(L.NT / 2, L.NKB, mb, h->sms / 2);
+              if (S2 > 1) fl = std::max(fl, (size_t)L.NT * mb * S2 * 128 * 256);
+            }
+          return fl;
         };
         const size_t ws1s = ss_ws(h->L1), ws2s = ss_ws(h->L2);
         if ((r = A(&h->d_w1, h->pk1.size())) || (r = A(&h->d_w2, h->pk2.size())) ||
@@ -766,19 +773,20 @@ int check_fwd(tpq_mlp* h, const void* X, int64_t M, const void* Y) {
 // AllGather (tp > 1); otherwise the naive path must be at tp == 1.
 
 
-// One dequant-GEMM layer for mc rows: the GEMV (mc <= 16) or the A7 tensor-core GEMM (mc <= 256).
+// One dequant-GEMM layer for mc rows: the GEMV (mc <= 16) or the A7 tensor-core GEMM (mc <= 512:
+// k_dqgemm below 128 rows, the SS GEMMs from 128).
 cudaError_t run_layer(tpq_mlp* h, int layer, int mc, void* out, int64_t out_ld, cudaStream_t st) {
   const tpq::LayerDev& L = layer == 1 ? h->L1 : h->L2;
   if (mc <= tpq::kMaxM)
     return tpq::launch_gemv(L, layer == 1 ? h->xmap1 : h->xmap2, layer == 1 && L.gated ? &h->xmap1u : nullptr, mc, out,
                             out_ld, st);
-  if (mc >= 128 && !getenv("TPQ_NO_SS"))  // compute-bound: activations as the reused A operand
+  if (mc > kMmRows || (mc >= 128 && !getenv("TPQ_NO_SS")))  // compute-bound: activations as the reused A operand
     return tpq::launch_gemm_ss(L, layer == 1 ? h->ss1 : h->ss2, mc, h->sms, out, out_ld, st);
   const int v = mc <= 64 ? 0 : mc <= 128 ? 1 : 2;
   return tpq::launch_gemm(L, layer == 1 ? h->mm1[v] : h->mm2[v], 64 << v, mc, out, out_ld, st);
 }
 
-// Rows per pass of the forward: 16 (GEMV) while M <= 16, else up to 256 (A7).
+// Rows per pass of the forward: 16 (GEMV) while M <= 16, else up to 512 (A7).
 int64_t pass_rows(const tpq_mlp* h, int64_t M) { return M <= tpq::kMaxM ? tpq::kMaxM : h->rows; }
 
 int chunk_forward(tpq_mlp* h, const uint16_t* X, int mc, void* Y, cudaStream_t st, bool collective) {
@@ -908,7 +916,8 @@ int tpq_debug_trace(long long* out) { return tpq::trace_read(out) ? TPQ_ECUDA : 
 int tpq_mlp_run_step(tpq_mlp* h, int step, int64_t M, void* stream) {
   if (!h) return fail(TPQ_EINVAL, "NULL handle");
   if (h->device < 0) return fail(TPQ_ESTATE, "host-only handle (device=-1)");
-  if (M < 1 || M > std::min<int64_t>(tpq::kMaxM, h->M_max)) return fail(TPQ_EINVAL, "M=%lld not in [1, 16]", (long long)M);
+  const int64_t mmax = std::min<int64_t>(h->rows, h->M_max);  // one pass: 16 rows (GEMV) or 512 (A7)
+  if (M < 1 || M > mmax) return fail(TPQ_EINVAL, "M=%lld not in [1, %lld]", (long long)M, (long long)mmax);
   cudaStream_t st = (cudaStream_t)stream;
   TPQ_CUDA(cudaSetDevice(h->device));
   const int mc = (int)M;

@@ -110,9 +110,13 @@ __device__ __forceinline__ unsigned long long gtime() {
 __device__ long long g_tpq_trace[24][64][4];
 #define TPQ_EV(e, i) \
   if (blockIdx.x == 0 && a.NT * kTileCols < a.NKB * kUnitK && lane == 0 && (i) < 64) g_tpq_trace[warp][i][e] = clock64();
+// k-step event timeline of pair 0 of the layer-1 k_dqgemm_ss2 launch: [row][k-step < 64][event], globaltimer
+#define TPQ_EV2(row, e, i) \
+  if (blockIdx.x < 2 && a.NG * 256 < a.NKB * kUnitK && lane == 0 && (i) < 64) g_tpq_trace[row][i][e] = (long long)gtime();
 #else
 #define TPQ_CTA(e, v)
 #define TPQ_EV(e, i)
+#define TPQ_EV2(row, e, i)
 #endif
 // 1-D TMA bulk copy global -> shared, completion counted on `bar` in bytes.
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
@@ -1018,7 +1022,7 @@ struct TS {
 
 struct SsArgs {
   const uint8_t* packed;
-  int M;              // rows of this pass (<= 256: m-blocks of 128)
+  int M;              // rows of this pass (<= 512)
   int MB, NG, NKB, S; // m-blocks, column groups of BN, k-blocks, k-splits
   int items;          // NG * MB * S: item = (ng * MB + mb) * S + ks
   int grid;
@@ -1130,19 +1134,21 @@ __global__ void __launch_bounds__(TS<G, BN>::WARPS * 32, 1) k_dqgemm_ss(const Ss
     int n_it = 0;
     for (int it = blockIdx.x; it < a.items; it += a.grid, ++n_it) {
       const int db = n_it & 1, mb = (it / a.S) % a.MB, ng = it / (a.S * a.MB);
+      float cfv[BN / 32];  // column factors 2^(12 - E_n), lane = column within each 32: loaded under the MMAs
+#pragma unroll
+      for (int i = 0; i < BN / 32; ++i) cfv[i] = __ldg(a.colf + (int64_t)ng * BN + 32 * i + lane) * 2.44140625e-4f;
       mbar_wait(d_full + db, (uint32_t)((n_it >> 1) & 1));
       tc_fence_after();
       const int m = mb * C::BM + qw * 32 + lane;  // batch row of this thread (TMEM lane)
+#pragma unroll
       for (int c0 = 0; c0 < BN; c0 += 32) {
         uint32_t v[32];
         tmem_ld16(tmem + ((uint32_t)(qw * 32) << 16) + db * BN + c0, v);
         tmem_ld16(tmem + ((uint32_t)(qw * 32) << 16) + db * BN + c0 + 16, v + 16);
         tmem_wait_ld();
-        {
-          const float* cf = a.colf + (int64_t)ng * BN + c0;  // same 32 columns for every lane (broadcast)
 #pragma unroll
-          for (int q = 0; q < 32; ++q) v[q] = __float_as_uint(__uint_as_float(v[q]) * (__ldg(cf + q) * 2.44140625e-4f));
-        }
+        for (int q = 0; q < 32; ++q)
+          v[q] = __float_as_uint(__uint_as_float(v[q]) * __shfl_sync(0xffffffffu, cfv[c0 / 32], q));
         if (m < a.M) {
           if (a.S == 1) {
             __half* o = a.out + (int64_t)m * a.out_ld + (int64_t)ng * BN + c0;
@@ -1240,10 +1246,340 @@ __global__ void __launch_bounds__(TS<G, BN>::WARPS * 32, 1) k_dqgemm_ss(const Ss
   }
 }
 
+// ------------------------------------------------------------------ A7, CTA pair: k_dqgemm_ss2<G>
+// The SS GEMM of k_dqgemm_ss as a CTA pair (cta_group::2, cluster of 2 on one TPC): MMA M = 256 batch
+// rows (CTA r supplies rows [128 r, +128) of the activation tile), N = 256 weight columns (CTA r
+// dequantizes weight tile 2 ng + r = pair columns [128 r, +128)), and CTA r's TMEM receives D rows
+// [128 r, +128) x all 256 columns (layout verified by tools/probe_2cta.cu).  Per CTA and 128-row
+// k-step the shared memory moves 32 KB of activations (TMA), 32 KB of dequantized weights, 8.5 KB
+// of records and 64 KB of operand reads for 2 x the work of a 1-CTA 128 x 128 k-step.
+// Hand-offs: both CTAs' activation TMAs complete on the LEADER's a_full (cta_group::2 TMA, 64 KB
+// expected); each CTA's dequant warps arrive on the leader's b_full (remote arrive); the leader's MMA
+// warp issues and commits to both CTAs' k_done / d_full (multicast); each epilogue arrives on the
+// leader's d_empty.  Weight records and activations have their own producer warps, so the weight
+// ring runs ahead of the MMA by the HBM latency, not by the activation ring.
+// k-split partials leave through shared memory: each epilogue warp stages its 32 rows x 32 columns
+// (4 KB, 16-byte chunks XOR-swizzled by row: conflict-free) and one lane bulk-copies them to a
+// contiguous 4 KB of the partial buffer [grp][ks][c / 32][128 rows][32] (same swizzle; k_ss_fixup
+// swz = 1).  Per-lane row stores (16 B to 32 rows per instruction) took 9 us per item (trace).
+template <int G>
+struct TS2 {
+  static constexpr int DW = 8, EPI0 = 8, WPROD = 12, APROD = 13, MMAW = 14, WARPS = 15;
+  static constexpr int KG = kUnitK / G, GPH = G >= kUnitK / 2 ? 1 : (kUnitK / 2) / G;
+  static constexpr int UB = (int)unit_bytes_c(G), STAGE = (UB + 127) / 128 * 128;
+  static constexpr int BM = 128, BN = 128;        // per CTA: activation rows, weight columns
+  static constexpr int XT = BM * kUnitK * 2;      // A tile per k-step: 32 KB
+  static constexpr int WT = BN * kUnitK * 2;      // B half per k-step: 32 KB
+  static constexpr int NW = 4, NA = 3, NB = 2, KR = 6;
+  static constexpr int EST = 32 * 128;            // epilogue staging per warp: 32 rows x 32 fp32
+  static constexpr int AR = 0, BR = AR + NA * XT, WR = BR + NB * WT, ER = WR + NW * STAGE;
+  static constexpr int BARS = ER + 4 * EST;
+  static constexpr int SMEM = BARS + 8 * (2 * NW + NA + NB + KR + 4);
+  // pair MMA: D f32, A/B f16 K-major, N = 256, M = 256
+  static constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(256 >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+  static_assert(KR >= NA + NB, "done ring");
+};
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// shared::cluster address of the same variable in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa_shared(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+// Arrive on an mbarrier of a CTA of the cluster with the default (.release.cta) semantics: the data
+// it publishes is in shared memory read by the pair's tensor cores (after fence.proxy.async) or is
+// TMEM read back by tcgen05.ld (ordered by tcgen05.fence), not generic loads of another CTA, and
+// .release.cluster costs a MEMBAR.ALL.GPU + ERRBAR per arrive (ncu: the pair's top stall).
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void umma_commit2(uint64_t* bar) {  // arrive on the barrier in BOTH CTAs
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+// TMA tile into this CTA's shared memory, completion (bytes) signalled on the pair leader's barrier
+__device__ __forceinline__ void tma_load_3d_pair(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                                 uint32_t leader_bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3, %4}], [%5];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(leader_bar)
+      : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+template <int G>
+__global__ void __launch_bounds__(TS2<G>::WARPS * 32, 1) k_dqgemm_ss2(const SsArgs a, const __grid_constant__ CUtensorMap xmap) {
+  using C = TS2<G>;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BARS);
+  uint64_t* w_full = bars;              // [NW] raw weight record landed
+  uint64_t* w_empty = w_full + C::NW;   // [NW] dequant warps read it (DW)
+  uint64_t* a_full = w_empty + C::NW;   // [NA] leader: both CTAs' activation tiles landed (2 XT bytes)
+  uint64_t* b_full = a_full + C::NA;    // [NB] leader: both CTAs' dequantized weight halves written (2 DW)
+  uint64_t* k_done = b_full + C::NB;    // [KR] k-step t's MMAs completed (multicast commit)
+  uint64_t* d_full = k_done + C::KR;    // [2] item's accumulator final (multicast commit)
+  uint64_t* d_empty = d_full + 2;       // [2] leader: both epilogues read it (2 x 4)
+  __shared__ uint32_t s_tmem;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const int pair = blockIdx.x >> 1, npairs = a.grid >> 1;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::NW; ++s) {
+      mbar_init(w_full + s, 1);
+      mbar_init(w_empty + s, C::DW);
+    }
+    for (int s = 0; s < C::NA; ++s) mbar_init(a_full + s, 1);
+    for (int s = 0; s < C::NB; ++s) mbar_init(b_full + s, 2 * C::DW);
+    for (int s = 0; s < C::KR; ++s) mbar_init(k_done + s, 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(d_full + s, 1);
+      mbar_init(d_empty + s, 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == C::MMAW) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&s_tmem)) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync_all();  // barriers initialised and TMEM allocated in both CTAs before any remote arrive
+  tc_fence_after();
+  pdl_launch_dependents();
+  const uint32_t tmem = __shfl_sync(0xffffffffu, s_tmem, 0);
+  auto krange = [&](int ks, int& k0, int& k1) {
+    k0 = (int)((int64_t)ks * a.NKB / a.S);
+    k1 = (int)((int64_t)(ks + 1) * a.NKB / a.S);
+  };
+  // pair item it = (ng * MB + mb) * S + ks: MB counts 256-row blocks, ng 256-column groups
+
+  if (warp < C::DW) {
+    // ===================== dequant: this CTA's weight tile 2 ng + rank -> B half (SW128) ==========
+    const int jj = warp * 16 + (lane & 15), kh = lane >> 4, j = jj;
+    const __half2 k16 = __float2half2_rn(0.0625f);
+    const uint32_t bfull_leader = mapa_shared(b_full, 0);
+    int t = 0;
+    for (int it = pair; it < a.items; it += npairs) {
+      int k0, k1;
+      krange(it % a.S, k0, k1);
+      for (int kb = k0; kb < k1; ++kb, ++t) {
+        const int ws = t % C::NW, ks = t % C::NB;
+        if (warp == 0) { TPQ_EV2(rank, 0, t) }
+        mbar_wait(w_full + ws, (uint32_t)((t / C::NW) & 1));
+        if (warp == 0) { TPQ_EV2(rank, 1, t) }
+        const uint8_t* st = smem + C::WR + ws * C::STAGE;
+        const uint4 c0 = *reinterpret_cast<const uint4*>(st + code_block(kh * 2 + 0, j) * 16);
+        const uint4 c1 = *reinterpret_cast<const uint4*>(st + code_block(kh * 2 + 1, j) * 16);
+        const uint32_t wv[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+        __half2 zl[C::GPH], zh[C::GPH], sc[C::GPH];
+#pragma unroll
+        for (int g = 0; g < C::GPH; ++g) {
+          const int gi = (kh * (kUnitK / 2)) / G + g;
+          const uint8_t* meta = st + kUnitK * kTileCols / 2;
+          const int z = (meta[C::KG * 256 + gi * 64 + (j >> 1)] >> (4 * (j & 1))) & 0xF;
+          const __half sv = *reinterpret_cast<const __half*>(meta + gi * 256 + 2 * j);
+          zl[g] = __float2half2_rn((float)(1024 + z));
+          zh[g] = __float2half2_rn((float)(-64 - z));
+          sc[g] = __float2half2_rn(__half2float(sv) * 2.44140625e-4f);  // s' 2^-12
+        }
+        {
+          uint32_t dep = c0.x ^ c0.w ^ c1.x ^ c1.w;
+#pragma unroll
+          for (int g = 0; g < C::GPH; ++g) dep ^= h2u(zl[g]) ^ h2u(sc[g]);
+          release_loaded(w_empty + ws, dep, lane, a.ws, a.M);
+        }
+        // B slot free in BOTH CTAs: k-step t - NB's MMAs completed (multicast commit)
+        if (t >= C::NB) mbar_wait(k_done + (t - C::NB) % C::KR, (uint32_t)(((t - C::NB) / C::KR) & 1));
+        if (warp == 0) { TPQ_EV2(rank, 2, t) }
+        uint8_t* brow = smem + C::BR + ks * C::WT + kh * (C::BN * 128) + jj * 128;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+          const int g = C::GPH == 1 ? 0 : (w * 8) / G;
+          const uint32_t x = wv[w], x8 = x >> 8;
+          uint4 o;
+          o.x = h2u(__hmul2(__hsub2(u2h(lop3_and_or(x, 0x000F000Fu, 0x64006400u)), zl[g]), sc[g]));
+          o.y = h2u(__hmul2(__hfma2(u2h(lop3_and_or(x, 0x00F000F0u, 0x64006400u)), k16, zh[g]), sc[g]));
+          o.z = h2u(__hmul2(__hsub2(u2h(lop3_and_or(x8, 0x000F000Fu, 0x64006400u)), zl[g]), sc[g]));
+          o.w = h2u(__hmul2(__hfma2(u2h(lop3_and_or(x8, 0x00F000F0u, 0x64006400u)), k16, zh[g]), sc[g]));
+          *reinterpret_cast<uint4*>(brow + ((w ^ (jj & 7)) << 4)) = o;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor cores
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(bfull_leader + ks * 8);
+        if (warp == 0) { TPQ_EV2(rank, 3, t) }
+      }
+    }
+  } else if (warp < C::WPROD) {
+    // ===================== epilogue: this CTA's 128 rows x 256 columns of the item =================
+    const int qw = warp - C::EPI0;
+    const uint32_t dempty_leader = mapa_shared(d_empty, 0);
+    pdl_wait();
+    int n_it = 0;
+    for (int it = pair; it < a.items; it += npairs, ++n_it) {
+      const int db = n_it & 1, mb = (it / a.S) % a.MB, ng = it / (a.S * a.MB);
+      float cfv[8];  // column factors 2^(12 - E_n) of the item, lane = column within each 32: loaded under the MMAs
+#pragma unroll
+      for (int i = 0; i < 8; ++i) cfv[i] = __ldg(a.colf + (int64_t)ng * 256 + 32 * i + lane) * 2.44140625e-4f;
+      mbar_wait(d_full + db, (uint32_t)((n_it >> 1) & 1));
+      if (qw == 0) { TPQ_EV2(6 + rank, 0, n_it) }
+      tc_fence_after();
+      const int ml = qw * 32 + lane, m = mb * 256 + (int)rank * 128 + ml;  // batch row (TMEM lane)
+#pragma unroll
+      for (int c0 = 0; c0 < 256; c0 += 32) {
+        uint32_t v[32];
+        tmem_ld16(tmem + ((uint32_t)(qw * 32) << 16) + db * 256 + c0, v);
+        tmem_ld16(tmem + ((uint32_t)(qw * 32) << 16) + db * 256 + c0 + 16, v + 16);
+        tmem_wait_ld();
+#pragma unroll
+        for (int q = 0; q < 32; ++q)
+          v[q] = __float_as_uint(__uint_as_float(v[q]) * __shfl_sync(0xffffffffu, cfv[c0 / 32], q));
+        if (m < a.M) {
+          if (a.S == 1) {
+            __half* o = a.out + (int64_t)m * a.out_ld + (int64_t)ng * 256 + c0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              uint4 pk;
+              uint32_t* pw = reinterpret_cast<uint32_t*>(&pk);
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                pw[e] = h2u(__floats2half2_rn(__uint_as_float(v[8 * q + 2 * e]), __uint_as_float(v[8 * q + 2 * e + 1])));
+              *reinterpret_cast<uint4*>(o + 8 * q) = pk;
+            }
+          }
+        }
+        if (a.S > 1) {
+          // partial block of group 2 (ng MB + mb) + rank, split ks, column chunk c0 / 32: this warp's 4 KB
+          const int grp = ng * (2 * a.MB) + 2 * mb + (int)rank;
+          float* o = a.ws + ((((size_t)grp * a.S + it % a.S) * 8 + c0 / 32) * 128 + qw * 32) * 32;
+          uint8_t* stg = smem + C::ER + qw * C::EST;
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // previous chunk read out
+          __syncwarp();
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            *reinterpret_cast<uint4*>(stg + lane * 128 + ((q ^ (lane & 7)) << 4)) =
+                make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) {
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(o), "r"(smem_u32(stg)),
+                         "n"(C::EST)
+                         : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(dempty_leader + db * 8);
+      if (qw == 0) { TPQ_EV2(6 + rank, 1, n_it) }
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // partials written before exit
+  } else if (warp == C::WPROD) {
+    // ===================== weight producer: this CTA's records, NW k-steps ahead ====================
+    const uint64_t pw = policy_evict_first();
+    int t = 0;
+    for (int it = pair; it < a.items; it += npairs) {
+      const int ng = it / (a.S * a.MB);
+      int k0, k1;
+      krange(it % a.S, k0, k1);
+      for (int kb = k0; kb < k1; ++kb, ++t) {
+        const int ws = t % C::NW;
+        TPQ_EV2(4 + rank, 0, t)
+        if (t >= C::NW) mbar_wait(w_empty + ws, (uint32_t)(((t / C::NW) & 1) ^ 1));
+        TPQ_EV2(4 + rank, 1, t)
+        if (elect_one()) {
+          mbar_arrive_expect_tx(w_full + ws, C::UB);
+          bulk_g2s(smem + C::WR + ws * C::STAGE, a.packed + ((int64_t)(ng * 2 + (int)rank) * a.NKB + kb) * C::UB, C::UB,
+                   w_full + ws, pw);
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp == C::APROD) {
+    // ===================== activation producer: this CTA's 128 rows, onto the leader's a_full =======
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&xmap)) : "memory");
+    const uint32_t afull_leader = mapa_shared(a_full, 0);
+    pdl_wait();  // activations come from the previous kernel in the stream
+    int t = 0;
+    for (int it = pair; it < a.items; it += npairs) {
+      const int mb = (it / a.S) % a.MB;
+      int k0, k1;
+      krange(it % a.S, k0, k1);
+      for (int kb = k0; kb < k1; ++kb, ++t) {
+        const int sa = t % C::NA;
+        TPQ_EV2(2 + rank, 0, t)
+        if (t >= C::NA) mbar_wait(k_done + (t - C::NA) % C::KR, (uint32_t)(((t - C::NA) / C::KR) & 1));  // A slot free
+        TPQ_EV2(2 + rank, 1, t)
+        if (elect_one()) {
+          if (rank == 0) mbar_arrive_expect_tx(a_full + sa, 2 * C::XT);
+          tma_load_3d_pair(smem + C::AR + sa * C::XT, &xmap, 0, mb * 256 + (int)rank * C::BM, 2 * kb,
+                           afull_leader + sa * 8);
+        }
+        __syncwarp();
+      }
+    }
+  } else if (rank == 0) {
+    // ===================== MMA issuer (leader) =====================
+    int t = 0, n_it = 0;
+    for (int it = pair; it < a.items; it += npairs, ++n_it) {
+      const int db = n_it & 1;
+      int k0, k1;
+      krange(it % a.S, k0, k1);
+      mbar_wait(d_empty + db, (uint32_t)(((n_it >> 1) & 1) ^ 1));
+      for (int kb = k0; kb < k1; ++kb, ++t) {
+        const int sa = t % C::NA, sb = t % C::NB;
+        TPQ_EV2(8, 0, t)
+        mbar_wait(a_full + sa, (uint32_t)((t / C::NA) & 1));
+        TPQ_EV2(8, 1, t)
+        mbar_wait(b_full + sb, (uint32_t)((t / C::NB) & 1));
+        TPQ_EV2(8, 2, t)
+        tc_fence_after();
+        const uint32_t abase = smem_u32(smem + C::AR + sa * C::XT), bbase = smem_u32(smem + C::BR + sb * C::WT);
+        uint64_t ad[8], bd[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {  // k16 block q: k-half q / 4, 32-byte step within the 128-byte row
+          ad[q] = bdesc_sw128(abase + (q / 4) * (C::BM * 128) + (q % 4) * 32);
+          bd[q] = bdesc_sw128(bbase + (q / 4) * (C::BN * 128) + (q % 4) * 32);
+        }
+        if (elect_one()) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem + db * 256),
+                "l"(ad[q]), "l"(bd[q]), "r"(C::IDESC), "r"((kb == k0 && q == 0) ? 0u : 1u)
+                : "memory");
+          umma_commit2(k_done + t % C::KR);
+          if (kb == k1 - 1) umma_commit2(d_full + db);
+        }
+        __syncwarp();
+        TPQ_EV2(8, 3, t)
+      }
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();  // both CTAs done with the pair's TMEM and barriers
+  if (warp == C::MMAW) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  }
+}
+
 // k-split fix-up of k_dqgemm_ss: out[m][ng BN + c] = sum over ks of the item's partial (split order).
 // Block (ng * MB + mb, r): rows mb 128 + 4 r + warp, thread = 4 consecutive columns, bn / 128 passes.
+// swz = 1 (k_dqgemm_ss2): partials in [grp][ks][c / 32][128 rows][32], 16-byte chunks XOR-swizzled by row.
 __global__ void k_ss_fixup(const float* __restrict__ ws, int M, int MB, int S, int bn, __half* __restrict__ out,
-                           int64_t out_ld) {
+                           int64_t out_ld, int swz) {
   pdl_launch_dependents();
   pdl_wait();
   const int grp = blockIdx.x, mb = grp % MB, ng = grp / MB;
@@ -1251,8 +1587,9 @@ __global__ void k_ss_fixup(const float* __restrict__ ws, int M, int MB, int S, i
   if (m >= M) return;
   for (int c = (threadIdx.x & 31) * 4; c < bn; c += 128) {
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    const size_t off = swz ? ((size_t)(c >> 5) * 128 + ml) * 32 + ((((c & 31) >> 2) ^ (ml & 7)) << 2) : (size_t)ml * bn + c;
     for (int ks = 0; ks < S; ++ks) {
-      const float4 v = __ldcg(reinterpret_cast<const float4*>(ws + (((size_t)grp * S + ks) * 128 + ml) * bn + c));
+      const float4 v = __ldcg(reinterpret_cast<const float4*>(ws + ((size_t)grp * S + ks) * 128 * bn + off));
       acc.x += v.x;
       acc.y += v.y;
       acc.z += v.z;
@@ -1278,6 +1615,26 @@ cudaError_t launch_pdl(Kern k, dim3 grid, dim3 block, size_t smem, cudaStream_t 
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, args...);
+}
+
+// launch_pdl for a kernel run as clusters of `cx` CTAs along x
+template <class Kern, class... Args>
+cudaError_t launch_pdl_cluster(Kern k, int cx, dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = (unsigned)cx;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
   return cudaLaunchKernelEx(&cfg, k, args...);
 }
 
@@ -1459,9 +1816,12 @@ __global__ void __launch_bounds__(128, 16) k_split_fixup(const float* __restrict
 // 32-byte sector per 2-byte element).  dst[m][k] = src[m ld + idx[k]].
 // At most 32 registers x 128 threads (4096) and one block per SM: the block fits beside a GEMV CTA
 // (96 x 640 registers), so the GEMV launched after it can become resident and stream weights at once.
-__global__ void __launch_bounds__(128, 16) k_gather_rows(const __half* __restrict__ src, int64_t ld,
-                                                         const int32_t* __restrict__ idx, int64_t K,
-                                                         __half* __restrict__ dst) {
+// NT = 512 for passes of more than 16 rows (one block per row): each thread then has <= 2 chunks of
+// a K = 8192 row instead of 8 sequential index round trips (M = 256: 6.3 us at 128 threads).
+template <int NT>
+__global__ void __launch_bounds__(NT, NT == 128 ? 16 : 4) k_gather_rows(const __half* __restrict__ src, int64_t ld,
+                                                                      const int32_t* __restrict__ idx, int64_t K,
+                                                                      __half* __restrict__ dst) {
   extern __shared__ __align__(16) uint8_t srow_raw[];
   __half* srow = reinterpret_cast<__half*>(srow_raw);
   pdl_launch_dependents();
@@ -1572,8 +1932,15 @@ bool prepare_ss_t() {
          cudaSuccess;
 }
 template <int G>
+bool prepare_ss2_t() {
+  static_assert(TS2<G>::SMEM + 1024 <= 227 * 1024, "SS pair GEMM smem (+ static) over the per-CTA limit");
+  return cudaFuncSetAttribute(k_dqgemm_ss2<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, TS2<G>::SMEM) ==
+         cudaSuccess;
+}
+template <int G>
 bool prepare_mm_g() {
-  bool ok = prepare_mm_t<G, 64>() && prepare_mm_t<G, 128>() && prepare_mm_t<G, 256>() && prepare_ss_t<G, 128>();
+  bool ok = prepare_mm_t<G, 64>() && prepare_mm_t<G, 128>() && prepare_mm_t<G, 256>() && prepare_ss_t<G, 128>() &&
+            prepare_ss2_t<G>();
   if constexpr (G == 128) ok = ok && prepare_ss_t<G, 256>();
   return ok;
 }
@@ -1590,7 +1957,7 @@ bool max_carveout(Kern k) {
 template <int G>
 bool carveout_g() {
   return max_carveout(k_dqgemv<G, false>) && max_carveout(k_dqgemv<G, true>) && max_carveout(k_dqgemm<G, 64>) && max_carveout(k_dqgemm<G, 128>) &&
-         max_carveout(k_dqgemm<G, 256>) && max_carveout(k_dqgemm_ss<G, 128>);
+         max_carveout(k_dqgemm<G, 256>) && max_carveout(k_dqgemm_ss<G, 128>) && max_carveout(k_dqgemm_ss2<G>);
 }
 
 template <int G, bool GT>
@@ -1609,7 +1976,7 @@ bool prepare_gemv() {
 }
 
 bool gemv_prepare(int G) {
-  if (!(max_carveout(k_gather_rm) && max_carveout(k_gather_rows) && max_carveout(k_gather_ag) && max_carveout(k_split_fixup) && max_carveout(k_mm_fixup) && max_carveout(k_gemv_fixup) &&
+  if (!(max_carveout(k_gather_rm) && max_carveout(k_gather_rows<128>) && max_carveout(k_gather_rows<512>) && max_carveout(k_gather_ag) && max_carveout(k_split_fixup) && max_carveout(k_mm_fixup) && max_carveout(k_gemv_fixup) &&
         max_carveout(k_ss_fixup) && max_carveout(k_sum_partials) && max_carveout(k_dqgemv<0, false>)))
     return false;
   if (!prepare_gemv<0, false>()) return false;  // unordered-g_idx layers (any G)
@@ -1713,9 +2080,38 @@ cudaError_t launch_ss_t(const SsArgs& a, const CUtensorMap& xmap, cudaStream_t s
   return launch_pdl(k_dqgemm_ss<G, BN>, dim3(a.grid), dim3(TS<G, BN>::WARPS * 32), TS<G, BN>::SMEM, st, a, xmap);
 }
 
+// CTA-pair SS GEMM: pair items (256-column group, 256-row block, k-split); k-split partials in the
+// k_ss_fixup swizzled layout with 128-row blocks (group = 2 (ng MB + mb) + rank) and bn = 256.
+cudaError_t launch_gemm_ss2(const LayerDev& L, const CUtensorMap& xmap, int M, int sms, void* out, int64_t out_ld,
+                            cudaStream_t st) {
+  SsArgs a;
+  a.packed = L.packed;
+  a.M = M;
+  a.MB = (M + 255) / 256;
+  a.NG = L.NT / 2;
+  a.NKB = L.NKB;
+  const int S = L.ws_ss ? ss_splits(a.NG, L.NKB, a.MB, sms / 2) : 1;
+  a.S = S;
+  a.items = a.NG * a.MB * S;
+  a.grid = 2 * std::min(a.items, sms / 2);
+  a.out = reinterpret_cast<__half*>(out);
+  a.out_ld = out_ld;
+  a.ws = L.ws_ss;
+  a.colf = L.colf;
+  cudaError_t e = cudaErrorInvalidValue;
+  const dim3 blk(TS2<128>::WARPS * 32);  // same warp layout for every G
+  if (L.G == 128) e = launch_pdl_cluster(k_dqgemm_ss2<128>, 2, dim3(a.grid), blk, TS2<128>::SMEM, st, a, xmap);
+  else if (L.G == 64) e = launch_pdl_cluster(k_dqgemm_ss2<64>, 2, dim3(a.grid), blk, TS2<64>::SMEM, st, a, xmap);
+  else if (L.G == 32) e = launch_pdl_cluster(k_dqgemm_ss2<32>, 2, dim3(a.grid), blk, TS2<32>::SMEM, st, a, xmap);
+  if (e != cudaSuccess || S == 1) return e;
+  return launch_pdl(k_ss_fixup, dim3((unsigned)(2 * a.MB * a.NG), 32), dim3(128), 0, st, (const float*)L.ws_ss, M,
+                    2 * a.MB, S, 256, reinterpret_cast<__half*>(out), out_ld, 1);
+}
+
 cudaError_t launch_gemm_ss(const LayerDev& L, const CUtensorMap& xmap, int M, int sms, void* out, int64_t out_ld,
                            cudaStream_t st) {
-  if (M < 1 || M > 256) return cudaErrorInvalidValue;
+  if (M < 1 || M > 512) return cudaErrorInvalidValue;
+  if (ss_pair(L.NT, M)) return launch_gemm_ss2(L, xmap, M, sms, out, out_ld, st);
   const int bn = ss_bn(L.NT, L.G);
   SsArgs a;
   a.packed = L.packed;
@@ -1742,7 +2138,7 @@ cudaError_t launch_gemm_ss(const LayerDev& L, const CUtensorMap& xmap, int M, in
   }
   if (e != cudaSuccess || S == 1) return e;
   return launch_pdl(k_ss_fixup, dim3((unsigned)base, 32), dim3(128), 0, st, (const float*)L.ws_ss, M, a.MB, S, bn,
-                    reinterpret_cast<__half*>(out), out_ld);
+                    reinterpret_cast<__half*>(out), out_ld, 0);
 }
 
 cudaError_t launch_gather_rowmajor(const void* src, int64_t ld, const int32_t* idx, int mode, int64_t nn, int M,
@@ -1750,9 +2146,14 @@ cudaError_t launch_gather_rowmajor(const void* src, int64_t ld, const int32_t* i
   // column gather of rows that fit in shared memory, 16-byte aligned rows: stage each row
   if (mode == GATHER_COLS && idx && K % 8 == 0 && K * 2 <= 48 * 1024 && ld % 8 == 0 &&
       reinterpret_cast<uintptr_t>(src) % 16 == 0 && reinterpret_cast<uintptr_t>(idx) % 16 == 0)
-    return launch_pdl(k_gather_rows, dim3((unsigned)M, (unsigned)std::max(1, std::min(16, (co_res() ? 148 : 256) / M))),
-                      dim3(128), (size_t)K * 2, st, reinterpret_cast<const __half*>(src), ld, idx, K,
-                      reinterpret_cast<__half*>(dst));
+  {
+    const dim3 grid((unsigned)M, (unsigned)std::max(1, std::min(16, (co_res() ? 148 : 256) / M)));
+    if (M > kMaxM)
+      return launch_pdl(k_gather_rows<512>, grid, dim3(512), (size_t)K * 2, st, reinterpret_cast<const __half*>(src), ld,
+                        idx, K, reinterpret_cast<__half*>(dst));
+    return launch_pdl(k_gather_rows<128>, grid, dim3(128), (size_t)K * 2, st, reinterpret_cast<const __half*>(src), ld,
+                      idx, K, reinterpret_cast<__half*>(dst));
+  }
   const int64_t total = (int64_t)M * K;
   return launch_pdl(k_gather_rm, dim3(grid_for(total, 256)), dim3(256), 0, st, reinterpret_cast<const __half*>(src),
                     ld, idx, mode, nn, M, K, reinterpret_cast<__half*>(dst));

@@ -356,6 +356,31 @@ def test_a7_ss_wide_tiles(G, M):
     h.close()
 
 
+@pytest.mark.parametrize("G", [32, 64, 128])
+@pytest.mark.parametrize("M", [129, 256, 384])
+def test_a7_cta_pair(G, M):
+    """Passes of more than 128 rows over an even tile count run the CTA-pair SS GEMM (cta_group::2,
+    256 x 256 per pair): the 129-row pass leaves the second CTA's rows padding, 384 = a full pair
+    pass + a 128-row pass on the 1-CTA kernel; NKB = 9 gives ragged k-splits."""
+    p = synth.make_problem(1152, 2304, 512, G, M, seed=500 + G + M)
+    P1, P2 = _prep(p)
+    L1, L2 = _olayers(p)
+    Y1r, Y2r = O.dense_mlp(p.X, O.dequantize(L1), O.dequantize(L2))
+    h = tpq.TpMlp(p.w1, p.w2, P1, P2, M_max=512)
+    X = _dev(p.X)
+    Y = _empty(M, p.N2)
+    h.forward(X, M, Y)
+    _assert_close(_np(Y), Y2r, "Y2")
+    Y1 = _empty(M, p.N1)
+    h.layer1(X, M, Y1)
+    P2o, _ = O.alg1_reorder(L2.g)
+    _assert_close(_np(Y1), Y1r[:, P2o], "Y1 (P2 order)")
+    Yb = _empty(M, p.N2)
+    h.forward(X, M, Yb)
+    assert torch.equal(Y, Yb), "pair GEMM not deterministic"
+    h.close()
+
+
 def _check_elementwise(y, ref, absref, tol, what):
     """|y - ref| <= tol * absref element by element, absref = |inputs| . |W| (the worst-case
     rounding bound of a dot product: each term carries its own relative error, so a column made of
