@@ -120,7 +120,8 @@ cudaError_t launch_gemm_ss(const LayerDev& L, const CUtensorMap& xmap, int M, in
                            cudaStream_t st);
 
 // Row-major gather dst[m*K + k] = v(m, k):
-//   GATHER_COLS:      v(m, k) = src[m*ld + (idx ? idx[k] : k)]
+//   GATHER_COLS:      v(m, k) = src[m*ld + (idx ? idx[k] : k)]; idx holds K int32 indices followed by
+//                     the same K as uint16 (read by the staged-row kernel, K <= 24576 there)
 //   GATHER_ALLGATHER: c = idx[k]; v(m, k) = src[(c / nn) * M * nn + m * nn + c % nn]
 cudaError_t launch_gather_rowmajor(const void* src, int64_t ld, const int32_t* idx, int mode, int64_t nn, int M,
                                    int64_t K, void* dst, cudaStream_t st);

@@ -240,6 +240,16 @@ inline uint32_t nib(uint32_t w, int i) { return (w >> (4 * i)) & 0xFu; }
 constexpr int kGemmRows = 512;  // A7: activation rows per GEMM pass (the SS GEMMs take up to 512)
 constexpr int kMmRows = 256;    // A7 below 128 rows: k_dqgemm's largest N
 
+// A column permutation on the device as the gathers read it: K int32 indices, then the same K as
+// uint16 (the staged-row gather keeps 8 of them per 16-byte register quad; K <= 24576 there).
+cudaError_t upload_perm(int32_t* d, const int32_t* P, int64_t K) {
+  std::vector<uint16_t> p16((size_t)K);
+  for (int64_t k = 0; k < K; ++k) p16[(size_t)k] = (uint16_t)P[k];
+  cudaError_t e = cudaMemcpy(d, P, (size_t)K * 4, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return e;
+  return cudaMemcpy(d + K, p16.data(), (size_t)K * 2, cudaMemcpyHostToDevice);
+}
+
 struct tpq_comm {
   ncclComm_t comm;
   int tp, rank, device;
@@ -592,22 +602,22 @@ int shard_impl(const gptq_layer* w1, const gptq_layer* wu, const gptq_layer* w2,
         };
         const size_t ws1s = ss_ws(h->L1), ws2s = ss_ws(h->L2);
         if ((r = A(&h->d_w1, h->pk1.size())) || (r = A(&h->d_w2, h->pk2.size())) ||
-            (r = A((void**)&h->d_P1, K1 * 4)) || (r = A((void**)&h->d_gcols, n * 8)) || (r = A(&h->d_x1, (size_t)h->rows * K1 * 2)) ||
+            (r = A((void**)&h->d_P1, K1 * 6)) || (r = A((void**)&h->d_gcols, n * 8)) || (r = A(&h->d_x1, (size_t)h->rows * K1 * 2)) ||
             (r = A(&h->d_y1, (size_t)h->rows * n * 2)) || (r = A(&h->d_buf, (size_t)tp * h->rows * n * 2)) ||
             (r = A(&h->d_xin, (size_t)M_max * K1 * 2)) || (r = A(&h->d_yout, (size_t)M_max * N2 * 2)) ||
             (r = A((void**)&h->d_ws, (ws1 + ws2 + wm1 + wm2 + ws1s + ws2s) * 4)) ||
             (r = A((void**)&h->d_colf, (size_t)(n + N2) * 4)) ||
             (r = A(&h->d_tab, (h->tab1.size() + h->tab2.size()) * 4)) ||
-            (gated && (r = A((void**)&h->d_P1u, K1 * 4))) || (gated && (r = A(&h->d_x1u, (size_t)h->rows * K1 * 2))))
+            (gated && (r = A((void**)&h->d_P1u, K1 * 6))) || (gated && (r = A(&h->d_x1u, (size_t)h->rows * K1 * 2))))
           return r;
         if (gated) {
-          TPQ_CUDA(cudaMemcpy(h->d_P1u, P1u, K1 * 4, cudaMemcpyHostToDevice));
+          TPQ_CUDA(upload_perm(h->d_P1u, P1u, K1));
           if (!tpq::make_xmap(&h->xmap1u, h->d_x1u, K1, tpq::kNPad))
             return fail(TPQ_ECUDA, "cuTensorMapEncodeTiled failed for the up_proj activation buffer");
         }
         TPQ_CUDA(cudaMemcpy(h->d_w1, h->pk1.data(), h->pk1.size(), cudaMemcpyHostToDevice));
         TPQ_CUDA(cudaMemcpy(h->d_w2, h->pk2.data(), h->pk2.size(), cudaMemcpyHostToDevice));
-        TPQ_CUDA(cudaMemcpy(h->d_P1, P1, K1 * 4, cudaMemcpyHostToDevice));
+        TPQ_CUDA(upload_perm(h->d_P1, P1, K1));
         {
           std::vector<float> cf((size_t)(n + N2));
           for (int64_t j = 0; j < n; ++j) cf[(size_t)j] = std::ldexp(1.f, 24 - h->E1[(size_t)j]);

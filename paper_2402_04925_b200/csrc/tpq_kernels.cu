@@ -110,9 +110,10 @@ __device__ __forceinline__ unsigned long long gtime() {
 __device__ long long g_tpq_trace[24][64][4];
 #define TPQ_EV(e, i) \
   if (blockIdx.x == 0 && a.NT * kTileCols < a.NKB * kUnitK && lane == 0 && (i) < 64) g_tpq_trace[warp][i][e] = clock64();
-// k-step event timeline of pair 0 of the layer-1 k_dqgemm_ss2 launch: [row][k-step < 64][event], globaltimer
+// k-step event timeline of pair 0 of a k_dqgemm_ss2 launch: [row (+ 12 when N > K)][k-step < 64][event], clock64
+// (SM-local: compare times within one CTA's rows only; globaltimer reads cost ~100 ns each)
 #define TPQ_EV2(row, e, i) \
-  if (blockIdx.x < 2 && a.NG * 256 < a.NKB * kUnitK && lane == 0 && (i) < 64) g_tpq_trace[row][i][e] = (long long)gtime();
+  if (blockIdx.x < 2 && lane == 0 && (i) < 64) g_tpq_trace[(row) + (a.NG * 256 > a.NKB * kUnitK ? 12 : 0)][i][e] = clock64();
 #else
 #define TPQ_CTA(e, v)
 #define TPQ_EV(e, i)
@@ -1264,16 +1265,17 @@ __global__ void __launch_bounds__(TS<G, BN>::WARPS * 32, 1) k_dqgemm_ss(const Ss
 // swz = 1).  Per-lane row stores (16 B to 32 rows per instruction) took 9 us per item (trace).
 template <int G>
 struct TS2 {
-  static constexpr int DW = 8, EPI0 = 8, WPROD = 12, APROD = 13, MMAW = 14, WARPS = 15;
+  static constexpr int DW = 8, EPI0 = 8, EW = 8, WPROD = EPI0 + EW, APROD = WPROD + 1, MMAW = APROD + 1, WARPS = MMAW + 1;
   static constexpr int KG = kUnitK / G, GPH = G >= kUnitK / 2 ? 1 : (kUnitK / 2) / G;
   static constexpr int UB = (int)unit_bytes_c(G), STAGE = (UB + 127) / 128 * 128;
   static constexpr int BM = 128, BN = 128;        // per CTA: activation rows, weight columns
   static constexpr int XT = BM * kUnitK * 2;      // A tile per k-step: 32 KB
   static constexpr int WT = BN * kUnitK * 2;      // B half per k-step: 32 KB
-  static constexpr int NW = 4, NA = 3, NB = 2, KR = 6;
+  static constexpr int NW = 3, NA = 3, NB = 2, KR = 6;
   static constexpr int EST = 32 * 128;            // epilogue staging per warp: 32 rows x 32 fp32
   static constexpr int AR = 0, BR = AR + NA * XT, WR = BR + NB * WT, ER = WR + NW * STAGE;
-  static constexpr int BARS = ER + 4 * EST;
+  static constexpr int CF = ER + EW * EST;        // per epilogue warp: its item's 128 column factors
+  static constexpr int BARS = CF + EW * 512;
   static constexpr int SMEM = BARS + 8 * (2 * NW + NA + NB + KR + 4);
   // pair MMA: D f32, A/B f16 K-major, N = 256, M = 256
   static constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(256 >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
@@ -1329,7 +1331,7 @@ __global__ void __launch_bounds__(TS2<G>::WARPS * 32, 1) k_dqgemm_ss2(const SsAr
   uint64_t* b_full = a_full + C::NA;    // [NB] leader: both CTAs' dequantized weight halves written (2 DW)
   uint64_t* k_done = b_full + C::NB;    // [KR] k-step t's MMAs completed (multicast commit)
   uint64_t* d_full = k_done + C::KR;    // [2] item's accumulator final (multicast commit)
-  uint64_t* d_empty = d_full + 2;       // [2] leader: both epilogues read it (2 x 4)
+  uint64_t* d_empty = d_full + 2;       // [2] leader: both epilogues read it (2 x EW)
   __shared__ uint32_t s_tmem;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
@@ -1344,7 +1346,7 @@ __global__ void __launch_bounds__(TS2<G>::WARPS * 32, 1) k_dqgemm_ss2(const SsAr
     for (int s = 0; s < C::KR; ++s) mbar_init(k_done + s, 1);
     for (int s = 0; s < 2; ++s) {
       mbar_init(d_full + s, 1);
-      mbar_init(d_empty + s, 8);
+      mbar_init(d_empty + s, 2 * C::EW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -1421,49 +1423,74 @@ __global__ void __launch_bounds__(TS2<G>::WARPS * 32, 1) k_dqgemm_ss2(const SsAr
     }
   } else if (warp < C::WPROD) {
     // ===================== epilogue: this CTA's 128 rows x 256 columns of the item =================
-    const int qw = warp - C::EPI0;
+    // 8 warps: TMEM lane quarter qw (32 batch rows) x column half hc (4 chunks of 32 columns).  Each
+    // chunk is staged in this warp's 4 KB of shared memory: fp32 partials (S > 1) leave by one 4 KB
+    // bulk copy, fp16 results (S = 1) by row-contiguous 64-byte stores (8 rows per instruction).
+    const int ew = warp - C::EPI0, qw = ew & 3, hc = ew >> 2;
     const uint32_t dempty_leader = mapa_shared(d_empty, 0);
+    uint8_t* stg = smem + C::ER + ew * C::EST;
+    float* cfs = reinterpret_cast<float*>(smem + C::CF + ew * 512);
     pdl_wait();
     int n_it = 0;
     for (int it = pair; it < a.items; it += npairs, ++n_it) {
       const int db = n_it & 1, mb = (it / a.S) % a.MB, ng = it / (a.S * a.MB);
-      float cfv[8];  // column factors 2^(12 - E_n) of the item, lane = column within each 32: loaded under the MMAs
+      // column factors 2^(12 - E_n) of this warp's 128 columns, staged under the MMAs (read back as
+      // broadcast float4: shuffles serialised on the 96-register budget)
+      float cfv[4];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) cfv[i] = __ldg(a.colf + (int64_t)ng * 256 + 32 * i + lane) * 2.44140625e-4f;
+      for (int i = 0; i < 4; ++i) cfv[i] = __ldg(a.colf + (int64_t)ng * 256 + 128 * hc + 32 * i + lane) * 2.44140625e-4f;
+      __syncwarp();  // previous item's factors read
+#pragma unroll
+      for (int i = 0; i < 4; ++i) cfs[32 * i + lane] = cfv[i];
+      __syncwarp();
       mbar_wait(d_full + db, (uint32_t)((n_it >> 1) & 1));
-      if (qw == 0) { TPQ_EV2(6 + rank, 0, n_it) }
+      if (ew == 0) { TPQ_EV2(6 + rank, 0, n_it) }
       tc_fence_after();
-      const int ml = qw * 32 + lane, m = mb * 256 + (int)rank * 128 + ml;  // batch row (TMEM lane)
+      const int mrow0 = mb * 256 + (int)rank * 128 + qw * 32;  // batch row of lane 0 (TMEM lane qw 32)
 #pragma unroll
-      for (int c0 = 0; c0 < 256; c0 += 32) {
+      for (int i = 0; i < 4; ++i) {
+        const int c0 = 128 * hc + 32 * i;
         uint32_t v[32];
         tmem_ld16(tmem + ((uint32_t)(qw * 32) << 16) + db * 256 + c0, v);
         tmem_ld16(tmem + ((uint32_t)(qw * 32) << 16) + db * 256 + c0 + 16, v + 16);
         tmem_wait_ld();
+        if (ew == 0) { TPQ_EV2(9 + rank, 0, i + 8 * n_it) }
 #pragma unroll
-        for (int q = 0; q < 32; ++q)
-          v[q] = __float_as_uint(__uint_as_float(v[q]) * __shfl_sync(0xffffffffu, cfv[c0 / 32], q));
-        if (m < a.M) {
-          if (a.S == 1) {
-            __half* o = a.out + (int64_t)m * a.out_ld + (int64_t)ng * 256 + c0;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              uint4 pk;
-              uint32_t* pw = reinterpret_cast<uint32_t*>(&pk);
-#pragma unroll
-              for (int e = 0; e < 4; ++e)
-                pw[e] = h2u(__floats2half2_rn(__uint_as_float(v[8 * q + 2 * e]), __uint_as_float(v[8 * q + 2 * e + 1])));
-              *reinterpret_cast<uint4*>(o + 8 * q) = pk;
-            }
-          }
+        for (int q = 0; q < 8; ++q) {
+          const float4 f = *reinterpret_cast<const float4*>(cfs + 32 * i + 4 * q);
+          v[4 * q] = __float_as_uint(__uint_as_float(v[4 * q]) * f.x);
+          v[4 * q + 1] = __float_as_uint(__uint_as_float(v[4 * q + 1]) * f.y);
+          v[4 * q + 2] = __float_as_uint(__uint_as_float(v[4 * q + 2]) * f.z);
+          v[4 * q + 3] = __float_as_uint(__uint_as_float(v[4 * q + 3]) * f.w);
         }
-        if (a.S > 1) {
+        if (ew == 0) { TPQ_EV2(9 + rank, 1, i + 8 * n_it) }
+        if (a.S == 1) {
+          // fp16 [32 rows][32 cols] = 64 B per row, 16-byte chunks swizzled by (row >> 1) & 3
+          __syncwarp();  // previous chunk's rows read back
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            uint4 pk;
+            uint32_t* pw = reinterpret_cast<uint32_t*>(&pk);
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              pw[e] = h2u(__floats2half2_rn(__uint_as_float(v[8 * q + 2 * e]), __uint_as_float(v[8 * q + 2 * e + 1])));
+            *reinterpret_cast<uint4*>(stg + lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4)) = pk;
+          }
+          __syncwarp();
+          if (ew == 0) { TPQ_EV2(9 + rank, 2, i + 8 * n_it) }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int r = 8 * j + (lane >> 2), q = lane & 3, m = mrow0 + r;
+            const uint4 pk = *reinterpret_cast<const uint4*>(stg + r * 64 + ((q ^ ((r >> 1) & 3)) << 4));
+            if (m < a.M) *reinterpret_cast<uint4*>(a.out + (int64_t)m * a.out_ld + (int64_t)ng * 256 + c0 + 8 * q) = pk;
+          }
+        } else {
           // partial block of group 2 (ng MB + mb) + rank, split ks, column chunk c0 / 32: this warp's 4 KB
           const int grp = ng * (2 * a.MB) + 2 * mb + (int)rank;
           float* o = a.ws + ((((size_t)grp * a.S + it % a.S) * 8 + c0 / 32) * 128 + qw * 32) * 32;
-          uint8_t* stg = smem + C::ER + qw * C::EST;
           if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // previous chunk read out
           __syncwarp();
+          if (ew == 0) { TPQ_EV2(9 + rank, 2, i + 8 * n_it) }
 #pragma unroll
           for (int q = 0; q < 8; ++q)
             *reinterpret_cast<uint4*>(stg + lane * 128 + ((q ^ (lane & 7)) << 4)) =
@@ -1477,11 +1504,12 @@ __global__ void __launch_bounds__(TS2<G>::WARPS * 32, 1) k_dqgemm_ss2(const SsAr
             asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           }
         }
+        if (ew == 0) { TPQ_EV2(9 + rank, 3, i + 8 * n_it) }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(dempty_leader + db * 8);
-      if (qw == 0) { TPQ_EV2(6 + rank, 1, n_it) }
+      if (ew == 0) { TPQ_EV2(6 + rank, 1, n_it) }
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // partials written before exit
   } else if (warp == C::WPROD) {
@@ -1817,40 +1845,48 @@ __global__ void __launch_bounds__(128, 16) k_split_fixup(const float* __restrict
 // At most 32 registers x 128 threads (4096) and one block per SM: the block fits beside a GEMV CTA
 // (96 x 640 registers), so the GEMV launched after it can become resident and stream weights at once.
 // NT = 512 for passes of more than 16 rows (one block per row): each thread then has <= 2 chunks of
-// a K = 8192 row instead of 8 sequential index round trips (M = 256: 6.3 us at 128 threads).
+// a K = 8192 row.  The indices (P1 as uint16, constant) are fetched before griddepcontrol.wait, so
+// after the producer of `src` completes only the row's bulk copy and the shared-memory gather remain.
 template <int NT>
-__global__ void __launch_bounds__(NT, NT == 128 ? 16 : 4) k_gather_rows(const __half* __restrict__ src, int64_t ld,
-                                                                      const int32_t* __restrict__ idx, int64_t K,
+__global__ void __launch_bounds__(NT, NT == 128 ? 16 : 4) k_gather_rows(const __half* __restrict__ src, int ld,
+                                                                      const uint16_t* __restrict__ idx, int K,
                                                                       __half* __restrict__ dst) {
   extern __shared__ __align__(16) uint8_t srow_raw[];
+  __shared__ __align__(8) uint64_t row_full;
   __half* srow = reinterpret_cast<__half*>(srow_raw);
-  pdl_launch_dependents();
-  pdl_wait();
+  constexpr int PER = NT == 128 ? 1 : 2;  // chunks of 8 indices (one uint4) per thread prefetched ahead of the wait
+  if (threadIdx.x == 0) mbar_init(&row_full, 1);
   const int m = blockIdx.x;
-  const __half* row = src + (int64_t)m * ld;
-  const int64_t nc = K / 8, c0 = nc * blockIdx.y / gridDim.y, c1 = nc * (blockIdx.y + 1) / gridDim.y;
-  // the first chunk's indices are requested before the row stage and the barrier, so the two L2
-  // round trips overlap (usually the only chunk of a thread)
-  int4 n0 = make_int4(0, 0, 0, 0), n1 = n0;
-  if (c0 + threadIdx.x < c1) {
-    n0 = __ldg(reinterpret_cast<const int4*>(idx) + 2 * (c0 + threadIdx.x));
-    n1 = __ldg(reinterpret_cast<const int4*>(idx) + 2 * (c0 + threadIdx.x) + 1);
+  const int nc = K >> 3, c0 = nc * (int)blockIdx.y / (int)gridDim.y, c1 = nc * ((int)blockIdx.y + 1) / (int)gridDim.y;
+  const uint4* idx8 = reinterpret_cast<const uint4*>(idx);
+  uint4 ix[PER];
+#pragma unroll
+  for (int p = 0; p < PER; ++p) {
+    const int c = c0 + (int)threadIdx.x + p * NT;
+    if (c < c1) ix[p] = __ldg(idx8 + c);
   }
-  for (int64_t c = threadIdx.x; c < K / 8; c += blockDim.x)
-    reinterpret_cast<uint4*>(srow)[c] = __ldg(reinterpret_cast<const uint4*>(row) + c);
-  __syncthreads();
-  __half* out = dst + (int64_t)m * K;
-  for (int64_t c = c0 + threadIdx.x; c < c1; c += blockDim.x) {
-    const bool first = c == c0 + threadIdx.x;
-    const int4 i0 = first ? n0 : __ldg(reinterpret_cast<const int4*>(idx) + 2 * c);
-    const int4 i1 = first ? n1 : __ldg(reinterpret_cast<const int4*>(idx) + 2 * c + 1);
-    uint4 pk;
-    pk.x = (uint32_t)__half_as_ushort(srow[i0.x]) | ((uint32_t)__half_as_ushort(srow[i0.y]) << 16);
-    pk.y = (uint32_t)__half_as_ushort(srow[i0.z]) | ((uint32_t)__half_as_ushort(srow[i0.w]) << 16);
-    pk.z = (uint32_t)__half_as_ushort(srow[i1.x]) | ((uint32_t)__half_as_ushort(srow[i1.y]) << 16);
-    pk.w = (uint32_t)__half_as_ushort(srow[i1.z]) | ((uint32_t)__half_as_ushort(srow[i1.w]) << 16);
-    reinterpret_cast<uint4*>(out)[c] = pk;
+  pdl_launch_dependents();
+  __syncthreads();  // row_full initialised
+  pdl_wait();
+  if (threadIdx.x == 0) {  // the whole row by one bulk copy: no registers, no per-thread latency chain
+    mbar_arrive_expect_tx(&row_full, (uint32_t)K * 2);
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(srow)),
+                 "l"(src + (size_t)m * (unsigned)ld), "r"((uint32_t)K * 2), "r"(smem_u32(&row_full))
+                 : "memory");
   }
+  mbar_wait(&row_full, 0);
+  uint4* out = reinterpret_cast<uint4*>(dst + (size_t)m * (unsigned)K);
+  const uint16_t* sh = reinterpret_cast<const uint16_t*>(srow);
+  auto pair = [&](uint32_t w) { return (uint32_t)sh[w & 0xFFFFu] | ((uint32_t)sh[w >> 16] << 16); };
+  auto gather8 = [&](const uint4 i) { return make_uint4(pair(i.x), pair(i.y), pair(i.z), pair(i.w)); };
+#pragma unroll
+  for (int p = 0; p < PER; ++p) {
+    const int c = c0 + (int)threadIdx.x + p * NT;
+    if (c < c1) out[c] = gather8(ix[p]);
+  }
+  for (int c = c0 + (int)threadIdx.x + PER * NT; c < c1; c += NT)  // rows longer than PER chunks per thread
+    out[c] = gather8(__ldg(idx8 + c));
 }
 
 // Naive Alg. 2 L3-4 for rank r: dst[m][i] = buf[slice(i)][m][off(i)], the AllGather
@@ -2144,15 +2180,16 @@ cudaError_t launch_gemm_ss(const LayerDev& L, const CUtensorMap& xmap, int M, in
 cudaError_t launch_gather_rowmajor(const void* src, int64_t ld, const int32_t* idx, int mode, int64_t nn, int M,
                                    int64_t K, void* dst, cudaStream_t st) {
   // column gather of rows that fit in shared memory, 16-byte aligned rows: stage each row
-  if (mode == GATHER_COLS && idx && K % 8 == 0 && K * 2 <= 48 * 1024 && ld % 8 == 0 &&
+  if (mode == GATHER_COLS && idx && K % 8 == 0 && K * 2 <= 48 * 1024 && ld % 8 == 0 && ld < (1ll << 31) &&
       reinterpret_cast<uintptr_t>(src) % 16 == 0 && reinterpret_cast<uintptr_t>(idx) % 16 == 0)
   {
     const dim3 grid((unsigned)M, (unsigned)std::max(1, std::min(16, (co_res() ? 148 : 256) / M)));
+    const uint16_t* idx16 = reinterpret_cast<const uint16_t*>(idx + K);
     if (M > kMaxM)
-      return launch_pdl(k_gather_rows<512>, grid, dim3(512), (size_t)K * 2, st, reinterpret_cast<const __half*>(src), ld,
-                        idx, K, reinterpret_cast<__half*>(dst));
-    return launch_pdl(k_gather_rows<128>, grid, dim3(128), (size_t)K * 2, st, reinterpret_cast<const __half*>(src), ld,
-                      idx, K, reinterpret_cast<__half*>(dst));
+      return launch_pdl(k_gather_rows<512>, grid, dim3(512), (size_t)K * 2, st, reinterpret_cast<const __half*>(src),
+                        (int)ld, idx16, (int)K, reinterpret_cast<__half*>(dst));
+    return launch_pdl(k_gather_rows<128>, grid, dim3(128), (size_t)K * 2, st, reinterpret_cast<const __half*>(src),
+                      (int)ld, idx16, (int)K, reinterpret_cast<__half*>(dst));
   }
   const int64_t total = (int64_t)M * K;
   return launch_pdl(k_gather_rm, dim3(grid_for(total, 256)), dim3(256), 0, st, reinterpret_cast<const __half*>(src),

@@ -34,12 +34,26 @@ L = tpq.lib()
 L.tpq_debug_trace.argtypes = [C.c_void_p]
 tr = (C.c_longlong * (24 * 64 * 4))()
 L.tpq_debug_trace(C.cast(tr, C.c_void_p))
-t = np.array(tr, dtype=np.int64).reshape(24, 64, 4)[:9]
-t0 = t[t > 0].min()
-rel = np.where(t > 0, t - t0, -1)
-names = ["deq0", "deq1", "apr0", "apr1", "wpr0", "wpr1", "epi0", "epi1", "mma"]
-n = int((rel[8, :, 0] >= 0).sum())
-print("k-steps traced:", n)
-for i in range(n):
-    print(i, " | ".join(f"{names[r]} " + " ".join(f"{v:6d}" for v in rel[r, i]) for r in (0, 1, 2, 3, 4, 8)))
-print("epilogue", rel[6, :2], rel[7, :2])
+T = np.array(tr, dtype=np.int64).reshape(24, 64, 4)
+# clock64 per SM: rows of CTA 0 (deq0, apr0, wpr0, epi0, chunk rows 9) and the MMA row share one clock;
+# CTA 1's rows (deq1, apr1, wpr1, epi1, 10) another.  Times in ns at 1.965 GHz, relative per CTA.
+f = 1.0 / 1.965
+for lay, off in (("layer 1", 0), ("layer 2", 12)):
+    t = T[off:off + 11]
+    if not (t > 0).any():
+        continue
+    c0rows, c1rows = [0, 2, 4, 6, 8, 9], [1, 3, 5, 7, 10]
+    b0 = t[c0rows][t[c0rows] > 0].min()
+    b1 = t[c1rows][t[c1rows] > 0].min() if (t[c1rows] > 0).any() else 0
+    rel = np.full(t.shape, -1, np.int64)
+    for r in range(11):
+        b = b0 if r in c0rows else b1
+        rel[r] = np.where(t[r] > 0, ((t[r] - b) * f).astype(np.int64), -1)
+    n = int((rel[8, :, 0] >= 0).sum())
+    print(lay, "k-steps traced:", n)
+    names = ["deq0", "deq1", "apr0", "apr1", "wpr0", "wpr1", "epi0", "epi1", "mma"]
+    for i in range(n):
+        print(i, " | ".join(f"{names[r]} " + " ".join(f"{v:6d}" for v in rel[r, i]) for r in (0, 2, 4, 8, 1)))
+    print("epilogue cta0", rel[6, :3].tolist(), "cta1", rel[7, :3].tolist())
+    for c in range(8):
+        print("  epi chunk", c, "cta0", rel[9, c].tolist(), "cta1", rel[10, c].tolist())
