@@ -1276,7 +1276,7 @@ struct TS2 {
   static constexpr int AR = 0, BR = AR + NA * XT, WR = BR + NB * WT, ER = WR + NW * STAGE;
   static constexpr int CF = ER + EW * EST;        // per epilogue warp: its item's 128 column factors
   static constexpr int BARS = CF + EW * 512;
-  static constexpr int SMEM = BARS + 8 * (2 * NW + NA + NB + KR + 4);
+  static constexpr int SMEM = BARS + 8 * (2 * NW + NA + NB + KR + 6);
   // pair MMA: D f32, A/B f16 K-major, N = 256, M = 256
   static constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(256 >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
   static_assert(KR >= NA + NB, "done ring");
@@ -1300,12 +1300,19 @@ __device__ __forceinline__ uint32_t mapa_shared(const void* p, uint32_t rank) {
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
-__device__ __forceinline__ void umma_commit2(uint64_t* bar) {  // arrive on the barrier in BOTH CTAs
+// arrive on the barrier in both CTAs of the pair (mask = the pair's two cluster ranks)
+__device__ __forceinline__ void umma_commit2(uint64_t* bar, uint16_t mask) {
   asm volatile(
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
           smem_u32(bar)),
-      "h"((uint16_t)3)
+      "h"(mask)
       : "memory");
+}
+// 16-byte store into another CTA's shared memory, completion (bytes) counted on that CTA's barrier
+__device__ __forceinline__ void st_async16(uint32_t dst, uint4 v, uint32_t bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(dst),
+               "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "r"(bar)
+               : "memory");
 }
 // TMA tile into this CTA's shared memory, completion (bytes) signalled on the pair leader's barrier
 __device__ __forceinline__ void tma_load_3d_pair(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
@@ -1320,7 +1327,12 @@ __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-template <int G>
+// X2 = true: clusters of 4 CTAs = the two k-splits (S = 2, one item per pair) of one 256 x 256 tile.
+// Instead of fp32 partials and k_ss_fixup, the two pairs exchange halves through distributed shared
+// memory once their MMAs are done: split ks finalises columns [128 ks, +128) = its own accumulator
+// + the other split's (64 KB per CTA by st.async into the receiver's free activation ring), written
+// as fp16.  p0 + p1 is the fix-up's sum (commutative, one rounding), so the results are identical.
+template <int G, bool X2>
 __global__ void __launch_bounds__(TS2<G>::WARPS * 32, 1) k_dqgemm_ss2(const SsArgs a, const __grid_constant__ CUtensorMap xmap) {
   using C = TS2<G>;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -1332,9 +1344,12 @@ __global__ void __launch_bounds__(TS2<G>::WARPS * 32, 1) k_dqgemm_ss2(const SsAr
   uint64_t* k_done = b_full + C::NB;    // [KR] k-step t's MMAs completed (multicast commit)
   uint64_t* d_full = k_done + C::KR;    // [2] item's accumulator final (multicast commit)
   uint64_t* d_empty = d_full + 2;       // [2] leader: both epilogues read it (2 x EW)
+  uint64_t* x_free = d_empty + 2;       // X2: the other split's operands are done (remote arrive)
+  uint64_t* x_full = x_free + 1;        // X2: the other split's half of this CTA's rows landed (64 KB)
   __shared__ uint32_t s_tmem;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = cluster_rank();
+  const uint32_t crank = cluster_rank(), rank = crank & 1u, lead = crank & ~1u;  // rank within the pair, its leader
+  const uint16_t pmask = (uint16_t)(3u << lead);
   const int pair = blockIdx.x >> 1, npairs = a.grid >> 1;
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::NW; ++s) {
@@ -1348,6 +1363,8 @@ __global__ void __launch_bounds__(TS2<G>::WARPS * 32, 1) k_dqgemm_ss2(const SsAr
       mbar_init(d_full + s, 1);
       mbar_init(d_empty + s, 2 * C::EW);
     }
+    mbar_init(x_free, 1);
+    mbar_init(x_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == C::MMAW) {
@@ -1355,7 +1372,7 @@ __global__ void __launch_bounds__(TS2<G>::WARPS * 32, 1) k_dqgemm_ss2(const SsAr
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
   }
   tc_fence_before();
-  cluster_sync_all();  // barriers initialised and TMEM allocated in both CTAs before any remote arrive
+  cluster_sync_all();  // barriers initialised and TMEM allocated in every CTA before any remote arrive
   tc_fence_after();
   pdl_launch_dependents();
   const uint32_t tmem = __shfl_sync(0xffffffffu, s_tmem, 0);
@@ -1369,7 +1386,7 @@ __global__ void __launch_bounds__(TS2<G>::WARPS * 32, 1) k_dqgemm_ss2(const SsAr
     // ===================== dequant: this CTA's weight tile 2 ng + rank -> B half (SW128) ==========
     const int jj = warp * 16 + (lane & 15), kh = lane >> 4, j = jj;
     const __half2 k16 = __float2half2_rn(0.0625f);
-    const uint32_t bfull_leader = mapa_shared(b_full, 0);
+    const uint32_t bfull_leader = mapa_shared(b_full, lead);
     int t = 0;
     for (int it = pair; it < a.items; it += npairs) {
       int k0, k1;
@@ -1427,10 +1444,83 @@ __global__ void __launch_bounds__(TS2<G>::WARPS * 32, 1) k_dqgemm_ss2(const SsAr
     // chunk is staged in this warp's 4 KB of shared memory: fp32 partials (S > 1) leave by one 4 KB
     // bulk copy, fp16 results (S = 1) by row-contiguous 64-byte stores (8 rows per instruction).
     const int ew = warp - C::EPI0, qw = ew & 3, hc = ew >> 2;
-    const uint32_t dempty_leader = mapa_shared(d_empty, 0);
+    const uint32_t dempty_leader = mapa_shared(d_empty, lead);
     uint8_t* stg = smem + C::ER + ew * C::EST;
     float* cfs = reinterpret_cast<float*>(smem + C::CF + ew * 512);
     pdl_wait();
+    if constexpr (X2) {
+      // ---- split exchange: one item per pair, it = pair, ks = pq ----
+      const int pq = (int)(crank >> 1), it = pair, mb = (it / 2) % a.MB, ng = it / (2 * a.MB);
+      const uint32_t partner = crank ^ 2u;  // same rows, other split
+      const int ml = qw * 32 + lane;
+      mbar_wait(d_full, 0);
+      tc_fence_after();
+      if (hc != pq) {
+        // send this warp's 32 rows x 128 columns (the partner finalises them), fp32 unscaled
+        mbar_wait(x_free, 0);
+        const uint32_t dst = mapa_shared(smem + C::AR, partner) + ml * 512, bar = mapa_shared(x_full, partner);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          uint32_t v[32];
+          tmem_ld16(tmem + ((uint32_t)(qw * 32) << 16) + 128 * hc + 32 * i, v);
+          tmem_ld16(tmem + ((uint32_t)(qw * 32) << 16) + 128 * hc + 32 * i + 16, v + 16);
+          tmem_wait_ld();
+#pragma unroll
+          for (int q = 0; q < 8; ++q)  // 16-byte chunk 8 i + q of the row, swizzled by row
+            st_async16(dst + ((((8 * i + q) ^ (ml & 7))) << 4), make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]),
+                       bar);
+        }
+      } else {
+        float cfv[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) cfv[i] = __ldg(a.colf + (int64_t)ng * 256 + 128 * hc + 32 * i + lane) * 2.44140625e-4f;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) cfs[32 * i + lane] = cfv[i];
+        if (ew == 4 * pq && lane == 0) {  // this CTA's operands are free: the partner may write its half here
+          mbar_arrive_expect_tx(x_full, 4 * 32 * 4 * 8 * 16);
+          mbar_arrive_cluster(mapa_shared(x_free, partner));
+        }
+        __syncwarp();
+        mbar_wait(x_full, 0);
+        const uint8_t* inc = smem + C::AR + ml * 512;
+        const int mrow0 = mb * 256 + (int)rank * 128 + qw * 32;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int c0 = 128 * hc + 32 * i;
+          uint32_t v[32];
+          tmem_ld16(tmem + ((uint32_t)(qw * 32) << 16) + c0, v);
+          tmem_ld16(tmem + ((uint32_t)(qw * 32) << 16) + c0 + 16, v + 16);
+          tmem_wait_ld();
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const float4 f = *reinterpret_cast<const float4*>(cfs + 32 * i + 4 * q);
+            const float4 o = *reinterpret_cast<const float4*>(inc + ((((8 * i + q) ^ (ml & 7))) << 4));
+            v[4 * q] = __float_as_uint(__uint_as_float(v[4 * q]) * f.x + o.x * f.x);
+            v[4 * q + 1] = __float_as_uint(__uint_as_float(v[4 * q + 1]) * f.y + o.y * f.y);
+            v[4 * q + 2] = __float_as_uint(__uint_as_float(v[4 * q + 2]) * f.z + o.z * f.z);
+            v[4 * q + 3] = __float_as_uint(__uint_as_float(v[4 * q + 3]) * f.w + o.w * f.w);
+          }
+          __syncwarp();
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            uint4 pk;
+            uint32_t* pw = reinterpret_cast<uint32_t*>(&pk);
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              pw[e] = h2u(__floats2half2_rn(__uint_as_float(v[8 * q + 2 * e]), __uint_as_float(v[8 * q + 2 * e + 1])));
+            *reinterpret_cast<uint4*>(stg + lane * 64 + ((q ^ ((lane >> 1) & 3)) << 4)) = pk;
+          }
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int r = 8 * j + (lane >> 2), q = lane & 3, m = mrow0 + r;
+            const uint4 pk = *reinterpret_cast<const uint4*>(stg + r * 64 + ((q ^ ((r >> 1) & 3)) << 4));
+            if (m < a.M) *reinterpret_cast<uint4*>(a.out + (int64_t)m * a.out_ld + (int64_t)ng * 256 + c0 + 8 * q) = pk;
+          }
+        }
+      }
+      tc_fence_before();
+    } else {
     int n_it = 0;
     for (int it = pair; it < a.items; it += npairs, ++n_it) {
       const int db = n_it & 1, mb = (it / a.S) % a.MB, ng = it / (a.S * a.MB);
@@ -1512,6 +1602,7 @@ __global__ void __launch_bounds__(TS2<G>::WARPS * 32, 1) k_dqgemm_ss2(const SsAr
       if (ew == 0) { TPQ_EV2(6 + rank, 1, n_it) }
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // partials written before exit
+    }
   } else if (warp == C::WPROD) {
     // ===================== weight producer: this CTA's records, NW k-steps ahead ====================
     const uint64_t pw = policy_evict_first();
@@ -1536,7 +1627,7 @@ __global__ void __launch_bounds__(TS2<G>::WARPS * 32, 1) k_dqgemm_ss2(const SsAr
   } else if (warp == C::APROD) {
     // ===================== activation producer: this CTA's 128 rows, onto the leader's a_full =======
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&xmap)) : "memory");
-    const uint32_t afull_leader = mapa_shared(a_full, 0);
+    const uint32_t afull_leader = mapa_shared(a_full, lead);
     pdl_wait();  // activations come from the previous kernel in the stream
     int t = 0;
     for (int it = pair; it < a.items; it += npairs) {
@@ -1587,8 +1678,8 @@ __global__ void __launch_bounds__(TS2<G>::WARPS * 32, 1) k_dqgemm_ss2(const SsAr
                 "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem + db * 256),
                 "l"(ad[q]), "l"(bd[q]), "r"(C::IDESC), "r"((kb == k0 && q == 0) ? 0u : 1u)
                 : "memory");
-          umma_commit2(k_done + t % C::KR);
-          if (kb == k1 - 1) umma_commit2(d_full + db);
+          umma_commit2(k_done + t % C::KR, pmask);
+          if (kb == k1 - 1) umma_commit2(d_full + db, pmask);
         }
         __syncwarp();
         TPQ_EV2(8, 3, t)
@@ -1596,7 +1687,7 @@ __global__ void __launch_bounds__(TS2<G>::WARPS * 32, 1) k_dqgemm_ss2(const SsAr
     }
   }
   tc_fence_before();
-  cluster_sync_all();  // both CTAs done with the pair's TMEM and barriers
+  cluster_sync_all();  // every CTA of the cluster done with the pair's TMEM, its barriers and shared memory
   if (warp == C::MMAW) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
@@ -1970,8 +2061,10 @@ bool prepare_ss_t() {
 template <int G>
 bool prepare_ss2_t() {
   static_assert(TS2<G>::SMEM + 1024 <= 227 * 1024, "SS pair GEMM smem (+ static) over the per-CTA limit");
-  return cudaFuncSetAttribute(k_dqgemm_ss2<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, TS2<G>::SMEM) ==
-         cudaSuccess;
+  return cudaFuncSetAttribute(k_dqgemm_ss2<G, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, TS2<G>::SMEM) ==
+             cudaSuccess &&
+         cudaFuncSetAttribute(k_dqgemm_ss2<G, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, TS2<G>::SMEM) ==
+             cudaSuccess;
 }
 template <int G>
 bool prepare_mm_g() {
@@ -1993,7 +2086,7 @@ bool max_carveout(Kern k) {
 template <int G>
 bool carveout_g() {
   return max_carveout(k_dqgemv<G, false>) && max_carveout(k_dqgemv<G, true>) && max_carveout(k_dqgemm<G, 64>) && max_carveout(k_dqgemm<G, 128>) &&
-         max_carveout(k_dqgemm<G, 256>) && max_carveout(k_dqgemm_ss<G, 128>) && max_carveout(k_dqgemm_ss2<G>);
+         max_carveout(k_dqgemm<G, 256>) && max_carveout(k_dqgemm_ss<G, 128>) && max_carveout(k_dqgemm_ss2<G, false>) && max_carveout(k_dqgemm_ss2<G, true>);
 }
 
 template <int G, bool GT>
@@ -2136,9 +2229,18 @@ cudaError_t launch_gemm_ss2(const LayerDev& L, const CUtensorMap& xmap, int M, i
   a.colf = L.colf;
   cudaError_t e = cudaErrorInvalidValue;
   const dim3 blk(TS2<128>::WARPS * 32);  // same warp layout for every G
-  if (L.G == 128) e = launch_pdl_cluster(k_dqgemm_ss2<128>, 2, dim3(a.grid), blk, TS2<128>::SMEM, st, a, xmap);
-  else if (L.G == 64) e = launch_pdl_cluster(k_dqgemm_ss2<64>, 2, dim3(a.grid), blk, TS2<64>::SMEM, st, a, xmap);
-  else if (L.G == 32) e = launch_pdl_cluster(k_dqgemm_ss2<32>, 2, dim3(a.grid), blk, TS2<32>::SMEM, st, a, xmap);
+  // two k-splits that fit one wave: clusters of 4 exchange halves in distributed shared memory
+  static const bool no_x2 = getenv("TPQ_NO_X2") != nullptr;
+  if (S == 2 && a.items <= sms / 2 && !no_x2) {
+    a.grid = 2 * a.items;
+    if (L.G == 128) return launch_pdl_cluster(k_dqgemm_ss2<128, true>, 4, dim3(a.grid), blk, TS2<128>::SMEM, st, a, xmap);
+    if (L.G == 64) return launch_pdl_cluster(k_dqgemm_ss2<64, true>, 4, dim3(a.grid), blk, TS2<64>::SMEM, st, a, xmap);
+    if (L.G == 32) return launch_pdl_cluster(k_dqgemm_ss2<32, true>, 4, dim3(a.grid), blk, TS2<32>::SMEM, st, a, xmap);
+    return cudaErrorInvalidValue;
+  }
+  if (L.G == 128) e = launch_pdl_cluster(k_dqgemm_ss2<128, false>, 2, dim3(a.grid), blk, TS2<128>::SMEM, st, a, xmap);
+  else if (L.G == 64) e = launch_pdl_cluster(k_dqgemm_ss2<64, false>, 2, dim3(a.grid), blk, TS2<64>::SMEM, st, a, xmap);
+  else if (L.G == 32) e = launch_pdl_cluster(k_dqgemm_ss2<32, false>, 2, dim3(a.grid), blk, TS2<32>::SMEM, st, a, xmap);
   if (e != cudaSuccess || S == 1) return e;
   return launch_pdl(k_ss_fixup, dim3((unsigned)(2 * a.MB * a.NG), 32), dim3(128), 0, st, (const float*)L.ws_ss, M,
                     2 * a.MB, S, 256, reinterpret_cast<__half*>(out), out_ld, 1);
