@@ -50,6 +50,9 @@ struct LayerDev {
   int grid = 0;            // persistent CTAs of the M <= 16 GEMV (stream-K), at most one per SM
   int grid_mm = 0;         // persistent CTAs of the A7 k_dqgemm (every SM)
   float* ws = nullptr;     // [grid][2 slots][16][128] fp32 stream-K partials of the GEMV (slot 0 = first segment)
+  int inred = 0;           // 1: split tiles reduced inside the GEMV (cnt); 0: by the fix-up kernel after it
+  int* cnt = nullptr;      // [NT][4] split-tile arrival counters of the GEMV, one per epilogue warp (zeroed at upload,
+                           // re-armed by each reducer)
   float* ws_mm = nullptr;  // [grid_mm][2 slots][256][128] fp32 stream-K partials (A7 GEMM)
   float* ws_ss = nullptr;  // [items][128][128] fp32 k-split partials (A7 SS GEMM, M >= 128)
   const float* colf = nullptr;  // [N] 2^(24 - E_n): records hold s' = s 2^E_n (tpq_host.cpp column_exponents)

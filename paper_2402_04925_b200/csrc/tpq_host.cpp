@@ -361,10 +361,19 @@ void plan_layer(tpq::LayerDev& L, int64_t K, int64_t N, int G, int device) {
   if (L.U < 64LL * sms) g = std::max(1, sms * 128 / 148);
   if (const char* e = getenv("TPQ_GRID")) g = std::max(1, std::min(sms, atoi(e)));  // tuning aid
   L.grid = (int)std::min<int64_t>((int64_t)g, cap);
+  // Split tiles are reduced inside the GEMV (c_first waits for the later contributors' partials)
+  // unless a tile spans more than 4 CTA ranges: then the middle contributors, which finish with the
+  // reducer, make a chain the separate fix-up kernel resolves faster (Llama TP=8 layer 1: 14 units
+  // per CTA against 64-unit tiles; same-box 22.0 vs 21.4 us at M = 16).
+  {
+    const int64_t per = std::max<int64_t>(1, L.U / L.grid);
+    const int64_t most = (L.NKB - 1 + per - 1) / per + 1;  // contributors of a tile, at most
+    L.inred = most <= 4 && !getenv("TPQ_FIXUP_KERNEL");
+  }
   L.grid_mm = (int)std::min<int64_t>((int64_t)sms, cap);
   if (getenv("TPQ_VERBOSE"))
-    fprintf(stderr, "[tpq] layer K=%lld N=%lld G=%d: grid %d over %lld units\n", (long long)K, (long long)N, G,
-            L.grid, (long long)L.U);
+    fprintf(stderr, "[tpq] layer K=%lld N=%lld G=%d: grid %d over %lld units, split tiles reduced %s\n", (long long)K,
+            (long long)N, G, L.grid, (long long)L.U, L.inred ? "in-kernel" : "by the fix-up kernel");
 }
 
 }  // namespace
@@ -659,7 +668,11 @@ int shard_impl(const gptq_layer* w1, const gptq_layer* wu, const gptq_layer* w2,
               if (cta_of((int64_t)t * L.NKB) != cta_of((int64_t)(t + 1) * L.NKB - 1)) sp.push_back(t);
             if (layer == 0) n1 = (int)sp.size();
           }
-          if ((r = A((void**)&h->d_split, std::max<size_t>(1, sp.size()) * 4))) return r;
+          const size_t nsp = std::max<size_t>(1, sp.size()), ncnt = 4 * (size_t)(h->L1.NT + h->L2.NT);
+          if ((r = A((void**)&h->d_split, (nsp + ncnt) * 4))) return r;
+          TPQ_CUDA(cudaMemset(h->d_split + nsp, 0, ncnt * 4));
+          h->L1.cnt = h->d_split + nsp;  // split-tile arrival counters of the in-kernel reduction
+          h->L2.cnt = h->L1.cnt + 4 * h->L1.NT;  // [NT][4 epilogue warps] per layer
           if (!sp.empty()) TPQ_CUDA(cudaMemcpy(h->d_split, sp.data(), sp.size() * 4, cudaMemcpyHostToDevice));
           h->L1.split_tiles = h->d_split;
           h->L1.nsplit = n1;

@@ -96,9 +96,10 @@ __device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity
 }
 
 // Per-CTA timeline (build with -DTPQ_PROF; profiling aid, not in the product build): entry,
-// work start, end (globaltimer ns) and SM id per CTA, per layer (N > K selects the slot).
+// work start, end (globaltimer ns), SM id, split-tile publish, reducer wait start / end, reducer's own
+// accumulator final, per CTA, per layer (slot 1: N > K, i.e. layer 1 of the MLP).
 #ifdef TPQ_PROF
-__device__ unsigned long long g_tpq_cta[2][1024][4];
+__device__ unsigned long long g_tpq_cta[2][1024][8];
 __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -108,8 +109,15 @@ __device__ __forceinline__ unsigned long long gtime() {
   if (blockIdx.x < 1024) g_tpq_cta[a.NT * kTileCols > a.NKB * kUnitK][blockIdx.x][e] = (v);
 // per-unit event timeline of CTA 0 of the layer-2 launch: [warp][unit < 64][event]
 __device__ long long g_tpq_trace[24][64][4];
+#ifndef TPQ_TRACE_CTA
+#define TPQ_TRACE_CTA 0  // traced CTA; TPQ_TRACE_N_GT_K=1 traces the launch with N > K (layer 1 of the MLP)
+#endif
+#ifndef TPQ_TRACE_N_GT_K
+#define TPQ_TRACE_N_GT_K 0
+#endif
 #define TPQ_EV(e, i) \
-  if (blockIdx.x == 0 && a.NT * kTileCols < a.NKB * kUnitK && lane == 0 && (i) < 64) g_tpq_trace[warp][i][e] = clock64();
+  if (blockIdx.x == TPQ_TRACE_CTA && (a.NT * kTileCols > a.NKB * kUnitK) == TPQ_TRACE_N_GT_K && lane == 0 && (i) < 64) \
+    g_tpq_trace[warp][i][e] = clock64();
 // k-step event timeline of pair 0 of a k_dqgemm_ss2 launch: [row (+ 12 when N > K)][k-step < 64][event], clock64
 // (SM-local: compare times within one CTA's rows only; globaltimer reads cost ~100 ns each)
 #define TPQ_EV2(row, e, i) \
@@ -161,6 +169,52 @@ __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepc
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+// Split-tile hand-off between the CTAs of one GEMV launch, per epilogue warp (lane quarter qw, no
+// cross-warp barrier): each contributor warp stores its 32 columns, then lane 0 adds 1 with release
+// semantics to the tile's counter cnt[4 t + qw] (__syncwarp orders the warp's stores before it); the
+// reducer's warp qw polls that counter with relaxed loads, acquires once it reaches the number of
+// contributors, reads the partials and re-arms the counter to 0 for the next launch (stream order).
+__device__ __forceinline__ void red_release_add(int* p, int v) {
+  asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ int ld_relaxed(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void warp_publish(int* cnt, int lane) {
+  __syncwarp();
+  if (lane == 0) red_release_add(cnt, 1);
+}
+// non-blocking: true (with acquire) once *cnt >= n
+__device__ __forceinline__ bool warp_poll(const int* cnt, int n, int lane) {
+  int ok = 0;
+  if (lane == 0 && ld_relaxed(cnt) >= n) ok = ld_acquire(cnt) >= n;
+  ok = __shfl_sync(0xffffffffu, ok, 0);
+  __syncwarp();
+  return ok;
+}
+__device__ __forceinline__ void warp_wait(const int* cnt, int n, int lane) {
+  if (lane == 0) {
+    while (ld_relaxed(cnt) < n) __nanosleep(128);
+    (void)ld_acquire(cnt);
+  }
+  __syncwarp();
+}
+// acc[m] += p[m * 128] for rows m < M, all loads in flight together
+template <int NR>
+__device__ __forceinline__ void add_partial(const float* p, int M, float (&acc)[NR]) {
+  float t[NR];
+#pragma unroll
+  for (int m = 0; m < NR; ++m) t[m] = m < M ? __ldcg(p + m * 128) : 0.f;
+#pragma unroll
+  for (int m = 0; m < NR; ++m) acc[m] += t[m];
+}
 
 // tcgen05.st 32x32b: each thread of the warp writes N consecutive 32-bit TMEM columns of its lane.
 #define TPQ_R4(b) "r"(r[b]), "r"(r[b + 1]), "r"(r[b + 2]), "r"(r[b + 3])
@@ -267,6 +321,7 @@ struct GemvArgs {
   const float* colf;  // [N] 2^(24 - E_n): the records hold s' = s 2^E_n per column n
   const uint32_t* meta;  // unordered layers: [ng][ldm] {lo: fp16 s', hi: fp16 C = -z s' 2^-24}
   int64_t ldm;
+  int* cnt;         // [NT] split-tile arrival counters (0 between launches); NULL: the fix-up kernel after
 };
 
 // ------------------------------------------------------------------ GEMV (M <= 16)
@@ -505,11 +560,15 @@ __global__ void __launch_bounds__(kGemvThreads, 1)
       int tile = (int)(v0 / a.NKB);
       int64_t seg_start = v0;
       const int64_t vend = v0 + nv;
+      constexpr int SLOT = 2 * kNPad * kTileCols;  // gate then up partials
       for (int seg = 0; seg_start < vend; ++seg, ++tile) {
-        const int64_t tile_end = (int64_t)(tile + 1) * a.NKB;
+        const int64_t tile_start = (int64_t)tile * a.NKB, tile_end = tile_start + a.NKB;
         const int64_t seg_end = tile_end < vend ? tile_end : vend;
         const int lo = (int)(seg_start - v0), hi = (int)(seg_end - 1 - v0);
         const int d = seg & 1;
+        const bool reduce = a.cnt && seg_start == tile_start && seg_end < tile_end;  // as in the plain epilogue
+        const bool publish = a.cnt && seg_start > tile_start;
+        int* cnt = a.cnt ? a.cnt + 4 * tile + qw : nullptr;
         const float up = __ldg(a.colf + (int64_t)tile * kTileCols + col);
         mbar_wait_backoff(d_full + d, (uint32_t)((seg >> 1) & 1), 256);
         tc_fence_after();
@@ -531,13 +590,33 @@ __global__ void __launch_bounds__(kGemvThreads, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(d_empty + d);
         const int64_t n = (int64_t)tile * kTileCols + col;
-        if (seg_start == (int64_t)tile * a.NKB && seg_end == tile_end) {
+        if (publish) {
+          float* mine = a.ws + (size_t)blockIdx.x * 2 * SLOT + col;
+#pragma unroll
+          for (int kind = 0; kind < 2; ++kind)
+#pragma unroll
+            for (int m = 0; m < kNPad; ++m)
+              if (m < a.M) __stcg(mine + (kind * kNPad + m) * kTileCols, gu[kind][m]);
+          warp_publish(cnt, lane);
+        } else if (reduce) {
+          const int nother = cta_of_unit(tile_end - 1, a.U, a.grid) - (int)blockIdx.x;
+          warp_wait(cnt, nother, lane);
+          for (int q = 0; q < nother; ++q) {  // CTA order after the own partial
+            const float* src = a.ws + (size_t)(blockIdx.x + 1 + q) * 2 * SLOT + col;
+#pragma unroll
+            for (int kind = 0; kind < 2; ++kind) add_partial(src + kind * kNPad * kTileCols, a.M, gu[kind]);
+          }
+          if (lane == 0) *cnt = 0;
+#pragma unroll
+          for (int m = 0; m < kNPad; ++m)
+            if (m < a.M) a.out[m * a.out_ld + n] = __float2half_rn(silu_f(gu[0][m]) * gu[1][m]);
+        } else if (seg_start == tile_start && seg_end == tile_end) {
 #pragma unroll
           for (int m = 0; m < kNPad; ++m)
             if (m < a.M) a.out[m * a.out_ld + n] = __float2half_rn(silu_f(gu[0][m]) * gu[1][m]);
         } else {
-          // split tile: gate and up partials into this CTA's slot; k_mm_fixup (gated) finishes them
-          float* mine = a.ws + ((size_t)blockIdx.x * 2 + (seg_start == v0 ? 0 : 1)) * (2 * kNPad * kTileCols);
+          // (cnt == NULL) split tile: gate and up partials into this CTA's slot; k_mm_fixup (gated) finishes them
+          float* mine = a.ws + ((size_t)blockIdx.x * 2 + (seg_start == v0 ? 0 : 1)) * SLOT;
 #pragma unroll
           for (int kind = 0; kind < 2; ++kind)
 #pragma unroll
@@ -550,13 +629,44 @@ __global__ void __launch_bounds__(kGemvThreads, 1)
       int tile = (int)(u0 / a.NKB);
       int64_t seg_start = u0;
       const int64_t uend = u0 + nu;
+      constexpr int SLOT = kNPad * kTileCols;
+      // split tile t (contributors c_first < ... < c_last): c_first holds its first units as its LAST
+      // segment and reduces; every later contributor holds it as its FIRST segment and publishes
+      // slot 0 -- early in its run, except the middle CTAs of a tile longer than a CTA's range.
+      // The reducer takes the next contributor's partial as soon as it is there (polled while waiting
+      // for its own accumulators), so a layer whose tiles are shorter than a range has no cross-CTA
+      // wait at its end.
+      const int64_t lt = (uend - 1) / a.NKB;  // tile of the CTA's last unit
+      const bool red_last = a.cnt && lt * a.NKB >= u0 && uend < (lt + 1) * a.NKB;
+      const int nother = red_last ? cta_of_unit((lt + 1) * a.NKB - 1, a.U, a.grid) - (int)blockIdx.x : 0;
+      int* cnt_last = red_last ? a.cnt + 4 * lt + qw : nullptr;
+      float pre[kNPad] = {};  // contributor c_first + 1's partial
+      bool have = !red_last;
       for (int seg = 0; seg_start < uend; ++seg, ++tile) {
-        const int64_t tile_end = (int64_t)(tile + 1) * a.NKB;
+        const int64_t tile_start = (int64_t)tile * a.NKB, tile_end = tile_start + a.NKB;
         const int64_t seg_end = tile_end < uend ? tile_end : uend;  // exclusive
         const int lo = (int)(seg_start - u0), hi = (int)(seg_end - 1 - u0);
         const int d = seg & 1;
+        const uint32_t par = (uint32_t)((seg >> 1) & 1);
+        const bool reduce = red_last && seg_end == uend;
+        const bool publish = a.cnt && seg_start > tile_start;
+        if (!have) {
+          if (reduce && threadIdx.x == 0) { TPQ_CTA(5, gtime()) }
+          for (;;) {  // wait for the accumulators, taking the partial if it arrives first
+            int ok = 0;
+            if (lane == 0) ok = mbar_try(d_full + d, par);
+            if (__shfl_sync(0xffffffffu, ok, 0)) break;
+            if (warp_poll(cnt_last, nother, lane)) {
+              add_partial(a.ws + (size_t)(blockIdx.x + 1) * 2 * SLOT + col, a.M, pre);
+              have = true;
+              if (threadIdx.x == 0) { TPQ_CTA(6, gtime()) }
+              break;
+            }
+            __nanosleep(256);
+          }
+        }
         const float up = __ldg(a.colf + (int64_t)tile * kTileCols + col);  // 2^(24 - E) of this column
-        mbar_wait_backoff(d_full + d, (uint32_t)((seg >> 1) & 1), 256);
+        mbar_wait_backoff(d_full + d, par, 256);
         tc_fence_after();
         const bool w0 = hi - lo >= 3 || ((lo >> 1) & 1) == 0 || ((hi >> 1) & 1) == 0;
         const bool w1 = hi - lo >= 3 || ((lo >> 1) & 1) == 1 || ((hi >> 1) & 1) == 1;
@@ -573,14 +683,39 @@ __global__ void __launch_bounds__(kGemvThreads, 1)
           v[m] = __float_as_uint(up * (w0 ? (w1 ? __uint_as_float(v[m]) + __uint_as_float(v1[m]) : __uint_as_float(v[m]))
                                           : __uint_as_float(v1[m])));
         const int64_t n = (int64_t)tile * kTileCols + col;
-        if (seg_start == (int64_t)tile * a.NKB && seg_end == tile_end) {
+        if (publish) {
+          float* mine = a.ws + (size_t)blockIdx.x * 2 * SLOT + col;
+  #pragma unroll
+          for (int m = 0; m < kNPad; ++m)
+            if (m < a.M) __stcg(mine + m * kTileCols, __uint_as_float(v[m]));
+          warp_publish(a.cnt + 4 * tile + qw, lane);
+          if (threadIdx.x == 0) { TPQ_CTA(4, gtime()) }
+        } else if (reduce) {
+          // CTA order: own partial, then c_first + 1, ..., c_last (deterministic)
+          if (threadIdx.x == 0) { TPQ_CTA(7, gtime()) }
+          if (!have) {  // a middle contributor finishes with this CTA: wait for it now
+            warp_wait(cnt_last, nother, lane);
+            add_partial(a.ws + (size_t)(blockIdx.x + 1) * 2 * SLOT + col, a.M, pre);
+            if (threadIdx.x == 0) { TPQ_CTA(6, gtime()) }
+          }
+          float acc[kNPad];
+  #pragma unroll
+          for (int m = 0; m < kNPad; ++m) acc[m] = __uint_as_float(v[m]);
+  #pragma unroll
+          for (int m = 0; m < kNPad; ++m) acc[m] += pre[m];
+          for (int q = 1; q < nother; ++q) add_partial(a.ws + (size_t)(blockIdx.x + 1 + q) * 2 * SLOT + col, a.M, acc);
+  #pragma unroll
+          for (int m = 0; m < kNPad; ++m)
+            if (m < a.M) a.out[m * a.out_ld + n] = __float2half_rn(acc[m]);
+          if (lane == 0) *cnt_last = 0;
+        } else if (seg_start == tile_start && seg_end == tile_end) {
   #pragma unroll
           for (int m = 0; m < kNPad; ++m)
             if (m < a.M) a.out[m * a.out_ld + n] = __float2half_rn(__uint_as_float(v[m]));
         } else {
-          // split tile: partial into this CTA's slot (0 = its first segment, 1 = its last), summed by
-          // the fix-up kernel in CTA order after this kernel
-          float* mine = a.ws + ((size_t)blockIdx.x * 2 + (seg_start == u0 ? 0 : 1)) * (kNPad * kTileCols);
+          // (cnt == NULL) split tile: partial into this CTA's slot (0 = its first segment, 1 = its
+          // last), summed by the fix-up kernel in CTA order after this kernel
+          float* mine = a.ws + ((size_t)blockIdx.x * 2 + (seg_start == u0 ? 0 : 1)) * SLOT;
   #pragma unroll
           for (int m = 0; m < kNPad; ++m)
             if (m < a.M) __stcg(mine + m * kTileCols + col, __uint_as_float(v[m]));
@@ -700,6 +835,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1)
       const int i0 = 2 * p, sg = (kb0 + i0) / a.NKB;
       const int lo = sg * a.NKB - kb0 > 0 ? sg * a.NKB - kb0 : 0;
       const int hi = (sg + 1) * a.NKB - kb0 - 1 < nu - 1 ? (sg + 1) * a.NKB - kb0 - 1 : nu - 1;
+      while (sw < sg) skip_seg();  // before the a_full wait: a segment's d_full never waits for the next pair's dequant
       const bool fast = sg == sw && i0 - 3 >= lo && i0 + 4 <= hi;
       const uint32_t at = tmem + kA0 + b * 2 * C::AU;
       TPQ_EV(0, p)
@@ -2020,7 +2156,7 @@ int grid_for(int64_t work, int per_block) {
 // ------------------------------------------------------------------ launchers
 #ifdef TPQ_PROF
 int cta_read(unsigned long long* out) {
-  return cudaMemcpyFromSymbol(out, g_tpq_cta, sizeof(unsigned long long) * 2 * 1024 * 4) != cudaSuccess;
+  return cudaMemcpyFromSymbol(out, g_tpq_cta, sizeof(unsigned long long) * 2 * 1024 * 8) != cudaSuccess;
 }
 int trace_read(long long* out) {
   return cudaMemcpyFromSymbol(out, g_tpq_trace, sizeof(long long) * 24 * 64 * 4) != cudaSuccess;
@@ -2144,6 +2280,7 @@ cudaError_t launch_gemv(const LayerDev& L, const CUtensorMap& xmap, const CUtens
   a.colf = L.colf;
   a.meta = L.meta;
   a.ldm = L.N;
+  a.cnt = L.inred ? L.cnt : nullptr;
   const CUtensorMap& xu = xmapu ? *xmapu : xmap;
   cudaError_t e = cudaErrorInvalidValue;
   if (L.unord) e = launch_gemv_t<0, false>(a, xmap, xu, st);
@@ -2153,7 +2290,7 @@ cudaError_t launch_gemv(const LayerDev& L, const CUtensorMap& xmap, const CUtens
   else e = L.G == 128 ? launch_gemv_t<128, false>(a, xmap, xu, st)
            : L.G == 64 ? launch_gemv_t<64, false>(a, xmap, xu, st)
            : L.G == 32 ? launch_gemv_t<32, false>(a, xmap, xu, st) : cudaErrorInvalidValue;
-  if (e != cudaSuccess) return e;
+  if (e != cudaSuccess || a.cnt) return e;  // split tiles reduced inside the GEMV
   // split tiles, summed in CTA order after the GEMV: M <= 4 one thread per column with every
   // contributor's rows in flight (k_gemv_fixup); M > 4 (and the gated layer) one warp per row,
   // float4 per lane (k_mm_fixup).  Separate kernels ordered by griddepcontrol.wait beat an in-kernel

@@ -1,5 +1,7 @@
-"""Per-CTA entry / work-start / end times of the GEMV kernels of the last forward (profiling build):
-    TPQ_LIB_PATH=paper_2402_04925_b200/libtpq_prof.so python tools/cta_times.py --m 1"""
+"""Per-CTA timeline of the GEMV kernels of the last forward (profiling build):
+    TPQ_LIB_PATH=paper_2402_04925_b200/libtpq_prof.so python tools/cta_times.py --m 1
+Per CTA (globaltimer): entry, work start (activations available), end, SM id, split-tile publish,
+reducer wait start / end, reducer's own accumulator final."""
 import argparse
 import ctypes as C
 import os
@@ -29,68 +31,43 @@ for i in range(10 * R + 1):
 torch.cuda.synchronize()
 L = tpq.lib()
 L.tpq_debug_cta.argtypes = [C.c_void_p]
-buf = (C.c_ulonglong * (2 * 1024 * 4))()
+buf = (C.c_ulonglong * (2 * 1024 * 8))()
 L.tpq_debug_cta(C.cast(buf, C.c_void_p))
-t = np.array(buf, dtype=np.int64).reshape(2, 1024, 4)
-for layer in (0, 1):
-    v = t[layer]
-    v = v[v[:, 0] > 0]
-    n = len(v)
-    t0 = v[:, 1].min()
-    ent, ws, end, sm = (v[:, 0] - t0) / 1e3, (v[:, 1] - t0) / 1e3, (v[:, 2] - t0) / 1e3, v[:, 3]
-    print(f"layer {layer + 1}: {n} CTAs; entry [{ent.min():.2f}, {ent.max():.2f}] us; work start [{ws.min():.2f},"
-          f" {ws.max():.2f}]; end min {end.min():.2f} p10 {np.percentile(end, 10):.2f} med {np.median(end):.2f}"
-          f" p90 {np.percentile(end, 90):.2f} max {end.max():.2f}")
-    dur = end - ws
-    print(f"   busy (end - work start): min {dur.min():.2f} med {np.median(dur):.2f} max {dur.max():.2f}")
-    for lo, hi in ((0, 74), (74, 148)):
-        sel = (sm >= lo) & (sm < hi)
-        if sel.any():
-            print(f"   smid {lo}-{hi - 1}: {sel.sum()} CTAs, end med {np.median(end[sel]):.2f} max {end[sel].max():.2f}")
-    order = np.argsort(end)
-    print("   earliest:", [(int(i), int(sm[i]), round(float(end[i]), 2)) for i in order[:6]])
-    print("   latest:  ", [(int(i), int(sm[i]), round(float(end[i]), 2)) for i in order[-6:]])
-    # GPC-ish buckets of smid
-    bk = {}
-    for s_, e_ in zip(sm, end):
-        bk.setdefault(int(s_) // 16, []).append(e_)
-    print("   end med by smid//16:", {k: round(float(np.median(x)), 1) for k, x in sorted(bk.items())})
-    # the CTAs sharing an SM
-    by = {}
-    for e_, s_ in zip(end, sm):
-        by.setdefault(int(s_), []).append(e_)
-    pairs = [sorted(x) for x in by.values() if len(x) == 2]
-    if pairs:
-        d = np.array([x[1] - x[0] for x in pairs])
-        lo_ = np.array([x[0] for x in pairs])
-        hi_ = np.array([x[1] for x in pairs])
-        print(f"   SM pairs: {len(pairs)}; |dt| med {np.median(d):.2f} max {d.max():.2f}; first-finisher med "
-              f"{np.median(lo_):.2f}, second med {np.median(hi_):.2f} max {hi_.max():.2f}")
-
-# correlate layer-1 end times with the CTA's stream-K range: offset of its first unit in its tile,
-# number of tile segments, whether it is the last arriver (fix-up) of its first / last tile
-if os.environ.get("TPQ_CTA_CORR"):
-    K1, N1 = p.K1, p.N1 // a.sim_tp
-    NKB, NT = K1 // 128, N1 // 128
-    U = NKB * NT
-    v = t[0]
+t = np.array(buf, dtype=np.int64).reshape(2, 1024, 8)
+n1 = p.N1 // a.sim_tp
+geo = {1: (p.K1 // 128, n1 // 128), 2: (n1 // 128, p.N2 // 128)}  # (NKB, NT)
+slot = {1: int(n1 > p.K1), 2: int(p.N2 > n1)}  # the kernel files a launch under slot N > K
+assert slot[1] != slot[2]
+T0 = t[slot[1]][t[slot[1]][:, 0] > 0][:, 1].min()  # layer-1 work start: common origin
+for layer in (1, 2):
+    v = t[slot[layer]]
     grid = int((v[:, 0] > 0).sum())
-    t0 = v[:grid, 1].min()
-    ends = (v[:grid, 2] - t0) / 1e3
-    rows = []
-    for c in range(grid):
+    v = v[:grid]
+    us = lambda x: (x - T0) / 1e3  # noqa: E731
+    ent, ws, end = us(v[:, 0]), us(v[:, 1]), us(v[:, 3 - 1])
+    print(f"layer {layer}: {grid} CTAs; entry [{ent.min():.2f}, {ent.max():.2f}]; work start [{ws.min():.2f}, {ws.max():.2f}];"
+          f" end min {end.min():.2f} p10 {np.percentile(end, 10):.2f} med {np.median(end):.2f} p90 {np.percentile(end, 90):.2f}"
+          f" max {end.max():.2f}  (us from layer-1 work start)")
+    NKB, NT = geo[layer]
+    U = NKB * NT
+    pub = v[:, 4] > 0
+    red = v[:, 5] > 0
+    if pub.any():
+        print(f"   publish (after start): med {np.median(us(v[pub, 4]) - ws[pub]):.2f}")
+    if red.any():
+        wstart, wend, own = us(v[red, 5]), us(v[red, 6]), us(v[red, 7])
+        print(f"   reducers {red.sum()}: wait {np.median(wend - wstart):.2f} med / {np.max(wend - wstart):.2f} max; "
+              f"own final - wait end med {np.median(own - wend):.2f}; end - own final med {np.median(end[red] - own):.2f} max {np.max(end[red] - own):.2f}")
+    order = np.argsort(end)
+    for c in list(order[:3]) + list(order[-8:]):
         u0, u1 = c * U // grid, (c + 1) * U // grid
-        off = u0 % NKB
-        nseg = (u1 - 1) // NKB - u0 // NKB + 1
-        rows.append((ends[c], c, off, nseg, u1 - u0, (u1 - 1) % NKB))
-    rows.sort()
-    import collections
-    by = collections.defaultdict(list)
-    for e, c, off, nseg, n, last in rows:
-        by[nseg].append(e)
-    print("layer 1 end by #segments:", {k: (len(x), round(float(np.median(x)), 2)) for k, x in sorted(by.items())})
-    for e, c, off, nseg, n, last in rows[:8] + rows[-12:]:
-        print(f"  cta {c:3d} end {e:6.2f} first-kb {off:2d} last-kb {last:2d} segs {nseg} units {n}")
-    offs = np.array([r[2] for r in rows]); es = np.array([r[0] for r in rows])
-    print("corr(end, first-kb) =", round(float(np.corrcoef(offs, es)[0, 1]), 3),
-          " corr(end, last-kb) =", round(float(np.corrcoef(np.array([r[5] for r in rows]), es)[0, 1]), 3))
+        c_last = lambda tile: ((((tile + 1) * NKB - 1) + 1) * grid + U - 1) // U - 1  # noqa: E731
+        info = f"units {u1 - u0} first-kb {u0 % NKB} last-tile-units {(u1 - 1) % NKB + 1}"
+        if v[c, 5] > 0:
+            tile = (u1 - 1) // NKB
+            others = range(c + 1, c_last(tile) + 1)
+            pubs = [round(float(us(v[o, 4])), 2) if v[o, 4] > 0 else None for o in others]
+            ends = [round(float(end[o]), 2) for o in others]
+            info += (f" | reduce: wait {us(v[c, 5]):.2f}->{us(v[c, 6]):.2f} own {us(v[c, 7]):.2f}; others {list(others)}"
+                     f" publish {pubs} end {ends}")
+        print(f"   cta {c:3d} sm {int(v[c, 3]):3d} end {end[c]:.2f} {info}")

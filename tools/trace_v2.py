@@ -38,7 +38,7 @@ t = np.array(tr, dtype=np.int64).reshape(24, 64, 4)
 t0 = t[t > 0].min()
 rel = np.where(t > 0, t - t0, -1)
 print("pair | set0 w4: start landed free arrive | set1 w8 | set2 w12 | mma18: wait got - commit | mma19")
-for pi in range(48):
+for pi in range(49):
     row = []
     w = [4, 8, 12][pi % 3]
     row.append(f"{pi:3d} s{pi % 3} " + " ".join(f"{v:7d}" for v in rel[w, pi]))
