@@ -97,9 +97,10 @@ __device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity
 
 // Per-CTA timeline (build with -DTPQ_PROF; profiling aid, not in the product build): entry,
 // work start, end (globaltimer ns), SM id, split-tile publish, reducer wait start / end, reducer's own
-// accumulator final, per CTA, per layer (slot 1: N > K, i.e. layer 1 of the MLP).
+// accumulator final, clock64 at entry and end, first pair's A operands stored, last MMA commit, per CTA,
+// per layer (slot 1: N > K, i.e. layer 1 of the MLP).
 #ifdef TPQ_PROF
-__device__ unsigned long long g_tpq_cta[2][1024][8];
+__device__ unsigned long long g_tpq_cta[2][1024][12];
 __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -108,20 +109,24 @@ __device__ __forceinline__ unsigned long long gtime() {
 #define TPQ_CTA(e, v) \
   if (blockIdx.x < 1024) g_tpq_cta[a.NT * kTileCols > a.NKB * kUnitK][blockIdx.x][e] = (v);
 // per-unit event timeline of CTA 0 of the layer-2 launch: [warp][unit < 64][event]
-__device__ long long g_tpq_trace[24][64][4];
+__device__ long long g_tpq_trace[2][24][64][4];
 #ifndef TPQ_TRACE_CTA
 #define TPQ_TRACE_CTA 0  // traced CTA; TPQ_TRACE_N_GT_K=1 traces the launch with N > K (layer 1 of the MLP)
 #endif
 #ifndef TPQ_TRACE_N_GT_K
 #define TPQ_TRACE_N_GT_K 0
 #endif
+#ifndef TPQ_TRACE_CTA2
+#define TPQ_TRACE_CTA2 (-1)  // a second traced CTA (globaltimer in both when set)
+#endif
 #define TPQ_EV(e, i) \
-  if (blockIdx.x == TPQ_TRACE_CTA && (a.NT * kTileCols > a.NKB * kUnitK) == TPQ_TRACE_N_GT_K && lane == 0 && (i) < 64) \
-    g_tpq_trace[warp][i][e] = clock64();
+  if ((blockIdx.x == TPQ_TRACE_CTA || (int)blockIdx.x == TPQ_TRACE_CTA2) && \
+      (a.NT * kTileCols > a.NKB * kUnitK) == TPQ_TRACE_N_GT_K && lane == 0 && (i) < 64) \
+    g_tpq_trace[blockIdx.x == TPQ_TRACE_CTA ? 0 : 1][warp][i][e] = TPQ_TRACE_CTA2 >= 0 ? (long long)gtime() : clock64();
 // k-step event timeline of pair 0 of a k_dqgemm_ss2 launch: [row (+ 12 when N > K)][k-step < 64][event], clock64
 // (SM-local: compare times within one CTA's rows only; globaltimer reads cost ~100 ns each)
 #define TPQ_EV2(row, e, i) \
-  if (blockIdx.x < 2 && lane == 0 && (i) < 64) g_tpq_trace[(row) + (a.NG * 256 > a.NKB * kUnitK ? 12 : 0)][i][e] = clock64();
+  if (blockIdx.x < 2 && lane == 0 && (i) < 64) g_tpq_trace[0][(row) + (a.NG * 256 > a.NKB * kUnitK ? 12 : 0)][i][e] = clock64();
 #else
 #define TPQ_CTA(e, v)
 #define TPQ_EV(e, i)
@@ -159,16 +164,10 @@ __device__ __forceinline__ void release_loaded(uint64_t* bar, uint32_t dep, int 
   if (all == 0x9e3779b9u && never < 0) sink[threadIdx.x] = 0.f;
   if (lane == 0) mbar_arrive(bar);
 }
-__device__ __forceinline__ int atom_add_acq_rel_gpu(int* p, int v) {
-  int old;
-  asm volatile("atom.add.acq_rel.gpu.global.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
-  return old;
-}
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 // Split-tile hand-off between the CTAs of one GEMV launch, per epilogue warp (lane quarter qw, no
 // cross-warp barrier): each contributor warp stores its 32 columns, then lane 0 adds 1 with release
 // semantics to the tile's counter cnt[4 t + qw] (__syncwarp orders the warp's stores before it); the
@@ -189,7 +188,11 @@ __device__ __forceinline__ int ld_relaxed(const int* p) {
 }
 __device__ __forceinline__ void warp_publish(int* cnt, int lane) {
   __syncwarp();
+#ifdef TPQ_EXP_RELAXED
+  if (lane == 0) asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" ::"l"(cnt), "r"(1) : "memory");
+#else
   if (lane == 0) red_release_add(cnt, 1);
+#endif
 }
 // non-blocking: true (with acquire) once *cnt >= n
 __device__ __forceinline__ bool warp_poll(const int* cnt, int n, int lane) {
@@ -200,10 +203,8 @@ __device__ __forceinline__ bool warp_poll(const int* cnt, int n, int lane) {
   return ok;
 }
 __device__ __forceinline__ void warp_wait(const int* cnt, int n, int lane) {
-  if (lane == 0) {
-    while (ld_relaxed(cnt) < n) __nanosleep(128);
-    (void)ld_acquire(cnt);
-  }
+  if (lane == 0)
+    while (ld_acquire(cnt) < n) __nanosleep(32);
   __syncwarp();
 }
 // acc[m] += p[m * 128] for rows m < M, all loads in flight together
@@ -400,6 +401,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1)
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
     TPQ_CTA(0, gtime())
     TPQ_CTA(3, smid)
+    TPQ_CTA(8, clock64())
     for (int s = 0; s < C::NS; ++s) {
       mbar_init(full + s, 1);
       mbar_init(empty + s, 4);
@@ -543,6 +545,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(a_full + p % C::NAF);
+      if (p == 0 && warp == kDeq0 && lane == 0) { TPQ_CTA(10, gtime()) }
       TPQ_EV(3, p)
       st += 2 * kSets;
       if (st >= C::NS) {
@@ -650,7 +653,11 @@ __global__ void __launch_bounds__(kGemvThreads, 1)
         const uint32_t par = (uint32_t)((seg >> 1) & 1);
         const bool reduce = red_last && seg_end == uend;
         const bool publish = a.cnt && seg_start > tile_start;
+#ifdef TPQ_NO_EARLY
+        if (!have && reduce) {
+#else
         if (!have) {
+#endif
           if (reduce && threadIdx.x == 0) { TPQ_CTA(5, gtime()) }
           for (;;) {  // wait for the accumulators, taking the partial if it arrives first
             int ok = 0;
@@ -685,25 +692,42 @@ __global__ void __launch_bounds__(kGemvThreads, 1)
         const int64_t n = (int64_t)tile * kTileCols + col;
         if (publish) {
           float* mine = a.ws + (size_t)blockIdx.x * 2 * SLOT + col;
+#ifndef TPQ_EXP_NOPUB
   #pragma unroll
           for (int m = 0; m < kNPad; ++m)
             if (m < a.M) __stcg(mine + m * kTileCols, __uint_as_float(v[m]));
+#endif
           warp_publish(a.cnt + 4 * tile + qw, lane);
           if (threadIdx.x == 0) { TPQ_CTA(4, gtime()) }
         } else if (reduce) {
           // CTA order: own partial, then c_first + 1, ..., c_last (deterministic)
           if (threadIdx.x == 0) { TPQ_CTA(7, gtime()) }
-          if (!have) {  // a middle contributor finishes with this CTA: wait for it now
-            warp_wait(cnt_last, nother, lane);
-            add_partial(a.ws + (size_t)(blockIdx.x + 1) * 2 * SLOT + col, a.M, pre);
-            if (threadIdx.x == 0) { TPQ_CTA(6, gtime()) }
-          }
           float acc[kNPad];
   #pragma unroll
           for (int m = 0; m < kNPad; ++m) acc[m] = __uint_as_float(v[m]);
+          int q0 = 1;  // first contributor (c_first + q0) still to add
+          if (have) {
   #pragma unroll
-          for (int m = 0; m < kNPad; ++m) acc[m] += pre[m];
-          for (int q = 1; q < nother; ++q) add_partial(a.ws + (size_t)(blockIdx.x + 1 + q) * 2 * SLOT + col, a.M, acc);
+            for (int m = 0; m < kNPad; ++m) acc[m] += pre[m];
+          } else {  // a middle contributor finishes with this CTA: wait for all of them now
+            warp_wait(cnt_last, nother, lane);
+            q0 = 0;
+            if (threadIdx.x == 0) { TPQ_CTA(6, gtime()) }
+          }
+          // the remaining contributors' partials, up to three per round trip, added in CTA order
+          for (int q = q0; q < nother; q += 3) {
+            const float* src = a.ws + (size_t)(blockIdx.x + 1 + q) * 2 * SLOT + col;
+            float t[3][kNPad];
+  #pragma unroll
+            for (int j = 0; j < 3; ++j)
+  #pragma unroll
+              for (int m = 0; m < kNPad; ++m)
+                t[j][m] = q + j < nother && m < a.M ? __ldcg(src + (size_t)j * 2 * SLOT + m * kTileCols) : 0.f;
+  #pragma unroll
+            for (int j = 0; j < 3; ++j)
+  #pragma unroll
+              for (int m = 0; m < kNPad; ++m) acc[m] += t[j][m];
+          }
   #pragma unroll
           for (int m = 0; m < kNPad; ++m)
             if (m < a.M) a.out[m * a.out_ld + n] = __float2half_rn(acc[m]);
@@ -802,12 +826,17 @@ __global__ void __launch_bounds__(kGemvThreads, 1)
       // one pair = one (tile, k-block): gate record -> gate accumulator, up record -> up accumulator
       const int kbv = (int)(v0 % a.NKB);
       const int nsegv = nv > 0 ? (kbv + nv - 1) / a.NKB + 1 : 0;
+      // k-block and segment of pair p tracked incrementally (no division per pair: the segment
+      // boundaries must not slow the issue)
+      int kbq = kbv + w, sg = 0;
+      while (kbq >= a.NKB) {
+        kbq -= a.NKB;
+        ++sg;
+      }
       for (int p = w; p < np; p += 2) {
-        const int sg = (kbv + p) / a.NKB;
         while (sw < sg) skip_seg();
-        const int lo = sg * a.NKB - kbv > 0 ? sg * a.NKB - kbv : 0;
-        const int hi = (sg + 1) * a.NKB - kbv - 1 < nv - 1 ? (sg + 1) * a.NKB - kbv - 1 : nv - 1;
-        const bool first = p - 2 < lo, last = p + 2 > hi;
+        const bool first = kbq < 2 || p < 2;                  // this issuer's previous pair, p - 2, is outside the segment
+        const bool last = kbq + 2 > a.NKB - 1 || p + 2 > nv - 1;  // so is its next, p + 2
         const int x = p % C::NX, b = p % kSets, d = sg & 1;
         const uint64_t bd0 = bdesc_sw128(xring + 2 * x * C::XU);
         const uint32_t at = tmem + kA0 + b * 2 * C::AU;
@@ -826,24 +855,32 @@ __global__ void __launch_bounds__(kGemvThreads, 1)
         }
         __syncwarp();
         if (last) ++sw;
+        for (kbq += 2; kbq >= a.NKB; kbq -= a.NKB) ++sg;
       }
       while (sw < nsegv) skip_seg();
     } else {
+    // k-block (kbp) and segment (sgp) of unit 2p tracked incrementally: a division per unit in
+    // the segment-boundary path cost ~0.3 us per unit of issue there, which stalled the pipeline
+    // ~1 us at every boundary (tools/trace_pair.py)
+    int kbp = kb0 + 2 * w, sgp = 0;
+    while (kbp >= a.NKB) {
+      kbp -= a.NKB;
+      ++sgp;
+    }
     for (int p = w; p < np; p += 2) {
       const int x = p % C::NX, b = p % kSets;
       const uint64_t bd0 = bdesc_sw128(xring + 2 * x * C::XU);
-      const int i0 = 2 * p, sg = (kb0 + i0) / a.NKB;
-      const int lo = sg * a.NKB - kb0 > 0 ? sg * a.NKB - kb0 : 0;
-      const int hi = (sg + 1) * a.NKB - kb0 - 1 < nu - 1 ? (sg + 1) * a.NKB - kb0 - 1 : nu - 1;
-      while (sw < sg) skip_seg();  // before the a_full wait: a segment's d_full never waits for the next pair's dequant
-      const bool fast = sg == sw && i0 - 3 >= lo && i0 + 4 <= hi;
+      const int i0 = 2 * p;
+      while (sw < sgp) skip_seg();  // before the a_full wait: a segment's d_full never waits for the next pair's dequant
+      // units i0 - 3 .. i0 + 4 (this issuer's previous and next) all inside the segment
+      const bool fast = sgp == sw && kbp >= 3 && kbp + 4 <= a.NKB - 1 && i0 >= 3 && i0 + 4 <= nu - 1;
       const uint32_t at = tmem + kA0 + b * 2 * C::AU;
       TPQ_EV(0, p)
       mbar_wait_backoff(a_full + p % C::NAF, (uint32_t)((p / C::NAF) & 1), 0);
       TPQ_EV(1, p)
       tc_fence_after();
       if (fast) {
-        const uint32_t dt = tmem + (2 * (sg & 1) + w) * kNPad;
+        const uint32_t dt = tmem + (2 * (sgp & 1) + w) * kNPad;
         if (elect_one()) {
           umma_unit16(dt, at, bd0, kIdesc, 1u);
           umma_unit16(dt, at + C::AU, bd0 + (C::XU >> 4), kIdesc, 1u);
@@ -851,40 +888,50 @@ __global__ void __launch_bounds__(kGemvThreads, 1)
         }
         __syncwarp();
         TPQ_EV(3, p)
-        continue;
-      }
+      } else {
 #pragma unroll 1
-      for (int h = 0; h < 2; ++h) {
-        const int i = 2 * p + h;
-        if (i >= nu) break;
-        const int sg = (kb0 + i) / a.NKB;
-        while (sw < sg) skip_seg();
-        const int lo = sg * a.NKB - kb0 > 0 ? sg * a.NKB - kb0 : 0;
-        const int hi = (sg + 1) * a.NKB - kb0 - 1 < nu - 1 ? (sg + 1) * a.NKB - kb0 - 1 : nu - 1;
-        const bool first = (h ? i - 1 : i - 3) < lo, last = (h ? i + 3 : i + 1) > hi;
-        const int d = sg & 1;
-        if (first) {
-          mbar_wait(d_empty + d, (uint32_t)(((sg >> 1) & 1) ^ 1));
-          tc_fence_after();
+        for (int h = 0; h < 2; ++h) {
+          const int i = i0 + h;
+          if (i >= nu) break;
+          int kbi = kbp + h, sgi = sgp;
+          if (kbi >= a.NKB) {
+            kbi -= a.NKB;
+            ++sgi;
+          }
+          while (sw < sgi) skip_seg();
+          // this issuer's previous unit is i - 3 (h = 0) or i - 1, its next i + 1 (h = 0) or i + 3
+          const int back = h ? 1 : 3, fwd = h ? 3 : 1;
+          const bool first = kbi < back || i < back, last = kbi + fwd > a.NKB - 1 || i + fwd > nu - 1;
+          const int d = sgi & 1;
+          if (first) {
+            mbar_wait(d_empty + d, (uint32_t)(((sgi >> 1) & 1) ^ 1));
+            tc_fence_after();
+          }
+          const uint32_t dt = tmem + (2 * d + w) * kNPad;
+          if (elect_one()) {
+            umma_unit16(dt, at + h * C::AU, bd0 + (uint64_t)((h * C::XU) >> 4), kIdesc, first ? 0u : 1u);
+            if (last) umma_commit1(d_full + d);
+          }
+          __syncwarp();
+          if (last) ++sw;
+          if (h == 0) { TPQ_EV(2, p) }
         }
-        const uint32_t dt = tmem + (2 * d + w) * kNPad;
-        if (elect_one()) {
-          umma_unit16(dt, at + h * C::AU, bd0 + (uint64_t)((h * C::XU) >> 4), kIdesc, first ? 0u : 1u);
-          if (last) umma_commit1(d_full + d);
-        }
+        if (elect_one()) umma_commit1(done + p % C::RD);
         __syncwarp();
-        if (last) ++sw;
+        TPQ_EV(3, p)
       }
-      if (elect_one()) umma_commit1(done + p % C::RD);
-      __syncwarp();
-      TPQ_EV(3, p)
+      for (kbp += 4; kbp >= a.NKB; kbp -= a.NKB) ++sgp;
     }
     while (sw < nseg) skip_seg();
+    if (lane == 0) { TPQ_CTA(11, gtime()) }  // (both issuers write; the later one stays)
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (threadIdx.x == 0) { TPQ_CTA(2, gtime()) }
+  if (threadIdx.x == 0) {
+    TPQ_CTA(2, gtime())
+    TPQ_CTA(9, clock64())
+  }
   if (warp == kMmaWarp) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(C::TCOLS) : "memory");
@@ -2156,10 +2203,10 @@ int grid_for(int64_t work, int per_block) {
 // ------------------------------------------------------------------ launchers
 #ifdef TPQ_PROF
 int cta_read(unsigned long long* out) {
-  return cudaMemcpyFromSymbol(out, g_tpq_cta, sizeof(unsigned long long) * 2 * 1024 * 8) != cudaSuccess;
+  return cudaMemcpyFromSymbol(out, g_tpq_cta, sizeof(unsigned long long) * 2 * 1024 * 12) != cudaSuccess;
 }
 int trace_read(long long* out) {
-  return cudaMemcpyFromSymbol(out, g_tpq_trace, sizeof(long long) * 24 * 64 * 4) != cudaSuccess;
+  return cudaMemcpyFromSymbol(out, g_tpq_trace, sizeof(long long) * 2 * 24 * 64 * 4) != cudaSuccess;
 }
 #endif
 bool make_xmap(CUtensorMap* map, const void* base, int64_t K, int rows, int box_rows) {

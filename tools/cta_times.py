@@ -31,9 +31,9 @@ for i in range(10 * R + 1):
 torch.cuda.synchronize()
 L = tpq.lib()
 L.tpq_debug_cta.argtypes = [C.c_void_p]
-buf = (C.c_ulonglong * (2 * 1024 * 8))()
+buf = (C.c_ulonglong * (2 * 1024 * 12))()
 L.tpq_debug_cta(C.cast(buf, C.c_void_p))
-t = np.array(buf, dtype=np.int64).reshape(2, 1024, 8)
+t = np.array(buf, dtype=np.int64).reshape(2, 1024, 12)
 n1 = p.N1 // a.sim_tp
 geo = {1: (p.K1 // 128, n1 // 128), 2: (n1 // 128, p.N2 // 128)}  # (NKB, NT)
 slot = {1: int(n1 > p.K1), 2: int(p.N2 > n1)}  # the kernel files a launch under slot N > K
@@ -48,6 +48,8 @@ for layer in (1, 2):
     print(f"layer {layer}: {grid} CTAs; entry [{ent.min():.2f}, {ent.max():.2f}]; work start [{ws.min():.2f}, {ws.max():.2f}];"
           f" end min {end.min():.2f} p10 {np.percentile(end, 10):.2f} med {np.median(end):.2f} p90 {np.percentile(end, 90):.2f}"
           f" max {end.max():.2f}  (us from layer-1 work start)")
+    mhz = (v[:, 9] - v[:, 8]) / np.maximum(1, v[:, 2] - v[:, 0]) * 1e3
+    print(f"   SM clock over the CTA's life: med {np.median(mhz):.0f} MHz (min {mhz.min():.0f})")
     NKB, NT = geo[layer]
     U = NKB * NT
     pub = v[:, 4] > 0
@@ -58,6 +60,10 @@ for layer in (1, 2):
         wstart, wend, own = us(v[red, 5]), us(v[red, 6]), us(v[red, 7])
         print(f"   reducers {red.sum()}: wait {np.median(wend - wstart):.2f} med / {np.max(wend - wstart):.2f} max; "
               f"own final - wait end med {np.median(own - wend):.2f}; end - own final med {np.median(end[red] - own):.2f} max {np.max(end[red] - own):.2f}")
+    fa, lc = us(v[:, 10]), us(v[:, 11])
+    print(f"   first pair stored - work start: med {np.median(fa - ws):.2f} max {np.max(fa - ws):.2f}; "
+          f"last commit - first pair: med {np.median(lc - fa):.2f} min {np.min(lc - fa):.2f} max {np.max(lc - fa):.2f}; "
+          f"end - last commit: med {np.median(end - lc):.2f} max {np.max(end - lc):.2f}")
     order = np.argsort(end)
     for c in list(order[:3]) + list(order[-8:]):
         u0, u1 = c * U // grid, (c + 1) * U // grid
@@ -70,4 +76,4 @@ for layer in (1, 2):
             ends = [round(float(end[o]), 2) for o in others]
             info += (f" | reduce: wait {us(v[c, 5]):.2f}->{us(v[c, 6]):.2f} own {us(v[c, 7]):.2f}; others {list(others)}"
                      f" publish {pubs} end {ends}")
-        print(f"   cta {c:3d} sm {int(v[c, 3]):3d} end {end[c]:.2f} {info}")
+        print(f"   cta {c:3d} sm {int(v[c, 3]):3d} end {end[c]:.2f} (first pair {fa[c]:.2f}, last commit {lc[c]:.2f}) {info}")

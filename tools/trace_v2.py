@@ -32,9 +32,9 @@ for i in range(10 * R + 1):
 torch.cuda.synchronize()
 L = tpq.lib()
 L.tpq_debug_trace.argtypes = [C.c_void_p]
-tr = (C.c_longlong * (24 * 64 * 4))()
+tr = (C.c_longlong * (2 * 24 * 64 * 4))()
 L.tpq_debug_trace(C.cast(tr, C.c_void_p))
-t = np.array(tr, dtype=np.int64).reshape(24, 64, 4)
+t = np.array(tr, dtype=np.int64).reshape(2, 24, 64, 4)[0]
 t0 = t[t > 0].min()
 rel = np.where(t > 0, t - t0, -1)
 print("pair | set0 w4: start landed free arrive | set1 w8 | set2 w12 | mma18: wait got - commit | mma19")
@@ -52,3 +52,13 @@ for pi in range(6, 45):
     w = [4, 8, 12][pi % 3]
     d.append(rel[w, pi, 3] - rel[w, pi - 3, 3])
 print("set cycle (arrive-to-arrive, cycles) median", np.median(d), "-> per unit", np.median(d) / 6)
+L.tpq_debug_cta.argtypes = [C.c_void_p]
+buf = (C.c_ulonglong * (2 * 1024 * 10))()
+L.tpq_debug_cta(C.cast(buf, C.c_void_p))
+ct = np.array(buf, dtype=np.int64).reshape(2, 1024, 10)
+cta = int(os.environ.get("TPQ_TRACE_CTA_ID", "0"))
+for sl in (0, 1):
+    r = ct[sl, cta]
+    if r[0] > 0:
+        print(f"slot {sl} cta {cta}: entry->work start {(r[1] - r[0]) / 1e3:.2f} us, entry->end {(r[2] - r[0]) / 1e3:.2f} us, "
+              f"clock {(r[9] - r[8]) / max(1, r[2] - r[0]) * 1e3:.0f} MHz; entry clock64 {r[8]} (trace t0 {t0})")
