@@ -889,35 +889,40 @@ __global__ void __launch_bounds__(kGemvThreads, 1)
         __syncwarp();
         TPQ_EV(3, p)
       } else {
-#pragma unroll 1
-        for (int h = 0; h < 2; ++h) {
-          const int i = i0 + h;
-          if (i >= nu) break;
-          int kbi = kbp + h, sgi = sgp;
-          if (kbi >= a.NKB) {
-            kbi -= a.NKB;
-            ++sgi;
-          }
-          while (sw < sgi) skip_seg();
-          // this issuer's previous unit is i - 3 (h = 0) or i - 1, its next i + 1 (h = 0) or i + 3
-          const int back = h ? 1 : 3, fwd = h ? 3 : 1;
-          const bool first = kbi < back || i < back, last = kbi + fwd > a.NKB - 1 || i + fwd > nu - 1;
-          const int d = sgi & 1;
-          if (first) {
-            mbar_wait(d_empty + d, (uint32_t)(((sgi >> 1) & 1) ^ 1));
-            tc_fence_after();
-          }
-          const uint32_t dt = tmem + (2 * d + w) * kNPad;
-          if (elect_one()) {
-            umma_unit16(dt, at + h * C::AU, bd0 + (uint64_t)((h * C::XU) >> 4), kIdesc, first ? 0u : 1u);
-            if (last) umma_commit1(d_full + d);
-          }
-          __syncwarp();
-          if (last) ++sw;
-          if (h == 0) { TPQ_EV(2, p) }
+        // a pair at a segment boundary (or the CTA's first / last pairs): per-unit accumulate and
+        // commit flags, both units still under one elected issue.  This issuer's units around the
+        // pair are i0 - 3, (i0, i0 + 1), i0 + 4, so unit 0 is first if i0 - 3 is outside its segment
+        // and last if i0 + 1 is; unit 1 is first if i0 is outside its segment and last if i0 + 4 is.
+        // A unit 1 in the next segment makes unit 0 last, so no segment is skipped between them.
+        while (sw < sgp) skip_seg();
+        const bool has1 = i0 + 1 < nu;
+        int kb1 = kbp + 1, sg1 = sgp;
+        if (kb1 >= a.NKB) {
+          kb1 -= a.NKB;
+          ++sg1;
         }
-        if (elect_one()) umma_commit1(done + p % C::RD);
+        const bool f0 = kbp < 3 || i0 < 3, l0 = kbp + 1 > a.NKB - 1 || i0 + 1 > nu - 1;
+        const bool f1 = has1 && kb1 < 1, l1 = has1 && (kb1 + 3 > a.NKB - 1 || i0 + 4 > nu - 1);
+        const int d0 = sgp & 1, d1 = sg1 & 1;
+        if (f0) {
+          mbar_wait(d_empty + d0, (uint32_t)(((sgp >> 1) & 1) ^ 1));
+          tc_fence_after();
+        }
+        if (f1) {
+          mbar_wait(d_empty + d1, (uint32_t)(((sg1 >> 1) & 1) ^ 1));
+          tc_fence_after();
+        }
+        if (elect_one()) {
+          umma_unit16(tmem + (2 * d0 + w) * kNPad, at, bd0, kIdesc, f0 ? 0u : 1u);
+          if (l0) umma_commit1(d_full + d0);
+          if (has1) {
+            umma_unit16(tmem + (2 * d1 + w) * kNPad, at + C::AU, bd0 + (C::XU >> 4), kIdesc, f1 ? 0u : 1u);
+            if (l1) umma_commit1(d_full + d1);
+          }
+          umma_commit1(done + p % C::RD);
+        }
         __syncwarp();
+        sw += (int)l0 + (int)l1;
         TPQ_EV(3, p)
       }
       for (kbp += 4; kbp >= a.NKB; kbp -= a.NKB) ++sgp;
