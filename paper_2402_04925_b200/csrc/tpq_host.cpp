@@ -368,7 +368,8 @@ void plan_layer(tpq::LayerDev& L, int64_t K, int64_t N, int G, int device) {
   {
     const int64_t per = std::max<int64_t>(1, L.U / L.grid);
     const int64_t most = (L.NKB - 1 + per - 1) / per + 1;  // contributors of a tile, at most
-    L.inred = most <= 4 && !getenv("TPQ_FIXUP_KERNEL");
+    const char* e = getenv("TPQ_INRED_MAX");  // tuning aid (A/B): most contributors reduced in-kernel
+    L.inred = most <= (e ? atoi(e) : 4) && !getenv("TPQ_FIXUP_KERNEL");
   }
   L.grid_mm = (int)std::min<int64_t>((int64_t)sms, cap);
   if (getenv("TPQ_VERBOSE"))

@@ -97,10 +97,10 @@ __device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity
 
 // Per-CTA timeline (build with -DTPQ_PROF; profiling aid, not in the product build): entry,
 // work start, end (globaltimer ns), SM id, split-tile publish, reducer wait start / end, reducer's own
-// accumulator final, clock64 at entry and end, first pair's A operands stored, last MMA commit, per CTA,
-// per layer (slot 1: N > K, i.e. layer 1 of the MLP).
+// accumulator final, clock64 at entry and end, first pair's A operands stored, last MMA commit, and
+// each epilogue warp's reduced tile stored, per CTA, per layer (slot 1: N > K, i.e. layer 1 of the MLP).
 #ifdef TPQ_PROF
-__device__ unsigned long long g_tpq_cta[2][1024][12];
+__device__ unsigned long long g_tpq_cta[2][1024][16];
 __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -732,6 +732,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1)
           for (int m = 0; m < kNPad; ++m)
             if (m < a.M) a.out[m * a.out_ld + n] = __float2half_rn(acc[m]);
           if (lane == 0) *cnt_last = 0;
+          if (lane == 0) { TPQ_CTA(12 + qw, gtime()) }  // this warp's reduced tile stored
         } else if (seg_start == tile_start && seg_end == tile_end) {
   #pragma unroll
           for (int m = 0; m < kNPad; ++m)
@@ -2208,7 +2209,7 @@ int grid_for(int64_t work, int per_block) {
 // ------------------------------------------------------------------ launchers
 #ifdef TPQ_PROF
 int cta_read(unsigned long long* out) {
-  return cudaMemcpyFromSymbol(out, g_tpq_cta, sizeof(unsigned long long) * 2 * 1024 * 12) != cudaSuccess;
+  return cudaMemcpyFromSymbol(out, g_tpq_cta, sizeof(unsigned long long) * 2 * 1024 * 16) != cudaSuccess;
 }
 int trace_read(long long* out) {
   return cudaMemcpyFromSymbol(out, g_tpq_trace, sizeof(long long) * 2 * 24 * 64 * 4) != cudaSuccess;

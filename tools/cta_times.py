@@ -31,9 +31,9 @@ for i in range(10 * R + 1):
 torch.cuda.synchronize()
 L = tpq.lib()
 L.tpq_debug_cta.argtypes = [C.c_void_p]
-buf = (C.c_ulonglong * (2 * 1024 * 12))()
+buf = (C.c_ulonglong * (2 * 1024 * 16))()
 L.tpq_debug_cta(C.cast(buf, C.c_void_p))
-t = np.array(buf, dtype=np.int64).reshape(2, 1024, 12)
+t = np.array(buf, dtype=np.int64).reshape(2, 1024, 16)
 n1 = p.N1 // a.sim_tp
 geo = {1: (p.K1 // 128, n1 // 128), 2: (n1 // 128, p.N2 // 128)}  # (NKB, NT)
 slot = {1: int(n1 > p.K1), 2: int(p.N2 > n1)}  # the kernel files a launch under slot N > K
@@ -74,6 +74,7 @@ for layer in (1, 2):
             others = range(c + 1, c_last(tile) + 1)
             pubs = [round(float(us(v[o, 4])), 2) if v[o, 4] > 0 else None for o in others]
             ends = [round(float(end[o]), 2) for o in others]
-            info += (f" | reduce: wait {us(v[c, 5]):.2f}->{us(v[c, 6]):.2f} own {us(v[c, 7]):.2f}; others {list(others)}"
+            info += (f" | reduce: wait {us(v[c, 5]):.2f}->{us(v[c, 6]):.2f} own {us(v[c, 7]):.2f} warps done "
+                     f"{[round(float(us(v[c, 12 + q])), 2) for q in range(4)]}; others {list(others)}"
                      f" publish {pubs} end {ends}")
         print(f"   cta {c:3d} sm {int(v[c, 3]):3d} end {end[c]:.2f} (first pair {fa[c]:.2f}, last commit {lc[c]:.2f}) {info}")

@@ -1,6 +1,7 @@
 """Small forwards through every kernel path, for compute-sanitizer (memcheck / racecheck / synccheck):
     compute-sanitizer --tool memcheck python tools/sanitize_fwd.py
-GEMV k_dqgemv (M = 1 / 4 / 5, G = 32 / 128; split fix-up and k_mm_fixup), gated k_dqgemv<G,true>,
+GEMV k_dqgemv (M = 1 / 4 / 5, G = 32 / 128; split tiles reduced in-kernel, and by k_split_fixup /
+k_mm_fixup where a tile spans more than 4 CTA ranges: K1 = 4096, N1 = 1024), gated k_dqgemv<G,true>,
 unordered k_dqgemv<0>, A7 weights-as-TMEM (M = 40), A7 SS GEMM (M = 160), naive staged path with the
 P2 gather (k_gather_ag)."""
 import os
@@ -25,7 +26,8 @@ def run(h, p, M, label):
 
 for (K1, N1, N2, G, M, variant) in [(256, 512, 256, 32, 4, tpq.TPQ_TP_AWARE), (1024, 1408, 640, 128, 1, tpq.TPQ_TP_AWARE),
                                      (1024, 1408, 640, 128, 5, tpq.TPQ_TP_AWARE), (1024, 1408, 640, 128, 40, tpq.TPQ_TP_AWARE),
-                                     (1024, 2048, 768, 128, 160, tpq.TPQ_TP_AWARE), (512, 1024, 512, 64, 5, tpq.TPQ_NAIVE)]:
+                                     (1024, 2048, 768, 128, 160, tpq.TPQ_TP_AWARE), (512, 1024, 512, 64, 5, tpq.TPQ_NAIVE),
+                                     (4096, 1024, 512, 128, 5, tpq.TPQ_TP_AWARE), (4096, 1024, 512, 128, 1, tpq.TPQ_TP_AWARE)]:
     p = synth.make_problem(K1, N1, N2, G, M, seed=1)
     P1, _ = tpq.gptq_reorder(p.w1.g_idx, p.w1.G)
     P2, _ = tpq.gptq_reorder(p.w2.g_idx, p.w2.G)
