@@ -50,6 +50,7 @@ struct LayerDev {
   int grid = 0;            // persistent CTAs of the M <= 16 GEMV (stream-K), at most one per SM
   int grid_mm = 0;         // persistent CTAs of the A7 k_dqgemm (every SM)
   float* ws = nullptr;     // [grid][2 slots][16][128] fp32 stream-K partials of the GEMV (slot 0 = first segment)
+  int csize = 1;           // > 1: cluster split-K (grid = NT x csize, one tile per cluster, DSMEM reduction)
   int inred = 0;           // 1: split tiles reduced inside the GEMV (cnt); 0: by the fix-up kernel after it
   int* cnt = nullptr;      // [NT][4] split-tile arrival counters of the GEMV, one per epilogue warp (zeroed at upload,
                            // re-armed by each reducer)
@@ -67,6 +68,8 @@ enum GatherMode { GATHER_COLS = 0, GATHER_ALLGATHER = 1 };
 
 // Set the GEMV kernel attributes (dynamic shared memory) on the current device; false on failure.
 bool gemv_prepare(int G);
+// Largest cluster size of the GEMV's cluster split-K for group size G (shared-memory landing zone).
+int gemv_cluster_max(int G);
 
 // out[m][n] = sum_k x[m][k] deq(W)[k][n] for M <= 16 rows (k_dqgemv + its split-tile fix-up); x is
 // a [16][K] fp16 row-major buffer described by `xmap` (make_xmap, 16-row boxes), out is [M][out_ld]

@@ -343,7 +343,7 @@ int dev_alloc(void** p, size_t bytes) {
 
 // Stream-K plan: a persistent grid of one CTA per SM, each CTA a contiguous range of
 // (tile, k-block) units; at least 4 units per CTA so the TMA ring has work to overlap.
-void plan_layer(tpq::LayerDev& L, int64_t K, int64_t N, int G, int device) {
+void plan_layer(tpq::LayerDev& L, int64_t K, int64_t N, int G, int device, bool cluster_ok) {
   L.K = K;
   L.N = N;
   L.G = G;
@@ -371,10 +371,34 @@ void plan_layer(tpq::LayerDev& L, int64_t K, int64_t N, int G, int device) {
     const char* e = getenv("TPQ_INRED_MAX");  // tuning aid (A/B): most contributors reduced in-kernel
     L.inred = most <= (e ? atoi(e) : 4) && !getenv("TPQ_FIXUP_KERNEL");
   }
+  // Cluster split-K for small shards: one tile per cluster of cs CTAs, each a 1/cs k-range of it,
+  // reduced through distributed shared memory (no cross-CTA hand-off through L2 at the end of the
+  // layer, no fix-up kernel) -- when the clusters fit on the SMs and a CTA gets at most 4 units more
+  // than under stream-K (~0.8 us, less than the hand-off it removes).  Llama TP=8: layer 1 in
+  // clusters of 4 (16 units vs 14), layer 2 of 2 (14 vs 14): 16.8 -> 13.8 us at M = 1 (same box);
+  // TP=4: both layers of 2, 22.8 -> 19.8 us; TP=1 layer 2 (112 units vs 97) stays stream-K.
+  L.csize = 1;
+  if (cluster_ok && device >= 0) {
+    const int64_t per = (L.U + L.grid - 1) / L.grid;
+    const char* ce = getenv("TPQ_CLUSTER");  // tuning aid: force a cluster size (1 = stream-K)
+    const int cmax = tpq::gemv_cluster_max(G);
+    for (int cs : {4, 2}) {
+      if (cs > cmax || (int64_t)L.NT * cs > sms || L.NKB < 2 * cs) continue;
+      if (ce ? atoi(ce) == cs : (L.NKB + cs - 1) / cs <= per + 4) {
+        L.csize = cs;
+        break;
+      }
+    }
+    if (L.csize > 1) {
+      L.grid = L.NT * L.csize;
+      L.inred = 0;
+    }
+  }
   L.grid_mm = (int)std::min<int64_t>((int64_t)sms, cap);
   if (getenv("TPQ_VERBOSE"))
     fprintf(stderr, "[tpq] layer K=%lld N=%lld G=%d: grid %d over %lld units, split tiles reduced %s\n", (long long)K,
-            (long long)N, G, L.grid, (long long)L.U, L.inred ? "in-kernel" : "by the fix-up kernel");
+            (long long)N, G, L.grid, (long long)L.U,
+            L.csize > 1 ? "in clusters (split-K)" : L.inred ? "in-kernel" : "by the fix-up kernel");
 }
 
 }  // namespace
@@ -573,9 +597,9 @@ int shard_impl(const gptq_layer* w1, const gptq_layer* wu, const gptq_layer* w2,
       h->pk1 = pack_layer(c1, h->E1);
       h->pk2 = pack_layer(c2, h->E2);
     }
-    plan_layer(h->L1, K1, n, w1->G, device);
+    plan_layer(h->L1, K1, n, w1->G, device, !gated && !unord);
     h->L1.gated = gated ? 1 : 0;
-    plan_layer(h->L2, n, N2, w2->G, device);
+    plan_layer(h->L2, n, N2, w2->G, device, !unord);
 
     if (device >= 0) {
       auto upload = [&]() -> int {
@@ -665,7 +689,7 @@ int shard_impl(const gptq_layer* w1, const gptq_layer* wu, const gptq_layer* w2,
           for (int layer = 0; layer < 2; ++layer) {
             const tpq::LayerDev& L = layer ? h->L2 : h->L1;
             auto cta_of = [&](int64_t u) { return (int)(((u + 1) * L.grid + L.U - 1) / L.U) - 1; };
-            for (int t = 0; t < L.NT; ++t)
+            for (int t = 0; t < L.NT && L.csize == 1; ++t)
               if (cta_of((int64_t)t * L.NKB) != cta_of((int64_t)(t + 1) * L.NKB - 1)) sp.push_back(t);
             if (layer == 0) n1 = (int)sp.size();
           }

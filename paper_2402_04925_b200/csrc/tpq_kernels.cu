@@ -168,6 +168,28 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+// cluster helpers (also used by the A7 CTA-pair GEMM)
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// shared::cluster address of the same variable in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa_shared(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// 4-byte store into another CTA's shared memory, completion (bytes) counted on that CTA's barrier
+__device__ __forceinline__ void st_async4(uint32_t dst, float v, uint32_t bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(dst),
+               "r"(__float_as_uint(v)), "r"(bar)
+               : "memory");
+}
+
 // Split-tile hand-off between the CTAs of one GEMV launch, per epilogue warp (lane quarter qw, no
 // cross-warp barrier): each contributor warp stores its 32 columns, then lane 0 adds 1 with release
 // semantics to the tile's counter cnt[4 t + qw] (__syncwarp orders the warp's stores before it); the
@@ -322,6 +344,7 @@ struct GemvArgs {
   const float* colf;  // [N] 2^(24 - E_n): the records hold s' = s 2^E_n per column n
   const uint32_t* meta;  // unordered layers: [ng][ldm] {lo: fp16 s', hi: fp16 C = -z s' 2^-24}
   int64_t ldm;
+  int csize;        // > 1: cluster split-K (grid = NT x csize, clusters of csize CTAs, one tile each)
   int* cnt;         // [NT] split-tile arrival counters (0 between launches); NULL: the fix-up kernel after
 };
 
@@ -371,7 +394,13 @@ struct TC {
   static constexpr int XRING = 0;
   static constexpr int WRING = NX * 2 * XU;
   static constexpr int BARS = WRING + NS * STAGE;
-  static constexpr int SMEM = BARS + 8 * (2 * NS + NX + NAF + RD + 4);
+  static constexpr int SMEM = BARS + 8 * (2 * NS + NX + NAF + RD + 5);
+  // cluster split-K (small shards, GemvArgs::csize > 1): rank 0 of a cluster receives the other ranks'
+  // fp32 partials of its tile, [rank - 1][16 rows][128 columns], in a landing zone after the barriers
+  static constexpr int LAND = (SMEM + 127) / 128 * 128;
+  static constexpr int CSMAX = GT || UN ? 1 : (227 * 1024 - 1024 - LAND) / (kNPad * kTileCols * 4) + 1 >= 4 ? 4
+                               : (227 * 1024 - 1024 - LAND) / (kNPad * kTileCols * 4) + 1 >= 2 ? 2 : 1;
+  static constexpr int SMEM_CL = LAND + (CSMAX - 1) * kNPad * kTileCols * 4;
 };
 
 template <int G, bool GT>
@@ -387,11 +416,16 @@ __global__ void __launch_bounds__(kGemvThreads, 1)
   uint64_t* done = a_full + C::NAF;     // [RD] pair p's MMAs completed (tcgen05.commit)
   uint64_t* d_full = done + C::RD;      // [2] segment accumulators final (both issuers)
   uint64_t* d_empty = d_full + 2;       // [2] epilogue read them (4 warps)
+  uint64_t* land_full = d_empty + 2;    // [1] cluster split-K: the other ranks' partials landed (rank 0)
   __shared__ uint32_t s_tmem;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // stream-K over a.U units; gated (GT): over a.U (tile, k-block) pairs of gate + up records
-  const int64_t v0 = cta_start(blockIdx.x, a.U, a.grid);
-  const int nv = (int)(cta_start(blockIdx.x + 1, a.U, a.grid) - v0);
+  // stream-K over a.U units; gated (GT): over a.U (tile, k-block) pairs of gate + up records.
+  // Cluster split-K (a.csize > 1): cluster c = tile c, rank r takes k-blocks [r NKB / S, (r+1) NKB / S).
+  const int crank = a.csize > 1 ? (int)(blockIdx.x % (unsigned)a.csize) : 0;
+  const int64_t v0 = a.csize > 1 ? (int64_t)(blockIdx.x / a.csize) * a.NKB + crank * a.NKB / a.csize
+                                  : cta_start(blockIdx.x, a.U, a.grid);
+  const int nv = a.csize > 1 ? (crank + 1) * a.NKB / a.csize - crank * a.NKB / a.csize
+                             : (int)(cta_start(blockIdx.x + 1, a.U, a.grid) - v0);
   const int64_t u0 = GT ? 2 * v0 : v0;  // first record of the CTA
   const int nu = GT ? 2 * nv : nv;      // records of the CTA
   const int np = (nu + 1) / 2;
@@ -413,6 +447,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1)
       mbar_init(d_full + d, 2);
       mbar_init(d_empty + d, 4);
     }
+    mbar_init(land_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == kMmaWarp) {
@@ -423,6 +458,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (a.csize > 1) cluster_sync_all();  // rank 0's land_full initialised before any st.async to it
   tc_fence_after();
   pdl_launch_dependents();
   const uint32_t tmem = __shfl_sync(0xffffffffu, s_tmem, 0);
@@ -449,6 +485,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1)
         if (i >= nu) break;
         mbar_wait(full + sh_, phh);
         if (h == 0) { TPQ_EV(1, p) }
+        if (p == 0 && h == 0 && warp == kDeq0 && lane == 0) { TPQ_CTA(14, gtime()) }  // unit 0's weights landed
         const uint8_t* sp = smem + C::WRING + sh_ * C::STAGE;
         if constexpr (C::UN) {
           // Fig. 1 formulation: every row k has its own group g(k); the pair (k, k+1) of a half2 gets
@@ -542,6 +579,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1)
       }
       tmem_wait_st();
       if (xw) mbar_wait(xfull + p % C::NX, (uint32_t)((p / C::NX) & 1));
+      if (p == 0 && warp == kDeq0 && lane == 0) { TPQ_CTA(13, gtime()) }  // pair 0's activations landed
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(a_full + p % C::NAF);
@@ -627,6 +665,49 @@ __global__ void __launch_bounds__(kGemvThreads, 1)
               if (m < a.M) __stcg(mine + (kind * kNPad + m) * kTileCols + col, gu[kind][m]);
         }
         seg_start = seg_end;
+      }
+    } else if (a.csize > 1) {
+      // cluster split-K: one segment, this rank's k-range of tile u0 / NKB.  Ranks > 0 send their
+      // scaled fp32 partial into rank 0's landing zone (st.async, bytes counted on its land_full);
+      // rank 0 adds them in rank order to its own and writes the fp16 tile: no global partials, no
+      // counters, one distributed-shared-memory hop at the end of the layer.
+      const int tile = (int)(u0 / a.NKB);
+      const float up = __ldg(a.colf + (int64_t)tile * kTileCols + col);
+      if (crank == 0 && threadIdx.x == 0)
+        mbar_arrive_expect_tx(land_full, (uint32_t)((a.csize - 1) * a.M * kTileCols * 4));
+      mbar_wait_backoff(d_full, 0u, 256);
+      tc_fence_after();
+      const int hi = nu - 1;  // units 0 .. hi: issuer 0 has pair 0, issuer 1 any pair 1
+      const bool w0 = true, w1 = hi >= 3 || ((hi >> 1) & 1) == 1;
+      uint32_t v[kNPad], v1[kNPad];
+      if (w0) tmem_ld16(tmem + lane_base, v);
+      if (w1) tmem_ld16(tmem + lane_base + kNPad, v1);
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(d_empty);
+      float acc[kNPad];
+  #pragma unroll
+      for (int m = 0; m < kNPad; ++m)
+        acc[m] = up * (w0 ? (w1 ? __uint_as_float(v[m]) + __uint_as_float(v1[m]) : __uint_as_float(v[m]))
+                          : __uint_as_float(v1[m]));
+      if (crank > 0) {
+        const uint32_t dst = mapa_shared(smem + C::LAND, 0) + (uint32_t)(((crank - 1) * kNPad * kTileCols + col) * 4);
+        const uint32_t bar = mapa_shared(land_full, 0);
+  #pragma unroll
+        for (int m = 0; m < kNPad; ++m)
+          if (m < a.M) st_async4(dst + m * kTileCols * 4, acc[m], bar);
+      } else {
+        mbar_wait_backoff(land_full, 0u, 64);
+        const float* land = reinterpret_cast<const float*>(smem + C::LAND) + col;
+        for (int r = 1; r < a.csize; ++r)
+  #pragma unroll
+          for (int m = 0; m < kNPad; ++m)
+            if (m < a.M) acc[m] += land[((r - 1) * kNPad + m) * kTileCols];
+        const int64_t n = (int64_t)tile * kTileCols + col;
+  #pragma unroll
+        for (int m = 0; m < kNPad; ++m)
+          if (m < a.M) a.out[m * a.out_ld + n] = __float2half_rn(acc[m]);
       }
     } else {
       int tile = (int)(u0 / a.NKB);
@@ -1471,17 +1552,6 @@ struct TS2 {
   static_assert(KR >= NA + NB, "done ring");
 };
 
-__device__ __forceinline__ uint32_t cluster_rank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-// shared::cluster address of the same variable in CTA `rank` of the cluster
-__device__ __forceinline__ uint32_t mapa_shared(const void* p, uint32_t rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
-  return r;
-}
 // Arrive on an mbarrier of a CTA of the cluster with the default (.release.cta) semantics: the data
 // it publishes is in shared memory read by the pair's tensor cores (after fence.proxy.async) or is
 // TMEM read back by tcgen05.ld (ordered by tcgen05.fence), not generic loads of another CTA, and
@@ -1512,10 +1582,6 @@ __device__ __forceinline__ void tma_load_3d_pair(void* dst, const CUtensorMap* m
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(leader_bar)
       : "memory");
 }
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-
 // X2 = true: clusters of 4 CTAs = the two k-splits (S = 2, one item per pair) of one 256 x 256 tile.
 // Instead of fp32 partials and k_ss_fixup, the two pairs exchange halves through distributed shared
 // memory once their MMAs are done: split ks finalises columns [128 ks, +128) = its own accumulator
@@ -2282,7 +2348,11 @@ template <int G, bool GT>
 bool prepare_gemv() {
   using C = TC<G, GT>;
   static_assert(C::SMEM <= 227 * 1024 && 2 * C::SMEM > 228 * 1024, "GEMV: one CTA per SM (TMEM 512 columns)");
-  if (cudaFuncSetAttribute(k_dqgemv<G, GT>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM) != cudaSuccess)
+  static_assert(C::SMEM_CL <= 227 * 1024 - 1024, "GEMV: landing zone of the cluster split-K");
+  if (cudaFuncSetAttribute(k_dqgemv<G, GT>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_CL) != cudaSuccess)
+    return false;
+  if (C::CSMAX > 1 &&
+      cudaFuncSetAttribute(k_dqgemv<G, GT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 0) != cudaSuccess)
     return false;
   if (getenv("TPQ_VERBOSE")) {
     cudaFuncAttributes fa;
@@ -2314,7 +2384,14 @@ bool co_res() {
 
 template <int G, bool GT>
 cudaError_t launch_gemv_t(const GemvArgs& a, const CUtensorMap& xmap, const CUtensorMap& xmapu, cudaStream_t st) {
+  if (a.csize > 1)
+    return launch_pdl_cluster(k_dqgemv<G, GT>, a.csize, dim3(a.grid), dim3(kGemvThreads), TC<G, GT>::SMEM_CL, st, a, xmap,
+                              xmapu);
   return launch_pdl(k_dqgemv<G, GT>, dim3(a.grid), dim3(kGemvThreads), TC<G, GT>::SMEM, st, a, xmap, xmapu);
+}
+
+int gemv_cluster_max(int G) {
+  return G == 128 ? TC<128, false>::CSMAX : G == 64 ? TC<64, false>::CSMAX : G == 32 ? TC<32, false>::CSMAX : 1;
 }
 
 cudaError_t launch_gemv(const LayerDev& L, const CUtensorMap& xmap, const CUtensorMap* xmapu, int M, void* out,
@@ -2333,7 +2410,8 @@ cudaError_t launch_gemv(const LayerDev& L, const CUtensorMap& xmap, const CUtens
   a.colf = L.colf;
   a.meta = L.meta;
   a.ldm = L.N;
-  a.cnt = L.inred ? L.cnt : nullptr;
+  a.csize = L.csize;
+  a.cnt = L.inred && L.csize == 1 ? L.cnt : nullptr;
   const CUtensorMap& xu = xmapu ? *xmapu : xmap;
   cudaError_t e = cudaErrorInvalidValue;
   if (L.unord) e = launch_gemv_t<0, false>(a, xmap, xu, st);
@@ -2343,7 +2421,7 @@ cudaError_t launch_gemv(const LayerDev& L, const CUtensorMap& xmap, const CUtens
   else e = L.G == 128 ? launch_gemv_t<128, false>(a, xmap, xu, st)
            : L.G == 64 ? launch_gemv_t<64, false>(a, xmap, xu, st)
            : L.G == 32 ? launch_gemv_t<32, false>(a, xmap, xu, st) : cudaErrorInvalidValue;
-  if (e != cudaSuccess || a.cnt) return e;  // split tiles reduced inside the GEMV
+  if (e != cudaSuccess || a.cnt || a.csize > 1) return e;  // split tiles reduced inside the GEMV
   // split tiles, summed in CTA order after the GEMV: M <= 4 one thread per column with every
   // contributor's rows in flight (k_gemv_fixup); M > 4 (and the gated layer) one warp per row,
   // float4 per lane (k_mm_fixup).  Separate kernels ordered by griddepcontrol.wait beat an in-kernel

@@ -64,6 +64,10 @@ for layer in (1, 2):
     print(f"   first pair stored - work start: med {np.median(fa - ws):.2f} max {np.max(fa - ws):.2f}; "
           f"last commit - first pair: med {np.median(lc - fa):.2f} min {np.min(lc - fa):.2f} max {np.max(lc - fa):.2f}; "
           f"end - last commit: med {np.median(end - lc):.2f} max {np.max(end - lc):.2f}")
+    wl, xl = us(v[:, 14]), us(v[:, 13])
+    print(f"   unit 0 weights landed - work start: med {np.median(wl - ws):.2f} max {np.max(wl - ws):.2f}; "
+          f"pair 0 activations seen - work start: med {np.median(xl - ws):.2f} max {np.max(xl - ws):.2f} "
+          f"(after the pair's dequant)")
     order = np.argsort(end)
     for c in list(order[:3]) + list(order[-8:]):
         u0, u1 = c * U // grid, (c + 1) * U // grid
