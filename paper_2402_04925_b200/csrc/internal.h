@@ -76,8 +76,10 @@ int gemv_cluster_max(int G);
 // fp16 row-major.
 // Gated layer (L.gated): xmap = X[:, P1g] (gate records), xmapu = X[:, P1u] (up records), out =
 // fp16(SiLU(gate) * up); otherwise xmapu may be NULL.
+// pf / pf_bytes (optional): a weight range (the next layer of a small shard) each CTA prefetches a
+// share of into L2 after its own ring fill.
 cudaError_t launch_gemv(const LayerDev& L, const CUtensorMap& xmap, const CUtensorMap* xmapu, int M, void* out,
-                        int64_t out_ld, cudaStream_t st);
+                        int64_t out_ld, cudaStream_t st, const void* pf = nullptr, int64_t pf_bytes = 0);
 
 // A7 (M > 16): out[m][n] = sum_k x[m][k] deq(W)[k][n] for M <= nb rows (nb in {64, 128, 256}), x a
 // [nb][K] fp16 row-major buffer described by xmap (make_xmap with rows = nb), out [M][out_ld].
@@ -129,8 +131,11 @@ cudaError_t launch_gemm_ss(const LayerDev& L, const CUtensorMap& xmap, int M, in
 //   GATHER_COLS:      v(m, k) = src[m*ld + (idx ? idx[k] : k)]; idx holds K int32 indices followed by
 //                     the same K as uint16 (read by the staged-row kernel, K <= 24576 there)
 //   GATHER_ALLGATHER: c = idx[k]; v(m, k) = src[(c / nn) * M * nn + m * nn + c % nn]
+// pf / pf_bytes (optional, staged-row path): a weight range prefetched into L2 before the gather's
+// grid dependency (layer 1 of a small shard).
 cudaError_t launch_gather_rowmajor(const void* src, int64_t ld, const int32_t* idx, int mode, int64_t nn, int M,
-                                   int64_t K, void* dst, cudaStream_t st);
+                                   int64_t K, void* dst, cudaStream_t st, const void* pf = nullptr,
+                                   int64_t pf_bytes = 0);
 
 #ifdef TPQ_PROF
 int cta_read(unsigned long long* out);

@@ -168,6 +168,19 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+// Prefetch part `part` of `parts` of [p, p + bytes) into L2 (bulk prefetch, 32 KB per instruction):
+// the next layer's weights of a small shard, fetched while this kernel is latency-bound.
+__device__ __forceinline__ void prefetch_l2_part(const uint8_t* p, int64_t bytes, int part, int parts) {
+  if (!p || bytes <= 0) return;
+  int64_t lo = bytes * part / parts, hi = bytes * (part + 1) / parts;
+  lo &= ~(int64_t)15;
+  hi &= ~(int64_t)15;
+  for (int64_t o = lo; o < hi; o += 32768) {
+    const uint32_t n = (uint32_t)(hi - o < 32768 ? hi - o : 32768);
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p + o), "r"(n) : "memory");
+  }
+}
+
 // cluster helpers (also used by the A7 CTA-pair GEMM)
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
@@ -344,6 +357,8 @@ struct GemvArgs {
   const float* colf;  // [N] 2^(24 - E_n): the records hold s' = s 2^E_n per column n
   const uint32_t* meta;  // unordered layers: [ng][ldm] {lo: fp16 s', hi: fp16 C = -z s' 2^-24}
   int64_t ldm;
+  const uint8_t* pf;  // (small shards) the next layer's packed weights, prefetched into L2; else NULL
+  int64_t pf_bytes;
   int csize;        // > 1: cluster split-K (grid = NT x csize, clusters of csize CTAs, one tile each)
   int* cnt;         // [NT] split-tile arrival counters (0 between launches); NULL: the fix-up kernel after
 };
@@ -840,6 +855,8 @@ __global__ void __launch_bounds__(kGemvThreads, 1)
       }
       __syncwarp();
     }
+    // small shards: the next layer's weights into L2 behind this CTA's own ring fill
+    if (a.pf && lane == 0) prefetch_l2_part(a.pf, a.pf_bytes, (int)blockIdx.x, (int)gridDim.x);
     for (int i = 0, s = 0, ph = 0; i + C::NS < nu; ++i) {
       TPQ_EV(0, i)
       mbar_wait_sleep(empty + s, (uint32_t)ph);
@@ -2196,7 +2213,8 @@ __global__ void __launch_bounds__(128, 16) k_split_fixup(const float* __restrict
 template <int NT>
 __global__ void __launch_bounds__(NT, NT == 128 ? 16 : 4) k_gather_rows(const __half* __restrict__ src, int ld,
                                                                       const uint16_t* __restrict__ idx, int K,
-                                                                      __half* __restrict__ dst) {
+                                                                      __half* __restrict__ dst, const uint8_t* pf,
+                                                                      int64_t pf_bytes) {
   extern __shared__ __align__(16) uint8_t srow_raw[];
   __shared__ __align__(8) uint64_t row_full;
   __half* srow = reinterpret_cast<__half*>(srow_raw);
@@ -2212,6 +2230,8 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 16 : 4) k_gather_rows(const __
     if (c < c1) ix[p] = __ldg(idx8 + c);
   }
   pdl_launch_dependents();
+  if (pf && threadIdx.x == 0)  // (small shards) layer 1's weights into L2 before the grid dependency
+    prefetch_l2_part(pf, pf_bytes, (int)(blockIdx.y * gridDim.x + blockIdx.x), (int)(gridDim.x * gridDim.y));
   __syncthreads();  // row_full initialised
   pdl_wait();
   if (threadIdx.x == 0) {  // the whole row by one bulk copy: no registers, no per-thread latency chain
@@ -2395,7 +2415,7 @@ int gemv_cluster_max(int G) {
 }
 
 cudaError_t launch_gemv(const LayerDev& L, const CUtensorMap& xmap, const CUtensorMap* xmapu, int M, void* out,
-                        int64_t out_ld, cudaStream_t st) {
+                        int64_t out_ld, cudaStream_t st, const void* pf, int64_t pf_bytes) {
   if (M < 1 || M > kMaxM || (L.gated && !xmapu)) return cudaErrorInvalidValue;
   GemvArgs a;
   a.packed = L.packed;
@@ -2411,6 +2431,8 @@ cudaError_t launch_gemv(const LayerDev& L, const CUtensorMap& xmap, const CUtens
   a.meta = L.meta;
   a.ldm = L.N;
   a.csize = L.csize;
+  a.pf = (const uint8_t*)pf;
+  a.pf_bytes = pf_bytes;
   a.cnt = L.inred && L.csize == 1 ? L.cnt : nullptr;
   const CUtensorMap& xu = xmapu ? *xmapu : xmap;
   cudaError_t e = cudaErrorInvalidValue;
@@ -2548,7 +2570,7 @@ cudaError_t launch_gemm_ss(const LayerDev& L, const CUtensorMap& xmap, int M, in
 }
 
 cudaError_t launch_gather_rowmajor(const void* src, int64_t ld, const int32_t* idx, int mode, int64_t nn, int M,
-                                   int64_t K, void* dst, cudaStream_t st) {
+                                   int64_t K, void* dst, cudaStream_t st, const void* pf, int64_t pf_bytes) {
   // column gather of rows that fit in shared memory, 16-byte aligned rows: stage each row
   if (mode == GATHER_COLS && idx && K % 8 == 0 && K * 2 <= 48 * 1024 && ld % 8 == 0 && ld < (1ll << 31) &&
       reinterpret_cast<uintptr_t>(src) % 16 == 0 && reinterpret_cast<uintptr_t>(idx) % 16 == 0)
@@ -2557,9 +2579,9 @@ cudaError_t launch_gather_rowmajor(const void* src, int64_t ld, const int32_t* i
     const uint16_t* idx16 = reinterpret_cast<const uint16_t*>(idx + K);
     if (M > kMaxM)
       return launch_pdl(k_gather_rows<512>, grid, dim3(512), (size_t)K * 2, st, reinterpret_cast<const __half*>(src),
-                        (int)ld, idx16, (int)K, reinterpret_cast<__half*>(dst));
+                        (int)ld, idx16, (int)K, reinterpret_cast<__half*>(dst), (const uint8_t*)pf, pf_bytes);
     return launch_pdl(k_gather_rows<128>, grid, dim3(128), (size_t)K * 2, st, reinterpret_cast<const __half*>(src),
-                      (int)ld, idx16, (int)K, reinterpret_cast<__half*>(dst));
+                      (int)ld, idx16, (int)K, reinterpret_cast<__half*>(dst), (const uint8_t*)pf, pf_bytes);
   }
   const int64_t total = (int64_t)M * K;
   return launch_pdl(k_gather_rm, dim3(grid_for(total, 256)), dim3(256), 0, st, reinterpret_cast<const __half*>(src),
