@@ -314,19 +314,33 @@ def extra_workload(torch, tpq, shape, M_list, sim_tp, seed, local, dev, stream):
         b = algorithmic_bytes(K1, N1, N2, G, M, tp)[2]
         res[str(M)] = {"us": us, "hbm_frac": b / (us * 1e-6) / 1e9 / peak,
                        "kernel_us": kernel_times(torch, tpq, hs, R, stream, M, 1)}
+    def steps_us(handles, Rh, M, steps):
+        """Graph-timed per-forward time of `steps` run back to back through tpq_mlp_run_step."""
+        per = Rh * max(1, 16 // Rh)
+
+        def one(i):
+            for st_ in steps:
+                handles[i % Rh].run_step(st_, M, stream=stream)
+        with torch.cuda.stream(stream):
+            for i in range(per):
+                one(i)
+            g = graph_of(torch, stream, per, one)
+        return time_graph(torch, stream, g, 40, per)
+
+    if sim_tp:
+        for M in M_list:
+            res[str(M)]["tp_aware_steps_us"] = steps_us(
+                hs, R, M, (tpq.TPQ_STEP_GATHER, tpq.TPQ_STEP_LAYER1, tpq.TPQ_STEP_LAYER2))
     for h in hs:
         h.close()
     if sim_tp:
-        # the naive Alg. 2 rank's extra compute on the same box: its Y1[:, P2] + CHUNK gather (the
-        # AllGather itself needs the other ranks); the layers are the same kernels
+        # the naive Alg. 2 rank's compute on the same box: the same steps plus its Y1[:, P2] + CHUNK
+        # gather (the AllGather itself needs the other ranks; the layers are the same kernels)
         hn, Rn, _ = make_handles(tpq, p, P1, P2, tp, 0, tpq.TPQ_NAIVE, local, step_b, dev)
         for M in M_list:
-            per = Rn * max(1, 16 // Rn)
-            with torch.cuda.stream(stream):
-                for i in range(per):
-                    hn[i % Rn].run_step(tpq.TPQ_STEP_NAIVE_GATHER, M, stream=stream)
-                g = graph_of(torch, stream, per, lambda i: hn[i % Rn].run_step(tpq.TPQ_STEP_NAIVE_GATHER, M, stream=stream))
-            res[str(M)]["naive_p2_gather_us"] = time_graph(torch, stream, g, 40, per)
+            res[str(M)]["naive_p2_gather_us"] = steps_us(hn, Rn, M, (tpq.TPQ_STEP_NAIVE_GATHER,))
+            res[str(M)]["naive_steps_us"] = steps_us(
+                hn, Rn, M, (tpq.TPQ_STEP_GATHER, tpq.TPQ_STEP_LAYER1, tpq.TPQ_STEP_NAIVE_GATHER, tpq.TPQ_STEP_LAYER2))
         for h in hn:
             h.close()
     return res
@@ -608,7 +622,9 @@ def main():
         h.close()
     if world == 1 and not a.quick and not sim_tp and a.shape == "llama70b":
         line["granite20b_tp1"] = extra_workload(torch, tpq, "granite20b", (1, 16), 0, a.seed, local, dev, stream)
-        line["llama70b_tp8_shard"] = extra_workload(torch, tpq, "llama70b", (1, 16), 8, a.seed, local, dev, stream)
+        for k in (2, 4, 8):  # one rank's shard of the TP = k MLP (the metric's TP grid; no collective)
+            line[f"llama70b_tp{k}_shard"] = extra_workload(torch, tpq, "llama70b", (1, 16), k, a.seed, local, dev, stream)
+        line["granite20b_tp8_shard"] = extra_workload(torch, tpq, "granite20b", (1, 16), 8, a.seed, local, dev, stream)
         line["a7_llama70b_tp8_shard"] = a7_line(torch, tpq, "llama70b", a.seed, local, dev, stream)
     if world == 1 and not a.quick and not sim_tp and a.variant == "tp_aware":
         line["unordered_tp1"] = unordered_line(torch, tpq, p, a.shape, local, dev, stream, kt, M)

@@ -227,8 +227,14 @@ typedef struct tpq_mlp_info_t {
   int32_t G1, G2, tp, rank, variant, device;
   int64_t w1_bytes, w2_bytes;       /* packed device bytes of each layer shard (int4 + meta) */
   int64_t units1, units2;           /* (128-column tile x 128-row k-block) units per layer */
-  int32_t grid1, grid2;             /* CTAs launched per layer (stream-K split)          */
+  int32_t grid1, grid2;             /* CTAs launched per layer by the M <= 16 GEMV        */
   int32_t has_comm;
+  /* how the M <= 16 GEMV finishes tiles split between CTAs, per layer: 0 = stream-K with the
+   * split tiles summed inside the kernel (per-tile release counters), 1 = stream-K with the
+   * fix-up kernel after it, c >= 2 = cluster split-K, one tile per cluster of c CTAs reduced
+   * through distributed shared memory.  All sum the partials in a fixed order (bit-identical
+   * repeats). */
+  int32_t split1, split2;
 } tpq_mlp_info_t;
 int tpq_mlp_info(const tpq_mlp* h, tpq_mlp_info_t* out);
 

@@ -49,7 +49,7 @@ class MlpInfo(C.Structure):
                 ("rank", C.c_int32), ("variant", C.c_int32), ("device", C.c_int32),
                 ("w1_bytes", C.c_int64), ("w2_bytes", C.c_int64), ("units1", C.c_int64),
                 ("units2", C.c_int64), ("grid1", C.c_int32), ("grid2", C.c_int32),
-                ("has_comm", C.c_int32)]
+                ("has_comm", C.c_int32), ("split1", C.c_int32), ("split2", C.c_int32)]
 
 
 _lib = None

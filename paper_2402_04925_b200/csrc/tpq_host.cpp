@@ -1028,6 +1028,9 @@ int tpq_mlp_info(const tpq_mlp* h, tpq_mlp_info_t* o) {
   o->grid1 = h->L1.grid;
   o->grid2 = h->L2.grid;
   o->has_comm = h->comm != nullptr;
+  auto split = [](const tpq::LayerDev& L) { return L.csize > 1 ? L.csize : L.inred ? 0 : 1; };
+  o->split1 = split(h->L1);
+  o->split2 = split(h->L2);
   return TPQ_OK;
 }
 

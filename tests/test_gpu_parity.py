@@ -573,3 +573,55 @@ def test_gated_full_size_llama(M):
     _assert_close(_np(Y1), Y1r[:, Ps[2]], "gated Y1 full size (P2 order)")
     _assert_close(_np(Y)[:, cols], Y2r, "gated Y2 full size, sampled")
     h.close()
+
+
+# Split-tile reduction modes of the M <= 16 GEMV (tpq.h tpq_mlp_info_t.split1/2): stream-K with the
+# in-kernel reduction (0), stream-K with the fix-up kernel (1), cluster split-K of 2 or 4 CTAs
+# reduced through distributed shared memory.  TPQ_CLUSTER / TPQ_FIXUP_KERNEL / TPQ_INRED_MAX are
+# read when the handle is built.
+_MODES = {"inkernel": {"TPQ_CLUSTER": "1", "TPQ_INRED_MAX": "64"}, "fixup": {"TPQ_CLUSTER": "1", "TPQ_FIXUP_KERNEL": "1"},
+          "cluster2": {"TPQ_CLUSTER": "2"}, "cluster4": {"TPQ_CLUSTER": "4"}}
+
+
+def _mode_handle(monkeypatch, mode, *args, **kw):
+    for k in ("TPQ_CLUSTER", "TPQ_FIXUP_KERNEL", "TPQ_INRED_MAX"):
+        monkeypatch.delenv(k, raising=False)
+    for k, v in _MODES[mode].items():
+        monkeypatch.setenv(k, v)
+    h = _mlp(*args, **kw)
+    for k in _MODES[mode]:
+        monkeypatch.delenv(k, raising=False)
+    return h
+
+
+@pytest.mark.parametrize("mode", ["inkernel", "fixup", "cluster2", "cluster4"])
+@pytest.mark.parametrize("G", [32, 64, 128])
+@pytest.mark.parametrize("M", [1, 7, 16])
+def test_split_tile_reduction_modes(monkeypatch, mode, G, M):
+    """Every split-tile reduction mode against the oracle's Alg. 3 (tp = 2 shards of a small MLP whose
+    tiles span several CTAs), bit-identical across repeats; the mode is the one requested."""
+    tp = 2
+    p = synth.make_problem(2048, 2048, 2048, G, M, seed=G + M)
+    P1, P2 = _prep(p)
+    L1, L2 = _olayers(p)
+    ref = O.alg3_tp_aware(p.X, L1, L2, tp)
+    X = _dev(p.X)
+    want = {"inkernel": 0, "fixup": 1, "cluster2": 2, "cluster4": 4}[mode]
+    for r in range(tp):
+        h = _mode_handle(monkeypatch, mode, p.w1, p.w2, P1, P2, tp=tp, rank=r, M_max=16)
+        info = h.info
+        if want == 4 and G != 128:  # the landing zone holds one partial only below G = 128
+            assert info.split1 in (1, 0, 2) and info.split2 in (0, 1, 2)
+        else:
+            assert info.split1 == want and info.split2 == want, (info.split1, info.split2)
+        y2, y2b = _empty(M, p.N2), _empty(M, p.N2)
+        h.forward_local(X, M, y2)
+        y1 = _empty(M, p.N1 // tp)
+        h.layer1(X, M, y1)
+        _assert_close(_np(y1), ref["Y1_local"][r], f"{mode} Y1 rank {r}")
+        _assert_close(_np(y2), ref["Y2_local"][r], f"{mode} Y2_local rank {r}")
+        for _ in range(2):
+            h.forward_local(X, M, y2b)
+            torch.cuda.synchronize()
+            assert torch.equal(y2, y2b), f"{mode}: repeated forward differs"
+        h.close()
