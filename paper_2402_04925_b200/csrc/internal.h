@@ -131,11 +131,8 @@ cudaError_t launch_gemm_ss(const LayerDev& L, const CUtensorMap& xmap, int M, in
 //   GATHER_COLS:      v(m, k) = src[m*ld + (idx ? idx[k] : k)]; idx holds K int32 indices followed by
 //                     the same K as uint16 (read by the staged-row kernel, K <= 24576 there)
 //   GATHER_ALLGATHER: c = idx[k]; v(m, k) = src[(c / nn) * M * nn + m * nn + c % nn]
-// pf / pf_bytes (optional, staged-row path): a weight range prefetched into L2 before the gather's
-// grid dependency (layer 1 of a small shard).
 cudaError_t launch_gather_rowmajor(const void* src, int64_t ld, const int32_t* idx, int mode, int64_t nn, int M,
-                                   int64_t K, void* dst, cudaStream_t st, const void* pf = nullptr,
-                                   int64_t pf_bytes = 0);
+                                   int64_t K, void* dst, cudaStream_t st);
 
 #ifdef TPQ_PROF
 int cta_read(unsigned long long* out);

@@ -823,22 +823,23 @@ int check_fwd(tpq_mlp* h, const void* X, int64_t M, const void* Y) {
 
 // One dequant-GEMM layer for mc rows: the GEMV (mc <= 16) or the A7 tensor-core GEMM (mc <= 512:
 // k_dqgemm below 128 rows, the SS GEMMs from 128).
-// Small shards (both layers' weights well inside L2) are latency-bound, not bandwidth-bound: the
-// forward's gather prefetches layer 1's weights into L2 and layer 1 prefetches layer 2's.
+// Small shards (both layers' weights well inside L2) are latency-bound, not bandwidth-bound: layer 1
+// prefetches layer 2's weights into L2 (Llama TP=8 M=1: 13.9 -> 13.5 us; prefetching layer 1's from
+// the gather kernel as well gained nothing and stretched the gather).
 constexpr int64_t kPrefetchMax = 48ll << 20;
-const void* pf_weights(const tpq_mlp* h, int layer, int64_t* bytes) {
+const void* pf_layer2(const tpq_mlp* h, int64_t* bytes) {
   const int64_t b1 = h->L1.U * tpq::unit_bytes(h->L1.G) * (h->L1.gated ? 2 : 1), b2 = h->L2.U * tpq::unit_bytes(h->L2.G);
   *bytes = 0;
   if (b1 + b2 > kPrefetchMax || getenv("TPQ_NO_PF")) return nullptr;
-  *bytes = layer == 1 ? b1 : b2;
-  return layer == 1 ? (const void*)h->L1.packed : (const void*)h->L2.packed;
+  *bytes = b2;
+  return h->L2.packed;
 }
 
 cudaError_t run_layer(tpq_mlp* h, int layer, int mc, void* out, int64_t out_ld, cudaStream_t st) {
   const tpq::LayerDev& L = layer == 1 ? h->L1 : h->L2;
   if (mc <= tpq::kMaxM) {
     int64_t pfb = 0;
-    const void* pf = layer == 1 ? pf_weights(h, 2, &pfb) : nullptr;
+    const void* pf = layer == 1 ? pf_layer2(h, &pfb) : nullptr;
     return tpq::launch_gemv(L, layer == 1 ? h->xmap1 : h->xmap2, layer == 1 && L.gated ? &h->xmap1u : nullptr, mc, out,
                             out_ld, st, pf, pfb);
   }
@@ -852,9 +853,7 @@ cudaError_t run_layer(tpq_mlp* h, int layer, int mc, void* out, int64_t out_ld, 
 int64_t pass_rows(const tpq_mlp* h, int64_t M) { return M <= tpq::kMaxM ? tpq::kMaxM : h->rows; }
 
 int chunk_forward(tpq_mlp* h, const uint16_t* X, int mc, void* Y, cudaStream_t st, bool collective) {
-  int64_t pfb = 0;
-  const void* pf = mc <= tpq::kMaxM ? pf_weights(h, 1, &pfb) : nullptr;
-  TPQ_CUDA(tpq::launch_gather_rowmajor(X, h->K1, h->d_P1, tpq::GATHER_COLS, 0, mc, h->K1, h->d_x1, st, pf, pfb));  // X[:,P1]
+  TPQ_CUDA(tpq::launch_gather_rowmajor(X, h->K1, h->d_P1, tpq::GATHER_COLS, 0, mc, h->K1, h->d_x1, st));  // X[:,P1]
   if (h->gated)  // gate_proj variant: the up layer's own act_order, X[:, P1u]
     TPQ_CUDA(tpq::launch_gather_rowmajor(X, h->K1, h->d_P1u, tpq::GATHER_COLS, 0, mc, h->K1, h->d_x1u, st));
   if (h->variant != TPQ_NAIVE) {

@@ -2213,8 +2213,7 @@ __global__ void __launch_bounds__(128, 16) k_split_fixup(const float* __restrict
 template <int NT>
 __global__ void __launch_bounds__(NT, NT == 128 ? 16 : 4) k_gather_rows(const __half* __restrict__ src, int ld,
                                                                       const uint16_t* __restrict__ idx, int K,
-                                                                      __half* __restrict__ dst, const uint8_t* pf,
-                                                                      int64_t pf_bytes) {
+                                                                      __half* __restrict__ dst) {
   extern __shared__ __align__(16) uint8_t srow_raw[];
   __shared__ __align__(8) uint64_t row_full;
   __half* srow = reinterpret_cast<__half*>(srow_raw);
@@ -2230,8 +2229,6 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 16 : 4) k_gather_rows(const __
     if (c < c1) ix[p] = __ldg(idx8 + c);
   }
   pdl_launch_dependents();
-  if (pf && threadIdx.x == 0)  // (small shards) layer 1's weights into L2 before the grid dependency
-    prefetch_l2_part(pf, pf_bytes, (int)(blockIdx.y * gridDim.x + blockIdx.x), (int)(gridDim.x * gridDim.y));
   __syncthreads();  // row_full initialised
   pdl_wait();
   if (threadIdx.x == 0) {  // the whole row by one bulk copy: no registers, no per-thread latency chain
@@ -2570,7 +2567,7 @@ cudaError_t launch_gemm_ss(const LayerDev& L, const CUtensorMap& xmap, int M, in
 }
 
 cudaError_t launch_gather_rowmajor(const void* src, int64_t ld, const int32_t* idx, int mode, int64_t nn, int M,
-                                   int64_t K, void* dst, cudaStream_t st, const void* pf, int64_t pf_bytes) {
+                                   int64_t K, void* dst, cudaStream_t st) {
   // column gather of rows that fit in shared memory, 16-byte aligned rows: stage each row
   if (mode == GATHER_COLS && idx && K % 8 == 0 && K * 2 <= 48 * 1024 && ld % 8 == 0 && ld < (1ll << 31) &&
       reinterpret_cast<uintptr_t>(src) % 16 == 0 && reinterpret_cast<uintptr_t>(idx) % 16 == 0)
@@ -2579,9 +2576,9 @@ cudaError_t launch_gather_rowmajor(const void* src, int64_t ld, const int32_t* i
     const uint16_t* idx16 = reinterpret_cast<const uint16_t*>(idx + K);
     if (M > kMaxM)
       return launch_pdl(k_gather_rows<512>, grid, dim3(512), (size_t)K * 2, st, reinterpret_cast<const __half*>(src),
-                        (int)ld, idx16, (int)K, reinterpret_cast<__half*>(dst), (const uint8_t*)pf, pf_bytes);
+                        (int)ld, idx16, (int)K, reinterpret_cast<__half*>(dst));
     return launch_pdl(k_gather_rows<128>, grid, dim3(128), (size_t)K * 2, st, reinterpret_cast<const __half*>(src),
-                      (int)ld, idx16, (int)K, reinterpret_cast<__half*>(dst), (const uint8_t*)pf, pf_bytes);
+                      (int)ld, idx16, (int)K, reinterpret_cast<__half*>(dst));
   }
   const int64_t total = (int64_t)M * K;
   return launch_pdl(k_gather_rm, dim3(grid_for(total, 256)), dim3(256), 0, st, reinterpret_cast<const __half*>(src),
