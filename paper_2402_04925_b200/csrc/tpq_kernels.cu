@@ -2254,16 +2254,19 @@ __global__ void __launch_bounds__(NT, NT == 128 ? 16 : 4) k_gather_rows(const __
 
 // Naive Alg. 2 L3-4 for rank r: dst[m][i] = buf[slice(i)][m][off(i)], the AllGather
 // buffer buf[tp][M][n] read through the precomputed (slice, offset) = (c / n, c % n), c = P2[r n + i]
-// (reading c17): one index load and one data load per element, no division.
-__global__ void k_gather_ag(const __half* __restrict__ buf, const int2* __restrict__ so, int n, int M,
-                            __half* __restrict__ dst) {
+// (reading c17).  One element per thread over many SMs: the element loads are scattered 2-byte
+// sectors, bounded by per-SM sector throughput (an 8-column x 4-row per-thread version on few blocks
+// was 1.6x slower) and by the row's spread over all tp slices (staging whole Y1_global rows in shared
+// memory fetches tp x the needed bytes: slower at TP=8); the constant (slice, offset) is loaded
+// before the grid dependency, so only the element load follows it.
+__global__ void __launch_bounds__(256) k_gather_ag(const __half* __restrict__ buf, const int2* __restrict__ so, int n,
+                                                  int M, __half* __restrict__ dst) {
   pdl_launch_dependents();
+  const int i = blockIdx.x * 256 + (int)threadIdx.x, m = blockIdx.y;
+  int2 t = make_int2(0, 0);
+  if (i < n) t = __ldg(so + i);
   pdl_wait();
-  const int m = blockIdx.y;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const int2 t = __ldg(so + i);
-    dst[(int64_t)m * n + i] = buf[((int64_t)t.x * M + m) * n + t.y];
-  }
+  if (i < n) dst[(int64_t)m * n + i] = buf[((int64_t)t.x * M + m) * n + t.y];
 }
 
 struct PartsArg {
@@ -2586,7 +2589,7 @@ cudaError_t launch_gather_rowmajor(const void* src, int64_t ld, const int32_t* i
 }
 
 cudaError_t launch_gather_allgather(const void* buf, const void* so, int n, int M, void* dst, cudaStream_t st) {
-  return launch_pdl(k_gather_ag, dim3((unsigned)std::max(1, std::min(148, (n + 255) / 256)), (unsigned)M), dim3(256), 0,
+  return launch_pdl(k_gather_ag, dim3((unsigned)((n + 255) / 256), (unsigned)M), dim3(256), 0,
                     st, reinterpret_cast<const __half*>(buf), reinterpret_cast<const int2*>(so), n, M,
                     reinterpret_cast<__half*>(dst));
 }
