@@ -11,9 +11,12 @@
 //                  activation slice (tensor TMA); two warps issue tcgen05.mma kind::f16 (M = 128
 //                  columns, N = 16 batch rows, A from TMEM, B = activations from smem); the
 //                  accumulator of a tile segment stays in TMEM and four warps read it back once per
-//                  segment.  Persistent stream-K over units; split tiles are summed after the
-//                  kernel by k_gemv_fixup / k_mm_fixup in CTA order (deterministic); programmatic
-//                  dependent launch (the weight prefetch overlaps the previous kernel).
+//                  segment.  Persistent stream-K over units with tiles split between CTAs
+//                  reduced inside the kernel (per-tile release counters; the fix-up kernels
+//                  k_split_fixup / k_mm_fixup only when a tile spans > 4 CTA ranges), or, for small
+//                  TP shards, cluster split-K reduced through distributed shared memory; fixed sum
+//                  order (deterministic); programmatic dependent launch (the weight prefetch
+//                  overlaps the previous kernel).
 //  k_dqgemm<G,NB>  A7 (17 <= M < 128): same records, weights as the TMEM A operand, N = 64..256.
 //  k_dqgemm_ss<G>  A7 (M >= 128): mixed-input SS GEMM, activations as the reused smem A operand.
 //  k_gather_rm     X[:, P1] gather (Alg. 3 L1) or the naive AllGather re-permute
@@ -2101,70 +2104,6 @@ __global__ void k_mm_fixup(const float* __restrict__ ws, int nb, int M, int NKB,
   *reinterpret_cast<uint2*>(out + (int64_t)m * out_ld + (int64_t)t * kTileCols + j) = pk;
 }
 
-// GEMV stream-K fix-up (tcgen05 GEMV, partial slots [grid][2][16][128]): block t sums tile t's
-// contributors in CTA order, one thread per column, every load of a batch in flight before any add
-// (16 contributors for M = 1, 4 contributors x 4 rows for M <= 4, else 2 x 16).  Used for M <= 4,
-// where k_mm_fixup (one warp per row) cost ~1 us per extra row; k_mm_fixup is faster for M > 4.
-__global__ void __launch_bounds__(128) k_gemv_fixup(const float* __restrict__ ws, int M, int NKB, int64_t U, int grid,
-                                                    __half* __restrict__ out, int64_t out_ld) {
-  pdl_launch_dependents();
-  pdl_wait();  // the partials come from the GEMV just before
-  const int t = blockIdx.x, col = threadIdx.x;
-  const int c_first = cta_of_unit((int64_t)t * NKB, U, grid), c_last = cta_of_unit((int64_t)(t + 1) * NKB - 1, U, grid);
-  if (c_first == c_last) return;  // the tile lies inside one CTA's range: written by the GEMV
-  // slot of contributor c: every CTA after c_first starts inside tile t (slot 0, its first segment);
-  // c_first's slot is 0 only if its range starts exactly at the tile (no 64-bit division per load)
-  const int s_first = cta_start(c_first, U, grid) == (int64_t)t * NKB ? 0 : 1;
-  auto slot_ptr = [&](int c) { return ws + ((size_t)c * 2 + (c > c_first ? 0 : s_first)) * (kNPad * kTileCols) + col; };
-  float r[kNPad];
-#pragma unroll
-  for (int m = 0; m < kNPad; ++m) r[m] = 0.f;
-  if (M == 1) {
-    for (int c = c_first; c <= c_last; c += 16) {
-      float v[16];
-#pragma unroll
-      for (int q = 0; q < 16; ++q) v[q] = __ldcg(slot_ptr(c + q <= c_last ? c + q : c_last));
-#pragma unroll
-      for (int q = 0; q < 16; ++q)
-        if (c + q <= c_last) r[0] += v[q];
-    }
-  } else if (M <= 4) {
-    for (int c = c_first; c <= c_last; c += 4) {
-      float v[4][4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const float* src = slot_ptr(c + q <= c_last ? c + q : c_last);
-#pragma unroll
-        for (int m = 0; m < 4; ++m) v[q][m] = __ldcg(src + m * kTileCols);
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (c + q <= c_last)
-#pragma unroll
-          for (int m = 0; m < 4; ++m) r[m] += v[q][m];
-    }
-  } else {
-    for (int c = c_first; c <= c_last; c += 2) {
-      float v[2][kNPad];
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const float* src = slot_ptr(c + q <= c_last ? c + q : c_last);
-#pragma unroll
-        for (int m = 0; m < kNPad; ++m) v[q][m] = __ldcg(src + m * kTileCols);
-      }
-#pragma unroll
-      for (int q = 0; q < 2; ++q)
-        if (c + q <= c_last)
-#pragma unroll
-          for (int m = 0; m < kNPad; ++m) r[m] += v[q][m];
-    }
-  }
-  __half* o = out + (int64_t)t * kTileCols + col;
-#pragma unroll
-  for (int m = 0; m < kNPad; ++m)
-    if (m < M) o[m * out_ld] = __float2half_rn(r[m]);
-}
-
 // Split-tile fix-up sized to sit beside a GEMV CTA (<= 32 registers x 128 threads, one block per split
 // tile): block b sums split tile tiles[b]'s contributors in CTA order, one thread per column, 4 rows
 // x 2 contributors in flight; gated: gate and up partials, then fp16(SiLU(gate) * up).
@@ -2384,7 +2323,7 @@ bool prepare_gemv() {
 }
 
 bool gemv_prepare(int G) {
-  if (!(max_carveout(k_gather_rm) && max_carveout(k_gather_rows<128>) && max_carveout(k_gather_rows<512>) && max_carveout(k_gather_ag) && max_carveout(k_split_fixup) && max_carveout(k_mm_fixup) && max_carveout(k_gemv_fixup) &&
+  if (!(max_carveout(k_gather_rm) && max_carveout(k_gather_rows<128>) && max_carveout(k_gather_rows<512>) && max_carveout(k_gather_ag) && max_carveout(k_split_fixup) && max_carveout(k_mm_fixup) &&
         max_carveout(k_ss_fixup) && max_carveout(k_sum_partials) && max_carveout(k_dqgemv<0, false>)))
     return false;
   if (!prepare_gemv<0, false>()) return false;  // unordered-g_idx layers (any G)
@@ -2393,13 +2332,6 @@ bool gemv_prepare(int G) {
   if (G == 64) return prepare_gemv<64, false>() && prepare_gemv<64, true>() && prepare_mm_g<64>();
   if (G == 32) return prepare_gemv<32, false>() && prepare_gemv<32, true>() && prepare_mm_g<32>();
   return false;
-}
-
-// Small kernels sized to co-reside with a GEMV CTA (default); TPQ_NO_CORES=1 restores the round-2
-// first-half launch shapes (k_gemv_fixup / k_mm_fixup, 256-thread gathers) for A/B measurements.
-bool co_res() {
-  static const bool on = getenv("TPQ_NO_CORES") == nullptr;
-  return on;
 }
 
 template <int G, bool GT>
@@ -2444,21 +2376,15 @@ cudaError_t launch_gemv(const LayerDev& L, const CUtensorMap& xmap, const CUtens
            : L.G == 64 ? launch_gemv_t<64, false>(a, xmap, xu, st)
            : L.G == 32 ? launch_gemv_t<32, false>(a, xmap, xu, st) : cudaErrorInvalidValue;
   if (e != cudaSuccess || a.cnt || a.csize > 1) return e;  // split tiles reduced inside the GEMV
-  // split tiles, summed in CTA order after the GEMV: M <= 4 one thread per column with every
-  // contributor's rows in flight (k_gemv_fixup); M > 4 (and the gated layer) one warp per row,
-  // float4 per lane (k_mm_fixup).  Separate kernels ordered by griddepcontrol.wait beat an in-kernel
-  // last-arriver reduction (branch exp-fused-forward, profiles/r02_summary.md).
-  // M <= 4: k_split_fixup, one <= 32-register block per split tile that sits beside the next GEMV's
+  // (tiles spanning > 4 CTA ranges) split tiles summed in CTA order after the GEMV by a fix-up
+  // kernel ordered by griddepcontrol.wait.  M <= 4: k_split_fixup, one <= 32-register block per split tile that sits beside the next GEMV's
   // CTA (same-box: Llama TP=1 M=1 59.3 -> 57.0 us); M > 4: k_mm_fixup (one warp per row, float4 per
   // lane, 8 contributors in flight), faster there than 32 registers allow.
-  if (co_res() && L.split_tiles && M <= 4) {
+  if (L.split_tiles && M <= 4) {
     if (L.nsplit == 0) return cudaSuccess;
     return launch_pdl(k_split_fixup, dim3((unsigned)L.nsplit), dim3(128), 0, st, (const float*)L.ws, L.split_tiles, M, L.NKB,
                       L.U, L.grid, reinterpret_cast<__half*>(out), out_ld, L.gated);
   }
-  if (M <= 4 && !L.gated)  // (TPQ_NO_CORES=1 only)
-    return launch_pdl(k_gemv_fixup, dim3((unsigned)L.NT), dim3(128), 0, st, (const float*)L.ws, M, L.NKB, L.U, L.grid,
-                      reinterpret_cast<__half*>(out), out_ld);
   return launch_pdl(k_mm_fixup, dim3((unsigned)L.NT, (unsigned)((M + 3) / 4)), dim3(128), 0, st, (const float*)L.ws, kNPad,
                     M, L.NKB, L.U, L.grid, reinterpret_cast<__half*>(out), out_ld, L.gated);
 }
@@ -2575,7 +2501,7 @@ cudaError_t launch_gather_rowmajor(const void* src, int64_t ld, const int32_t* i
   if (mode == GATHER_COLS && idx && K % 8 == 0 && K * 2 <= 48 * 1024 && ld % 8 == 0 && ld < (1ll << 31) &&
       reinterpret_cast<uintptr_t>(src) % 16 == 0 && reinterpret_cast<uintptr_t>(idx) % 16 == 0)
   {
-    const dim3 grid((unsigned)M, (unsigned)std::max(1, std::min(16, (co_res() ? 148 : 256) / M)));
+    const dim3 grid((unsigned)M, (unsigned)std::max(1, std::min(16, 148 / M)));
     const uint16_t* idx16 = reinterpret_cast<const uint16_t*>(idx + K);
     if (M > kMaxM)
       return launch_pdl(k_gather_rows<512>, grid, dim3(512), (size_t)K * 2, st, reinterpret_cast<const __half*>(src),
