@@ -599,7 +599,9 @@ def main():
         "step_roofline": {"bytes": step_bytes, "GBps": step_bytes / (ms_per_step * 1e-3) / 1e9,
                           "frac": step_bytes / (ms_per_step * 1e-3) / 1e9 / peak},
         "e2e": e2e,
-        "gpu_launches": K * launches_per_step(M, variant == tpq.TPQ_NAIVE),
+        "gpu_launches": K * launches_per_step(hs[0].info, variant == tpq.TPQ_NAIVE),
+        "split_tile_modes": {"layer1": hs[0].info.split1, "layer2": hs[0].info.split2,
+                             "legend": "0 in-kernel (stream-K), 1 fix-up kernel, c >= 2 cluster split-K of c CTAs"},
         "clocks": clk,
     }
     if world > 1 and variant == tpq.TPQ_TP_AWARE and not a.no_naive:
@@ -655,10 +657,11 @@ def main():
         dist.destroy_process_group()
 
 
-def launches_per_step(M, naive):
-    """Our kernels per forward (M <= 16): the X[:, P1] gather, per layer the GEMV and its split-tile
-    fix-up kernel, and the naive path's P2 gather; NCCL kernels not counted."""
-    return 1 + 2 * 2 + (1 if naive else 0)
+def launches_per_step(info, naive):
+    """Our kernels per forward (M <= 16): the X[:, P1] gather, per layer the GEMV plus a split-tile
+    fix-up kernel where the layer uses one (tpq_mlp_info split mode 1), and the naive path's P2
+    gather; NCCL kernels not counted."""
+    return 1 + 2 + int(info.split1 == 1) + int(info.split2 == 1) + (1 if naive else 0)
 
 
 def time_naive(a, p, P1, P2, tp, rank, local, R, comm, X, Y, stream, sync_all, world, dev, ours_ms):
