@@ -226,11 +226,7 @@ __device__ __forceinline__ int ld_relaxed(const int* p) {
 }
 __device__ __forceinline__ void warp_publish(int* cnt, int lane) {
   __syncwarp();
-#ifdef TPQ_EXP_RELAXED
-  if (lane == 0) asm volatile("red.relaxed.gpu.global.add.s32 [%0], %1;" ::"l"(cnt), "r"(1) : "memory");
-#else
   if (lane == 0) red_release_add(cnt, 1);
-#endif
 }
 // non-blocking: true (with acquire) once *cnt >= n
 __device__ __forceinline__ bool warp_poll(const int* cnt, int n, int lane) {
@@ -752,11 +748,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1)
         const uint32_t par = (uint32_t)((seg >> 1) & 1);
         const bool reduce = red_last && seg_end == uend;
         const bool publish = a.cnt && seg_start > tile_start;
-#ifdef TPQ_NO_EARLY
-        if (!have && reduce) {
-#else
         if (!have) {
-#endif
           if (reduce && threadIdx.x == 0) { TPQ_CTA(5, gtime()) }
           for (;;) {  // wait for the accumulators, taking the partial if it arrives first
             int ok = 0;
@@ -791,11 +783,9 @@ __global__ void __launch_bounds__(kGemvThreads, 1)
         const int64_t n = (int64_t)tile * kTileCols + col;
         if (publish) {
           float* mine = a.ws + (size_t)blockIdx.x * 2 * SLOT + col;
-#ifndef TPQ_EXP_NOPUB
   #pragma unroll
           for (int m = 0; m < kNPad; ++m)
             if (m < a.M) __stcg(mine + m * kTileCols, __uint_as_float(v[m]));
-#endif
           warp_publish(a.cnt + 4 * tile + qw, lane);
           if (threadIdx.x == 0) { TPQ_CTA(4, gtime()) }
         } else if (reduce) {
