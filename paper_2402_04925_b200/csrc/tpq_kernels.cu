@@ -408,7 +408,7 @@ struct TC {
   static constexpr int XRING = 0;
   static constexpr int WRING = NX * 2 * XU;
   static constexpr int BARS = WRING + NS * STAGE;
-  static constexpr int SMEM = BARS + 8 * (2 * NS + NX + NAF + RD + 5);
+  static constexpr int SMEM = BARS + 8 * (2 * NS + NX + NAF + RD + 6);
   // cluster split-K (small shards, GemvArgs::csize > 1): rank 0 of a cluster receives the other ranks'
   // fp32 partials of its tile, [rank - 1][16 rows][128 columns], in a landing zone after the barriers
   static constexpr int LAND = (SMEM + 127) / 128 * 128;
@@ -431,6 +431,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1)
   uint64_t* d_full = done + C::RD;      // [2] segment accumulators final (both issuers)
   uint64_t* d_empty = d_full + 2;       // [2] epilogue read them (4 warps)
   uint64_t* land_full = d_empty + 2;    // [1] cluster split-K: the other ranks' partials landed (rank 0)
+  uint64_t* red_full = land_full + 1;   // [1] stream-K reducer: the contributors' partials staged in smem
   __shared__ uint32_t s_tmem;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // stream-K over a.U units; gated (GT): over a.U (tile, k-block) pairs of gate + up records.
@@ -462,6 +463,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1)
       mbar_init(d_empty + d, 4);
     }
     mbar_init(land_full, 1);
+    mbar_init(red_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == kMmaWarp) {
@@ -739,7 +741,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1)
       const int nother = red_last ? cta_of_unit((lt + 1) * a.NKB - 1, a.U, a.grid) - (int)blockIdx.x : 0;
       int* cnt_last = red_last ? a.cnt + 4 * lt + qw : nullptr;
       float pre[kNPad] = {};  // contributor c_first + 1's partial
-      bool have = !red_last;
+      bool have = !red_last || nother != 1;  // the early take is for a single contributor only
       for (int seg = 0; seg_start < uend; ++seg, ++tile) {
         const int64_t tile_start = (int64_t)tile * a.NKB, tile_end = tile_start + a.NKB;
         const int64_t seg_end = tile_end < uend ? tile_end : uend;  // exclusive
@@ -794,28 +796,37 @@ __global__ void __launch_bounds__(kGemvThreads, 1)
           float acc[kNPad];
   #pragma unroll
           for (int m = 0; m < kNPad; ++m) acc[m] = __uint_as_float(v[m]);
-          int q0 = 1;  // first contributor (c_first + q0) still to add
-          if (have) {
+          if (nother == 1) {  // (tiles shorter than a CTA range: the partial was usually taken early)
+            if (!have) {
+              warp_wait(cnt_last, 1, lane);
+              add_partial(a.ws + (size_t)(blockIdx.x + 1) * 2 * SLOT + col, a.M, pre);
+              if (threadIdx.x == 0) { TPQ_CTA(6, gtime()) }
+            }
   #pragma unroll
             for (int m = 0; m < kNPad; ++m) acc[m] += pre[m];
-          } else {  // a middle contributor finishes with this CTA: wait for all of them now
-            warp_wait(cnt_last, nother, lane);
-            q0 = 0;
-            if (threadIdx.x == 0) { TPQ_CTA(6, gtime()) }
-          }
-          // the remaining contributors' partials, up to three per round trip, added in CTA order
-          for (int q = q0; q < nother; q += 3) {
-            const float* src = a.ws + (size_t)(blockIdx.x + 1 + q) * 2 * SLOT + col;
-            float t[3][kNPad];
-  #pragma unroll
-            for (int j = 0; j < 3; ++j)
+          } else {
+            // Several contributors (middle CTAs finish with this one): once all four warps' counters
+            // are complete, thread 0 bulk-copies every partial (M rows) into the activation ring --
+            // free, every MMA of this CTA has completed -- so all of them arrive in one round trip
+            // whatever the register budget, then each warp adds its columns in CTA order.
+            float* stage = reinterpret_cast<float*>(smem + C::XRING);
+            const int nst = nother < C::WRING / (SLOT * 4) ? nother : C::WRING / (SLOT * 4);
+            if (threadIdx.x == 0) {
+              for (int w = 0; w < 4; ++w)
+                while (ld_acquire(a.cnt + 4 * lt + w) < nother) __nanosleep(32);
+              asm volatile("fence.proxy.async.global;" ::: "memory");  // generic stores -> bulk-copy reads
+              mbar_arrive_expect_tx(red_full, (uint32_t)(nst * a.M * kTileCols * 4));
+              for (int q = 0; q < nst; ++q)
+                bulk_g2s(stage + q * SLOT, a.ws + (size_t)(blockIdx.x + 1 + q) * 2 * SLOT, (uint32_t)(a.M * kTileCols * 4),
+                         red_full, policy_evict_first());
+              TPQ_CTA(6, gtime())
+            }
+            mbar_wait(red_full, 0u);
+            for (int q = 0; q < nst; ++q)
   #pragma unroll
               for (int m = 0; m < kNPad; ++m)
-                t[j][m] = q + j < nother && m < a.M ? __ldcg(src + (size_t)j * 2 * SLOT + m * kTileCols) : 0.f;
-  #pragma unroll
-            for (int j = 0; j < 3; ++j)
-  #pragma unroll
-              for (int m = 0; m < kNPad; ++m) acc[m] += t[j][m];
+                if (m < a.M) acc[m] += stage[q * SLOT + m * kTileCols + col];
+            for (int q = nst; q < nother; ++q) add_partial(a.ws + (size_t)(blockIdx.x + 1 + q) * 2 * SLOT + col, a.M, acc);
           }
   #pragma unroll
           for (int m = 0; m < kNPad; ++m)
