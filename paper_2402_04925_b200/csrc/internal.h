@@ -79,7 +79,8 @@ int gemv_cluster_max(int G);
 // pf / pf_bytes (optional): a weight range (the next layer of a small shard) each CTA prefetches a
 // share of into L2 after its own ring fill.
 cudaError_t launch_gemv(const LayerDev& L, const CUtensorMap& xmap, const CUtensorMap* xmapu, int M, void* out,
-                        int64_t out_ld, cudaStream_t st, const void* pf = nullptr, int64_t pf_bytes = 0);
+                        int64_t out_ld, cudaStream_t st, const void* pf = nullptr, int64_t pf_bytes = 0,
+                        const LayerDev* next = nullptr);
 
 // A7 (M > 16): out[m][n] = sum_k x[m][k] deq(W)[k][n] for M <= nb rows (nb in {64, 128, 256}), x a
 // [nb][K] fp16 row-major buffer described by xmap (make_xmap with rows = nb), out [M][out_ld].

@@ -841,7 +841,7 @@ cudaError_t run_layer(tpq_mlp* h, int layer, int mc, void* out, int64_t out_ld, 
     int64_t pfb = 0;
     const void* pf = layer == 1 ? pf_layer2(h, &pfb) : nullptr;
     return tpq::launch_gemv(L, layer == 1 ? h->xmap1 : h->xmap2, layer == 1 && L.gated ? &h->xmap1u : nullptr, mc, out,
-                            out_ld, st, pf, pfb);
+                            out_ld, st, pf, pfb, layer == 1 ? &h->L2 : nullptr);
   }
   if (mc > kMmRows || (mc >= 128 && !getenv("TPQ_NO_SS")))  // compute-bound: activations as the reused A operand
     return tpq::launch_gemm_ss(L, layer == 1 ? h->ss1 : h->ss2, mc, h->sms, out, out_ld, st);
