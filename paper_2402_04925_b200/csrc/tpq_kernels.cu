@@ -361,6 +361,7 @@ struct GemvArgs {
   const uint8_t* pf_next;  // (full layers) the next layer's records: the first pf_units of each of its
   int64_t pf_U;            // pf_grid stream-K CTAs (c pf_U / pf_grid) are prefetched into L2; else NULL
   int pf_grid, pf_units;
+  int pf_cs, pf_nkb;       // the next layer's cluster size (> 1: CTA c starts at (c / cs) NKB + (c % cs) NKB / cs)
   int csize;        // > 1: cluster split-K (grid = NT x csize, clusters of csize CTAs, one tile each)
   int* cnt;         // [NT] split-tile arrival counters (0 between launches); NULL: the fix-up kernel after
 };
@@ -881,10 +882,12 @@ __global__ void __launch_bounds__(kGemvThreads, 1)
     // full layers: the first units of the next layer's CTA of the same index into L2 once this CTA's
     // own records are all requested, so that CTA's ring fill (it becomes resident when a CTA of this
     // layer exits) hits L2 instead of waiting ~1.5 us on HBM
-    if (a.pf_next && lane == 0 && (int)blockIdx.x < a.pf_grid) {
-      const int64_t s0 = (int64_t)blockIdx.x * a.pf_U / a.pf_grid;
-      prefetch_l2_part(a.pf_next + s0 * C::UB, (int64_t)a.pf_units * C::UB, 0, 1);
-    }
+    if (a.pf_next && lane == 0)
+      for (int c = (int)blockIdx.x; c < a.pf_grid; c += (int)gridDim.x) {
+        const int64_t s0 = a.pf_cs > 1 ? (int64_t)(c / a.pf_cs) * a.pf_nkb + (c % a.pf_cs) * a.pf_nkb / a.pf_cs
+                                       : (int64_t)c * a.pf_U / a.pf_grid;
+        prefetch_l2_part(a.pf_next + s0 * C::UB, (int64_t)a.pf_units * C::UB, 0, 1);
+      }
   } else if (warp == kStageWarp) {
     // ===================== activation stager =====================
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&xmap)) : "memory");
@@ -2378,11 +2381,13 @@ cudaError_t launch_gemv(const LayerDev& L, const CUtensorMap& xmap, const CUtens
   a.pf_bytes = pf_bytes;
   // 0 / 6 / 12 units: Llama TP=1 M=1 51.7 / 50.5 / 50.5 us, M=16 53.4 / 52.1 / 52.2 (same box)
   static const int pf_units = getenv("TPQ_PF_NEXT") ? atoi(getenv("TPQ_PF_NEXT")) : 8;
-  const bool pn = next && !pf && next->csize == 1 && next->G == L.G && !next->gated && !next->unord && pf_units > 0;
+  const bool pn = next && !pf && next->G == L.G && !next->gated && !next->unord && pf_units > 0;
   a.pf_next = pn ? next->packed : nullptr;
   a.pf_U = pn ? next->U : 0;
   a.pf_grid = pn ? next->grid : 0;
   a.pf_units = pf_units;
+  a.pf_cs = pn ? next->csize : 1;
+  a.pf_nkb = pn ? next->NKB : 0;
   a.cnt = L.inred && L.csize == 1 ? L.cnt : nullptr;
   const CUtensorMap& xu = xmapu ? *xmapu : xmap;
   cudaError_t e = cudaErrorInvalidValue;
