@@ -70,6 +70,7 @@ enum GatherMode { GATHER_COLS = 0, GATHER_ALLGATHER = 1 };
 bool gemv_prepare(int G);
 // Largest cluster size of the GEMV's cluster split-K for group size G (shared-memory landing zone).
 int gemv_cluster_max(int G);
+int gemv_cluster_max32(int G);  // the same for the N = 32 pipeline (17 <= M <= 32)
 
 // out[m][n] = sum_k x[m][k] deq(W)[k][n] for M <= 16 rows (k_dqgemv + its split-tile fix-up); x is
 // a [16][K] fp16 row-major buffer described by `xmap` (make_xmap, 16-row boxes), out is [M][out_ld]

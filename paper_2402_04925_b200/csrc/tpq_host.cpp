@@ -287,6 +287,7 @@ struct tpq_mlp {
   int32_t* d_P1u = nullptr;
   void* d_x1u = nullptr;
   CUtensorMap xmap1u = {};
+  CUtensorMap xmap1_32 = {}, xmap2_32 = {};  // 32-row boxes of d_x1 / d_y1 (the N = 32 GEMV, 17 <= M <= 32)
   CUtensorMap mm1[3] = {}, mm2[3] = {};  // A7 views of d_x1 / d_y1 with 64 / 128 / 256 rows
   CUtensorMap ss1 = {}, ss2 = {};        // A7 SS views: 256-row buffers, 128-row boxes
   int sms = 148;
@@ -612,8 +613,10 @@ int shard_impl(const gptq_layer* w1, const gptq_layer* wu, const gptq_layer* w2,
           }
         int r;
         auto A = [&](void** p, size_t b) { return dev_alloc(p, b); };
-        const size_t ws1 = (size_t)h->L1.grid * 2 * tpq::kNPad * tpq::kTileCols * (gated ? 2 : 1);  // [grid][2 slots][gate, up][16][128]
-        const size_t ws2 = (size_t)h->L2.grid * 2 * tpq::kNPad * tpq::kTileCols;
+        // [grid][2 slots][gate, up][16 rows][128]; 32 rows when passes of 17..32 rows run the N = 32 GEMV
+        const size_t wr = M_max > tpq::kMaxM ? 2 * tpq::kNPad : tpq::kNPad;
+        const size_t ws1 = (size_t)h->L1.grid * 2 * wr * tpq::kTileCols * (gated ? 2 : 1);
+        const size_t ws2 = (size_t)h->L2.grid * 2 * wr * tpq::kTileCols;
         h->rows = M_max > tpq::kMaxM ? kGemmRows : tpq::kMaxM;
         const size_t wm1 = M_max > tpq::kMaxM ? (size_t)h->L1.grid_mm * 2 * kMmRows * tpq::kTileCols : 0;
         const size_t wm2 = M_max > tpq::kMaxM ? (size_t)h->L2.grid_mm * 2 * kMmRows * tpq::kTileCols : 0;
@@ -668,6 +671,8 @@ int shard_impl(const gptq_layer* w1, const gptq_layer* wu, const gptq_layer* w2,
         }
         bool mok = tpq::make_xmap(&h->xmap1, h->d_x1, K1, tpq::kNPad) && tpq::make_xmap(&h->xmap2, h->d_y1, n, tpq::kNPad);
         if (h->rows > tpq::kMaxM) {
+          mok = mok && tpq::make_xmap(&h->xmap1_32, h->d_x1, K1, 2 * tpq::kNPad) &&
+                tpq::make_xmap(&h->xmap2_32, h->d_y1, n, 2 * tpq::kNPad);
           for (int v = 0; v < 3; ++v)
             mok = mok && tpq::make_xmap(&h->mm1[v], h->d_x1, K1, 64 << v) && tpq::make_xmap(&h->mm2[v], h->d_y1, n, 64 << v);
           mok = mok && tpq::make_xmap(&h->ss1, h->d_x1, K1, kGemmRows, 128) &&
@@ -821,6 +826,13 @@ int check_fwd(tpq_mlp* h, const void* X, int64_t M, const void* Y) {
 // AllGather (tp > 1); otherwise the naive path must be at tp == 1.
 
 
+// Passes of 17..32 rows run the GEMV pipeline with N = 32 (dequant-bound like M <= 16, one weight
+// pass instead of the A7 GEMM's) for the plain TP-aware / naive MLP.
+bool gemv32(const tpq_mlp* h, int64_t mc) {
+  return mc > tpq::kMaxM && mc <= 2 * tpq::kMaxM && h->rows > tpq::kMaxM && !h->gated && h->variant != TPQ_UNORDERED &&
+         !getenv("TPQ_NO_GEMV32");
+}
+
 // One dequant-GEMM layer for mc rows: the GEMV (mc <= 16) or the A7 tensor-core GEMM (mc <= 512:
 // k_dqgemm below 128 rows, the SS GEMMs from 128).
 // Small shards (both layers' weights well inside L2) are latency-bound, not bandwidth-bound: layer 1
@@ -837,11 +849,16 @@ const void* pf_layer2(const tpq_mlp* h, int64_t* bytes) {
 
 cudaError_t run_layer(tpq_mlp* h, int layer, int mc, void* out, int64_t out_ld, cudaStream_t st) {
   const tpq::LayerDev& L = layer == 1 ? h->L1 : h->L2;
-  if (mc <= tpq::kMaxM) {
+  // N = 32 passes keep the layer's partition: stream-K, or clusters small enough for the N = 32 landing
+  // zone (a layer planned in clusters of 4 -- Llama TP=8 layer 1 -- runs the A7 GEMM instead: its
+  // stream-K fallback with ~6 contributors per tile measured 19.6 against 11.7 us)
+  if (mc <= tpq::kMaxM || (gemv32(h, mc) && L.csize <= tpq::gemv_cluster_max32(L.G))) {
     int64_t pfb = 0;
     const void* pf = layer == 1 ? pf_layer2(h, &pfb) : nullptr;
-    return tpq::launch_gemv(L, layer == 1 ? h->xmap1 : h->xmap2, layer == 1 && L.gated ? &h->xmap1u : nullptr, mc, out,
-                            out_ld, st, pf, pfb, layer == 1 ? &h->L2 : nullptr);
+    const bool w = mc > tpq::kMaxM;
+    return tpq::launch_gemv(L, layer == 1 ? (w ? h->xmap1_32 : h->xmap1) : (w ? h->xmap2_32 : h->xmap2),
+                            layer == 1 && L.gated ? &h->xmap1u : nullptr, mc, out, out_ld, st, pf, pfb,
+                            layer == 1 ? &h->L2 : nullptr);
   }
   if (mc > kMmRows || (mc >= 128 && !getenv("TPQ_NO_SS")))  // compute-bound: activations as the reused A operand
     return tpq::launch_gemm_ss(L, layer == 1 ? h->ss1 : h->ss2, mc, h->sms, out, out_ld, st);
@@ -850,7 +867,9 @@ cudaError_t run_layer(tpq_mlp* h, int layer, int mc, void* out, int64_t out_ld, 
 }
 
 // Rows per pass of the forward: 16 (GEMV) while M <= 16, else up to 512 (A7).
-int64_t pass_rows(const tpq_mlp* h, int64_t M) { return M <= tpq::kMaxM ? tpq::kMaxM : h->rows; }
+int64_t pass_rows(const tpq_mlp* h, int64_t M) {
+  return M <= tpq::kMaxM ? tpq::kMaxM : gemv32(h, M) ? 2 * tpq::kMaxM : h->rows;
+}
 
 int chunk_forward(tpq_mlp* h, const uint16_t* X, int mc, void* Y, cudaStream_t st, bool collective) {
   TPQ_CUDA(tpq::launch_gather_rowmajor(X, h->K1, h->d_P1, tpq::GATHER_COLS, 0, mc, h->K1, h->d_x1, st));  // X[:,P1]

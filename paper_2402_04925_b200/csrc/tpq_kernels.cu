@@ -269,6 +269,12 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t* v) {
       : "r"(taddr)
       : "memory");
 }
+// NP consecutive TMEM columns of this lane (NP / 16 loads)
+template <int NP>
+__device__ __forceinline__ void tmem_ld_np(uint32_t taddr, uint32_t* v) {
+#pragma unroll
+  for (int j = 0; j < NP / 16; ++j) tmem_ld16(taddr + 16 * j, v + 16 * j);
+}
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
@@ -299,6 +305,7 @@ __device__ __forceinline__ void umma_commit1(uint64_t* bar) {
 // first MMA accumulates iff acc0 != 0.  One asm block so the operands are formed with uniform adds
 // right before the issue (a per-MMA C++ loop cost ~110 instructions per unit, most of them
 // control flow, which the issuing warp could not afford among four dequant warps per SMSP).
+template <int HB = 128>  // descriptor units (16 B) from a slice's k-half 0 to k-half 1: NP rows x 128 B / 16
 __device__ __forceinline__ void umma_unit16(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc, uint32_t acc0) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t.reg .b32 a1, a2, a3, a4, a5, a6, a7;\n\t"
@@ -306,8 +313,8 @@ __device__ __forceinline__ void umma_unit16(uint32_t d, uint32_t a, uint64_t b, 
       "setp.ne.b32 p, %4, 0;\n\t"
       "add.u32 a1, %1, 8;\n\tadd.u32 a2, %1, 16;\n\tadd.u32 a3, %1, 24;\n\tadd.u32 a4, %1, 32;\n\t"
       "add.u32 a5, %1, 40;\n\tadd.u32 a6, %1, 48;\n\tadd.u32 a7, %1, 56;\n\t"
-      "add.u64 b1, %2, 2;\n\tadd.u64 b2, %2, 4;\n\tadd.u64 b3, %2, 6;\n\tadd.u64 b4, %2, 128;\n\t"
-      "add.u64 b5, %2, 130;\n\tadd.u64 b6, %2, 132;\n\tadd.u64 b7, %2, 134;\n\t"
+      "add.u64 b1, %2, 2;\n\tadd.u64 b2, %2, 4;\n\tadd.u64 b3, %2, 6;\n\tadd.u64 b4, %2, %5;\n\t"
+      "add.u64 b5, %2, %6;\n\tadd.u64 b6, %2, %7;\n\tadd.u64 b7, %2, %8;\n\t"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], [a1], b1, %3, 1;\n\t"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], [a2], b2, %3, 1;\n\t"
@@ -316,7 +323,7 @@ __device__ __forceinline__ void umma_unit16(uint32_t d, uint32_t a, uint64_t b, 
       "tcgen05.mma.cta_group::1.kind::f16 [%0], [a5], b5, %3, 1;\n\t"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], [a6], b6, %3, 1;\n\t"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], [a7], b7, %3, 1;\n\t}" ::"r"(d),
-      "r"(a), "l"(b), "r"(idesc), "r"(acc0)
+      "r"(a), "l"(b), "r"(idesc), "r"(acc0), "n"(HB), "n"(HB + 2), "n"(HB + 4), "n"(HB + 6)
       : "memory");
 }
 // K-major SWIZZLE_128B smem descriptor (sm_100 version 1, layout type 2 in bits 61-63): rows of
@@ -328,7 +335,8 @@ __device__ __forceinline__ uint64_t bdesc_sw128(uint32_t saddr) {
          (2ull << 61);
 }
 // instruction descriptor: D f32, A/B f16, both K-major, N = 16, M = 128
-constexpr uint32_t kIdesc = (1u << 4) | ((uint32_t)(kNPad >> 3) << 17) | ((uint32_t)(kTileCols >> 4) << 24);
+constexpr uint32_t idesc_n(int n) { return (1u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(kTileCols >> 4) << 24); }
+constexpr uint32_t kIdesc = idesc_n(kNPad);
 
 // ------------------------------------------------------------------ stream-K partition
 // CTA c of `grid` owns units [c U / grid, (c + 1) U / grid) of a layer.
@@ -386,16 +394,19 @@ constexpr int kGemvThreads = 20 * 32;
 // GT: the gated layer 1 of the gate_proj variant (f2, readings c23-c25): records stream as gate(t, kb),
 // up(t, kb) pairs, so a dequant pair IS one (tile, k-block) of both layers; gate and up accumulate in
 // separate TMEM accumulators and the epilogue writes fp16(SiLU(gate) * up).
-template <int G, bool GT = false>
+// NP: batch rows per MMA (N) and per activation slice: 16 for M <= 16, 32 for 17 <= M <= 32 (the same
+// dequant-bound pipeline with twice the MMA N, accumulator columns and activation bytes).
+template <int G, bool GT = false, int NP = kNPad>
 struct TC {
+  static_assert(NP == 16 || (NP == 32 && !GT), "N = 32 for the plain layer only (TMEM budget)");
   static constexpr bool UN = G == 0;
   static_assert(!(UN && GT), "the unordered baseline has no gated variant");
   static constexpr int KG = UN ? 1 : kUnitK / G;
   static constexpr int UB = UN ? kUnitK * kTileCols / 2 + kUnitK : (int)unit_bytes_c(G == 0 ? 128 : G);
   static constexpr int STAGE = (UB + 127) / 128 * 128;
-  static constexpr int NS = 18;                   // weight ring stages (units)
-  static constexpr int XU = kNPad * kUnitK * 2;   // activation bytes per unit
-  static constexpr int NX = 6;                    // activation pair slots
+  static constexpr int NS = NP == 16 ? 18 : 16;                   // weight ring stages (units)
+  static constexpr int XU = NP * kUnitK * 2;   // activation bytes per unit
+  static constexpr int NX = NP == 16 ? 6 : 4;                    // activation pair slots
   static constexpr int AU = kUnitK / 2;           // TMEM columns per unit of A
   static constexpr int RD = 6;                    // done ring: pair p on p % 6
   // a_full(p) on barrier p % NAF: the previous completion there, pair p - 6, had the same MMA issuer
@@ -407,7 +418,9 @@ struct TC {
   // done(p - NX) before reusing slot p % NX: the next one, p - NX + RD >= p, needs its own later load.
   static_assert(RD % kSets == 0 && RD >= NX, "done ring aliasing");
   static constexpr int TCOLS = 512;
-  static constexpr int DC = (GT ? 8 : 4) * kNPad;  // [2 segment buffers][2 issuers][gate, up if GT] x 16 columns
+  static constexpr uint32_t IDESC = idesc_n(NP);
+  static constexpr int HB = NP * 128 / 16;  // k-half offset of a slice in descriptor units
+  static constexpr int DC = (GT ? 8 : 4) * NP;  // [2 segment buffers][2 issuers][gate, up if GT] x 16 columns
   static_assert(DC + kSets * 2 * AU <= TCOLS, "TMEM budget");
   static constexpr int XRING = 0;
   static constexpr int WRING = NX * 2 * XU;
@@ -416,15 +429,15 @@ struct TC {
   // cluster split-K (small shards, GemvArgs::csize > 1): rank 0 of a cluster receives the other ranks'
   // fp32 partials of its tile, [rank - 1][16 rows][128 columns], in a landing zone after the barriers
   static constexpr int LAND = (SMEM + 127) / 128 * 128;
-  static constexpr int CSMAX = GT || UN ? 1 : (227 * 1024 - 1024 - LAND) / (kNPad * kTileCols * 4) + 1 >= 4 ? 4
-                               : (227 * 1024 - 1024 - LAND) / (kNPad * kTileCols * 4) + 1 >= 2 ? 2 : 1;
-  static constexpr int SMEM_CL = LAND + (CSMAX - 1) * kNPad * kTileCols * 4;
+  static constexpr int CSMAX = GT || UN ? 1 : (227 * 1024 - 1024 - LAND) / (NP * kTileCols * 4) + 1 >= 4 ? 4
+                               : (227 * 1024 - 1024 - LAND) / (NP * kTileCols * 4) + 1 >= 2 ? 2 : 1;
+  static constexpr int SMEM_CL = LAND + (CSMAX - 1) * NP * kTileCols * 4;
 };
 
-template <int G, bool GT>
+template <int G, bool GT, int NP>
 __global__ void __launch_bounds__(kGemvThreads, 1)
     k_dqgemv(const GemvArgs a, const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap xmapu) {
-  using C = TC<G, GT>;
+  using C = TC<G, GT, NP>;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BARS);
   uint64_t* full = bars;                // [NS] weight record landed
@@ -621,7 +634,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1)
       int tile = (int)(v0 / a.NKB);
       int64_t seg_start = v0;
       const int64_t vend = v0 + nv;
-      constexpr int SLOT = 2 * kNPad * kTileCols;  // gate then up partials
+      constexpr int SLOT = 2 * NP * kTileCols;  // gate then up partials
       for (int seg = 0; seg_start < vend; ++seg, ++tile) {
         const int64_t tile_start = (int64_t)tile * a.NKB, tile_end = tile_start + a.NKB;
         const int64_t seg_end = tile_end < vend ? tile_end : vend;
@@ -634,16 +647,16 @@ __global__ void __launch_bounds__(kGemvThreads, 1)
         mbar_wait_backoff(d_full + d, (uint32_t)((seg >> 1) & 1), 256);
         tc_fence_after();
         const bool w0 = hi > lo || (lo & 1) == 0, w1 = hi > lo || (lo & 1) == 1;
-        float gu[2][kNPad];
+        float gu[2][NP];
 #pragma unroll
         for (int kind = 0; kind < 2; ++kind) {  // 0 gate, 1 up: accumulator ((2 d + w) 2 + kind) x 16
-          uint32_t v[kNPad], v1[kNPad];
-          const uint32_t base = tmem + lane_base + (4 * d + kind) * kNPad;
-          if (w0) tmem_ld16(base, v);
-          if (w1) tmem_ld16(base + 2 * kNPad, v1);
+          uint32_t v[NP], v1[NP];
+          const uint32_t base = tmem + lane_base + (4 * d + kind) * NP;
+          if (w0) tmem_ld_np<NP>(base, v);
+          if (w1) tmem_ld_np<NP>(base + 2 * NP, v1);
           tmem_wait_ld();
 #pragma unroll
-          for (int m = 0; m < kNPad; ++m)
+          for (int m = 0; m < NP; ++m)
             gu[kind][m] = up * (w0 ? (w1 ? __uint_as_float(v[m]) + __uint_as_float(v1[m]) : __uint_as_float(v[m]))
                                    : __uint_as_float(v1[m]));
         }
@@ -656,8 +669,8 @@ __global__ void __launch_bounds__(kGemvThreads, 1)
 #pragma unroll
           for (int kind = 0; kind < 2; ++kind)
 #pragma unroll
-            for (int m = 0; m < kNPad; ++m)
-              if (m < a.M) __stcg(mine + (kind * kNPad + m) * kTileCols, gu[kind][m]);
+            for (int m = 0; m < NP; ++m)
+              if (m < a.M) __stcg(mine + (kind * NP + m) * kTileCols, gu[kind][m]);
           warp_publish(cnt, lane);
         } else if (reduce) {
           const int nother = cta_of_unit(tile_end - 1, a.U, a.grid) - (int)blockIdx.x;
@@ -665,15 +678,15 @@ __global__ void __launch_bounds__(kGemvThreads, 1)
           for (int q = 0; q < nother; ++q) {  // CTA order after the own partial
             const float* src = a.ws + (size_t)(blockIdx.x + 1 + q) * 2 * SLOT + col;
 #pragma unroll
-            for (int kind = 0; kind < 2; ++kind) add_partial(src + kind * kNPad * kTileCols, a.M, gu[kind]);
+            for (int kind = 0; kind < 2; ++kind) add_partial(src + kind * NP * kTileCols, a.M, gu[kind]);
           }
           if (lane == 0) *cnt = 0;
 #pragma unroll
-          for (int m = 0; m < kNPad; ++m)
+          for (int m = 0; m < NP; ++m)
             if (m < a.M) a.out[m * a.out_ld + n] = __float2half_rn(silu_f(gu[0][m]) * gu[1][m]);
         } else if (seg_start == tile_start && seg_end == tile_end) {
 #pragma unroll
-          for (int m = 0; m < kNPad; ++m)
+          for (int m = 0; m < NP; ++m)
             if (m < a.M) a.out[m * a.out_ld + n] = __float2half_rn(silu_f(gu[0][m]) * gu[1][m]);
         } else {
           // (cnt == NULL) split tile: gate and up partials into this CTA's slot; k_mm_fixup (gated) finishes them
@@ -681,8 +694,8 @@ __global__ void __launch_bounds__(kGemvThreads, 1)
 #pragma unroll
           for (int kind = 0; kind < 2; ++kind)
 #pragma unroll
-            for (int m = 0; m < kNPad; ++m)
-              if (m < a.M) __stcg(mine + (kind * kNPad + m) * kTileCols + col, gu[kind][m]);
+            for (int m = 0; m < NP; ++m)
+              if (m < a.M) __stcg(mine + (kind * NP + m) * kTileCols + col, gu[kind][m]);
         }
         seg_start = seg_end;
       }
@@ -699,41 +712,41 @@ __global__ void __launch_bounds__(kGemvThreads, 1)
       tc_fence_after();
       const int hi = nu - 1;  // units 0 .. hi: issuer 0 has pair 0, issuer 1 any pair 1
       const bool w0 = true, w1 = hi >= 3 || ((hi >> 1) & 1) == 1;
-      uint32_t v[kNPad], v1[kNPad];
-      if (w0) tmem_ld16(tmem + lane_base, v);
-      if (w1) tmem_ld16(tmem + lane_base + kNPad, v1);
+      uint32_t v[NP], v1[NP];
+      if (w0) tmem_ld_np<NP>(tmem + lane_base, v);
+      if (w1) tmem_ld_np<NP>(tmem + lane_base + NP, v1);
       tmem_wait_ld();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(d_empty);
-      float acc[kNPad];
+      float acc[NP];
   #pragma unroll
-      for (int m = 0; m < kNPad; ++m)
+      for (int m = 0; m < NP; ++m)
         acc[m] = up * (w0 ? (w1 ? __uint_as_float(v[m]) + __uint_as_float(v1[m]) : __uint_as_float(v[m]))
                           : __uint_as_float(v1[m]));
       if (crank > 0) {
-        const uint32_t dst = mapa_shared(smem + C::LAND, 0) + (uint32_t)(((crank - 1) * kNPad * kTileCols + col) * 4);
+        const uint32_t dst = mapa_shared(smem + C::LAND, 0) + (uint32_t)(((crank - 1) * NP * kTileCols + col) * 4);
         const uint32_t bar = mapa_shared(land_full, 0);
   #pragma unroll
-        for (int m = 0; m < kNPad; ++m)
+        for (int m = 0; m < NP; ++m)
           if (m < a.M) st_async4(dst + m * kTileCols * 4, acc[m], bar);
       } else {
         mbar_wait_backoff(land_full, 0u, 64);
         const float* land = reinterpret_cast<const float*>(smem + C::LAND) + col;
         for (int r = 1; r < a.csize; ++r)
   #pragma unroll
-          for (int m = 0; m < kNPad; ++m)
-            if (m < a.M) acc[m] += land[((r - 1) * kNPad + m) * kTileCols];
+          for (int m = 0; m < NP; ++m)
+            if (m < a.M) acc[m] += land[((r - 1) * NP + m) * kTileCols];
         const int64_t n = (int64_t)tile * kTileCols + col;
   #pragma unroll
-        for (int m = 0; m < kNPad; ++m)
+        for (int m = 0; m < NP; ++m)
           if (m < a.M) a.out[m * a.out_ld + n] = __float2half_rn(acc[m]);
       }
     } else {
       int tile = (int)(u0 / a.NKB);
       int64_t seg_start = u0;
       const int64_t uend = u0 + nu;
-      constexpr int SLOT = kNPad * kTileCols;
+      constexpr int SLOT = NP * kTileCols;
       // split tile t (contributors c_first < ... < c_last): c_first holds its first units as its LAST
       // segment and reduces; every later contributor holds it as its FIRST segment and publishes
       // slot 0 -- early in its run, except the middle CTAs of a tile longer than a CTA's range.
@@ -744,8 +757,9 @@ __global__ void __launch_bounds__(kGemvThreads, 1)
       const bool red_last = a.cnt && lt * a.NKB >= u0 && uend < (lt + 1) * a.NKB;
       const int nother = red_last ? cta_of_unit((lt + 1) * a.NKB - 1, a.U, a.grid) - (int)blockIdx.x : 0;
       int* cnt_last = red_last ? a.cnt + 4 * lt + qw : nullptr;
-      float pre[kNPad] = {};  // contributor c_first + 1's partial
-      bool have = !red_last || nother != 1;  // the early take is for a single contributor only
+      float pre[NP] = {};  // contributor c_first + 1's partial
+      // the early take is for a single contributor of an N = 16 pass only (registers)
+      bool have = !red_last || nother != 1 || NP != kNPad;
       for (int seg = 0; seg_start < uend; ++seg, ++tile) {
         const int64_t tile_start = (int64_t)tile * a.NKB, tile_end = tile_start + a.NKB;
         const int64_t seg_end = tile_end < uend ? tile_end : uend;  // exclusive
@@ -774,40 +788,40 @@ __global__ void __launch_bounds__(kGemvThreads, 1)
         tc_fence_after();
         const bool w0 = hi - lo >= 3 || ((lo >> 1) & 1) == 0 || ((hi >> 1) & 1) == 0;
         const bool w1 = hi - lo >= 3 || ((lo >> 1) & 1) == 1 || ((hi >> 1) & 1) == 1;
-        uint32_t v[kNPad], v1[kNPad];
-        const uint32_t dcol = tmem + lane_base + 2 * d * kNPad;
-        if (w0) tmem_ld16(dcol, v);
-        if (w1) tmem_ld16(dcol + kNPad, v1);
+        uint32_t v[NP], v1[NP];
+        const uint32_t dcol = tmem + lane_base + 2 * d * NP;
+        if (w0) tmem_ld_np<NP>(dcol, v);
+        if (w1) tmem_ld_np<NP>(dcol + NP, v1);
         tmem_wait_ld();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(d_empty + d);
   #pragma unroll
-        for (int m = 0; m < kNPad; ++m)
+        for (int m = 0; m < NP; ++m)
           v[m] = __float_as_uint(up * (w0 ? (w1 ? __uint_as_float(v[m]) + __uint_as_float(v1[m]) : __uint_as_float(v[m]))
                                           : __uint_as_float(v1[m])));
         const int64_t n = (int64_t)tile * kTileCols + col;
         if (publish) {
           float* mine = a.ws + (size_t)blockIdx.x * 2 * SLOT + col;
   #pragma unroll
-          for (int m = 0; m < kNPad; ++m)
+          for (int m = 0; m < NP; ++m)
             if (m < a.M) __stcg(mine + m * kTileCols, __uint_as_float(v[m]));
           warp_publish(a.cnt + 4 * tile + qw, lane);
           if (threadIdx.x == 0) { TPQ_CTA(4, gtime()) }
         } else if (reduce) {
           // CTA order: own partial, then c_first + 1, ..., c_last (deterministic)
           if (threadIdx.x == 0) { TPQ_CTA(7, gtime()) }
-          float acc[kNPad];
+          float acc[NP];
   #pragma unroll
-          for (int m = 0; m < kNPad; ++m) acc[m] = __uint_as_float(v[m]);
-          if (nother == 1) {  // (tiles shorter than a CTA range: the partial was usually taken early)
+          for (int m = 0; m < NP; ++m) acc[m] = __uint_as_float(v[m]);
+          if (NP == kNPad && nother == 1) {  // (tiles shorter than a CTA range: the partial was usually taken early)
             if (!have) {
               warp_wait(cnt_last, 1, lane);
               add_partial(a.ws + (size_t)(blockIdx.x + 1) * 2 * SLOT + col, a.M, pre);
               if (threadIdx.x == 0) { TPQ_CTA(6, gtime()) }
             }
   #pragma unroll
-            for (int m = 0; m < kNPad; ++m) acc[m] += pre[m];
+            for (int m = 0; m < NP; ++m) acc[m] += pre[m];
           } else {
             // Several contributors (middle CTAs finish with this one): once all four warps' counters
             // are complete, thread 0 bulk-copies every partial (M rows) into the activation ring --
@@ -828,25 +842,25 @@ __global__ void __launch_bounds__(kGemvThreads, 1)
             mbar_wait(red_full, 0u);
             for (int q = 0; q < nst; ++q)
   #pragma unroll
-              for (int m = 0; m < kNPad; ++m)
+              for (int m = 0; m < NP; ++m)
                 if (m < a.M) acc[m] += stage[q * SLOT + m * kTileCols + col];
             for (int q = nst; q < nother; ++q) add_partial(a.ws + (size_t)(blockIdx.x + 1 + q) * 2 * SLOT + col, a.M, acc);
           }
   #pragma unroll
-          for (int m = 0; m < kNPad; ++m)
+          for (int m = 0; m < NP; ++m)
             if (m < a.M) a.out[m * a.out_ld + n] = __float2half_rn(acc[m]);
           if (lane == 0) *cnt_last = 0;
           if (lane == 0) { TPQ_CTA(12 + qw, gtime()) }  // this warp's reduced tile stored
         } else if (seg_start == tile_start && seg_end == tile_end) {
   #pragma unroll
-          for (int m = 0; m < kNPad; ++m)
+          for (int m = 0; m < NP; ++m)
             if (m < a.M) a.out[m * a.out_ld + n] = __float2half_rn(__uint_as_float(v[m]));
         } else {
           // (cnt == NULL) split tile: partial into this CTA's slot (0 = its first segment, 1 = its
           // last), summed by the fix-up kernel in CTA order after this kernel
           float* mine = a.ws + ((size_t)blockIdx.x * 2 + (seg_start == u0 ? 0 : 1)) * SLOT;
   #pragma unroll
-          for (int m = 0; m < kNPad; ++m)
+          for (int m = 0; m < NP; ++m)
             if (m < a.M) __stcg(mine + m * kTileCols + col, __uint_as_float(v[m]));
         }
         seg_start = seg_end;
@@ -937,7 +951,7 @@ __global__ void __launch_bounds__(kGemvThreads, 1)
       __syncwarp();
       ++sw;
     };
-    static_assert(C::XU == 4096 && C::AU == 64, "umma_unit16 offsets");
+    static_assert(C::AU == 64, "umma_unit16 A offsets");
     if constexpr (GT) {
       // one pair = one (tile, k-block): gate record -> gate accumulator, up record -> up accumulator
       const int kbv = (int)(v0 % a.NKB);
@@ -962,10 +976,10 @@ __global__ void __launch_bounds__(kGemvThreads, 1)
           mbar_wait(d_empty + d, (uint32_t)(((sg >> 1) & 1) ^ 1));
           tc_fence_after();
         }
-        const uint32_t dg = tmem + (4 * d + 2 * w) * kNPad;  // gate; up at + kNPad
+        const uint32_t dg = tmem + (4 * d + 2 * w) * NP;  // gate; up at + NP
         if (elect_one()) {
-          umma_unit16(dg, at, bd0, kIdesc, first ? 0u : 1u);
-          umma_unit16(dg + kNPad, at + C::AU, bd0 + (C::XU >> 4), kIdesc, first ? 0u : 1u);
+          umma_unit16<C::HB>(dg, at, bd0, C::IDESC, first ? 0u : 1u);
+          umma_unit16<C::HB>(dg + NP, at + C::AU, bd0 + (C::XU >> 4), C::IDESC, first ? 0u : 1u);
           if (last) umma_commit1(d_full + d);
           umma_commit1(done + p % C::RD);
         }
@@ -996,10 +1010,10 @@ __global__ void __launch_bounds__(kGemvThreads, 1)
       TPQ_EV(1, p)
       tc_fence_after();
       if (fast) {
-        const uint32_t dt = tmem + (2 * (sgp & 1) + w) * kNPad;
+        const uint32_t dt = tmem + (2 * (sgp & 1) + w) * NP;
         if (elect_one()) {
-          umma_unit16(dt, at, bd0, kIdesc, 1u);
-          umma_unit16(dt, at + C::AU, bd0 + (C::XU >> 4), kIdesc, 1u);
+          umma_unit16<C::HB>(dt, at, bd0, C::IDESC, 1u);
+          umma_unit16<C::HB>(dt, at + C::AU, bd0 + (C::XU >> 4), C::IDESC, 1u);
           umma_commit1(done + p % C::RD);
         }
         __syncwarp();
@@ -1029,10 +1043,10 @@ __global__ void __launch_bounds__(kGemvThreads, 1)
           tc_fence_after();
         }
         if (elect_one()) {
-          umma_unit16(tmem + (2 * d0 + w) * kNPad, at, bd0, kIdesc, f0 ? 0u : 1u);
+          umma_unit16<C::HB>(tmem + (2 * d0 + w) * NP, at, bd0, C::IDESC, f0 ? 0u : 1u);
           if (l0) umma_commit1(d_full + d0);
           if (has1) {
-            umma_unit16(tmem + (2 * d1 + w) * kNPad, at + C::AU, bd0 + (C::XU >> 4), kIdesc, f1 ? 0u : 1u);
+            umma_unit16<C::HB>(tmem + (2 * d1 + w) * NP, at + C::AU, bd0 + (C::XU >> 4), C::IDESC, f1 ? 0u : 1u);
             if (l1) umma_commit1(d_full + d1);
           }
           umma_commit1(done + p % C::RD);
@@ -2313,56 +2327,67 @@ bool max_carveout(Kern k) {
 }
 template <int G>
 bool carveout_g() {
-  return max_carveout(k_dqgemv<G, false>) && max_carveout(k_dqgemv<G, true>) && max_carveout(k_dqgemm<G, 64>) && max_carveout(k_dqgemm<G, 128>) &&
+  return max_carveout(k_dqgemv<G, false, kNPad>) && max_carveout(k_dqgemv<G, true, kNPad>) &&
+         max_carveout(k_dqgemv<G, false, 2 * kNPad>) && max_carveout(k_dqgemm<G, 64>) && max_carveout(k_dqgemm<G, 128>) &&
          max_carveout(k_dqgemm<G, 256>) && max_carveout(k_dqgemm_ss<G, 128>) && max_carveout(k_dqgemm_ss2<G, false>) && max_carveout(k_dqgemm_ss2<G, true>);
 }
 
-template <int G, bool GT>
+template <int G, bool GT, int NP = kNPad>
 bool prepare_gemv() {
-  using C = TC<G, GT>;
+  using C = TC<G, GT, NP>;
   static_assert(C::SMEM <= 227 * 1024 && 2 * C::SMEM > 228 * 1024, "GEMV: one CTA per SM (TMEM 512 columns)");
   static_assert(C::SMEM_CL <= 227 * 1024 - 1024, "GEMV: landing zone of the cluster split-K");
-  if (cudaFuncSetAttribute(k_dqgemv<G, GT>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_CL) != cudaSuccess)
+  if (cudaFuncSetAttribute(k_dqgemv<G, GT, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM_CL) != cudaSuccess)
     return false;
   if (C::CSMAX > 1 &&
-      cudaFuncSetAttribute(k_dqgemv<G, GT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 0) != cudaSuccess)
+      cudaFuncSetAttribute(k_dqgemv<G, GT, NP>, cudaFuncAttributeNonPortableClusterSizeAllowed, 0) != cudaSuccess)
     return false;
   if (getenv("TPQ_VERBOSE")) {
     cudaFuncAttributes fa;
-    cudaFuncGetAttributes(&fa, k_dqgemv<G, GT>);
-    fprintf(stderr, "[tpq] k_dqgemv<%d,%d>: regs %d, local %zu, smem dyn %d\n", G, (int)GT, fa.numRegs, fa.localSizeBytes,
-            C::SMEM);
+    cudaFuncGetAttributes(&fa, k_dqgemv<G, GT, NP>);
+    fprintf(stderr, "[tpq] k_dqgemv<%d,%d,%d>: regs %d, local %zu, smem dyn %d\n", G, (int)GT, NP, fa.numRegs,
+            fa.localSizeBytes, C::SMEM);
   }
   return true;
 }
 
 bool gemv_prepare(int G) {
   if (!(max_carveout(k_gather_rm) && max_carveout(k_gather_rows<128>) && max_carveout(k_gather_rows<512>) && max_carveout(k_gather_ag) && max_carveout(k_split_fixup) && max_carveout(k_mm_fixup) &&
-        max_carveout(k_ss_fixup) && max_carveout(k_sum_partials) && max_carveout(k_dqgemv<0, false>)))
+        max_carveout(k_ss_fixup) && max_carveout(k_sum_partials) && max_carveout(k_dqgemv<0, false, kNPad>)))
     return false;
   if (!prepare_gemv<0, false>()) return false;  // unordered-g_idx layers (any G)
   if (!(G == 128 ? carveout_g<128>() : G == 64 ? carveout_g<64>() : G == 32 ? carveout_g<32>() : false)) return false;
-  if (G == 128) return prepare_gemv<128, false>() && prepare_gemv<128, true>() && prepare_mm_g<128>();
-  if (G == 64) return prepare_gemv<64, false>() && prepare_gemv<64, true>() && prepare_mm_g<64>();
-  if (G == 32) return prepare_gemv<32, false>() && prepare_gemv<32, true>() && prepare_mm_g<32>();
+  if (G == 128)
+    return prepare_gemv<128, false>() && prepare_gemv<128, true>() && prepare_gemv<128, false, 2 * kNPad>() &&
+           prepare_mm_g<128>();
+  if (G == 64)
+    return prepare_gemv<64, false>() && prepare_gemv<64, true>() && prepare_gemv<64, false, 2 * kNPad>() && prepare_mm_g<64>();
+  if (G == 32)
+    return prepare_gemv<32, false>() && prepare_gemv<32, true>() && prepare_gemv<32, false, 2 * kNPad>() && prepare_mm_g<32>();
   return false;
 }
 
-template <int G, bool GT>
+template <int G, bool GT, int NP = kNPad>
 cudaError_t launch_gemv_t(const GemvArgs& a, const CUtensorMap& xmap, const CUtensorMap& xmapu, cudaStream_t st) {
   if (a.csize > 1)
-    return launch_pdl_cluster(k_dqgemv<G, GT>, a.csize, dim3(a.grid), dim3(kGemvThreads), TC<G, GT>::SMEM_CL, st, a, xmap,
-                              xmapu);
-  return launch_pdl(k_dqgemv<G, GT>, dim3(a.grid), dim3(kGemvThreads), TC<G, GT>::SMEM, st, a, xmap, xmapu);
+    return launch_pdl_cluster(k_dqgemv<G, GT, NP>, a.csize, dim3(a.grid), dim3(kGemvThreads), TC<G, GT, NP>::SMEM_CL, st, a,
+                              xmap, xmapu);
+  return launch_pdl(k_dqgemv<G, GT, NP>, dim3(a.grid), dim3(kGemvThreads), TC<G, GT, NP>::SMEM, st, a, xmap, xmapu);
 }
 
 int gemv_cluster_max(int G) {
   return G == 128 ? TC<128, false>::CSMAX : G == 64 ? TC<64, false>::CSMAX : G == 32 ? TC<32, false>::CSMAX : 1;
 }
+int gemv_cluster_max32(int G) {
+  return G == 128 ? TC<128, false, 32>::CSMAX : G == 64 ? TC<64, false, 32>::CSMAX : G == 32 ? TC<32, false, 32>::CSMAX : 1;
+}
 
 cudaError_t launch_gemv(const LayerDev& L, const CUtensorMap& xmap, const CUtensorMap* xmapu, int M, void* out,
                         int64_t out_ld, cudaStream_t st, const void* pf, int64_t pf_bytes, const LayerDev* next) {
-  if (M < 1 || M > kMaxM || (L.gated && !xmapu)) return cudaErrorInvalidValue;
+  // 17 <= M <= 32: the N = 32 pipeline (plain layers; xmap with 32-row boxes) in the layer's own partition
+  // (stream-K with the in-kernel reduction, or clusters that fit the N = 32 landing zone)
+  const bool n32 = M > kMaxM;
+  if (M < 1 || M > 2 * kMaxM || (L.gated && !xmapu) || (n32 && (L.gated || L.unord))) return cudaErrorInvalidValue;
   GemvArgs a;
   a.packed = L.packed;
   a.M = M;
@@ -2377,6 +2402,7 @@ cudaError_t launch_gemv(const LayerDev& L, const CUtensorMap& xmap, const CUtens
   a.meta = L.meta;
   a.ldm = L.N;
   a.csize = L.csize;
+  if (n32 && L.csize > gemv_cluster_max32(L.G)) return cudaErrorInvalidValue;  // (run_layer sends these to A7)
   a.pf = (const uint8_t*)pf;
   a.pf_bytes = pf_bytes;
   // 0 / 6 / 12 units: Llama TP=1 M=1 51.7 / 50.5 / 50.5 us, M=16 53.4 / 52.1 / 52.2 (same box)
@@ -2388,13 +2414,16 @@ cudaError_t launch_gemv(const LayerDev& L, const CUtensorMap& xmap, const CUtens
   a.pf_units = pf_units;
   a.pf_cs = pn ? next->csize : 1;
   a.pf_nkb = pn ? next->NKB : 0;
-  a.cnt = L.inred && L.csize == 1 ? L.cnt : nullptr;
+  a.cnt = (L.inred || n32) && a.csize == 1 ? L.cnt : nullptr;  // N = 32: never the fix-up kernel
   const CUtensorMap& xu = xmapu ? *xmapu : xmap;
   cudaError_t e = cudaErrorInvalidValue;
   if (L.unord) e = launch_gemv_t<0, false>(a, xmap, xu, st);
   else if (L.gated) e = L.G == 128 ? launch_gemv_t<128, true>(a, xmap, xu, st)
                       : L.G == 64 ? launch_gemv_t<64, true>(a, xmap, xu, st)
                       : L.G == 32 ? launch_gemv_t<32, true>(a, xmap, xu, st) : cudaErrorInvalidValue;
+  else if (n32) e = L.G == 128 ? launch_gemv_t<128, false, 2 * kNPad>(a, xmap, xu, st)
+                   : L.G == 64 ? launch_gemv_t<64, false, 2 * kNPad>(a, xmap, xu, st)
+                   : L.G == 32 ? launch_gemv_t<32, false, 2 * kNPad>(a, xmap, xu, st) : cudaErrorInvalidValue;
   else e = L.G == 128 ? launch_gemv_t<128, false>(a, xmap, xu, st)
            : L.G == 64 ? launch_gemv_t<64, false>(a, xmap, xu, st)
            : L.G == 32 ? launch_gemv_t<32, false>(a, xmap, xu, st) : cudaErrorInvalidValue;

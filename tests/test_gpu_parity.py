@@ -420,7 +420,7 @@ def test_wide_scale_range_per_column(M):
 
 
 @pytest.mark.parametrize("tp", [2, 4, 8])
-@pytest.mark.parametrize("M", [1, 16])
+@pytest.mark.parametrize("M", [1, 16, 32])
 def test_full_size_tp_shards(tp, M):
     """Llama-70B shards at TP = 2/4/8 in the launch configuration of a TP-rank (the small-shard
     grid, 5-6 stream-K contributors per layer-1 tile), first and last rank: Y1_local in full and
@@ -441,7 +441,7 @@ def test_full_size_tp_shards(tp, M):
         W2r = O.permute_rows(L2, mp["w2_rows"])
         W2rc = O.OLayer(q=W2r.q[:, cols], s=W2r.s[:, cols], z=W2r.z[:, cols], g=W2r.g, G=W2r.G)
         Y2r = Y1r @ O.dequantize(W2rc)
-        h = tpq.TpMlp(p.w1, p.w2, P1, P2, tp=tp, rank=r, M_max=16)
+        h = tpq.TpMlp(p.w1, p.w2, P1, P2, tp=tp, rank=r, M_max=max(16, M))  # M = 32: the N = 32 GEMV
         Y1 = _empty(M, n)
         h.layer1(X, M, Y1)
         Y2 = _empty(M, p.N2)
@@ -625,3 +625,32 @@ def test_split_tile_reduction_modes(monkeypatch, mode, G, M):
             torch.cuda.synchronize()
             assert torch.equal(y2, y2b), f"{mode}: repeated forward differs"
         h.close()
+
+
+@pytest.mark.parametrize("G", [32, 64, 128])
+@pytest.mark.parametrize("M", [17, 24, 32])
+def test_gemv_n32_passes(G, M):
+    """Passes of 17..32 rows run the GEMV pipeline with N = 32 (tpq_host.cpp gemv32): tiny / ragged
+    shapes at tp = 1 and a tp = 2 shard pair against the oracle, bit-identical repeats."""
+    p = synth.make_problem(1024, 2560, 768, G, M, seed=3 * G + M)
+    P1, P2 = _prep(p)
+    L1, L2 = _olayers(p)
+    X = _dev(p.X)
+    ref = O.alg3_tp_aware(p.X, L1, L2, 1)
+    h = _mlp(p.w1, p.w2, P1, P2, M_max=32)
+    Y, Yb = _empty(M, p.N2), _empty(M, p.N2)
+    h.forward(X, M, Y)
+    _assert_close(_np(Y), ref["Y2"], f"N=32 GEMV M={M} G={G}")
+    h.forward(X, M, Yb)
+    torch.cuda.synchronize()
+    assert torch.equal(Y, Yb)
+    h.close()
+    ref2 = O.alg3_tp_aware(p.X, L1, L2, 2)
+    parts = []
+    for r in range(2):
+        hr = _mlp(p.w1, p.w2, P1, P2, tp=2, rank=r, M_max=32)
+        y2 = _empty(M, p.N2)
+        hr.forward_local(X, M, y2)
+        _assert_close(_np(y2), ref2["Y2_local"][r], f"N=32 GEMV tp=2 rank {r}")
+        parts.append(y2)
+        hr.close()
