@@ -157,13 +157,14 @@ int tpq_mlp_set_comm(tpq_mlp* h, tpq_comm* c); /* c may be NULL to detach */
  *   Y  dev fp16 [M][N2] row-major, caller-owned; identical on every rank on completion.
  * Arithmetic (reading c22): the shard stores each column n's scales as
  * s' = s * 2^E_n (E_n >= 0, exact, the column's largest scale in [2^14, 2^16)); the tensor-core
- * A operand is the fp16 dequantized weight -- M <= 16: fp16(q s' 2^-24 + fp16(-z s' 2^-24)), one
+ * A operand is the fp16 dequantized weight -- passes of M <= 16 rows, and of 17..32 rows on the
+ * plain TP-aware / naive MLP (the same GEMV with N = 32): fp16(q s' 2^-24 + fp16(-z s' 2^-24)), one
  * HFMA2 per pair, i.e. s (q - z) with at most two fp16 roundings, normal while the group's scale
- * is >= ~2^-5 of the column's largest; M > 16: fp16((q - z) s' 2^-12), one rounding of the exact
- * (q - z) -- times fp16 activations, accumulated in fp32 over whole tile segments (the ordered
+ * is >= ~2^-5 of the column's largest; other passes (the A7 tensor-core GEMMs): fp16((q - z) s' 2^-12),
+ * one rounding of the exact (q - z) -- times fp16 activations, accumulated in fp32 over whole tile segments (the ordered
  * groups make the records self-contained), times 2^(24 - E_n) resp. 2^(12 - E_n)
  * in the epilogue (exact); Y1 rounded to fp16 (RN) between the layers (reading c10), fp16
- * AllReduce (c11).
+ * AllReduce (c11).  Tiles split between CTAs are summed in a fixed order (bit-identical repeats).
  * Collective when tp > 1: every rank must call it with the same M (NCCL semantics; a
  * mismatch is a documented precondition violation -> hang, not a status).  Asynchronous on
  * `stream`, no allocation, no host synchronisation, CUDA-graph capturable.
