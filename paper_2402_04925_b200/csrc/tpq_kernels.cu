@@ -404,7 +404,7 @@ struct TC {
   static constexpr int KG = UN ? 1 : kUnitK / G;
   static constexpr int UB = UN ? kUnitK * kTileCols / 2 + kUnitK : (int)unit_bytes_c(G == 0 ? 128 : G);
   static constexpr int STAGE = (UB + 127) / 128 * 128;
-  static constexpr int NS = NP == 16 ? 18 : 16;                   // weight ring stages (units)
+  static constexpr int NS = NP == 16 ? 18 : 12;  // N = 32: 14-18 stages measured alike; 12 leaves a 48 KB landing zone                   // weight ring stages (units)
   static constexpr int XU = NP * kUnitK * 2;   // activation bytes per unit
   static constexpr int NX = NP == 16 ? 6 : 4;                    // activation pair slots
   static constexpr int AU = kUnitK / 2;           // TMEM columns per unit of A
