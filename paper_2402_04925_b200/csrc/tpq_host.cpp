@@ -354,23 +354,23 @@ void plan_layer(tpq::LayerDev& L, int64_t K, int64_t N, int G, int device, bool 
   int sms = 148;
   if (device >= 0) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   const int64_t cap = std::max<int64_t>(1, L.U / 4);
-  // Small shards (< 64 units per SM: Llama / Granite at TP >= 2) are latency-bound, not
-  // bandwidth-bound: 128 of 148 CTAs measured 1-3.5 us faster per forward there (the next kernel
-  // can start on SMs the previous one has already left), while full-size layers need every SM
-  // (profiles/r01_summary.md, grid sweep).
+  // Small shards (< 56 units per SM: Llama / Granite at TP >= 2) are latency-bound, not
+  // bandwidth-bound: 128 of 148 CTAs measured faster per forward there (the next kernel can start on
+  // SMs the previous one has already left; Llama TP=2 31.5 vs 32.6 us at M=1), while full layers need
+  // every SM (Granite TP=1, 62 units per SM: 37.5 with 148 CTAs vs 39.3 with 128).
   int g = sms;
-  if (L.U < 64LL * sms) g = std::max(1, sms * 128 / 148);
+  if (L.U < 56LL * sms) g = std::max(1, sms * 128 / 148);
   if (const char* e = getenv("TPQ_GRID")) g = std::max(1, std::min(sms, atoi(e)));  // tuning aid
   L.grid = (int)std::min<int64_t>((int64_t)g, cap);
-  // Split tiles are reduced inside the GEMV (c_first waits for the later contributors' partials)
-  // unless a tile spans more than 4 CTA ranges: then the middle contributors, which finish with the
-  // reducer, make a chain the separate fix-up kernel resolves faster (Llama TP=8 layer 1: 14 units
-  // per CTA against 64-unit tiles; same-box 22.0 vs 21.4 us at M = 16).
+  // Split tiles are reduced inside the GEMV (c_first waits for the later contributors' partials,
+  // staged into shared memory in one round trip) unless a tile spans more than 6 CTA ranges; then
+  // the separate fix-up kernel after the GEMV.  (Granite TP=1 layer 2, 5 contributors per tile:
+  // in-kernel 36.8 / 38.6 us at M = 1 / 16 against 37.5 / 40.8 with the fix-up kernel.)
   {
     const int64_t per = std::max<int64_t>(1, L.U / L.grid);
     const int64_t most = (L.NKB - 1 + per - 1) / per + 1;  // contributors of a tile, at most
     const char* e = getenv("TPQ_INRED_MAX");  // tuning aid (A/B): most contributors reduced in-kernel
-    L.inred = most <= (e ? atoi(e) : 4) && !getenv("TPQ_FIXUP_KERNEL");
+    L.inred = most <= (e ? atoi(e) : 6) && !getenv("TPQ_FIXUP_KERNEL");
   }
   // Cluster split-K for small shards: one tile per cluster of cs CTAs, each a 1/cs k-range of it,
   // reduced through distributed shared memory (no cross-CTA hand-off through L2 at the end of the
