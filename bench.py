@@ -266,14 +266,22 @@ def time_graph(torch, stream, g, reps, per):
     return statistics.median(evs[i].elapsed_time(evs[i + 1]) for i in range(reps)) * 1e3 / per
 
 
-def step_latency(torch, tpq, hs, R, stream, M, sim_tp, X, Y, reps=40):
-    """Graph-timed forward latency (us) at M rows, rotating the weight replicas."""
+EXTRA_COOLDOWN_S = 0.3  # idle before each extra line: measured as a burst like the main line
+
+
+def step_latency(torch, tpq, hs, R, stream, M, sim_tp, X, Y, reps=8):
+    """Graph-timed forward latency (us) at M rows, rotating the weight replicas: the median of `reps`
+    replays of a graph of ~16 forwards after a short idle, i.e. a burst like the main line's 20 steps
+    (sustained replays reach the board's power cap and the dequant-bound GEMV slows with the SM clock,
+    see clocks_extra_lines)."""
     per = R * max(1, 16 // R)
     f = (lambda h: h.forward_local(X, M, Y, stream=stream)) if sim_tp else (lambda h: h.forward(X, M, Y, stream=stream))
     with torch.cuda.stream(stream):
         for i in range(per):
             f(hs[i % R])
         g = graph_of(torch, stream, per, lambda i: f(hs[i % R]))
+    torch.cuda.synchronize()
+    time.sleep(EXTRA_COOLDOWN_S)
     return time_graph(torch, stream, g, reps, per)
 
 
