@@ -336,7 +336,6 @@ __device__ __forceinline__ uint64_t bdesc_sw128(uint32_t saddr) {
 }
 // instruction descriptor: D f32, A/B f16, both K-major, N = 16, M = 128
 constexpr uint32_t idesc_n(int n) { return (1u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(kTileCols >> 4) << 24); }
-constexpr uint32_t kIdesc = idesc_n(kNPad);
 
 // ------------------------------------------------------------------ stream-K partition
 // CTA c of `grid` owns units [c U / grid, (c + 1) U / grid) of a layer.
