@@ -559,8 +559,21 @@ def main():
     kt = kernel_times(torch, tpq, hs, R, stream, M, tp)
     kt = {k: max_over_ranks(v) for k, v in kt.items()}
     peak, peak_kind = peaks()
-    gemv_us = kt["layer1"] + kt["layer2"]
-    achieved = (l1_bytes + l2_bytes) / (gemv_us * 1e-6) / 1e9
+    # the GEMV launches in their own sequence: a graph of layer-1, layer-2 launch pairs (no gather),
+    # CUDA events around the replays only; a pair's time is <= the step's (the step adds the gather)
+    per = R * max(1, 16 // R)
+
+    def pair(i):
+        hs[i % R].run_step(tpq.TPQ_STEP_LAYER1, M, stream=stream)
+        hs[i % R].run_step(tpq.TPQ_STEP_LAYER2, M, stream=stream)
+    with torch.cuda.stream(stream):
+        for i in range(per):
+            pair(i)
+        gp = graph_of(torch, stream, per, pair)
+    torch.cuda.synchronize()
+    time.sleep(EXTRA_COOLDOWN_S)
+    pair_us = max_over_ranks(time_graph(torch, stream, gp, 8, per))
+    achieved = (l1_bytes + l2_bytes) / (pair_us * 1e-6) / 1e9
 
     # ---------------- e2e through the public host-buffer API (pinned host memory)
     # (--sim-tp has no host-buffer path: one rank's shard alone is not a complete forward)
@@ -597,11 +610,12 @@ def main():
         "step_stats": stats,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": ncu_traffic(a, shard_tp), "peak_kind": peak_kind,
-                     "kernel": "k_dqgemv + split-tile fix-up, layer 1 and layer 2",
+                     "kernel": "k_dqgemv, layer 1 and layer 2 (split tiles reduced in-kernel)",
                      "algorithmic_bytes_per_launch": (l1_bytes + l2_bytes) / 2,
-                     "launch_us": {"layer1": kt["layer1"], "layer2": kt["layer2"]},
-                     "how": "each layer's GEMV (+ fix-up) alone in a CUDA graph of many launches over the cold "
-                            "replicas, CUDA events around the replays only"},
+                     "launch_us": {"mean_of_layer1_layer2": pair_us / 2, "pair": pair_us},
+                     "how": "a CUDA graph of layer-1, layer-2 GEMV launch pairs over the cold replicas (the "
+                            "forward without its gather), median of 8 replays, CUDA events around the replays "
+                            "only; achieved = both layers' algorithmic bytes / the pair's time"},
         "kernel_us": kt,
         "kernel_sum_us": sum(kt.values()),
         "step_roofline": {"bytes": step_bytes, "GBps": step_bytes / (ms_per_step * 1e-3) / 1e9,
