@@ -654,3 +654,34 @@ def test_gemv_n32_passes(G, M):
         _assert_close(_np(y2), ref2["Y2_local"][r], f"N=32 GEMV tp=2 rank {r}")
         parts.append(y2)
         hr.close()
+
+
+@pytest.mark.parametrize("tp", [1, 8])
+def test_partition_modes_repeat_under_graph_replay(tp):
+    """Race check of the split-tile reductions in their production launch configuration: 160
+    graph-replayed forwards (two cold weight replicas, back to back with programmatic dependent
+    launch) of one Llama rank's shard -- stream-K with the in-kernel reduction at TP=1, clusters of
+    4 and 2 at TP=8 -- all bit-identical to the first (tools/stress_modes.py runs more)."""
+    M = 16
+    p = synth.make_named("llama70b", M, 0)
+    P1, P2 = _prep(p)
+    hs = [_mlp(p.w1, p.w2, P1, P2, tp=tp, rank=tp - 1, M_max=16) for _ in range(2)]
+    X = _dev(p.X)
+    Ys = [_empty(M, p.N2) for _ in range(2)]
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        for i in range(4):
+            hs[i % 2].forward_local(X, M, Ys[i % 2], stream=st)
+    torch.cuda.synchronize()
+    ref = [y.clone() for y in Ys]
+    with torch.cuda.stream(st):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            for i in range(16):
+                hs[i % 2].forward_local(X, M, Ys[i % 2], stream=st)
+    for _ in range(10):
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(Ys[0], ref[0]) and torch.equal(Ys[1], ref[1])
+    for h in hs:
+        h.close()
